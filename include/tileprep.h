@@ -1,0 +1,167 @@
+/*
+ * tileprep.h — C-ABI of the B200-native VLM input-preprocessing path.
+ *
+ * The reference (vlmfp, /root/reference/pkg/src/vlmfp) is pure Python and has no
+ * FFI; its drop-in boundary is the Python call signatures re-exported at
+ * vlmfp/__init__.py:99-139.  Each entry point below replaces the arithmetic core
+ * of one of those calls; the Python mirror in paper_2603_16987_b200/ keeps the
+ * reference signatures and binds these symbols with ctypes.
+ *
+ * Conventions (all entry points):
+ *   - plain pointers and sizes only; every pointer named d_* is DEVICE memory,
+ *     every other pointer is host memory read before the call returns;
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream);
+ *   - calls are asynchronous on `stream` and never allocate: the caller passes
+ *     every output and workspace buffer;
+ *   - return TP_OK (0) or a TP_ERR_* code; tp_last_error() gives the message
+ *     (thread-local).  Argument errors map to the reference's ValueError.
+ */
+#ifndef TILEPREP_H_
+#define TILEPREP_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define TP_API __attribute__((visibility("default")))
+#else
+#define TP_API
+#endif
+
+#define TP_ABI_VERSION 1
+
+/* return codes */
+#define TP_OK 0
+#define TP_ERR_INVALID_ARGUMENT 1 /* -> ValueError (imgproc.py:106-114, :363-366, :458-459) */
+#define TP_ERR_CUDA 2             /* CUDA runtime failure / no device             */
+#define TP_ERR_UNSUPPORTED 3      /* outside the exactness domain documented below */
+
+/* element types of normalized output (dtypes.py:13-16) */
+#define TP_DTYPE_NONE 0 /* no normalized output (uint8 side output only)   */
+#define TP_DTYPE_F32 1  /* "float32"                                       */
+#define TP_DTYPE_BF16 2 /* "float16-wide" == ml_dtypes.bfloat16 (dtypes.py:19) */
+
+/* layouts of normalized output */
+#define TP_LAYOUT_NCHW 0 /* [tiles, C, E, E]: vision-encoder input layout      */
+#define TP_LAYOUT_NHWC 1 /* [tiles, E, E, C]: the reference ImageBuffer layout */
+
+/* per-sequence error flags written by tp_expand */
+#define TP_EXPAND_ERR_MARKER_COUNT 1 /* -> ExpansionError        (tokenizer.py:300-302) */
+#define TP_EXPAND_ERR_NO_ASSISTANT 2 /* -> MalformedSequenceError (tokenizer.py:318-322) */
+#define TP_EXPAND_ERR_OVERFLOW 4     /* output length exceeds int32 / capacity          */
+
+/* plan record: 6 x int32 per image, the TilePlan field order (imgproc.py:64-81) */
+#define TP_PLAN_ROWS 0
+#define TP_PLAN_COLS 1
+#define TP_PLAN_TILE_EDGE 2
+#define TP_PLAN_THUMB 3
+#define TP_PLAN_RESIZED_W 4
+#define TP_PLAN_RESIZED_H 5
+#define TP_PLAN_FIELDS 6
+
+/* Largest image edge / max_tiles for which the integer planner is proven equal
+ * to the reference's float-log planner. */
+#define TP_MAX_EDGE 65536
+#define TP_MAX_TILES_LIMIT 1024
+
+TP_API int tp_abi_version(void);
+TP_API const char* tp_last_error(void);
+/* number of SMs of the current device (0 when no device) */
+TP_API int tp_device_sm_count(void);
+
+/* K1 — tile-grid planner, one warp per image.
+ * Replaces select_tile_plan (imgproc.py:266-292) for a batch.
+ *   d_wh       [n][2]  (width, height) per image, each in [1, TP_MAX_EDGE]
+ *   d_plan     [n][6]  TilePlan records (TP_PLAN_*)
+ *   d_n_img    [n]     plan.n_images (tiles + thumbnail), feeds tp_expand counts
+ *   d_tile_off [n+1]   exclusive prefix sum of n_images (output tile offsets)
+ * An invalid width/height writes rows=cols=0 and is reported through the
+ * returned d_tile_off[n] == -1 (host wrappers check before use). */
+TP_API int tp_plan(const int32_t* d_wh, int32_t n, int32_t tile_edge, int32_t max_tiles,
+            int32_t* d_plan, int32_t* d_n_img, int32_t* d_tile_off, void* stream);
+
+/* K0 — normalize lookup table: lut[c][v] = ((float)v / 255.f - mean[c]) / std[c]
+ * in IEEE fp32 (true divides), optionally rounded to bf16 RNE.
+ * Replaces the arithmetic of _normalize_array (imgproc.py:471-478).
+ *   mean, std  host float[channels] (already rounded to fp32 like
+ *              np.asarray(cfg.mean[:c], dtype=np.float32), imgproc.py:473-474)
+ *   d_lut      [channels][256] of float or bf16 */
+TP_API int tp_build_lut(int32_t channels, const float* mean, const float* std, int32_t dtype,
+                 void* d_lut, void* stream);
+
+/* K2 — fused resample + crop + thumbnail + normalize + layout/cast.
+ * Replaces tile_image/_tile_fused (imgproc.py:373-412, :449-465) followed by
+ * normalize_tiles (imgproc.py:496-513), for a batch of images.
+ *   d_src       packed HWC uint8 images; image k starts at d_src + d_src_off[k]
+ *   d_wh        [n][2]
+ *   channels    1 or 3 (ImageBuffer invariant, imgproc.py:46-47)
+ *   d_plan, d_tile_off   from tp_plan (or uploaded TilePlans)
+ *   d_lut       from tp_build_lut (ignored when dtype == TP_DTYPE_NONE)
+ *   d_out       [tiles][C][E][E] (NCHW) or [tiles][E][E][C] (NHWC) of dtype
+ *   d_out_u8    nullable; [tiles][E][E][C] uint8 tiles (the deferred-normalize
+ *               payload, imgproc.py:581-585)
+ *   out_capacity tiles the output buffers hold; tiles beyond it are not written
+ *               (the host compares d_tile_off[n] against it)
+ * uint8 tiles are bit-exact with the reference; normalized values are the LUT
+ * entry of that uint8 value, hence also bit-exact. */
+TP_API int tp_tile(const uint8_t* d_src, const int64_t* d_src_off, const int32_t* d_wh, int32_t n,
+            int32_t channels, const int32_t* d_plan, const int32_t* d_tile_off,
+            int32_t tile_edge, const void* d_lut, int32_t dtype, int32_t layout, void* d_out,
+            uint8_t* d_out_u8, int64_t out_capacity, void* stream);
+
+/* K2 variant for resize_bilinear / _resize_array (imgproc.py:352-367): one
+ * full-frame half-pixel bilinear resize, uint8 HWC -> uint8 HWC. */
+TP_API int tp_resize(const uint8_t* d_src, int32_t width, int32_t height, int32_t channels,
+              int32_t out_w, int32_t out_h, uint8_t* d_dst, void* stream);
+
+/* K4 — LUT normalize of uint8 HWC pixels (normalize / normalize_tiles,
+ * imgproc.py:481-513, and the deferred-normalize completion step run past the
+ * transfer boundary, bench.py:405-409).
+ *   n_images x pixels_per_image pixels of `channels` bytes each;
+ *   layout NHWC keeps the reference layout, NCHW writes [n][C][pixels]. */
+TP_API int tp_normalize(const uint8_t* d_src, int64_t n_images, int64_t pixels_per_image,
+                 int32_t channels, const void* d_lut, int32_t dtype, int32_t layout,
+                 void* d_out, void* stream);
+
+/* K3 — image-placeholder expansion + supervision mask for a batch of ragged
+ * prompts.  Replaces expand_image_placeholders (tokenizer.py:294-315),
+ * _first_assistant (:318-322) and build_supervision_mask (:410-418).
+ *   d_ids [seq_off[n_seq]], d_seq_off [n_seq+1]: input ids per sequence
+ *   d_counts [count_off[n_seq]], d_count_off [n_seq+1]: tile count per marker
+ *   tokens_per_tile, marker/ctx/asst ids (SpecialIds, tokenizer.py:43-51)
+ *   with_mask: 1 = build_supervision_mask law, 0 = all-false mask
+ *   d_out_ids [out_capacity], d_out_off [n_seq+1] (exclusive prefix of lengths)
+ *   d_spans [count_off[n_seq]][2] (start, length) relative to the sequence
+ *   d_first_asst [n_seq], d_mask [out_capacity] (uint8 0/1), d_err [n_seq]
+ *   d_work: workspace of tp_expand_workspace_bytes(n_seq) bytes */
+TP_API int64_t tp_expand_workspace_bytes(int32_t n_seq);
+TP_API int tp_expand(const int32_t* d_ids, const int32_t* d_seq_off, int32_t n_seq,
+              const int32_t* d_counts, const int32_t* d_count_off, int32_t tokens_per_tile,
+              int32_t marker_id, int32_t ctx_id, int32_t asst_id, int32_t with_mask,
+              int32_t* d_out_ids, int64_t out_capacity, int32_t* d_out_off, int32_t* d_spans,
+              int32_t* d_first_asst, uint8_t* d_mask, int32_t* d_err, void* d_work,
+              void* stream);
+
+/* K3b — supervision mask of an already expanded sequence with a given first
+ * assistant index t (build_supervision_mask, tokenizer.py:410-418):
+ * mask[i] = i >= t && ids[i] != asst_id.  t outside [0, n] -> TP_ERR_INVALID_ARGUMENT
+ * (the reference raises MalformedSequenceError). */
+TP_API int tp_supervision_mask(const int32_t* d_ids, int64_t n, int64_t first_asst,
+                               int32_t asst_id, uint8_t* d_mask, void* stream);
+
+/* Synthetic HWC uint8 images generated on device (bench/test inputs).
+ * kind 0: uniform bytes  v = byte(q & 3) of mix32(key(seed, k) ^ (q >> 2) * golden)
+ * kind 1: smooth ramp    v = triangle wave of (3x + 2y + 40c + 17k) with period 510
+ * d_off[k] must be a multiple of 4.  The CPU twin lives in oracle/ (tests only). */
+TP_API int tp_synth(uint8_t* d_dst, const int64_t* d_off, const int32_t* d_wh, int32_t n,
+             int32_t channels, uint64_t seed, int32_t kind, int64_t max_image_bytes,
+             void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TILEPREP_H_ */

@@ -1,0 +1,235 @@
+// K0 (normalize LUT), K4 (LUT normalize of uint8 pixels), synthetic inputs,
+// and the C-ABI error plumbing.
+
+#include <cstdarg>
+#include <cstdio>
+
+#include "tp_common.cuh"
+
+namespace tp {
+
+namespace {
+thread_local char g_error[512] = "";
+}
+
+int set_error(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_error, sizeof(g_error), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int check_launch(const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(TP_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  return TP_OK;
+}
+
+int device_sm_count() {
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  if (dev < 0 || dev >= 64) return 0;
+  if (cache[dev] == 0) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+      cudaGetLastError();
+      return 0;
+    }
+    cache[dev] = v;
+  }
+  return cache[dev];
+}
+
+namespace {
+
+// K0: the exact fp32 arithmetic of _normalize_array (imgproc.py:471-478):
+// (x.astype(f32) / f32(255) - mean_f32) / std_f32, true IEEE divides, then
+// optional fp32 -> bf16 round-to-nearest-even (dtypes.py:41-43).
+__global__ void k_build_lut(int C, float m0, float m1, float m2, float s0, float s1, float s2,
+                            int dtype, void* lut) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= C * 256) return;
+  const int c = i >> 8, v = i & 255;
+  const float m = c == 0 ? m0 : (c == 1 ? m1 : m2);
+  const float s = c == 0 ? s0 : (c == 1 ? s1 : s2);
+  const float q = __fdiv_rn(static_cast<float>(v), 255.0f);
+  const float r = __fdiv_rn(__fsub_rn(q, m), s);
+  if (dtype == TP_DTYPE_F32)
+    static_cast<float*>(lut)[i] = r;
+  else
+    static_cast<__nv_bfloat16*>(lut)[i] = __float2bfloat16_rn(r);
+}
+
+// K4: one thread per 4 pixels-channels would need alignment guarantees the
+// reference ImageBuffer does not give; one element per thread, grid-stride.
+template <int C, typename OutT, int LAYOUT>
+__global__ void __launch_bounds__(256)
+    k_normalize(const uint8_t* __restrict__ src, int64_t n_elems, int64_t ppi,
+                const OutT* __restrict__ lut, OutT* __restrict__ out) {
+  __shared__ OutT s_lut[C * 256];
+  for (int i = threadIdx.x; i < C * 256; i += blockDim.x) s_lut[i] = lut[i];
+  __syncthreads();
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < n_elems;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int c = C == 1 ? 0 : static_cast<int>(idx % C);
+    const OutT v = s_lut[c * 256 + src[idx]];
+    if (LAYOUT == TP_LAYOUT_NHWC) {
+      out[idx] = v;
+    } else {
+      const int64_t pix = idx / C;
+      const int64_t img = pix / ppi, p = pix - img * ppi;
+      out[(img * C + c) * ppi + p] = v;
+    }
+  }
+}
+
+template <int C, typename OutT>
+int launch_normalize(const uint8_t* src, int64_t n_elems, int64_t ppi, const void* lut,
+                     int layout, void* out, cudaStream_t s) {
+  const int64_t want = (n_elems + 255) / 256;
+  const int grid = static_cast<int>(std::min<int64_t>(want, 32LL * std::max(1, device_sm_count())));
+  if (layout == TP_LAYOUT_NHWC)
+    k_normalize<C, OutT, TP_LAYOUT_NHWC><<<grid, 256, 0, s>>>(
+        src, n_elems, ppi, static_cast<const OutT*>(lut), static_cast<OutT*>(out));
+  else
+    k_normalize<C, OutT, TP_LAYOUT_NCHW><<<grid, 256, 0, s>>>(
+        src, n_elems, ppi, static_cast<const OutT*>(lut), static_cast<OutT*>(out));
+  return check_launch("tp_normalize");
+}
+
+// ---------------------------------------------------------------------------
+// synthetic images (bench/test inputs; CPU twin: oracle/tileprep_oracle.py)
+
+__host__ __device__ __forceinline__ uint32_t fmix32(uint32_t h) {
+  h ^= h >> 16;
+  h *= 0x85ebca6bu;
+  h ^= h >> 13;
+  h *= 0xc2b2ae35u;
+  h ^= h >> 16;
+  return h;
+}
+
+__device__ __forceinline__ uint32_t synth_key(uint64_t seed, uint32_t k) {
+  const uint32_t lo = static_cast<uint32_t>(seed), hi = static_cast<uint32_t>(seed >> 32);
+  return fmix32(lo ^ fmix32(hi + k * 0x9E3779B9u + 0x7F4A7C15u));
+}
+
+__device__ __forceinline__ uint32_t synth_word(uint32_t key, uint32_t q4) {
+  return fmix32(key ^ (q4 * 0x9E3779B1u + 0x632BE5ABu));
+}
+
+__device__ __forceinline__ uint32_t smooth_byte(int64_t q, int W, int C, uint32_t k) {
+  const int64_t row = static_cast<int64_t>(W) * C;
+  const int64_t y = q / row;
+  const int64_t rem = q - y * row;
+  const int64_t x = rem / C, c = rem - x * C;
+  const int64_t t = (3 * x + 2 * y + 40 * c + 17 * static_cast<int64_t>(k)) % 510;
+  return static_cast<uint32_t>(t < 256 ? t : 509 - t);
+}
+
+__global__ void __launch_bounds__(256)
+    k_synth(uint8_t* __restrict__ dst, const int64_t* __restrict__ off,
+            const int32_t* __restrict__ wh, int n, int C, uint64_t seed, int kind) {
+  for (int k = blockIdx.y; k < n; k += gridDim.y) {
+    const int W = wh[2 * k], H = wh[2 * k + 1];
+    const int64_t bytes = static_cast<int64_t>(W) * H * C;
+    uint8_t* img = dst + off[k];
+    const int64_t words = bytes >> 2;
+    const uint32_t key = synth_key(seed, static_cast<uint32_t>(k));
+    uint32_t* w32 = reinterpret_cast<uint32_t*>(img);  // off[k] % 4 == 0 (host checked)
+    for (int64_t q4 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q4 < words;
+         q4 += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+      uint32_t v;
+      if (kind == 0) {
+        v = synth_word(key, static_cast<uint32_t>(q4));
+      } else {
+        v = 0;
+        for (int b = 0; b < 4; ++b) v |= smooth_byte(4 * q4 + b, W, C, k) << (8 * b);
+      }
+      w32[q4] = v;
+    }
+    if (blockIdx.x == 0 && threadIdx.x < (bytes & 3)) {
+      const int64_t q = (words << 2) + threadIdx.x;
+      const uint32_t v = kind == 0 ? (synth_word(key, static_cast<uint32_t>(words)) >>
+                                      (8 * threadIdx.x)) & 0xFFu
+                                   : smooth_byte(q, W, C, k);
+      img[q] = static_cast<uint8_t>(v);
+    }
+  }
+}
+
+}  // namespace
+}  // namespace tp
+
+extern "C" int tp_abi_version(void) { return TP_ABI_VERSION; }
+
+extern "C" const char* tp_last_error(void) { return tp::g_error; }
+
+extern "C" int tp_device_sm_count(void) { return tp::device_sm_count(); }
+
+extern "C" int tp_build_lut(int32_t channels, const float* mean, const float* std,
+                            int32_t dtype, void* d_lut, void* stream) {
+  if (channels != 1 && channels != 3)
+    return tp::set_error(TP_ERR_INVALID_ARGUMENT, "channels must be 1 or 3, got %d", channels);
+  if (dtype != TP_DTYPE_F32 && dtype != TP_DTYPE_BF16)
+    return tp::set_error(TP_ERR_INVALID_ARGUMENT, "bad dtype %d", dtype);
+  if (!mean || !std || !d_lut) return tp::set_error(TP_ERR_INVALID_ARGUMENT, "null buffer");
+  float m[3] = {0.f, 0.f, 0.f}, s[3] = {1.f, 1.f, 1.f};
+  for (int c = 0; c < channels; ++c) {
+    if (!(std[c] > 0.f))
+      return tp::set_error(TP_ERR_INVALID_ARGUMENT, "std components must be strictly positive");
+    m[c] = mean[c];
+    s[c] = std[c];
+  }
+  tp::k_build_lut<<<(channels * 256 + 255) / 256, 256, 0, tp::as_stream(stream)>>>(
+      channels, m[0], m[1], m[2], s[0], s[1], s[2], dtype, d_lut);
+  return tp::check_launch("tp_build_lut");
+}
+
+extern "C" int tp_normalize(const uint8_t* d_src, int64_t n_images, int64_t pixels_per_image,
+                            int32_t channels, const void* d_lut, int32_t dtype, int32_t layout,
+                            void* d_out, void* stream) {
+  if (channels != 1 && channels != 3)
+    return tp::set_error(TP_ERR_INVALID_ARGUMENT, "channels must be 1 or 3, got %d", channels);
+  if (dtype != TP_DTYPE_F32 && dtype != TP_DTYPE_BF16)
+    return tp::set_error(TP_ERR_INVALID_ARGUMENT, "bad dtype %d", dtype);
+  if (layout != TP_LAYOUT_NCHW && layout != TP_LAYOUT_NHWC)
+    return tp::set_error(TP_ERR_INVALID_ARGUMENT, "bad layout %d", layout);
+  if (n_images < 0 || pixels_per_image < 0)
+    return tp::set_error(TP_ERR_INVALID_ARGUMENT, "negative size");
+  const int64_t n_elems = n_images * pixels_per_image * channels;
+  if (n_elems == 0) return TP_OK;
+  if (!d_src || !d_lut || !d_out) return tp::set_error(TP_ERR_INVALID_ARGUMENT, "null buffer");
+  cudaStream_t s = tp::as_stream(stream);
+  if (channels == 3) {
+    if (dtype == TP_DTYPE_F32)
+      return tp::launch_normalize<3, float>(d_src, n_elems, pixels_per_image, d_lut, layout, d_out, s);
+    return tp::launch_normalize<3, __nv_bfloat16>(d_src, n_elems, pixels_per_image, d_lut, layout,
+                                                  d_out, s);
+  }
+  if (dtype == TP_DTYPE_F32)
+    return tp::launch_normalize<1, float>(d_src, n_elems, pixels_per_image, d_lut, layout, d_out, s);
+  return tp::launch_normalize<1, __nv_bfloat16>(d_src, n_elems, pixels_per_image, d_lut, layout,
+                                                d_out, s);
+}
+
+extern "C" int tp_synth(uint8_t* d_dst, const int64_t* d_off, const int32_t* d_wh, int32_t n,
+                        int32_t channels, uint64_t seed, int32_t kind, int64_t max_image_bytes,
+                        void* stream) {
+  if (channels != 1 && channels != 3)
+    return tp::set_error(TP_ERR_INVALID_ARGUMENT, "channels must be 1 or 3, got %d", channels);
+  if (kind != 0 && kind != 1) return tp::set_error(TP_ERR_INVALID_ARGUMENT, "bad kind %d", kind);
+  if (n < 0 || max_image_bytes < 0) return tp::set_error(TP_ERR_INVALID_ARGUMENT, "negative size");
+  if (n == 0 || max_image_bytes == 0) return TP_OK;
+  if (!d_dst || !d_off || !d_wh) return tp::set_error(TP_ERR_INVALID_ARGUMENT, "null buffer");
+  const int64_t want_x = (max_image_bytes / 4 + 255) / 256;
+  dim3 grid(static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(want_x, 1024))),
+            static_cast<unsigned>(std::min(n, 8192)));
+  tp::k_synth<<<grid, 256, 0, tp::as_stream(stream)>>>(d_dst, d_off, d_wh, n, channels, seed, kind);
+  return tp::check_launch("tp_synth");
+}

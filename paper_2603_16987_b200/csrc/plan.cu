@@ -1,0 +1,157 @@
+// K1 — tile-grid planner (replaces select_tile_plan, imgproc.py:266-292).
+//
+// The reference minimises the key (|log(w/h) - log(c/r)|, r*c, r) over every
+// grid with r*c <= max_tiles, in float64 `math.log`.  Here the first key
+// component is compared exactly: |log(w r / (h c))| = log(M/m) with
+// M = max(w r, h c), m = min(w r, h c), so key1 < key2  <=>  M1 m2 < M2 m1
+// (64-bit products; w, h <= 2^16 and r, c <= 1024 keep them below 2^53).
+// DESIGN.md §K1 proves this equals the float ordering on that domain; the
+// golden/oracle tests pin it, including every exact tie.
+//
+// One warp per image: lane L owns rows r = L+1, L+33, ...; for a fixed r the
+// key is unimodal in c with its minimum at c ~ w r / h, so only
+// c = floor(w r / h) and c + 1 (clamped to [1, max_tiles / r]) can win.  The
+// per-lane winners are reduced across the warp with the exact comparator.
+// One CTA of 1024 threads walks the batch in chunks of 1024 images and
+// block-scans n_images into the output tile offsets.
+
+#include "tp_common.cuh"
+
+namespace tp {
+namespace {
+
+struct Cand {
+  uint32_t big, small;  // ratio = big / small >= 1
+  int32_t rows, cols;
+};
+
+__device__ __forceinline__ Cand make_cand(uint32_t w, uint32_t h, int r, int c) {
+  const uint32_t a = w * static_cast<uint32_t>(r);
+  const uint32_t b = h * static_cast<uint32_t>(c);
+  Cand k;
+  k.big = a > b ? a : b;
+  k.small = a > b ? b : a;
+  k.rows = r;
+  k.cols = c;
+  return k;
+}
+
+// strict "a precedes b" in the reference key order (ratio, tiles, rows)
+__device__ __forceinline__ bool precedes(const Cand& a, const Cand& b) {
+  if (b.rows == 0) return a.rows != 0;  // empty slot loses to anything
+  if (a.rows == 0) return false;
+  const uint64_t lhs = static_cast<uint64_t>(a.big) * b.small;
+  const uint64_t rhs = static_cast<uint64_t>(b.big) * a.small;
+  if (lhs != rhs) return lhs < rhs;
+  const int ta = a.rows * a.cols, tb = b.rows * b.cols;
+  if (ta != tb) return ta < tb;
+  return a.rows < b.rows;
+}
+
+// Whole warp plans one image; returns the winning (rows, cols) on every lane.
+__device__ Cand warp_plan(uint32_t w, uint32_t h, int max_tiles) {
+  const int lane = threadIdx.x & 31;
+  Cand best;
+  best.rows = 0;
+  best.cols = 0;
+  best.big = 1;
+  best.small = 1;
+  for (int r = lane + 1; r <= max_tiles; r += 32) {
+    const int cmax = max_tiles / r;
+    // c* = floor(w r / h), candidates c*, c*+1 clamped to [1, cmax]
+    int c0 = static_cast<int>((static_cast<uint64_t>(w) * r) / h);
+    c0 = max(1, min(c0, cmax));
+    const int c1 = min(c0 + 1, cmax);
+    Cand k0 = make_cand(w, h, r, c0);
+    if (precedes(k0, best)) best = k0;
+    if (c1 != c0) {
+      Cand k1 = make_cand(w, h, r, c1);
+      if (precedes(k1, best)) best = k1;
+    }
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    Cand o;
+    o.big = __shfl_xor_sync(0xffffffffu, best.big, d);
+    o.small = __shfl_xor_sync(0xffffffffu, best.small, d);
+    o.rows = __shfl_xor_sync(0xffffffffu, best.rows, d);
+    o.cols = __shfl_xor_sync(0xffffffffu, best.cols, d);
+    if (precedes(o, best)) best = o;
+  }
+  return best;
+}
+
+constexpr int kPlanThreads = 1024;
+
+__global__ void __launch_bounds__(kPlanThreads)
+    k_plan(const int32_t* __restrict__ wh, int32_t n, int32_t tile_edge, int32_t max_tiles,
+           int32_t* __restrict__ plan, int32_t* __restrict__ n_img,
+           int32_t* __restrict__ tile_off) {
+  __shared__ int32_t s_cnt[kPlanThreads];
+  __shared__ int64_t s_scan[33];
+  __shared__ int s_bad;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) s_bad = 0;
+  int64_t carry = 0;
+  for (int base = 0; base < n; base += kPlanThreads) {
+    const int chunk = min(kPlanThreads, n - base);
+    s_cnt[threadIdx.x] = 0;
+    __syncthreads();
+    // 32 warps x 32 images each
+    for (int j = warp; j < chunk; j += kPlanThreads / 32) {
+      const int k = base + j;
+      const int w = wh[2 * k], h = wh[2 * k + 1];
+      const bool ok = w >= 1 && h >= 1 && w <= TP_MAX_EDGE && h <= TP_MAX_EDGE;
+      Cand best;
+      best.rows = 0;
+      best.cols = 0;
+      if (ok) best = warp_plan(static_cast<uint32_t>(w), static_cast<uint32_t>(h), max_tiles);
+      if (lane == 0) {
+        const int tiles = best.rows * best.cols;
+        const int thumb = tiles > 1 ? 1 : 0;
+        int32_t* p = plan + static_cast<int64_t>(k) * TP_PLAN_FIELDS;
+        p[TP_PLAN_ROWS] = best.rows;
+        p[TP_PLAN_COLS] = best.cols;
+        p[TP_PLAN_TILE_EDGE] = tile_edge;
+        p[TP_PLAN_THUMB] = thumb;
+        p[TP_PLAN_RESIZED_W] = best.cols * tile_edge;
+        p[TP_PLAN_RESIZED_H] = best.rows * tile_edge;
+        const int cnt = tiles + thumb;
+        n_img[k] = cnt;
+        s_cnt[j] = cnt;
+        if (!ok) s_bad = 1;
+      }
+    }
+    __syncthreads();
+    int64_t total;
+    const int64_t ex = block_exclusive_scan<int64_t>(s_cnt[threadIdx.x], s_scan, &total);
+    if (threadIdx.x < chunk) tile_off[base + threadIdx.x] = static_cast<int32_t>(carry + ex);
+    carry += total;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const bool overflow = carry > INT32_MAX;
+    tile_off[n] = (s_bad || overflow) ? -1 : static_cast<int32_t>(carry);
+  }
+}
+
+}  // namespace
+}  // namespace tp
+
+extern "C" int tp_plan(const int32_t* d_wh, int32_t n, int32_t tile_edge, int32_t max_tiles,
+                       int32_t* d_plan, int32_t* d_n_img, int32_t* d_tile_off, void* stream) {
+  if (n < 0) return tp::set_error(TP_ERR_INVALID_ARGUMENT, "tp_plan: n must be >= 0");
+  if (tile_edge < 1) return tp::set_error(TP_ERR_INVALID_ARGUMENT, "tile_edge must be positive");
+  if (max_tiles < 1) return tp::set_error(TP_ERR_INVALID_ARGUMENT, "max_tiles must be >= 1");
+  if (max_tiles > TP_MAX_TILES_LIMIT)
+    return tp::set_error(TP_ERR_UNSUPPORTED, "max_tiles %d above the exact-planner limit %d",
+                         max_tiles, TP_MAX_TILES_LIMIT);
+  if (static_cast<int64_t>(tile_edge) * max_tiles > INT32_MAX)
+    return tp::set_error(TP_ERR_UNSUPPORTED, "tile_edge * max_tiles overflows int32");
+  if (!d_tile_off || (n > 0 && (!d_wh || !d_plan || !d_n_img)))
+    return tp::set_error(TP_ERR_INVALID_ARGUMENT, "tp_plan: null buffer");
+  tp::k_plan<<<1, tp::kPlanThreads, 0, tp::as_stream(stream)>>>(d_wh, n, tile_edge, max_tiles,
+                                                                d_plan, d_n_img, d_tile_off);
+  return tp::check_launch("tp_plan");
+}

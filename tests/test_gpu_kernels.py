@@ -1,0 +1,249 @@
+"""Parity of the CUDA path (through the C-ABI) with the oracle and the
+reference's golden vectors.  Runs on the B200 box (`-m gpu`)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from golden_data import IMAGENET_MEAN, IMAGENET_STD, make_input
+from oracle import tileprep_oracle as O
+from paper_2603_16987_b200 import _lib
+from paper_2603_16987_b200.engine import (
+    TilePreprocessor,
+    empty_packed,
+    pack_images,
+    synth_packed,
+)
+from paper_2603_16987_b200.imgproc import PreprocessConfig
+
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda:0"
+
+
+def _plans_on_gpu(wh: np.ndarray, tile_edge: int, max_tiles: int):
+    n = len(wh)
+    d_wh = torch.from_numpy(np.ascontiguousarray(wh, dtype=np.int32)).to(DEV)
+    plan = torch.empty((n, 6), dtype=torch.int32, device=DEV)
+    n_img = torch.empty((n,), dtype=torch.int32, device=DEV)
+    off = torch.empty((n + 1,), dtype=torch.int32, device=DEV)
+    _lib.call("tp_plan", _lib.ptr(d_wh), n, tile_edge, max_tiles, _lib.ptr(plan),
+              _lib.ptr(n_img), _lib.ptr(off), torch.cuda.current_stream().cuda_stream)
+    return plan.cpu().numpy(), n_img.cpu().numpy(), off.cpu().numpy()
+
+
+# ---------------------------------------------------------------------------
+# K1 planner
+
+def test_plan_matches_golden(golden):
+    data, _ = golden
+    pin, want = data["plan_in"], data["plan_out"]
+    for mt in np.unique(pin[:, 2]):
+        sel = pin[:, 2] == mt
+        plan, n_img, off = _plans_on_gpu(pin[sel, :2], 32, int(mt))
+        assert np.array_equal(plan, want[sel]), int(mt)
+        assert np.array_equal(n_img, want[sel, 0] * want[sel, 1] + want[sel, 3])
+        assert off[0] == 0 and np.array_equal(np.diff(off), n_img)
+
+
+def test_plan_dense_square_vs_oracle():
+    w, h = np.meshgrid(np.arange(1, 301), np.arange(1, 301))
+    wh = np.stack([w.ravel(), h.ravel()], axis=1)
+    for mt in (1, 2, 6, 12, 40):
+        plan, _, _ = _plans_on_gpu(wh, 448, mt)
+        for i in range(0, len(wh), 97):
+            assert tuple(plan[i]) == O.plan_float(int(wh[i, 0]), int(wh[i, 1]), 448, mt)
+        if mt == 12:  # full check of the config value
+            want = np.array([O.plan_int(int(a), int(b), 448, 12) for a, b in wh[::7]])
+            assert np.array_equal(plan[::7], want)
+
+
+def test_plan_invalid_size_flags_batch():
+    plan, n_img, off = _plans_on_gpu(np.array([[10, 10], [0, 5], [20, 10]]), 16, 12)
+    assert off[-1] == -1
+    assert n_img[1] == 0
+
+
+def test_plan_large_batch_offsets():
+    rng = np.random.default_rng(1)
+    wh = rng.integers(1, 4097, size=(5000, 2))
+    plan, n_img, off = _plans_on_gpu(wh, 448, 12)
+    assert off[-1] == n_img.sum() and np.array_equal(np.cumsum(n_img), off[1:])
+    for i in range(0, 5000, 250):
+        assert tuple(plan[i]) == O.plan_int(int(wh[i, 0]), int(wh[i, 1]), 448, 12)
+
+
+# ---------------------------------------------------------------------------
+# K2 fused tiling (+ normalize through the LUT)
+
+def _run_engine(arrs, cfg, layout="NCHW", emit_uint8=True, normalize=True):
+    packed = pack_images(arrs).to(DEV)
+    prep = TilePreprocessor(cfg, DEV, layout=layout, emit_uint8=emit_uint8, normalize=normalize)
+    out = prep(packed)
+    torch.cuda.synchronize()
+    T = out.num_tiles()
+    pv = out.pixel_values[:T].cpu() if out.pixel_values is not None else None
+    u8 = out.pixel_u8[:T].cpu().numpy() if out.pixel_u8 is not None else None
+    return out, pv, u8
+
+
+def test_tiles_match_golden_all_layouts(golden):
+    data, meta = golden
+    for name, h, w, c, e, mt, kind, seed in meta["tile_cases"]:
+        arr = make_input(h, w, c, kind, seed)
+        want_u8 = data[f"tile_{name}_u8"]
+        cfg = PreprocessConfig(tile_edge=e, max_tiles=mt, mean=IMAGENET_MEAN, std=IMAGENET_STD)
+        out, pv, u8 = _run_engine([arr], cfg, layout="NHWC")
+        assert np.array_equal(out.plans.plan.cpu().numpy()[0], data[f"tile_{name}_plan"]), name
+        assert np.array_equal(u8, want_u8), name
+        assert np.array_equal(pv.numpy(), data[f"tile_{name}_f32_imagenet"]), name
+        cfgb = PreprocessConfig(tile_edge=e, max_tiles=mt, reduced_precision_normalize=True)
+        _, pvb, _ = _run_engine([arr], cfgb, layout="NCHW", emit_uint8=False)
+        want_b = data[f"tile_{name}_bf16_half_bits"].transpose(0, 3, 1, 2)
+        assert np.array_equal(pvb.view(torch.int16).numpy().view(np.uint16), want_b), name
+
+
+def test_tiles_batch_mixed_sizes_vs_oracle():
+    rng = np.random.default_rng(5)
+    arrs = []
+    for i in range(12):
+        h, w = int(rng.integers(1, 120)), int(rng.integers(1, 120))
+        arrs.append(make_input(h, w, 3, "random" if i % 2 else "smooth", 100 + i))
+    cfg = PreprocessConfig(tile_edge=24, max_tiles=9)
+    out, pv, u8 = _run_engine(arrs, cfg)
+    off = out.plans.tile_off.cpu().numpy()
+    lut = O.lut((0.5,) * 3, (0.5,) * 3, 3, False)
+    for k, a in enumerate(arrs):
+        plan = O.plan_float(a.shape[1], a.shape[0], 24, 9)
+        want = O.tiles_u8(a, plan)
+        assert np.array_equal(u8[off[k]: off[k + 1]], want), k
+        norm = pv[off[k]: off[k + 1]].numpy()  # NCHW
+        assert np.array_equal(norm, O.normalize(want, (0.5,) * 3, (0.5,) * 3, False)
+                              .transpose(0, 3, 1, 2)), k
+    assert np.array_equal(lut[:, u8[..., 0].ravel()][0], pv[:, 0].numpy().ravel())
+
+
+def test_tiles_grayscale_channel():
+    arr = make_input(40, 70, 1, "random", 3)
+    cfg = PreprocessConfig(tile_edge=16, max_tiles=6, mean=IMAGENET_MEAN, std=IMAGENET_STD)
+    _, pv, u8 = _run_engine([arr], cfg, layout="NHWC")
+    plan = O.plan_float(70, 40, 16, 6)
+    want = O.tiles_u8(arr, plan)
+    assert np.array_equal(u8, want)
+    assert np.array_equal(pv.numpy(), O.normalize(want, IMAGENET_MEAN, IMAGENET_STD, False))
+
+
+@pytest.mark.parametrize("w,h,e,kind", [(1920, 1080, 448, "random"), (1920, 1080, 512, "smooth"),
+                                        (3840, 2160, 448, "random"), (640, 480, 448, "smooth"),
+                                        (333, 517, 448, "random")])
+def test_full_size_bit_exact(w, h, e, kind):
+    arr = make_input(h, w, 3, kind, w * 7 + h)
+    cfg = PreprocessConfig(tile_edge=e, max_tiles=12, mean=IMAGENET_MEAN, std=IMAGENET_STD,
+                           reduced_precision_normalize=True)
+    _, pv, u8 = _run_engine([arr], cfg)
+    plan = O.plan_float(w, h, e, 12)
+    want = O.tiles_u8(arr, plan)
+    assert np.array_equal(u8, want)
+    wb = O.normalize(want, IMAGENET_MEAN, IMAGENET_STD, True).transpose(0, 3, 1, 2)
+    assert np.array_equal(pv.view(torch.int16).numpy().view(np.uint16), wb.view(np.uint16))
+
+
+def test_capacity_guard_never_writes_past_buffer():
+    arrs = [make_input(100, 200, 3, "random", 1)]  # 1x2 + thumb = 3 tiles
+    cfg = PreprocessConfig(tile_edge=16, max_tiles=12)
+    packed = pack_images(arrs).to(DEV)
+    prep = TilePreprocessor(cfg, DEV, emit_uint8=True)
+    plans = prep.plan(packed)
+    guard = torch.full((3, 16, 16, 3), 7, dtype=torch.uint8, device=DEV)
+    pv = torch.zeros((2, 3, 16, 16), dtype=torch.float32, device=DEV)
+    prep.tile(packed, plans, pv, guard[:2])
+    torch.cuda.synchronize()
+    assert int(guard[2].min()) == 7 and int(guard[2].max()) == 7
+
+
+def test_resize_matches_golden(golden):
+    data, meta = golden
+    stream = torch.cuda.current_stream().cuda_stream
+    for i, (h, w, c, oh, ow, seed, kind) in enumerate(meta["resize_cases"]):
+        arr = make_input(h, w, c, kind, seed)
+        src = torch.from_numpy(np.ascontiguousarray(arr).reshape(-1)).to(DEV)
+        dst = torch.empty((oh, ow, arr.shape[2]), dtype=torch.uint8, device=DEV)
+        _lib.call("tp_resize", _lib.ptr(src), arr.shape[1], arr.shape[0], arr.shape[2], ow, oh,
+                  _lib.ptr(dst), stream)
+        assert np.array_equal(dst.cpu().numpy(), data[f"resize_{i}"]), i
+
+
+def test_lut_matches_golden(golden):
+    data, _ = golden
+    from paper_2603_16987_b200.runtime import normalize_lut
+
+    d = torch.device(DEV)
+    for tag, mean, std in (("half", (0.5,) * 3, (0.5,) * 3),
+                           ("imagenet", IMAGENET_MEAN, IMAGENET_STD)):
+        f = normalize_lut(mean, std, 3, _lib.TP_DTYPE_F32, d).cpu().numpy()
+        assert np.array_equal(f, data[f"lut_{tag}_f32"])
+        b = normalize_lut(mean, std, 3, _lib.TP_DTYPE_BF16, d).cpu().view(torch.int16).numpy()
+        assert np.array_equal(b.view(np.uint16), data[f"lut_{tag}_bf16"])
+        g = normalize_lut(mean, std, 1, _lib.TP_DTYPE_F32, d).cpu().numpy()
+        assert np.array_equal(g, data[f"lut_{tag}_f32_gray"])
+
+
+def test_normalize_kernel_layouts():
+    from paper_2603_16987_b200.runtime import normalize_lut
+
+    d = torch.device(DEV)
+    rng = np.random.default_rng(9)
+    u8 = rng.integers(0, 256, size=(5, 7, 11, 3), dtype=np.uint8)
+    lut = normalize_lut(IMAGENET_MEAN, IMAGENET_STD, 3, _lib.TP_DTYPE_F32, d)
+    src = torch.from_numpy(u8.reshape(-1)).to(DEV)
+    want = O.normalize(u8, IMAGENET_MEAN, IMAGENET_STD, False)
+    for layout, shape, ref in ((_lib.TP_LAYOUT_NHWC, u8.shape, want),
+                               (_lib.TP_LAYOUT_NCHW, (5, 3, 7, 11), want.transpose(0, 3, 1, 2))):
+        out = torch.empty(shape, dtype=torch.float32, device=DEV)
+        _lib.call("tp_normalize", _lib.ptr(src), 5, 77, 3, _lib.ptr(lut), _lib.TP_DTYPE_F32,
+                  layout, _lib.ptr(out), torch.cuda.current_stream().cuda_stream)
+        assert np.array_equal(out.cpu().numpy(), ref)
+
+
+# ---------------------------------------------------------------------------
+# synthetic inputs: device generator == CPU twin
+
+@pytest.mark.parametrize("kind", [0, 1])
+def test_synth_matches_cpu_twin(kind):
+    wh = np.array([[37, 11], [64, 48], [5, 3], [1920, 2]], dtype=np.int32)
+    packed = synth_packed(wh, 3, DEV, seed=20260817, kind=kind)
+    buf = packed.data.cpu().numpy()
+    for k, (w, h) in enumerate(wh):
+        off = packed.offsets_host[k]
+        got = buf[off: off + w * h * 3].reshape(h, w, 3)
+        assert np.array_equal(got, O.synth_image(20260817, k, int(w), int(h), 3, kind)), k
+
+
+def test_c4_style_batch_sample_bit_exact():
+    """A slice of the 8192-image mixed-aspect sweep (C4) checked image by image."""
+    from paper_2603_16987_b200.workloads import c4_shapes
+
+    wh = c4_shapes(48, start=0)
+    packed = synth_packed(wh, 3, DEV, seed=20261018, kind=0)
+    cfg = PreprocessConfig(tile_edge=448, max_tiles=12, mean=IMAGENET_MEAN, std=IMAGENET_STD,
+                           reduced_precision_normalize=True)
+    prep = TilePreprocessor(cfg, DEV, emit_uint8=True)
+    out = prep(packed)
+    torch.cuda.synchronize()
+    off = out.plans.tile_off.cpu().numpy()
+    for k in range(0, 48, 5):
+        w, h = (int(v) for v in wh[k])
+        arr = O.synth_image(20261018, k, w, h, 3, 0)
+        want = O.tiles_u8(arr, O.plan_float(w, h, 448, 12))
+        got = out.pixel_u8[off[k]: off[k + 1]].cpu().numpy()
+        assert np.array_equal(got, want), k
+    # normalized output is the LUT image of the uint8 tiles for the whole batch
+    T = out.num_tiles()
+    lut = torch.from_numpy(O.lut(IMAGENET_MEAN, IMAGENET_STD, 3, True).view(np.int16)).to(DEV)
+    u8 = out.pixel_u8[:T].long()
+    for c in range(3):
+        want_c = lut[c][u8[..., c]]
+        got_c = out.pixel_values[:T, c].view(torch.int16)
+        assert torch.equal(want_c, got_c)
