@@ -112,6 +112,20 @@ TP_API int tp_tile(const uint8_t* d_src, const int64_t* d_src_off, const int32_t
             int32_t tile_edge, const void* d_lut, int32_t dtype, int32_t layout, void* d_out,
             uint8_t* d_out_u8, int64_t out_capacity, void* stream);
 
+/* tp_tile with an explicit algorithm:
+ *   TP_TILE_ALGO_AUTO / _FAST: fp32 2-tap arithmetic with a proven error window,
+ *       exact fp64 recomputation of the values inside the window (bit-exact);
+ *   TP_TILE_ALGO_EXACT: every value in fp64 in the reference order (the
+ *       straightforward kernel, kept as an on-device cross-check). */
+#define TP_TILE_ALGO_AUTO 0
+#define TP_TILE_ALGO_FAST 1
+#define TP_TILE_ALGO_EXACT 2
+TP_API int tp_tile_ex(const uint8_t* d_src, const int64_t* d_src_off, const int32_t* d_wh,
+                      int32_t n, int32_t channels, const int32_t* d_plan,
+                      const int32_t* d_tile_off, int32_t tile_edge, const void* d_lut,
+                      int32_t dtype, int32_t layout, void* d_out, uint8_t* d_out_u8,
+                      int64_t out_capacity, int32_t algo, void* stream);
+
 /* K2 variant for resize_bilinear / _resize_array (imgproc.py:352-367): one
  * full-frame half-pixel bilinear resize, uint8 HWC -> uint8 HWC. */
 TP_API int tp_resize(const uint8_t* d_src, int32_t width, int32_t height, int32_t channels,

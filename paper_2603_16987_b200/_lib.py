@@ -29,6 +29,10 @@ TP_EXPAND_ERR_MARKER_COUNT = 1
 TP_EXPAND_ERR_NO_ASSISTANT = 2
 TP_EXPAND_ERR_OVERFLOW = 4
 
+TP_TILE_ALGO_AUTO = 0
+TP_TILE_ALGO_FAST = 1
+TP_TILE_ALGO_EXACT = 2
+
 TP_PLAN_FIELDS = 6
 TP_MAX_EDGE = 65536
 TP_MAX_TILES_LIMIT = 1024
@@ -46,6 +50,9 @@ SIGNATURES = {
     "tp_tile": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_void_p,
                           c_int32, c_void_p, c_int32, c_int32, c_void_p, c_void_p, c_int64,
                           c_void_p]),
+    "tp_tile_ex": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_void_p,
+                             c_int32, c_void_p, c_int32, c_int32, c_void_p, c_void_p, c_int64,
+                             c_int32, c_void_p]),
     "tp_resize": (c_int32, [c_void_p, c_int32, c_int32, c_int32, c_int32, c_int32, c_void_p,
                             c_void_p]),
     "tp_normalize": (c_int32, [c_void_p, c_int64, c_int64, c_int32, c_void_p, c_int32,

@@ -163,8 +163,13 @@ class TilePreprocessor:
     """
 
     def __init__(self, cfg, device=None, layout: str = "NCHW", emit_uint8: bool = False,
-                 normalize: bool = True):
+                 normalize: bool = True, algo: str = "auto"):
         self.cfg = cfg
+        algos = {"auto": _lib.TP_TILE_ALGO_AUTO, "fast": _lib.TP_TILE_ALGO_FAST,
+                 "exact": _lib.TP_TILE_ALGO_EXACT}
+        if algo not in algos:
+            raise ValueError(f"algo must be one of {sorted(algos)}, got {algo!r}")
+        self.algo = algos[algo]
         self.device = require_device(device)
         if layout not in ("NCHW", "NHWC"):
             raise ValueError(f"layout must be NCHW or NHWC, got {layout!r}")
@@ -228,11 +233,11 @@ class TilePreprocessor:
         if not caps:
             raise ValueError("no output buffer")
         with torch.cuda.device(self.device):
-            _lib.call("tp_tile", _lib.ptr(images.data), _lib.ptr(images.offsets),
+            _lib.call("tp_tile_ex", _lib.ptr(images.data), _lib.ptr(images.offsets),
                       _lib.ptr(images.wh), images.n, images.channels, _lib.ptr(plans.plan),
                       _lib.ptr(plans.tile_off), self.cfg.tile_edge, _lib.ptr(lut), self.dtype,
                       self.layout, _lib.ptr(pixel_values), _lib.ptr(pixel_u8), min(caps),
-                      stream_handle(self.device, stream))
+                      self.algo, stream_handle(self.device, stream))
 
     def __call__(self, images: PackedImages, capacity: Optional[int] = None,
                  out: Optional[TileBatch] = None,

@@ -247,3 +247,56 @@ def test_c4_style_batch_sample_bit_exact():
         want_c = lut[c][u8[..., c]]
         got_c = out.pixel_values[:T, c].view(torch.int16)
         assert torch.equal(want_c, got_c)
+
+
+# ---------------------------------------------------------------------------
+# fast kernel (fp32 + exactness window) == exact fp64 kernel, at full size
+
+def _fast_vs_exact(wh, seed, kind, cfg, layout="NCHW"):
+    packed = synth_packed(wh, 3, DEV, seed=seed, kind=kind)
+    outs = []
+    for algo in ("fast", "exact"):
+        prep = TilePreprocessor(cfg, DEV, layout=layout, emit_uint8=True, algo=algo)
+        outs.append(prep(packed))
+    torch.cuda.synchronize()
+    T = outs[0].num_tiles()
+    assert T == outs[1].num_tiles()
+    assert torch.equal(outs[0].pixel_u8[:T], outs[1].pixel_u8[:T])
+    assert torch.equal(outs[0].pixel_values[:T].view(torch.uint8),
+                       outs[1].pixel_values[:T].view(torch.uint8))
+    return T
+
+
+@pytest.mark.parametrize("kind", [0, 1])
+def test_fast_equals_exact_c4_slice(kind):
+    from paper_2603_16987_b200.workloads import c4_shapes
+
+    cfg = PreprocessConfig(tile_edge=448, max_tiles=12, mean=IMAGENET_MEAN, std=IMAGENET_STD,
+                           reduced_precision_normalize=True)
+    assert _fast_vs_exact(c4_shapes(256, start=512 * kind), 20261018 + kind, kind, cfg) > 256
+
+
+@pytest.mark.parametrize("e,layout", [(512, "NCHW"), (448, "NHWC"), (7, "NCHW"), (33, "NHWC")])
+def test_fast_equals_exact_edges(e, layout):
+    rng = np.random.default_rng(e)
+    wh = np.stack([rng.integers(1, 3000, 40), rng.integers(1, 3000, 40)], axis=1)
+    cfg = PreprocessConfig(tile_edge=e, max_tiles=12)
+    _fast_vs_exact(wh, 99, 0, cfg, layout)
+    _fast_vs_exact(wh, 98, 1, cfg, layout)
+
+
+def test_fast_integer_scale_ties():
+    # integer down/up-scales put many values exactly on k + 0.5: all go through the fallback
+    cfg = PreprocessConfig(tile_edge=64, max_tiles=4)
+    wh = np.array([[128, 128], [256, 128], [32, 32], [64, 128], [96, 96]])
+    for kind in (0, 1):
+        _fast_vs_exact(wh, 5, kind, cfg)
+        packed = synth_packed(wh, 3, DEV, seed=5, kind=kind)
+        prep = TilePreprocessor(cfg, DEV, emit_uint8=True)
+        out = prep(packed)
+        torch.cuda.synchronize()
+        off = out.plans.tile_off.cpu().numpy()
+        for k, (w, h) in enumerate(wh):
+            arr = O.synth_image(5, k, int(w), int(h), 3, kind)
+            want = O.tiles_u8(arr, O.plan_float(int(w), int(h), 64, 4))
+            assert np.array_equal(out.pixel_u8[off[k]: off[k + 1]].cpu().numpy(), want)
