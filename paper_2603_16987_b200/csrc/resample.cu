@@ -166,151 +166,6 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 
-// ---------------------------------------------------------------------------
-// Fast path: fp32 2-tap arithmetic + exactness window + exact fp64 fallback.
-//
-// With biased bytes s' = 2^23 + s (exact), per output channel value:
-//   L'' = fma(fy, b'-a', a' - (2^23 - 0.5))   = a + 0.5 + fy (b - a)
-//   R'' = fma(fy, d'-c', c' - (2^23 - 0.5))   = c + 0.5 + fy (d - c)
-//   t   = fma(fx, R'' - L'', L'')             ~ v + 0.5
-//   N   = round(t * 4096)   (one fma against 1.5 * 2^23)
-// |t - (v_ref + 0.5)| <= 3.8e-5 (DESIGN.md §K2 derives the bound; the fp64
-// reference itself is within 2e-13 of the exact rational value).  Whenever
-// N mod 4096 is in [2, 4094], t is >= 3.66e-4 away from every integer, so
-// floor(t) = N >> 12 equals the reference's floor(v64 + 0.5).  Otherwise the
-// value is recomputed exactly in fp64 in the reference order (blend_exact).
-
-constexpr int kFastMaxThreads = 256;
-constexpr int kFastBand = 8;
-
-__device__ __forceinline__ float biased(uint32_t byte) {
-  return __uint_as_float(0x4B000000u | byte);  // 2^23 + byte, exact
-}
-
-struct FastTap {
-  float fy;  // rows: fy; cols: fx
-  int i0, i1;
-};
-
-// returns the uint8 value; `amb` set when the exact fallback is needed
-__device__ __forceinline__ uint32_t blend_fast(uint32_t a, uint32_t b, uint32_t c, uint32_t d,
-                                               float fy, float fx, bool& amb) {
-  const float ha = __fsub_rn(biased(a), 8388607.5f);  // a + 0.5
-  const float hc = __fsub_rn(biased(c), 8388607.5f);  // c + 0.5
-  const float l = __fmaf_rn(fy, __fsub_rn(biased(b), biased(a)), ha);
-  const float r = __fmaf_rn(fy, __fsub_rn(biased(d), biased(c)), hc);
-  const float t = __fmaf_rn(fx, __fsub_rn(r, l), l);
-  const float m = __fmaf_rn(t, 4096.0f, 12582912.0f);
-  const uint32_t n = __float_as_uint(m) - 0x4B400000u;
-  amb = ((n + 1u) & 4095u) <= 2u;
-  return min(n >> 12, 255u);
-}
-
-template <int C, typename OutT, int LAYOUT, bool WRITE_OUT>
-__global__ void __launch_bounds__(kFastMaxThreads)
-    k_tile_fast(const uint8_t* __restrict__ src, const int64_t* __restrict__ src_off,
-                const int32_t* __restrict__ wh, int n, const int32_t* __restrict__ plan,
-                const int32_t* __restrict__ tile_off, int E, const OutT* __restrict__ lut,
-                OutT* __restrict__ out, uint8_t* __restrict__ out_u8, int64_t cap) {
-  __shared__ OutT s_lut[WRITE_OUT ? C * 256 : 1];
-  __shared__ int s_y0[kFastBand], s_y1[kFastBand];
-  __shared__ float s_fy[kFastBand];
-  if (WRITE_OUT)
-    for (int i = threadIdx.x; i < C * 256; i += blockDim.x) s_lut[i] = lut[i];
-  const int total = static_cast<int>(min(static_cast<int64_t>(__ldg(tile_off + n)), cap));
-  if (total <= 0) return;
-  const int bands = (E + kFastBand - 1) / kFastBand;
-  const int pairs = (E + 1) >> 1;
-  const int64_t items = static_cast<int64_t>(total) * bands;
-  const int64_t EE = static_cast<int64_t>(E) * E;
-  for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
-    const int g = static_cast<int>(item / bands);
-    const int j0 = static_cast<int>(item - static_cast<int64_t>(g) * bands) * kFastBand;
-    const int nrows = min(kFastBand, E - j0);
-    const TileGeom q = tile_geom(src, src_off, wh, plan, tile_off, n, E, g);
-    const double sy = axis_scale(q.H, q.RH), sx = axis_scale(q.W, q.RW);
-    __syncthreads();  // previous item done with the row table
-    if (threadIdx.x < nrows) {
-      const AxisTap ty = axis_tap(q.oy0 + j0 + threadIdx.x, q.H, sy);
-      s_y0[threadIdx.x] = ty.i0;
-      s_y1[threadIdx.x] = ty.i1;
-      s_fy[threadIdx.x] = __double2float_rn(ty.f);
-    }
-    __syncthreads();
-    const int64_t stride = static_cast<int64_t>(q.W) * C;
-    for (int p = threadIdx.x; p < pairs; p += blockDim.x) {
-      const int i = 2 * p;
-      const bool has_b = i + 1 < E;
-      const AxisTap txa = axis_tap(q.ox0 + i, q.W, sx);
-      const AxisTap txb = has_b ? axis_tap(q.ox0 + i + 1, q.W, sx) : txa;
-      const float fxa = __double2float_rn(txa.f), fxb = __double2float_rn(txb.f);
-      const int xa0 = txa.i0 * C, xa1 = txa.i1 * C, xb0 = txb.i0 * C, xb1 = txb.i1 * C;
-      for (int jj = 0; jj < nrows; ++jj) {
-        const int j = j0 + jj;
-        const uint8_t* r0 = q.img + s_y0[jj] * stride;
-        const uint8_t* r1 = q.img + s_y1[jj] * stride;
-        const float fy = s_fy[jj];
-        uint32_t ua[C], ub[C];
-        bool amb_any = false;
-        uint32_t ta[C][4], tb[C][4];
-#pragma unroll
-        for (int c = 0; c < C; ++c) {
-          ta[c][0] = __ldg(r0 + xa0 + c);
-          ta[c][1] = __ldg(r1 + xa0 + c);
-          ta[c][2] = __ldg(r0 + xa1 + c);
-          ta[c][3] = __ldg(r1 + xa1 + c);
-          tb[c][0] = __ldg(r0 + xb0 + c);
-          tb[c][1] = __ldg(r1 + xb0 + c);
-          tb[c][2] = __ldg(r0 + xb1 + c);
-          tb[c][3] = __ldg(r1 + xb1 + c);
-        }
-        bool amb_a[C], amb_b[C];
-#pragma unroll
-        for (int c = 0; c < C; ++c) {
-          ua[c] = blend_fast(ta[c][0], ta[c][1], ta[c][2], ta[c][3], fy, fxa, amb_a[c]);
-          ub[c] = blend_fast(tb[c][0], tb[c][1], tb[c][2], tb[c][3], fy, fxb, amb_b[c]);
-          amb_any |= amb_a[c] | amb_b[c];
-        }
-        if (amb_any) {  // rare: exact fp64 recomputation in the reference order
-          const AxisTap ty = axis_tap(q.oy0 + j, q.H, sy);
-#pragma unroll
-          for (int c = 0; c < C; ++c) {
-            if (amb_a[c]) ua[c] = blend_exact(ta[c][0], ta[c][2], ta[c][1], ta[c][3], ty, txa);
-            if (amb_b[c]) ub[c] = blend_exact(tb[c][0], tb[c][2], tb[c][1], tb[c][3], ty, txb);
-          }
-        }
-        const int64_t pix = q.out_tile * EE + static_cast<int64_t>(j) * E + i;
-        if (out_u8) {
-#pragma unroll
-          for (int c = 0; c < C; ++c) {
-            out_u8[pix * C + c] = static_cast<uint8_t>(ua[c]);
-            if (has_b) out_u8[(pix + 1) * C + c] = static_cast<uint8_t>(ub[c]);
-          }
-        }
-        if (WRITE_OUT) {
-#pragma unroll
-          for (int c = 0; c < C; ++c) {
-            const OutT va = s_lut[c * 256 + ua[c]];
-            const OutT vb = s_lut[c * 256 + ub[c]];
-            if (LAYOUT == TP_LAYOUT_NCHW) {
-              OutT* dst = out + (q.out_tile * C + c) * EE + static_cast<int64_t>(j) * E + i;
-              if (has_b && (E % 2 == 0)) {
-                store_pair(dst, va, vb);
-              } else {
-                dst[0] = va;
-                if (has_b) dst[1] = vb;
-              }
-            } else {
-              out[pix * C + c] = va;
-              if (has_b) out[(pix + 1) * C + c] = vb;
-            }
-          }
-        }
-      }
-    }
-  }
-}
-
 template <int C, typename OutT, int LAYOUT, bool WRITE_OUT>
 int launch_tile(const uint8_t* src, const int64_t* src_off, const int32_t* wh, int n,
                 const int32_t* plan, const int32_t* tile_off, int E, const void* lut, void* out,
@@ -325,14 +180,8 @@ int launch_tile(const uint8_t* src, const int64_t* src_off, const int32_t* wh, i
         static_cast<OutT*>(out), out_u8, cap);
     return check_launch("tp_tile(exact)");
   }
-  auto kern = k_tile_fast<C, OutT, LAYOUT, WRITE_OUT>;
-  const int pairs = (E + 1) / 2;
-  const int threads = min(kFastMaxThreads, max(32, (pairs + 31) / 32 * 32));
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, 0);
-  kern<<<max(1, per_sm) * sms, threads, 0, stream>>>(
-      src, src_off, wh, n, plan, tile_off, E, static_cast<const OutT*>(lut),
-      static_cast<OutT*>(out), out_u8, cap);
-  return check_launch("tp_tile(fast)");
+  return launch_tile_tma<C, OutT, LAYOUT, WRITE_OUT>(src, src_off, wh, n, plan, tile_off, E, lut,
+                                                     out, out_u8, cap, stream);
 }
 
 template <int C>

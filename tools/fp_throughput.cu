@@ -19,6 +19,17 @@ __global__ void k(double* outd, float* outf, int iters, double a, float af) {
       if (OP == 5) { f0 += (float)u0; f1 += (float)u1; f2 += (float)u2; f3 += (float)u3; u0 += 3; u1 += 3; u2 += 3; u3 += 3; }
       if (OP == 6) { x0 = __dadd_rd(x0, a); x1 = __dadd_rd(x1, a); x2 = __dadd_rd(x2, a); x3 = __dadd_rd(x3, a); }
       if (OP == 7) { x0 = floor(x0 * a); x1 = floor(x1 * a); x2 = floor(x2 * a); x3 = floor(x3 * a); }
+      if (OP == 8) {
+        unsigned long long p0, p1, q;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(p0) : "f"(f0), "f"(f1));
+        asm("mov.b64 %0, {%1, %2};" : "=l"(p1) : "f"(f2), "f"(f3));
+        asm("mov.b64 %0, {%1, %1};" : "=l"(q) : "f"(af));
+        asm("fma.rn.f32x2 %0, %0, %1, %1;" : "+l"(p0) : "l"(q));
+        asm("fma.rn.f32x2 %0, %0, %1, %1;" : "+l"(p1) : "l"(q));
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(f0), "=f"(f1) : "l"(p0));
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(f2), "=f"(f3) : "l"(p1));
+      }
+      if (OP == 9) { u0 = __byte_perm(u0, 0x4B000000u, 0x7440u); u1 = __byte_perm(u1, 0x4B000000u, 0x7441u); u2 = __byte_perm(u2, 0x4B000000u, 0x7442u); u3 = __byte_perm(u3, 0x4B000000u, 0x7443u); }
     }
   }
   outd[blockIdx.x * blockDim.x + threadIdx.x] = x0 + x1 + x2 + x3;
@@ -29,9 +40,9 @@ int main() {
   int sms = 0; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   int clk = 0; cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
   double* d; float* f; cudaMalloc(&d, 1 << 24); cudaMalloc(&f, 1 << 24);
-  const char* names[] = {"DMUL", "DADD", "FFMA", "FADD", "I2F.F64+DADD", "I2F.F32+FADD", "DADD.RM", "DMUL+FRND.F64"};
+  const char* names[] = {"DMUL", "DADD", "FFMA", "FADD", "I2F.F64+DADD", "I2F.F32+FADD", "DADD.RM", "DMUL+FRND.F64", "FFMA2 (x2 lanes)", "PRMT"};
   const int blocks = sms * 8, threads = 256, iters = 2000;
-  for (int op = 0; op < 8; ++op) {
+  for (int op = 0; op < 10; ++op) {
     cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
     auto launch = [&]() {
       switch (op) {
@@ -43,6 +54,8 @@ int main() {
         case 5: k<5><<<blocks, threads>>>(d, f, iters, 1.0000001, 1.0000001f); break;
         case 6: k<6><<<blocks, threads>>>(d, f, iters, 1.0000001, 1.0000001f); break;
         case 7: k<7><<<blocks, threads>>>(d, f, iters, 1.0000001, 1.0000001f); break;
+        case 8: k<8><<<blocks, threads>>>(d, f, iters, 1.0000001, 0.999999f); break;
+        case 9: k<9><<<blocks, threads>>>(d, f, iters, 1.0000001, 0.999999f); break;
       }
     };
     launch(); cudaDeviceSynchronize();
