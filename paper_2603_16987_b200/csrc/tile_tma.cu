@@ -29,7 +29,9 @@ namespace {
 
 constexpr int kBand = 8;                 // output rows per work item
 constexpr int kStages = 3;
-constexpr int kArena = 32 * 1024;        // bytes of staged source rows per stage
+constexpr int kArena = 23 * 1024;        // bytes of staged source rows per stage
+constexpr int kMaxThreads = 256;         // 1 producer warp + up to 7 consumer warps
+constexpr int kCtasPerSm = 3;
 constexpr int kRowSlack = 16;            // readable slack after each staged row
 
 struct Phase {
@@ -39,6 +41,7 @@ struct Phase {
   int nrows;   // output rows in this phase
   int c0, cw;  // output column range (tile coordinates)
   int xlo;     // first staged source column
+  int mis;     // common (offset & 3) of all staged rows, or -1 when they differ
   int W, H, RW, RH, oy0, ox0;
   double sx;                     // W / RW (fallback column taps)
   int off0[kBand], off1[kBand];  // arena byte offset of column xlo in rows y0 / y1
@@ -279,8 +282,7 @@ __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restri
       img_end = reinterpret_cast<uintptr_t>(img) + static_cast<uintptr_t>(stride) * H;
       sy = axis_scale(H, RH);
       sx = axis_scale(W, RW);
-      // column chunks: two staged rows (alignment + slack) must fit a stage, and
-      // a chunk must not exceed one pixel pair per consumer thread
+      // column chunks: two staged rows (alignment + slack) must fit a stage
       for (int nch = 1;; ++nch) {
         cwid = (E + nch - 1) / nch;
         cwid += cwid & 1;
@@ -365,6 +367,9 @@ __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restri
         const int off0 = __shfl_sync(0xffffffffu, ent_off, min(max(e0, 0), 31));
         const int off1 = __shfl_sync(0xffffffffu, ent_off, min(max(e1, 0), 31));
         Phase& ph = hdr.ph[s];
+        const int m0 = __shfl_sync(0xffffffffu, off0 & 3, 0);
+        const bool same =
+            __all_sync(0xffffffffu, lane >= nr || ((off0 & 3) == m0 && (off1 & 3) == m0));
         if (lane < nr) {
           ph.off0[lane] = off0;
           ph.off1[lane] = off1;
@@ -394,6 +399,7 @@ __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restri
           ph.c0 = c0;
           ph.cw = cw;
           ph.xlo = xlo;
+          ph.mis = same ? m0 : -1;
           ph.W = W;
           ph.H = H;
           ph.RW = RW;
@@ -427,17 +433,195 @@ __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restri
 // ---------------------------------------------------------------------------
 // consumers
 
-template <int C, typename OutT, int LAYOUT, bool WRITE_OUT>
+__device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
+  unsigned short v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
+  return v;
+}
+
+template <typename OutT>
+struct LutLoad;
+template <>
+struct LutLoad<__nv_bfloat16> {
+  typedef uint32_t Raw;  // low 16 bits hold the bf16
+  static __device__ __forceinline__ uint32_t load(uint32_t addr) { return lds_u16(addr); }
+  static __device__ __forceinline__ void store_pair(__nv_bfloat16* dst, uint32_t a, uint32_t b) {
+    *reinterpret_cast<uint32_t*>(dst) = __byte_perm(a, b, 0x5410);
+  }
+  static __device__ __forceinline__ void store_one(__nv_bfloat16* dst, uint32_t a) {
+    *reinterpret_cast<unsigned short*>(dst) = static_cast<unsigned short>(a);
+  }
+};
+template <>
+struct LutLoad<float> {
+  typedef uint32_t Raw;
+  static __device__ __forceinline__ uint32_t load(uint32_t addr) { return lds32(addr); }
+  static __device__ __forceinline__ void store_pair(float* dst, uint32_t a, uint32_t b) {
+    *reinterpret_cast<uint2*>(dst) = make_uint2(a, b);
+  }
+  static __device__ __forceinline__ void store_one(float* dst, uint32_t a) {
+    *reinterpret_cast<uint32_t*>(dst) = a;
+  }
+};
+
+// bits of 1.5*2^23 + N:  N >> 13 (the uint8 value) sits above 13 fraction bits;
+// kraw = bits >> 13 = 0x25A00 + k.  The window test uses (bits + 1) << 19: the value is
+// flagged iff N mod 8192 is 8191, 0 or 1 (within 1.83e-4 of a rounding boundary).
+constexpr uint32_t kKrawBias = 0x4B400000u >> 13;  // 0x25A00
+constexpr uint32_t kAmbLimit = 3u << 19;
+
+// Taps of one pixel in the two staged rows of output row jj: (row, word) pairs.
+struct PixTaps {
+  uint32_t r0w0, r0w1, r1w0, r1w1;
+};
+
+__device__ __forceinline__ float ldsf(uint32_t addr) { return __uint_as_float(lds32(addr)); }
+__device__ __forceinline__ double ldsd(uint32_t addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+  return v;
+}
+
+// shared-space addresses of the per-row phase fields
+struct PhaseRows {
+  uint32_t off0, off1, fy, fy64, omfy64;
+};
+
+template <bool UNIFORM>
+__device__ __forceinline__ PixTaps fetch_pix(const PhaseRows& pr, int jj, uint32_t sbase, int mis,
+                                             int xo, uint32_t wo, uint32_t sh) {
+  PixTaps t;
+  const uint32_t o0 = lds32(pr.off0 + 4 * jj), o1 = lds32(pr.off1 + 4 * jj);
+  if (UNIFORM) {
+    const uint32_t r0 = sbase + o0 - mis + wo, r1 = sbase + o1 - mis + wo;
+    uint32_t w0 = lds32(r0), w1 = lds32(r0 + 4), w2 = lds32(r0 + 8);
+    t.r0w0 = __funnelshift_r(w0, w1, sh);
+    t.r0w1 = __funnelshift_r(w1, w2, sh);
+    w0 = lds32(r1);
+    w1 = lds32(r1 + 4);
+    w2 = lds32(r1 + 8);
+    t.r1w0 = __funnelshift_r(w0, w1, sh);
+    t.r1w1 = __funnelshift_r(w1, w2, sh);
+  } else {
+    fetch8(sbase + o0 + xo, t.r0w0, t.r0w1);
+    fetch8(sbase + o1 + xo, t.r1w0, t.r1w1);
+  }
+  return t;
+}
+
+// One consumer thread: pixels a and b = a + 32 of a 64-pixel warp segment (lanes read
+// consecutive pixels, which halves shared-memory bank conflicts versus adjacent
+// pairs), all output rows of the phase, all channels.  Math is packed f32x2
+// (lane 0: pixel a, lane 1: pixel b).
+template <int C, typename OutT, int LAYOUT, bool WRITE_OUT, bool WRITE_U8, bool UNIFORM>
+__device__ __forceinline__ void consume_pair_rows(
+    const PhaseRows& pr, int g, int j0, int nrows, int mis_in, uint32_t sbase, uint32_t lut_u32,
+    int ia, int ib, bool has_a, bool has_b, int xoa, int xob, float fxa, float fxb, double fxa64,
+    double omfxa64, double fxb64, double omfxb64, int E, OutT* __restrict__ out,
+    uint8_t* __restrict__ out_u8) {
+  const int64_t EE = static_cast<int64_t>(E) * E;
+  const f32x2 FX = pk(fxa, fxb);
+  const f32x2 KH = pk(8388607.5f, 8388607.5f);  // 2^23 - 0.5: biased byte -> byte + 0.5
+  const f32x2 S13 = pk(8192.0f, 8192.0f);
+  const f32x2 MAG = pk(12582912.0f, 12582912.0f);  // 1.5 * 2^23
+  // uniform misalignment: word offsets and shift amounts are per-pixel constants
+  const int mis = UNIFORM ? mis_in : 0;
+  const uint32_t wa = static_cast<uint32_t>((mis + xoa) & ~3), wb = static_cast<uint32_t>((mis + xob) & ~3);
+  const uint32_t sha = static_cast<uint32_t>(mis + xoa) << 3, shb = static_cast<uint32_t>(mis + xob) << 3;
+  constexpr uint32_t SZ = sizeof(OutT);
+  const uint32_t lut0 = lut_u32 - kKrawBias * SZ;  // + kraw*SZ + c*256*SZ
+  // per-channel output row pointers, advanced by one output row per iteration
+  OutT* oa = out + (static_cast<int64_t>(g) * C * EE + static_cast<int64_t>(j0) * E + ia);
+  const int64_t ob_off = static_cast<int64_t>(ib) - ia;
+  PixTaps ta = fetch_pix<UNIFORM>(pr, 0, sbase, mis, xoa, wa, sha);
+  PixTaps tb = fetch_pix<UNIFORM>(pr, 0, sbase, mis, xob, wb, shb);
+  for (int jj = 0; jj < nrows; ++jj, oa += E) {
+    const int j = j0 + jj;
+    const float fy = ldsf(pr.fy + 4 * jj);
+    const f32x2 FY = pk(fy, fy);
+    const PixTaps a = ta, b = tb;
+    if (jj + 1 < nrows) {  // software pipeline: next row's taps while this row computes
+      ta = fetch_pix<UNIFORM>(pr, jj + 1, sbase, mis, xoa, wa, sha);
+      tb = fetch_pix<UNIFORM>(pr, jj + 1, sbase, mis, xob, wb, shb);
+    }
+    uint32_t ka[C], kb[C], xa[C], xb[C];
+    uint32_t worst = 0xFFFFFFFFu;
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      // lanes: (pixel a, pixel b); taps s00, s10, s01, s11 as 2^23 + byte
+      const f32x2 A = pk(biased_byte(a.r0w0, a.r0w1, c), biased_byte(b.r0w0, b.r0w1, c));
+      const f32x2 B = pk(biased_byte(a.r1w0, a.r1w1, c), biased_byte(b.r1w0, b.r1w1, c));
+      const f32x2 Cc = pk(biased_byte(a.r0w0, a.r0w1, C + c), biased_byte(b.r0w0, b.r0w1, C + c));
+      const f32x2 D = pk(biased_byte(a.r1w0, a.r1w1, C + c), biased_byte(b.r1w0, b.r1w1, C + c));
+      const f32x2 L = fma2(FY, sub2(B, A), sub2(A, KH));   // a + 0.5 + fy (b - a)
+      const f32x2 R = fma2(FY, sub2(D, Cc), sub2(Cc, KH));  // c + 0.5 + fy (d - c)
+      const f32x2 T = fma2(FX, sub2(R, L), L);              // ~ v + 0.5
+      uint32_t na, nb;
+      upk(fma2(T, S13, MAG), na, nb);  // bits of 1.5*2^23 + round(8192 t)
+      ka[c] = __umulhi(na, 1u << 19);  // na >> 13 on the FMA pipe
+      kb[c] = __umulhi(nb, 1u << 19);
+      xa[c] = na * (1u << 19) + (1u << 19);
+      xb[c] = nb * (1u << 19) + (1u << 19);
+      worst = min(worst, min(xa[c], xb[c]));
+    }
+    if (worst < kAmbLimit) {  // recompute only the flagged values, exactly, in fp64
+      const double fy64 = ldsd(pr.fy64 + 8 * jj), omfy64 = ldsd(pr.omfy64 + 8 * jj);
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        if (xa[c] < kAmbLimit)
+          ka[c] = kKrawBias + blend_exact_fast(byte_of(a.r0w0, a.r0w1, c),
+                                               byte_of(a.r0w0, a.r0w1, C + c),
+                                               byte_of(a.r1w0, a.r1w1, c),
+                                               byte_of(a.r1w0, a.r1w1, C + c), fy64, omfy64,
+                                               fxa64, omfxa64);
+        if (xb[c] < kAmbLimit)
+          kb[c] = kKrawBias + blend_exact_fast(byte_of(b.r0w0, b.r0w1, c),
+                                               byte_of(b.r0w0, b.r0w1, C + c),
+                                               byte_of(b.r1w0, b.r1w1, c),
+                                               byte_of(b.r1w0, b.r1w1, C + c), fy64, omfy64,
+                                               fxb64, omfxb64);
+      }
+    }
+    const int64_t row = static_cast<int64_t>(g) * EE + static_cast<int64_t>(j) * E;
+    if (WRITE_U8) {
+      uint8_t* ua = out_u8 + (row + ia) * C;
+      uint8_t* ub = out_u8 + (row + ib) * C;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        if (has_a) ua[c] = static_cast<uint8_t>(ka[c] - kKrawBias);
+        if (has_b) ub[c] = static_cast<uint8_t>(kb[c] - kKrawBias);
+      }
+    }
+    if (WRITE_OUT) {
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const uint32_t va = LutLoad<OutT>::load(lut0 + ka[c] * SZ + c * 256 * SZ);
+        const uint32_t vb = LutLoad<OutT>::load(lut0 + kb[c] * SZ + c * 256 * SZ);
+        if (LAYOUT == TP_LAYOUT_NCHW) {
+          OutT* o = oa + c * EE;
+          if (has_a) LutLoad<OutT>::store_one(o, va);
+          if (has_b) LutLoad<OutT>::store_one(o + ob_off, vb);
+        } else {
+          if (has_a) LutLoad<OutT>::store_one(out + (row + ia) * C + c, va);
+          if (has_b) LutLoad<OutT>::store_one(out + (row + ib) * C + c, vb);
+        }
+      }
+    }
+  }
+}
+
+template <int C, typename OutT, int LAYOUT, bool WRITE_OUT, bool WRITE_U8>
 __device__ void consume(SmemHeader& hdr, const uint8_t* arena, const OutT* s_lut, int E,
                         OutT* __restrict__ out, uint8_t* __restrict__ out_u8) {
   const int ctid = threadIdx.x - 32;
-  const int64_t EE = static_cast<int64_t>(E) * E;
+  const int ncons = blockDim.x - 32;
+  const int lane = ctid & 31, cwarp = ctid >> 5;
   const uint32_t arena_u32 = smem_u32(arena);
-  const bool even_e = (E & 1) == 0;
+  const uint32_t lut_u32 = smem_u32(s_lut);
   int stage = 0;
   uint32_t parity = 0;
-  // per-thread column-tap cache (valid while tile and column chunk are unchanged)
-  int cache_g = -1, cache_c0 = -1;
+  // per-thread column-tap cache (valid while tile, chunk and segment are unchanged)
+  int cache_g = -1, cache_c0 = -1, cache_q = -1;
   int xoa = 0, xob = 0;
   float fxa = 0.f, fxb = 0.f;
   double fxa64 = 0.0, omfxa64 = 1.0, fxb64 = 0.0, omfxb64 = 1.0;
@@ -446,16 +630,22 @@ __device__ void consume(SmemHeader& hdr, const uint8_t* arena, const OutT* s_lut
     const Phase& ph = hdr.ph[stage];
     const int g = ph.g;
     if (g < 0) break;
-    const int c0 = ph.c0, cw = ph.cw, nrows = ph.nrows, j0 = ph.j0;
-    const int pairs = (cw + 1) >> 1;
+    const int c0 = ph.c0, cw = ph.cw, j0 = ph.j0, nrows = ph.nrows, mis = ph.mis;
+    const int segs = (cw + 63) >> 6;  // 64-pixel segments, one per consumer warp
     const uint32_t sbase = arena_u32 + stage * kArena;
-    const int p = ctid;  // one pixel pair per consumer thread (cw <= 2 * ncons)
-    if (p < pairs) {
-      const int i = c0 + 2 * p;  // tile column of pixel a
-      const bool has_b = 2 * p + 1 < cw;
-      if (g != cache_g || c0 != cache_c0) {
-        const AxisTap ta = axis_tap(ph.ox0 + i, ph.W, ph.sx);
-        const AxisTap tb = has_b ? axis_tap(ph.ox0 + i + 1, ph.W, ph.sx) : ta;
+    PhaseRows pr;
+    pr.off0 = smem_u32(ph.off0);
+    pr.off1 = smem_u32(ph.off1);
+    pr.fy = smem_u32(ph.fy);
+    pr.fy64 = smem_u32(ph.fy64);
+    pr.omfy64 = smem_u32(ph.omfy64);
+    for (int q = cwarp; q < segs; q += ncons >> 5) {
+      const int la = 64 * q + lane, lb = la + 32;  // chunk-relative pixels
+      const bool has_a = la < cw, has_b = lb < cw;
+      const int ia = c0 + la, ib = c0 + lb;
+      if (g != cache_g || c0 != cache_c0 || q != cache_q) {
+        const AxisTap ta = axis_tap(ph.ox0 + min(ia, c0 + cw - 1), ph.W, ph.sx);
+        const AxisTap tb = axis_tap(ph.ox0 + min(ib, c0 + cw - 1), ph.W, ph.sx);
         xoa = (ta.i0 - ph.xlo) * C;
         xob = (tb.i0 - ph.xlo) * C;
         fxa = __double2float_rn(ta.f);
@@ -466,80 +656,16 @@ __device__ void consume(SmemHeader& hdr, const uint8_t* arena, const OutT* s_lut
         omfxb64 = tb.omf;
         cache_g = g;
         cache_c0 = c0;
+        cache_q = q;
       }
-      OutT* obase = out + static_cast<int64_t>(g) * C * EE + i;  // + c*EE + j*E
-      uint8_t* ubase = out_u8 ? out_u8 + (static_cast<int64_t>(g) * EE + i) * C : nullptr;
-      const f32x2 FX = pk(fxa, fxb);
-      const f32x2 KH = pk(8388607.5f, 8388607.5f);  // 2^23 - 0.5: biased byte -> byte + 0.5
-      const f32x2 S13 = pk(8192.0f, 8192.0f);
-      const f32x2 MAG = pk(12582912.0f, 12582912.0f);  // 1.5 * 2^23
-      for (int jj = 0; jj < nrows; ++jj) {
-        const int j = j0 + jj;
-        const uint32_t r0 = sbase + ph.off0[jj], r1 = sbase + ph.off1[jj];
-        const float fy = ph.fy[jj];
-        const f32x2 FY = pk(fy, fy);
-        uint32_t a00, a01, a10, a11, b00, b01, b10, b11;  // (pixel)(row)(word)
-        fetch8(r0 + xoa, a00, a01);
-        fetch8(r1 + xoa, a10, a11);
-        fetch8(r0 + xob, b00, b01);
-        fetch8(r1 + xob, b10, b11);
-        uint32_t ua[C], ub[C], xa[C], xb[C];
-        uint32_t worst = 0xFFFFFFFFu;
-#pragma unroll
-        for (int c = 0; c < C; ++c) {
-          // lanes: (pixel a, pixel b); taps s00, s10, s01, s11 as 2^23 + byte
-          const f32x2 A = pk(biased_byte(a00, a01, c), biased_byte(b00, b01, c));
-          const f32x2 B = pk(biased_byte(a10, a11, c), biased_byte(b10, b11, c));
-          const f32x2 Cc = pk(biased_byte(a00, a01, C + c), biased_byte(b00, b01, C + c));
-          const f32x2 D = pk(biased_byte(a10, a11, C + c), biased_byte(b10, b11, C + c));
-          const f32x2 L = fma2(FY, sub2(B, A), sub2(A, KH));   // a + 0.5 + fy (b - a)
-          const f32x2 R = fma2(FY, sub2(D, Cc), sub2(Cc, KH));  // c + 0.5 + fy (d - c)
-          const f32x2 T = fma2(FX, sub2(R, L), L);              // ~ v + 0.5
-          uint32_t na, nb;
-          upk(fma2(T, S13, MAG), na, nb);  // bits of 1.5*2^23 + round(8192 t)
-          ua[c] = (na >> 13) & 0xFFu;
-          ub[c] = (nb >> 13) & 0xFFu;
-          xa[c] = (na + 1u) & 8191u;  // <= 2: within 1.83e-4 of a rounding boundary
-          xb[c] = (nb + 1u) & 8191u;
-          worst = min(worst, min(xa[c], xb[c]));
-        }
-        if (worst <= 2u) {  // recompute only the flagged values, exactly, in fp64
-          const double fy64 = ph.fy64[jj], omfy64 = ph.omfy64[jj];
-#pragma unroll
-          for (int c = 0; c < C; ++c) {
-            if (xa[c] <= 2u)
-              ua[c] = blend_exact_fast(byte_of(a00, a01, c), byte_of(a00, a01, C + c),
-                                       byte_of(a10, a11, c), byte_of(a10, a11, C + c), fy64,
-                                       omfy64, fxa64, omfxa64);
-            if (xb[c] <= 2u)
-              ub[c] = blend_exact_fast(byte_of(b00, b01, c), byte_of(b00, b01, C + c),
-                                       byte_of(b10, b11, c), byte_of(b10, b11, C + c), fy64,
-                                       omfy64, fxb64, omfxb64);
-          }
-        }
-        if (ubase) {
-          uint8_t* u = ubase + static_cast<int64_t>(j) * E * C;
-#pragma unroll
-          for (int c = 0; c < C; ++c) {
-            u[c] = static_cast<uint8_t>(ua[c]);
-            if (has_b) u[C + c] = static_cast<uint8_t>(ub[c]);
-          }
-        }
-        if (WRITE_OUT) {
-#pragma unroll
-          for (int c = 0; c < C; ++c) {
-            const OutT va = s_lut[c * 256 + ua[c]];
-            const OutT vb = s_lut[c * 256 + ub[c]];
-            if (LAYOUT == TP_LAYOUT_NCHW) {
-              store2<OutT>(obase + c * EE + j * E, va, vb, has_b && even_e, has_b);
-            } else {
-              OutT* o = out + (static_cast<int64_t>(g) * EE + static_cast<int64_t>(j) * E + i) * C;
-              o[c] = va;
-              if (has_b) o[C + c] = vb;
-            }
-          }
-        }
-      }
+      if (mis >= 0)
+        consume_pair_rows<C, OutT, LAYOUT, WRITE_OUT, WRITE_U8, true>(
+            pr, g, j0, nrows, mis, sbase, lut_u32, ia, ib, has_a, has_b, xoa, xob, fxa, fxb,
+            fxa64, omfxa64, fxb64, omfxb64, E, out, out_u8);
+      else
+        consume_pair_rows<C, OutT, LAYOUT, WRITE_OUT, WRITE_U8, false>(
+            pr, g, j0, nrows, mis, sbase, lut_u32, ia, ib, has_a, has_b, xoa, xob, fxa, fxb,
+            fxa64, omfxa64, fxb64, omfxb64, E, out, out_u8);
     }
     mbar_arrive(&hdr.empty[stage]);
     if (++stage == kStages) {
@@ -549,8 +675,8 @@ __device__ void consume(SmemHeader& hdr, const uint8_t* arena, const OutT* s_lut
   }
 }
 
-template <int C, typename OutT, int LAYOUT, bool WRITE_OUT>
-__global__ void __launch_bounds__(288, 2)
+template <int C, typename OutT, int LAYOUT, bool WRITE_OUT, bool WRITE_U8>
+__global__ void __launch_bounds__(kMaxThreads, kCtasPerSm)
     k_tile_tma(const uint8_t* __restrict__ src, const int64_t* __restrict__ src_off,
                const int32_t* __restrict__ wh, int n, const int32_t* __restrict__ plan,
                const int32_t* __restrict__ tile_off, int E, const OutT* __restrict__ lut,
@@ -576,7 +702,7 @@ __global__ void __launch_bounds__(288, 2)
   if (threadIdx.x < 32)
     produce<C>(hdr, arena, src, src_off, wh, n, plan, tile_off, E, items, bands);
   else
-    consume<C, OutT, LAYOUT, WRITE_OUT>(hdr, arena, s_lut, E, out, out_u8);
+    consume<C, OutT, LAYOUT, WRITE_OUT, WRITE_U8>(hdr, arena, s_lut, E, out, out_u8);
 }
 
 template <int C, typename OutT>
@@ -585,33 +711,44 @@ size_t tma_smem_bytes() {
          ((C * 256 * sizeof(OutT) + 127) & ~size_t(127)) + kStages * kArena;
 }
 
+template <int C, typename OutT, int LAYOUT, bool WRITE_OUT, bool WRITE_U8>
+int launch_variant(const uint8_t* src, const int64_t* src_off, const int32_t* wh, int n,
+                   const int32_t* plan, const int32_t* tile_off, int E, const void* lut,
+                   void* out, uint8_t* out_u8, int64_t cap, cudaStream_t stream) {
+  auto kern = k_tile_tma<C, OutT, LAYOUT, WRITE_OUT, WRITE_U8>;
+  const size_t smem = tma_smem_bytes<C, OutT>();
+  static bool configured = false;  // one per template instance
+  static int per_sm = 0;
+  const int segs = (E + 63) / 64;  // 64-pixel segments: one consumer warp each
+  const int threads = 32 + 32 * min((kMaxThreads - 32) / 32, max(1, segs));
+  static int cached_threads = -1;
+  if (!configured) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+    configured = true;
+  }
+  if (threads != cached_threads) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+    cached_threads = threads;
+  }
+  const int grid = max(1, per_sm) * max(1, device_sm_count());
+  kern<<<grid, threads, smem, stream>>>(src, src_off, wh, n, plan, tile_off, E,
+                                        static_cast<const OutT*>(lut), static_cast<OutT*>(out),
+                                        out_u8, cap);
+  return check_launch("tp_tile(tma)");
+}
+
 }  // namespace
 
 template <int C, typename OutT, int LAYOUT, bool WRITE_OUT>
 int launch_tile_tma(const uint8_t* src, const int64_t* src_off, const int32_t* wh, int n,
                     const int32_t* plan, const int32_t* tile_off, int E, const void* lut,
                     void* out, uint8_t* out_u8, int64_t cap, cudaStream_t stream) {
-  auto kern = k_tile_tma<C, OutT, LAYOUT, WRITE_OUT>;
-  const size_t smem = tma_smem_bytes<C, OutT>();
-  static bool configured = false;  // one per template instance
-  if (!configured) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-    configured = true;
-  }
-  const int pairs = (E + 1) / 2;
-  const int threads = 32 + min(256, max(32, (pairs + 31) / 32 * 32));
-  static int cached_threads = -1, cached_per_sm = 0;
-  if (threads != cached_threads) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cached_per_sm, kern, threads, smem);
-    cached_threads = threads;
-  }
-  const int per_sm = cached_per_sm;
-  const int grid = max(1, per_sm) * max(1, device_sm_count());
-  kern<<<grid, threads, smem, stream>>>(src, src_off, wh, n, plan, tile_off, E,
-                                        static_cast<const OutT*>(lut), static_cast<OutT*>(out),
-                                        out_u8, cap);
-  return check_launch("tp_tile(tma)");
+  if (out_u8)
+    return launch_variant<C, OutT, LAYOUT, WRITE_OUT, true>(src, src_off, wh, n, plan, tile_off,
+                                                            E, lut, out, out_u8, cap, stream);
+  return launch_variant<C, OutT, LAYOUT, WRITE_OUT, false>(src, src_off, wh, n, plan, tile_off, E,
+                                                           lut, out, out_u8, cap, stream);
 }
 
 #define TP_INSTANTIATE(C, T, L, W)                                                             \
