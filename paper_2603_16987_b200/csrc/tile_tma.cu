@@ -529,21 +529,19 @@ __device__ __forceinline__ void consume_pair_rows(
   const uint32_t wa = static_cast<uint32_t>((mis + xoa) & ~3), wb = static_cast<uint32_t>((mis + xob) & ~3);
   const uint32_t sha = static_cast<uint32_t>(mis + xoa) << 3, shb = static_cast<uint32_t>(mis + xob) << 3;
   constexpr uint32_t SZ = sizeof(OutT);
-  const uint32_t lut0 = lut_u32 - kKrawBias * SZ;  // + kraw*SZ + c*256*SZ
-  // per-channel output row pointers, advanced by one output row per iteration
-  OutT* oa = out + (static_cast<int64_t>(g) * C * EE + static_cast<int64_t>(j0) * E + ia);
-  const int64_t ob_off = static_cast<int64_t>(ib) - ia;
-  PixTaps ta = fetch_pix<UNIFORM>(pr, 0, sbase, mis, xoa, wa, sha);
-  PixTaps tb = fetch_pix<UNIFORM>(pr, 0, sbase, mis, xob, wb, shb);
-  for (int jj = 0; jj < nrows; ++jj, oa += E) {
+  uint32_t lut0;  // + kraw*SZ + c*256*SZ; opaque so it stays in a register
+  asm volatile("mov.u32 %0, %1;" : "=r"(lut0) : "r"(lut_u32 - kKrawBias * SZ));
+  // per-channel output row pointers (NCHW), advanced by one output row per step
+  OutT* oc[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c)
+    oc[c] = out + (static_cast<int64_t>(g) * C + c) * EE + static_cast<int64_t>(j0) * E + ia;
+  const int ob_off = ib - ia;
+  // one output row: taps (a, b) already fetched
+  auto row = [&](int jj, const PixTaps& a, const PixTaps& b) {
     const int j = j0 + jj;
     const float fy = ldsf(pr.fy + 4 * jj);
     const f32x2 FY = pk(fy, fy);
-    const PixTaps a = ta, b = tb;
-    if (jj + 1 < nrows) {  // software pipeline: next row's taps while this row computes
-      ta = fetch_pix<UNIFORM>(pr, jj + 1, sbase, mis, xoa, wa, sha);
-      tb = fetch_pix<UNIFORM>(pr, jj + 1, sbase, mis, xob, wb, shb);
-    }
     uint32_t ka[C], kb[C], xa[C], xb[C];
     uint32_t worst = 0xFFFFFFFFu;
 #pragma unroll
@@ -582,10 +580,10 @@ __device__ __forceinline__ void consume_pair_rows(
                                                fxb64, omfxb64);
       }
     }
-    const int64_t row = static_cast<int64_t>(g) * EE + static_cast<int64_t>(j) * E;
+    const int64_t rowpix = static_cast<int64_t>(g) * EE + static_cast<int64_t>(j) * E;
     if (WRITE_U8) {
-      uint8_t* ua = out_u8 + (row + ia) * C;
-      uint8_t* ub = out_u8 + (row + ib) * C;
+      uint8_t* ua = out_u8 + (rowpix + ia) * C;
+      uint8_t* ub = out_u8 + (rowpix + ib) * C;
 #pragma unroll
       for (int c = 0; c < C; ++c) {
         if (has_a) ua[c] = static_cast<uint8_t>(ka[c] - kKrawBias);
@@ -598,16 +596,31 @@ __device__ __forceinline__ void consume_pair_rows(
         const uint32_t va = LutLoad<OutT>::load(lut0 + ka[c] * SZ + c * 256 * SZ);
         const uint32_t vb = LutLoad<OutT>::load(lut0 + kb[c] * SZ + c * 256 * SZ);
         if (LAYOUT == TP_LAYOUT_NCHW) {
-          OutT* o = oa + c * EE;
-          if (has_a) LutLoad<OutT>::store_one(o, va);
-          if (has_b) LutLoad<OutT>::store_one(o + ob_off, vb);
+          if (has_a) LutLoad<OutT>::store_one(oc[c], va);
+          if (has_b) LutLoad<OutT>::store_one(oc[c] + ob_off, vb);
+          oc[c] += E;
         } else {
-          if (has_a) LutLoad<OutT>::store_one(out + (row + ia) * C + c, va);
-          if (has_b) LutLoad<OutT>::store_one(out + (row + ib) * C + c, vb);
+          if (has_a) LutLoad<OutT>::store_one(out + (rowpix + ia) * C + c, va);
+          if (has_b) LutLoad<OutT>::store_one(out + (rowpix + ib) * C + c, vb);
         }
       }
     }
+  };
+  // software pipeline, unrolled by two so the prefetched taps need no register moves
+  PixTaps a0 = fetch_pix<UNIFORM>(pr, 0, sbase, mis, xoa, wa, sha);
+  PixTaps b0 = fetch_pix<UNIFORM>(pr, 0, sbase, mis, xob, wb, shb);
+  int jj = 0;
+  for (; jj + 1 < nrows; jj += 2) {
+    const PixTaps a1 = fetch_pix<UNIFORM>(pr, jj + 1, sbase, mis, xoa, wa, sha);
+    const PixTaps b1 = fetch_pix<UNIFORM>(pr, jj + 1, sbase, mis, xob, wb, shb);
+    row(jj, a0, b0);
+    if (jj + 2 < nrows) {
+      a0 = fetch_pix<UNIFORM>(pr, jj + 2, sbase, mis, xoa, wa, sha);
+      b0 = fetch_pix<UNIFORM>(pr, jj + 2, sbase, mis, xob, wb, shb);
+    }
+    row(jj + 1, a1, b1);
   }
+  if (jj < nrows) row(jj, a0, b0);
 }
 
 template <int C, typename OutT, int LAYOUT, bool WRITE_OUT, bool WRITE_U8>
