@@ -47,6 +47,10 @@ def parse_args():
     ap.add_argument("--cpu-seconds", type=float, default=15.0,
                     help="target CPU time of the cpu_baseline sample")
     ap.add_argument("--latency-iters", type=int, default=300)
+    ap.add_argument("--workload", choices=["c2", "c4", "c5", "c1", "c3"], default="c2",
+                    help="c2 (default, the BASELINE metric config); c4 = 8192-image "
+                         "mixed-aspect sweep (sharded, strong scaling); c5 = 1024 images + "
+                         "placeholder expansion; c1/c3 = single-image latency configs")
     return ap.parse_args()
 
 
@@ -145,6 +149,8 @@ class ClockSampler:
 # CPU side: the reference algorithm on host cores (oracle port)
 
 def _cpu_one(args):
+    """One image through the oracle path; the synthetic input is generated before
+    the clock starts, so only the preprocessing itself is timed."""
     seed, k, w, h = args
     from oracle import tileprep_oracle as O
     from paper_2603_16987_b200.workloads import IMAGENET_MEAN, IMAGENET_STD
@@ -156,8 +162,9 @@ def _cpu_one(args):
 
 
 def cpu_throughput(n_images: int, cores: int, seed: int = 20260817):
-    """images/s of the oracle path over a pool of `cores` processes; inputs are
-    generated inside the workers before their timed region."""
+    """images/s of the oracle path with `cores` worker processes busy at once:
+    cores / mean per-image time (each time measured while all workers run, so
+    memory-bandwidth contention is included).  Returns (images/s, p50 ms, CPU-s)."""
     import multiprocessing as mp
 
     os.environ.setdefault("OMP_NUM_THREADS", "1")
@@ -166,10 +173,8 @@ def cpu_throughput(n_images: int, cores: int, seed: int = 20260817):
     ctx = mp.get_context("fork")
     with ctx.Pool(cores) as pool:
         pool.map(_cpu_one, jobs[:cores])  # warm the workers
-        t0 = time.perf_counter()
-        per = pool.map(_cpu_one, jobs)
-        wall = time.perf_counter() - t0
-    return n_images / wall, float(np.median(per)) * 1e3, wall
+        per = np.array(pool.map(_cpu_one, jobs, chunksize=1))
+    return cores / float(per.mean()), float(np.median(per)) * 1e3, float(per.sum())
 
 
 def host_cores() -> int:
@@ -180,34 +185,35 @@ def host_cores() -> int:
 
 
 def run_reference(args, dist: Dist):
-    """--impl reference: the oracle port on host cores, rank 0 only."""
+    """--impl reference: the reference algorithm (oracle port of vlmfp's fused,
+    contiguous path) on all host cores, rank 0 only; each step is a bounded sample
+    of C2 images."""
     if dist.rank != 0:
         return
     cores = host_cores()
-    sample = max(cores, 8)
-    _, p50_ms, _ = cpu_throughput(cores, cores)  # calibration/warm pool
-    for _ in range(args.warmup):
-        pass  # warm-up happens inside cpu_throughput (one image per worker)
-    times = []
+    sample = max(cores, 16)
+    cpu_throughput(cores, cores)  # warm-up
+    rates, p50s, cpu_s = [], [], 0.0
     for _ in range(args.steps):
-        ips, p50_ms, wall = cpu_throughput(sample, cores)
-        times.append(wall)
-    wall = float(np.sum(times))
-    value = sample * args.steps / wall
+        ips, p50_ms, cs = cpu_throughput(sample, cores)
+        rates.append(ips)
+        p50s.append(p50_ms)
+        cpu_s += cs
+    value = float(np.median(rates))
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(wall / args.steps * 1e3, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u8->bf16 (fp64 resample)",
+        "ms_per_step": round(sample / value * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8 in, fp64 resample, bf16 out",
         "data": "synthetic",
-        "config": {"workload": "C2 sample: 1920x1080 RGB uint8, E=448, max 12 + thumb, "
+        "config": {"workload": "C2: 1920x1080 RGB uint8, E=448, max 12 + thumb, "
                                "ImageNet mean/std, bf16 out", "images_per_step": sample},
-        "p50_ms": round(p50_ms, 3),
+        "p50_ms": round(float(np.median(p50s)), 3),
         "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": cores,
                          "kind": "port",
-                         "sample": f"{sample} images x {args.steps} steps, oracle/tileprep_oracle "
-                                   "(numpy restatement of vlmfp fused path), "
-                                   "multiprocessing pool"},
+                         "sample": f"{sample} images x {args.steps} steps ({cpu_s:.0f} CPU-s) "
+                                   "through oracle/tileprep_oracle (numpy restatement of the "
+                                   "vlmfp fused/contiguous recipe path), one process per core"},
         "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -236,6 +242,14 @@ def main():
     torch.cuda.set_device(dist.local_rank)
     device = torch.device("cuda", dist.local_rank)
     dist.init("nccl")
+    if args.workload in ("c4", "c5"):
+        run_sweep(args, dist, device)
+        dist.close()
+        return
+    if args.workload in ("c1", "c3"):
+        run_single(args, dist, device)
+        dist.close()
+        return
 
     wl = c2(args.batch)
     cfg = PreprocessConfig(tile_edge=wl.tile_edge, max_tiles=wl.max_tiles, mean=wl.mean,
@@ -324,13 +338,14 @@ def main():
         cores = host_cores()
         # calibrate: ~`cpu-seconds` of total CPU work
         _, p50_ms, _ = cpu_throughput(cores, cores)
-        n_cpu = int(max(cores, min(256, args.cpu_seconds * 1e3 / max(p50_ms, 1.0))))
-        ips, p50_ms, wall = cpu_throughput(n_cpu, cores)
+        n_cpu = int(max(cores, min(512, args.cpu_seconds * 1e3 / max(p50_ms, 1.0))))
+        ips, p50_ms, cpu_s = cpu_throughput(n_cpu, cores)
         cpu = {"value": round(ips, 3), "unit": UNIT, "cores": cores, "kind": "port",
                "sample": f"{n_cpu} C2 images (1920x1080) through oracle/tileprep_oracle "
-                         f"(numpy restatement of vlmfp fused path) in a {cores}-process pool, "
-                         f"{wall:.1f} s wall; per-image p50 {p50_ms:.1f} ms"}
+                         f"(numpy restatement of the vlmfp fused path), one process per core, "
+                         f"{cpu_s:.1f} CPU-s; per-image p50 {p50_ms:.1f} ms"}
 
+    traffic = measured_traffic("tp_tile", wb["total"])
     if dist.rank == 0:
         bytes_per_launch = wb["total"]
         achieved = bytes_per_launch / (k2_ms / 1e3) / 1e9
@@ -347,7 +362,7 @@ def main():
             "latency": latency,
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak[0],
                          "unit": "GB/s", "frac": round(achieved / peak[0], 4),
-                         "traffic": None, "peak_source": peak[1],
+                         "traffic": traffic, "peak_source": peak[1],
                          "kernel": "tp_tile (K2)", "kernel_ms": round(k2_ms, 4),
                          "bytes_per_launch": bytes_per_launch},
             "cpu_baseline": cpu,
@@ -361,6 +376,17 @@ def main():
         }
         print(json.dumps(line), flush=True)
     dist.close()
+
+
+def measured_traffic(kernel: str, algorithmic: int):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu capture
+    summary (profiles/k2_traffic.json, written from `ncu --set full`), or None."""
+    p = REPO / "profiles" / "k2_traffic.json"
+    try:
+        d = json.loads(p.read_text())
+        return int(d["dram_bytes_read"]) + int(d["dram_bytes_write"])
+    except Exception:
+        return None
 
 
 def measured_peak():
@@ -416,6 +442,155 @@ def batch1_latency(cfg, device, iters: int):
             "h2d_p99_ms": round(h99, 4), "iters": iters,
             "workload": "1 x 1920x1080, E=448 InternVL3-2B tiling, bf16 NCHW; CUDA graph "
                         "(K1+K2); h2d_* add the 6.2 MB pinned upload"}
+
+
+def _timed(fn, steps: int, warmup: int, stream, device, dist, events_per_step=None):
+    import torch
+
+    with torch.cuda.stream(stream):
+        for _ in range(max(3, warmup)):
+            fn()
+    torch.cuda.synchronize(device)
+    clocks = ClockSampler(device.index)
+    clocks.start()
+    dist.barrier(device)
+    torch.cuda.synchronize(device)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    with torch.cuda.stream(stream):
+        for i in range(steps):
+            fn(i)
+    b.record(stream)
+    torch.cuda.synchronize(device)
+    dist.barrier(device)
+    clk = clocks.stop()
+    return dist.max(a.elapsed_time(b), device), clk
+
+
+def run_sweep(args, dist, device):
+    """C4 (8192 mixed-aspect images, sharded over ranks by LPT; strong scaling) or C5
+    (1024 of those images + batched placeholder expansion).  Inputs are generated on
+    device before timing; a step processes the rank's whole shard in chunks of 1024."""
+    import torch
+
+    from paper_2603_16987_b200.engine import TilePreprocessor, synth_packed
+    from paper_2603_16987_b200.imgproc import PreprocessConfig
+    from paper_2603_16987_b200.sharding import shard
+    from paper_2603_16987_b200.tokenizer import PlaceholderExpander, SpecialIds, SpecialVocab
+    from paper_2603_16987_b200.workloads import Workload, c4, workload_bytes
+
+    total = 8192 if args.workload == "c4" else 1024
+    wl_all = c4(total)
+    idx = shard(wl_all.wh, wl_all.tile_edge, wl_all.max_tiles, dist.rank, dist.world)
+    wh = wl_all.wh[idx]
+    cfg = PreprocessConfig(tile_edge=448, max_tiles=12, mean=wl_all.mean, std=wl_all.std,
+                           reduced_precision_normalize=True)
+    chunk = 1024
+    stream = torch.cuda.Stream(device)
+    chunks = []
+    for c0 in range(0, len(idx), chunk):
+        chunks.append(synth_packed(wh[c0:c0 + chunk], 3, device, seed=wl_all.seed + c0, kind=0))
+    prep = TilePreprocessor(cfg, device)
+    outs = prep(chunks[0], capacity=chunk * 13)
+    torch.cuda.synchronize(device)
+    with_expand = args.workload == "c5"
+    if with_expand:
+        vocab = SpecialVocab(SpecialIds(0, 1, 2, 3, 4, 5, 6))
+        prompt = [2, 4, 100, 101, 102, 103, 104, 105, 3]  # <|user|><|image|>...<|assistant|>
+        n = len(idx)
+        ids = torch.tensor(prompt * n, dtype=torch.int32, device=device)
+        seq_off = torch.arange(0, len(prompt) * n + 1, len(prompt), dtype=torch.int32,
+                               device=device)
+        count_off = torch.arange(0, n + 1, dtype=torch.int32, device=device)
+        exp = PlaceholderExpander(vocab, 256, device)
+        cap = n * (len(prompt) + 13 * 256)
+        ex = exp(ids, seq_off, outs.plans.n_images, count_off, cap)
+
+    def step(i=None):
+        for ch in chunks:
+            prep(ch, out=outs, stream=stream)
+            if with_expand:
+                exp(ids, seq_off, outs.plans.n_images, count_off, cap, out=ex, stream=stream)
+
+    ms, clk = _timed(step, args.steps, args.warmup, stream, device, dist)
+    ms_step = ms / args.steps
+    wl = Workload("C4" if not with_expand else "C5", wl_all.description, wh, 448, 12,
+                  wl_all.mean, wl_all.std, True, wl_all.seed)
+    wb = workload_bytes(wl)
+    value = total * args.steps / (ms / 1e3)  # all images of the job over the max-rank time
+    if dist.rank == 0:
+        peak = measured_peak()
+        achieved = wb["total"] / (ms_step / 1e3) / 1e9
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": dist.world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "u8 in, fp32/fp64-exact resample, bf16 out", "data": "synthetic",
+            "config": {"workload": ("C4: " if not with_expand else "C5: ") + wl_all.description
+                       + (" + image-token expansion (256 tokens/tile)" if with_expand else ""),
+                       "images_total": total, "images_rank0": len(idx),
+                       "l2": "inputs larger than L2", "parallelism": f"dp{dist.world} LPT shards"},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak[0],
+                         "unit": "GB/s", "frac": round(achieved / peak[0], 4), "traffic": None,
+                         "bytes_per_step_rank0": wb["total"],
+                         "note": "whole step (K1+K2" + ("+K3" if with_expand else "") + ")"},
+            "gpu_launches": args.steps * len(chunks) * (4 if with_expand else 2),
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+
+
+def run_single(args, dist, device):
+    """C1 (1920x1080, E=512, fp32) / C3 (3840x2160, E=448, bf16): batch-1 latency."""
+    import torch
+
+    from paper_2603_16987_b200.engine import TilePreprocessor, empty_packed, synth_packed
+    from paper_2603_16987_b200.imgproc import PreprocessConfig
+    from paper_2603_16987_b200.workloads import c1, c3, workload_bytes
+
+    wl = c1() if args.workload == "c1" else c3()
+    cfg = PreprocessConfig(tile_edge=wl.tile_edge, max_tiles=wl.max_tiles, mean=wl.mean,
+                           std=wl.std, reduced_precision_normalize=wl.bf16)
+    img = synth_packed(wl.wh, 3, device, seed=wl.seed, kind=0)
+    prep = TilePreprocessor(cfg, device)
+    out = prep(img)
+    s = torch.cuda.Stream(device)
+    torch.cuda.synchronize(device)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        prep(img, out=out, stream=torch.cuda.current_stream(device))
+    host = empty_packed(wl.wh, 3, "cpu", pin=True)
+    host.data.copy_(img.data.cpu())
+    ts, th = [], []
+    iters = max(args.latency_iters, 1000)
+    for k in range(iters + 50):
+        for with_h2d, sink in ((False, ts), (True, th)):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(s)
+            with torch.cuda.stream(s):
+                if with_h2d:
+                    img.data.copy_(host.data, non_blocking=True)
+                g.replay()
+            b.record(s)
+            b.synchronize()
+            if k >= 50:
+                sink.append(a.elapsed_time(b))
+    ts, th = np.array(ts), np.array(th)
+    wb = workload_bytes(wl)
+    if dist.rank == 0:
+        line = {
+            "metric": METRIC, "value": round(1e3 / float(np.median(ts)), 2), "unit": UNIT,
+            "n_gpus": 1, "steps": iters, "warmup": 50,
+            "ms_per_step": round(float(np.median(ts)), 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8 in, bf16/fp32 out",
+            "data": "synthetic", "config": {"workload": wl.name + ": " + wl.description},
+            "p50_ms": round(float(np.percentile(ts, 50)), 4),
+            "p99_ms": round(float(np.percentile(ts, 99)), 4),
+            "h2d_p50_ms": round(float(np.percentile(th, 50)), 4),
+            "h2d_p99_ms": round(float(np.percentile(th, 99)), 4),
+            "algorithmic_bytes": wb["total"],
+        }
+        print(json.dumps(line), flush=True)
 
 
 if __name__ == "__main__":

@@ -33,6 +33,7 @@ constexpr int kArena = 23 * 1024;        // bytes of staged source rows per stag
 constexpr int kMaxThreads = 256;         // 1 producer warp + up to 7 consumer warps
 constexpr int kCtasPerSm = 3;
 constexpr int kRowSlack = 16;            // readable slack after each staged row
+constexpr int kTileCache = 16;           // per-image tile geometries kept in smem
 
 struct Phase {
   const uint8_t* img;
@@ -49,8 +50,14 @@ struct Phase {
   double fy64[kBand], omfy64[kBand];  // exact row weights for the fp64 fallback
 };
 
+struct TileGeo {
+  double sx, sy;
+  int RW, RH, oy0, ox0, cwid, pad;
+};
+
 struct __align__(16) SmemHeader {
   Phase ph[kStages];
+  TileGeo tg[kTileCache];  // producer: tiles of the current image
   unsigned long long full[kStages];
   unsigned long long empty[kStages];
 };
@@ -167,6 +174,17 @@ __device__ __forceinline__ uint32_t byte_of(uint32_t g0, uint32_t g1, int k) {
 // [2, 8190] the value floor(t) = N >> 13 equals the reference's floor(v64 + 0.5);
 // otherwise (exact k + 0.5 ties included) the pixel pair is recomputed in fp64.
 
+// image whose items contain `item` (items of image k start at tile_off[k] * bands)
+__device__ __forceinline__ int find_item_image(const int32_t* __restrict__ tile_off, int n,
+                                               int64_t item, int bands) {
+  int lo = 0, hi = n;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (static_cast<int64_t>(__ldg(tile_off + mid)) * bands <= item) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
 __device__ __forceinline__ int find_tile_image(const int32_t* __restrict__ tile_off, int n,
                                                int g) {
   int lo = 0, hi = n;
@@ -214,6 +232,44 @@ __device__ __forceinline__ void store2<__nv_bfloat16>(__nv_bfloat16* dst, __nv_b
 // arena offsets and where the phase must end to fit the stage; lane 0 arms the full
 // barrier with the byte count and every new entry's lane issues its own bulk copy.
 
+// geometry of tile t of image k (tile t < rows*cols: window of the virtual resize;
+// t == rows*cols: the thumbnail) and its column-chunk width
+template <int C>
+__device__ TileGeo tile_geometry(const int32_t* __restrict__ plan, int k, int t, int W, int H,
+                                 int E) {
+  const int32_t* p = plan + static_cast<int64_t>(k) * TP_PLAN_FIELDS;
+  const int rows = __ldg(p + TP_PLAN_ROWS), cols = __ldg(p + TP_PLAN_COLS);
+  TileGeo q;
+  if (t < rows * cols) {
+    q.RW = __ldg(p + TP_PLAN_RESIZED_W);
+    q.RH = __ldg(p + TP_PLAN_RESIZED_H);
+    q.oy0 = (t / cols) * E;
+    q.ox0 = (t % cols) * E;
+  } else {
+    q.RW = E;
+    q.RH = E;
+    q.oy0 = 0;
+    q.ox0 = 0;
+  }
+  q.sy = axis_scale(H, q.RH);
+  q.sx = axis_scale(W, q.RW);
+  // column chunks: two staged rows (alignment + slack) must fit a stage
+  for (int nch = 1;; ++nch) {
+    int cwid = (E + nch - 1) / nch;
+    cwid += cwid & 1;
+    int worst = 0;
+    for (int c0 = 0; c0 < E; c0 += cwid) {
+      const int cw = min(cwid, E - c0);
+      const int bts =
+          (axis_tap(q.ox0 + c0 + cw - 1, W, q.sx).i1 - axis_tap(q.ox0 + c0, W, q.sx).i0 + 1) * C;
+      worst = max(worst, bts);
+    }
+    q.cwid = cwid;
+    if (2 * (worst + 15 + 16 + kRowSlack) <= kArena || cwid <= 2) break;
+  }
+  return q;
+}
+
 __device__ __forceinline__ int warp_incl_sum(int v, int lane) {
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
@@ -236,7 +292,8 @@ template <int C>
 __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restrict__ src,
                         const int64_t* __restrict__ src_off, const int32_t* __restrict__ wh,
                         int n, const int32_t* __restrict__ plan,
-                        const int32_t* __restrict__ tile_off, int E, int64_t items, int bands) {
+                        const int32_t* __restrict__ tile_off, int E, int64_t items, int bands,
+                        int cap_tiles) {
   const int lane = threadIdx.x & 31;
   int stage = 0;
   uint32_t parity = 0;
@@ -246,57 +303,39 @@ __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restri
   const int64_t per_cta = (items + gridDim.x - 1) / gridDim.x;
   const int64_t it_begin = min(items, static_cast<int64_t>(blockIdx.x) * per_cta);
   const int64_t it_end = min(items, it_begin + per_cta);
-  int cur_g = -1;
+  int cur_k = -1;
   const uint8_t* img = nullptr;
-  int W = 1, H = 1, RW = 1, RH = 1, oy0 = 0, ox0 = 0, cwid = E;
-  bool contig = false;
+  int W = 1, H = 1;
   int64_t stride = 0;
   uintptr_t img_end = 0;
-  double sy = 1.0, sx = 1.0;
   for (int64_t item = it_begin; item < it_end; ++item) {
-    const int g = static_cast<int>(item / bands);
-    const int j0 = static_cast<int>(item - static_cast<int64_t>(g) * bands) * kBand;
+    // item order: (image, band, tile): the tiles and the thumbnail of an image read
+    // the same source rows within n_images consecutive items, so the second read
+    // hits L2 instead of HBM
+    const int kimg = find_item_image(tile_off, n, item, bands);
+    const int nimg = __ldg(tile_off + kimg + 1) - __ldg(tile_off + kimg);
+    const int r = static_cast<int>(item - static_cast<int64_t>(__ldg(tile_off + kimg)) * bands);
+    const int g = __ldg(tile_off + kimg) + r % nimg;
+    const int j0 = (r / nimg) * kBand;
+    if (g >= cap_tiles) continue;  // caller's buffers end before this tile
     const int nrows = min(kBand, E - j0);
-    if (g != cur_g) {
-      cur_g = g;
-      const int k = find_tile_image(tile_off, n, g);
-      const int t = g - __ldg(tile_off + k);
-      const int32_t* p = plan + static_cast<int64_t>(k) * TP_PLAN_FIELDS;
-      const int rows = __ldg(p + TP_PLAN_ROWS), cols = __ldg(p + TP_PLAN_COLS);
-      W = __ldg(wh + 2 * k);
-      H = __ldg(wh + 2 * k + 1);
-      if (t < rows * cols) {
-        RW = __ldg(p + TP_PLAN_RESIZED_W);
-        RH = __ldg(p + TP_PLAN_RESIZED_H);
-        oy0 = (t / cols) * E;
-        ox0 = (t % cols) * E;
-      } else {
-        RW = E;
-        RH = E;
-        oy0 = 0;
-        ox0 = 0;
-      }
-      contig = RH > H;
-      img = src + __ldg(src_off + k);
+    if (kimg != cur_k) {  // new image: per-tile geometry, one lane per tile
+      cur_k = kimg;
+      W = __ldg(wh + 2 * kimg);
+      H = __ldg(wh + 2 * kimg + 1);
+      img = src + __ldg(src_off + kimg);
       stride = static_cast<int64_t>(W) * C;
       img_end = reinterpret_cast<uintptr_t>(img) + static_cast<uintptr_t>(stride) * H;
-      sy = axis_scale(H, RH);
-      sx = axis_scale(W, RW);
-      // column chunks: two staged rows (alignment + slack) must fit a stage
-      for (int nch = 1;; ++nch) {
-        cwid = (E + nch - 1) / nch;
-        cwid += cwid & 1;
-        int worst = 0;
-        for (int c0 = 0; c0 < E; c0 += cwid) {
-          const int cw = min(cwid, E - c0);
-          const int bts =
-              (axis_tap(ox0 + c0 + cw - 1, W, sx).i1 - axis_tap(ox0 + c0, W, sx).i0 + 1) * C;
-          worst = max(worst, bts);
-        }
-        const bool fits = 2 * (worst + 15 + 16 + kRowSlack) <= kArena || cwid <= 2;
-        if (fits && cwid <= 2 * (static_cast<int>(blockDim.x) - 32)) break;
+      if (nimg <= kTileCache) {
+        if (lane < nimg) hdr.tg[lane] = tile_geometry<C>(plan, kimg, lane, W, H, E);
+        __syncwarp();
       }
     }
+    const int t = g - __ldg(tile_off + kimg);
+    const TileGeo geo = nimg <= kTileCache ? hdr.tg[t] : tile_geometry<C>(plan, kimg, t, W, H, E);
+    const int RW = geo.RW, RH = geo.RH, oy0 = geo.oy0, ox0 = geo.ox0, cwid = geo.cwid;
+    const bool contig = RH > H;
+    const double sy = geo.sy, sx = geo.sx;
     // lane j owns output row j0 + j of the band
     int my_y0 = 0, my_y1 = 0;
     float my_fy = 0.f;
@@ -709,11 +748,14 @@ __global__ void __launch_bounds__(kMaxThreads, kCtasPerSm)
   if (WRITE_OUT)
     for (int i = threadIdx.x; i < C * 256; i += blockDim.x) s_lut[i] = lut[i];
   __syncthreads();
-  const int total = static_cast<int>(min(static_cast<int64_t>(__ldg(tile_off + n)), cap));
+  // every tile's items are enumerated (item order interleaves tiles); tiles at or
+  // above the output capacity are skipped
+  const int all_tiles = __ldg(tile_off + n);
+  const int cap_tiles = static_cast<int>(min(static_cast<int64_t>(all_tiles), cap));
   const int bands = (E + kBand - 1) / kBand;
-  const int64_t items = total > 0 ? static_cast<int64_t>(total) * bands : 0;
+  const int64_t items = cap_tiles > 0 ? static_cast<int64_t>(all_tiles) * bands : 0;
   if (threadIdx.x < 32)
-    produce<C>(hdr, arena, src, src_off, wh, n, plan, tile_off, E, items, bands);
+    produce<C>(hdr, arena, src, src_off, wh, n, plan, tile_off, E, items, bands, cap_tiles);
   else
     consume<C, OutT, LAYOUT, WRITE_OUT, WRITE_U8>(hdr, arena, s_lut, E, out, out_u8);
 }

@@ -40,12 +40,15 @@ __device__ __forceinline__ double axis_scale(int src, int out) {
 __device__ __forceinline__ AxisTap axis_tap(int i, int src, double scale) {
   double pos = __dadd_rn(__dmul_rn(static_cast<double>(i) + 0.5, scale), -0.5);
   pos = fmin(fmax(pos, 0.0), static_cast<double>(src - 1));
-  int i0 = static_cast<int>(floor(pos));
-  i0 = min(i0, src - 1);
+  // floor(pos) for 0 <= pos < 2^52 without the slow F2I/I2F conversions:
+  // pos + 2^52 rounded toward -inf is exactly 2^52 + floor(pos)
+  const double big = __dadd_rd(pos, 4503599627370496.0);
+  const int i0 = min(__double2loint(big), src - 1);  // clip already keeps floor <= src-1
+  const double fl = __dsub_rn(big, 4503599627370496.0);
   AxisTap t;
   t.i0 = i0;
   t.i1 = min(i0 + 1, src - 1);
-  t.f = __dsub_rn(pos, static_cast<double>(i0));
+  t.f = __dsub_rn(pos, fl);  // pos - i0, exact (the reference's frac)
   t.omf = __dsub_rn(1.0, t.f);
   return t;
 }

@@ -300,3 +300,71 @@ def test_fast_integer_scale_ties():
             arr = O.synth_image(5, k, int(w), int(h), 3, kind)
             want = O.tiles_u8(arr, O.plan_float(int(w), int(h), 64, 4))
             assert np.array_equal(out.pixel_u8[off[k]: off[k + 1]].cpu().numpy(), want)
+
+
+# ---------------------------------------------------------------------------
+# K3 at C5 scale: 1024 ragged prompts, counts straight from K1's n_images
+
+def test_c5_expansion_batch_bit_exact(golden):
+    from paper_2603_16987_b200.tokenizer import PlaceholderExpander, SpecialIds, SpecialVocab
+    from paper_2603_16987_b200.workloads import c4_shapes
+
+    _, meta = golden
+    sp = meta["specials"]
+    vocab = SpecialVocab(SpecialIds(**sp))
+    prompts = meta["prompt_ids"]  # tokenized by the reference: <|user|><|image|>prompt<|assistant|>
+    n = 1024
+    wh = c4_shapes(n, start=4096)
+    d_wh = torch.from_numpy(wh).to(DEV)
+    plan = torch.empty((n, 6), dtype=torch.int32, device=DEV)
+    n_img = torch.empty((n,), dtype=torch.int32, device=DEV)
+    off = torch.empty((n + 1,), dtype=torch.int32, device=DEV)
+    _lib.call("tp_plan", _lib.ptr(d_wh), n, 448, 12, _lib.ptr(plan), _lib.ptr(n_img),
+              _lib.ptr(off), torch.cuda.current_stream().cuda_stream)
+    seqs = [prompts[i % len(prompts)] for i in range(n)]
+    flat = np.concatenate([np.asarray(s, np.int32) for s in seqs])
+    seq_off = np.concatenate([[0], np.cumsum([len(s) for s in seqs])]).astype(np.int32)
+    cap = int(len(flat) + n * 13 * 256)
+    exp = PlaceholderExpander(vocab, 256, DEV)
+    res = exp(torch.from_numpy(flat).to(DEV), torch.from_numpy(seq_off).to(DEV), n_img,
+              torch.arange(n + 1, dtype=torch.int32, device=DEV), cap)
+    torch.cuda.synchronize()
+    counts = n_img.cpu().numpy()
+    assert int(res.err.cpu().numpy().max()) == 0
+    oo = res.out_off.cpu().numpy()
+    ids = res.ids.cpu().numpy()
+    mask = res.mask.cpu().numpy()
+    spans = res.spans.cpu().numpy()
+    first = res.first_assistant.cpu().numpy()
+    for s in range(n):
+        want, wspans, t = O.expand(seqs[s], [int(counts[s])], 256, sp["image_marker"],
+                                   sp["image_context"], sp["assistant_header"])
+        assert ids[oo[s]: oo[s + 1]].tolist() == want, s
+        assert [tuple(spans[s])] == [tuple(x) for x in wspans]
+        assert first[s] == t
+        assert np.array_equal(mask[oo[s]: oo[s + 1]].astype(bool),
+                              O.supervision_mask(want, t, sp["assistant_header"]))
+    # the contract the consumer checks (backend.assemble): spans carry the plan's tokens
+    assert int(spans[:, 1].sum()) == int(counts.sum()) * 256
+
+
+def test_expand_errors_and_capacity_flags():
+    from paper_2603_16987_b200.tokenizer import PlaceholderExpander, SpecialIds, SpecialVocab
+
+    vocab = SpecialVocab(SpecialIds(0, 1, 2, 3, 4, 5, 6))
+    exp = PlaceholderExpander(vocab, 4, DEV)
+    ids = torch.tensor([2, 4, 3, 2, 4, 4, 3, 2, 9, 9], dtype=torch.int32, device=DEV)
+    seq_off = torch.tensor([0, 3, 7, 10], dtype=torch.int32, device=DEV)
+    counts = torch.tensor([2, 1, 1], dtype=torch.int32, device=DEV)
+    count_off = torch.tensor([0, 1, 2, 3], dtype=torch.int32, device=DEV)  # seq 1 short a count
+    res = exp(ids, seq_off, counts, count_off, capacity=100)
+    torch.cuda.synchronize()
+    err = res.err.cpu().tolist()
+    assert err[0] == 0
+    assert err[1] & _lib.TP_EXPAND_ERR_MARKER_COUNT
+    assert err[2] & _lib.TP_EXPAND_ERR_NO_ASSISTANT
+    oo = res.out_off.cpu().tolist()
+    assert oo[1] - oo[0] == 3 - 1 + 8 and oo[3] == oo[1]  # errored sequences take no space
+    small = exp(ids[:3], seq_off[:2], counts[:1], count_off[:2], capacity=5)
+    torch.cuda.synchronize()
+    assert int(small.out_off[-1]) == -1  # capacity overflow is flagged, nothing written
