@@ -166,6 +166,12 @@ TP_API int tp_expand(const int32_t* d_ids, const int32_t* d_seq_off, int32_t n_s
 TP_API int tp_supervision_mask(const int32_t* d_ids, int64_t n, int64_t first_asst,
                                int32_t asst_id, uint8_t* d_mask, void* stream);
 
+/* pixel_unshuffle (tokenred.py:80-103): [h][w][d] patch grid of elem_bytes-sized
+ * elements -> [h/r][w/r][d*r*r], output cell (i, j) = input cells (i*r+a, j*r+b) with
+ * a outer, b inner.  A pure permutation (bit-exact for any element type). */
+TP_API int tp_pixel_unshuffle(const void* d_in, int32_t h, int32_t w, int64_t d,
+                              int32_t elem_bytes, int32_t r, void* d_out, void* stream);
+
 /* Synthetic HWC uint8 images generated on device (bench/test inputs).
  * kind 0: uniform bytes  v = byte(q & 3) of mix32(key(seed, k) ^ (q >> 2) * golden)
  * kind 1: smooth ramp    v = triangle wave of (3x + 2y + 40c + 17k) with period 510

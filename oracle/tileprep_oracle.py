@@ -221,6 +221,21 @@ def supervision_mask(ids: Sequence[int], t: int, asst: int) -> np.ndarray:
 
 
 # ---------------------------------------------------------------------------
+# token reduction
+
+def pixel_unshuffle(grid: np.ndarray, r: int) -> np.ndarray:
+    """pixel_unshuffle (tokenred.py:80-103) on an (h, w, d) array: output cell (i, j)
+    concatenates input cells (i*r + a, j*r + b), a outer, b inner."""
+    h, w, d = grid.shape
+    out = np.empty((h // r, w // r, d * r * r), dtype=grid.dtype)
+    for a in range(r):
+        for b in range(r):
+            k = a * r + b
+            out[:, :, k * d:(k + 1) * d] = grid[a::r, b::r, :]
+    return out
+
+
+# ---------------------------------------------------------------------------
 # synthetic inputs: CPU twin of tp_synth (misc.cu)
 
 _M32 = np.uint64(0xFFFFFFFF)

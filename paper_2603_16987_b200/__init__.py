@@ -44,7 +44,14 @@ from .tokenizer import (
     expand_image_placeholders,
     load_specials,
 )
-from .tokenred import TokenReductionConfig, tokens_per_tile, visual_token_count
+from .tokenred import (
+    PatchGrid,
+    TokenReductionConfig,
+    pixel_unshuffle,
+    pixel_unshuffle_tensor,
+    tokens_per_tile,
+    visual_token_count,
+)
 from .backend import AssembledSequence, assemble
 from .engine import PackedImages, TileBatch, TilePreprocessor, pack_images, synth_packed
 

@@ -62,6 +62,8 @@ SIGNATURES = {
                             c_int32, c_int32, c_int32, c_void_p, c_int64, c_void_p, c_void_p,
                             c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "tp_supervision_mask": (c_int32, [c_void_p, c_int64, c_int64, c_int32, c_void_p, c_void_p]),
+    "tp_pixel_unshuffle": (c_int32, [c_void_p, c_int32, c_int32, c_int64, c_int32, c_int32,
+                                     c_void_p, c_void_p]),
     "tp_synth": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_uint64, c_int32,
                            c_int64, c_void_p]),
 }

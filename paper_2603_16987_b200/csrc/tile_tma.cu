@@ -22,6 +22,8 @@
 // §K2 for the error bound) — checked against the exact fp64 kernel and the
 // oracle in tests/test_gpu_kernels.py.
 
+#include <cstddef>
+
 #include "tp_common.cuh"
 
 namespace tp {
@@ -35,20 +37,25 @@ constexpr int kCtasPerSm = 3;
 constexpr int kRowSlack = 16;            // readable slack after each staged row
 constexpr int kTileCache = 16;           // per-image tile geometries kept in smem
 
-struct Phase {
-  const uint8_t* img;
+struct __align__(16) Phase {
+  // consumer header, read as int4 / double loads (keep the layout)
   int g;       // global tile index; -1 terminates the consumers
   int j0;      // first output row (tile coordinates)
   int nrows;   // output rows in this phase
+  int mis;     // common (offset & 3) of all staged rows, or -1 when they differ
   int c0, cw;  // output column range (tile coordinates)
   int xlo;     // first staged source column
-  int mis;     // common (offset & 3) of all staged rows, or -1 when they differ
-  int W, H, RW, RH, oy0, ox0;
-  double sx;                     // W / RW (fallback column taps)
+  int W;
+  int ox0, pad0, pad1, pad2;
+  double sx;  // W / RW (column taps)
+  double pad3;
   int off0[kBand], off1[kBand];  // arena byte offset of column xlo in rows y0 / y1
   float fy[kBand];
   double fy64[kBand], omfy64[kBand];  // exact row weights for the fp64 fallback
 };
+constexpr uint32_t kPhOff0 = offsetof(Phase, off0), kPhOff1 = offsetof(Phase, off1),
+                   kPhFy = offsetof(Phase, fy), kPhFy64 = offsetof(Phase, fy64),
+                   kPhOmfy64 = offsetof(Phase, omfy64);
 
 struct TileGeo {
   double sx, sy;
@@ -355,8 +362,6 @@ __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restri
       int jj = 0;
       while (jj < nrows) {
         const int s = stage;
-        if (lane == 0) mbar_wait(&hdr.empty[s], parity ^ 1u);
-        __syncwarp();
         const int nleft = nrows - jj;
         // ---- entries
         int y_e, ymin = 0;
@@ -405,6 +410,9 @@ __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restri
         const int e1 = contig ? ry1 - ymin : 2 * lane + 1;
         const int off0 = __shfl_sync(0xffffffffu, ent_off, min(max(e0, 0), 31));
         const int off1 = __shfl_sync(0xffffffffu, ent_off, min(max(e1, 0), 31));
+        // the plan above needs no stage: only now wait until the consumers release it
+        if (lane == 0) mbar_wait(&hdr.empty[s], parity ^ 1u);
+        __syncwarp();
         Phase& ph = hdr.ph[s];
         const int m0 = __shfl_sync(0xffffffffu, off0 & 3, 0);
         const bool same =
@@ -431,7 +439,6 @@ __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restri
 #pragma unroll
         for (int d = 16; d > 0; d >>= 1) tx += __shfl_xor_sync(0xffffffffu, tx, d);
         if (lane == 0) {
-          ph.img = img;
           ph.g = g;
           ph.j0 = j0 + jj;
           ph.nrows = nr;
@@ -440,10 +447,6 @@ __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restri
           ph.xlo = xlo;
           ph.mis = same ? m0 : -1;
           ph.W = W;
-          ph.H = H;
-          ph.RW = RW;
-          ph.RH = RH;
-          ph.oy0 = oy0;
           ph.ox0 = ox0;
           ph.sx = sx;
         }
@@ -521,16 +524,24 @@ __device__ __forceinline__ double ldsd(uint32_t addr) {
   return v;
 }
 
-// shared-space addresses of the per-row phase fields
+__device__ __forceinline__ int4 lds128(uint32_t addr) {
+  int4 v;
+  asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(addr));
+  return v;
+}
+
+// per-row phase fields live at compile-time offsets from the phase's shared address
 struct PhaseRows {
-  uint32_t off0, off1, fy, fy64, omfy64;
+  uint32_t base;
 };
 
 template <bool UNIFORM>
 __device__ __forceinline__ PixTaps fetch_pix(const PhaseRows& pr, int jj, uint32_t sbase, int mis,
                                              int xo, uint32_t wo, uint32_t sh) {
   PixTaps t;
-  const uint32_t o0 = lds32(pr.off0 + 4 * jj), o1 = lds32(pr.off1 + 4 * jj);
+  const uint32_t o0 = lds32(pr.base + kPhOff0 + 4 * jj), o1 = lds32(pr.base + kPhOff1 + 4 * jj);
   if (UNIFORM) {
     const uint32_t r0 = sbase + o0 - mis + wo, r1 = sbase + o1 - mis + wo;
     uint32_t w0 = lds32(r0), w1 = lds32(r0 + 4), w2 = lds32(r0 + 8);
@@ -557,7 +568,7 @@ __device__ __forceinline__ void consume_pair_rows(
     const PhaseRows& pr, int g, int j0, int nrows, int mis_in, uint32_t sbase, uint32_t lut_u32,
     int ia, int ib, bool has_a, bool has_b, int xoa, int xob, float fxa, float fxb, double fxa64,
     double omfxa64, double fxb64, double omfxb64, int E, OutT* __restrict__ out,
-    uint8_t* __restrict__ out_u8) {
+    uint8_t* __restrict__ out_u8, OutT* __restrict__ tile_a) {
   const int64_t EE = static_cast<int64_t>(E) * E;
   const f32x2 FX = pk(fxa, fxb);
   const f32x2 KH = pk(8388607.5f, 8388607.5f);  // 2^23 - 0.5: biased byte -> byte + 0.5
@@ -571,15 +582,15 @@ __device__ __forceinline__ void consume_pair_rows(
   uint32_t lut0;  // + kraw*SZ + c*256*SZ; opaque so it stays in a register
   asm volatile("mov.u32 %0, %1;" : "=r"(lut0) : "r"(lut_u32 - kKrawBias * SZ));
   // per-channel output row pointers (NCHW), advanced by one output row per step
-  OutT* oc[C];
+  OutT* oc[C];  // tile_a = out + g*C*EE + ia, cached per (tile, column segment)
+  oc[0] = tile_a + j0 * E;
 #pragma unroll
-  for (int c = 0; c < C; ++c)
-    oc[c] = out + (static_cast<int64_t>(g) * C + c) * EE + static_cast<int64_t>(j0) * E + ia;
+  for (int c = 1; c < C; ++c) oc[c] = oc[c - 1] + EE;
   const int ob_off = ib - ia;
   // one output row: taps (a, b) already fetched
   auto row = [&](int jj, const PixTaps& a, const PixTaps& b) {
     const int j = j0 + jj;
-    const float fy = ldsf(pr.fy + 4 * jj);
+    const float fy = ldsf(pr.base + kPhFy + 4 * jj);
     const f32x2 FY = pk(fy, fy);
     uint32_t ka[C], kb[C], xa[C], xb[C];
     uint32_t worst = 0xFFFFFFFFu;
@@ -602,7 +613,8 @@ __device__ __forceinline__ void consume_pair_rows(
       worst = min(worst, min(xa[c], xb[c]));
     }
     if (worst < kAmbLimit) {  // recompute only the flagged values, exactly, in fp64
-      const double fy64 = ldsd(pr.fy64 + 8 * jj), omfy64 = ldsd(pr.omfy64 + 8 * jj);
+      const double fy64 = ldsd(pr.base + kPhFy64 + 8 * jj),
+                   omfy64 = ldsd(pr.base + kPhOmfy64 + 8 * jj);
 #pragma unroll
       for (int c = 0; c < C; ++c) {
         if (xa[c] < kAmbLimit)
@@ -677,35 +689,38 @@ __device__ void consume(SmemHeader& hdr, const uint8_t* arena, const OutT* s_lut
   int xoa = 0, xob = 0;
   float fxa = 0.f, fxb = 0.f;
   double fxa64 = 0.0, omfxa64 = 1.0, fxb64 = 0.0, omfxb64 = 1.0;
+  const int64_t EE = static_cast<int64_t>(E) * E;
+  OutT* tile_a = out;
+  const uint32_t ph0 = smem_u32(&hdr.ph[0]);
   while (true) {
     mbar_wait(&hdr.full[stage], parity);
-    const Phase& ph = hdr.ph[stage];
-    const int g = ph.g;
+    PhaseRows pr;
+    pr.base = ph0 + stage * static_cast<uint32_t>(sizeof(Phase));
+    const int4 h0 = lds128(pr.base), h1 = lds128(pr.base + 16);
+    const int g = h0.x;
     if (g < 0) break;
-    const int c0 = ph.c0, cw = ph.cw, j0 = ph.j0, nrows = ph.nrows, mis = ph.mis;
+    const int j0 = h0.y, nrows = h0.z, mis = h0.w;
+    const int c0 = h1.x, cw = h1.y, xlo = h1.z, W = h1.w;
     const int segs = (cw + 63) >> 6;  // 64-pixel segments, one per consumer warp
     const uint32_t sbase = arena_u32 + stage * kArena;
-    PhaseRows pr;
-    pr.off0 = smem_u32(ph.off0);
-    pr.off1 = smem_u32(ph.off1);
-    pr.fy = smem_u32(ph.fy);
-    pr.fy64 = smem_u32(ph.fy64);
-    pr.omfy64 = smem_u32(ph.omfy64);
     for (int q = cwarp; q < segs; q += ncons >> 5) {
       const int la = 64 * q + lane, lb = la + 32;  // chunk-relative pixels
       const bool has_a = la < cw, has_b = lb < cw;
       const int ia = c0 + la, ib = c0 + lb;
       if (g != cache_g || c0 != cache_c0 || q != cache_q) {
-        const AxisTap ta = axis_tap(ph.ox0 + min(ia, c0 + cw - 1), ph.W, ph.sx);
-        const AxisTap tb = axis_tap(ph.ox0 + min(ib, c0 + cw - 1), ph.W, ph.sx);
-        xoa = (ta.i0 - ph.xlo) * C;
-        xob = (tb.i0 - ph.xlo) * C;
+        const int ox0 = lds32(pr.base + 32);
+        const double sx = ldsd(pr.base + 48);
+        const AxisTap ta = axis_tap(ox0 + min(ia, c0 + cw - 1), W, sx);
+        const AxisTap tb = axis_tap(ox0 + min(ib, c0 + cw - 1), W, sx);
+        xoa = (ta.i0 - xlo) * C;
+        xob = (tb.i0 - xlo) * C;
         fxa = __double2float_rn(ta.f);
         fxb = __double2float_rn(tb.f);
         fxa64 = ta.f;
         omfxa64 = ta.omf;
         fxb64 = tb.f;
         omfxb64 = tb.omf;
+        tile_a = out + static_cast<int64_t>(g) * C * EE + ia;
         cache_g = g;
         cache_c0 = c0;
         cache_q = q;
@@ -713,11 +728,11 @@ __device__ void consume(SmemHeader& hdr, const uint8_t* arena, const OutT* s_lut
       if (mis >= 0)
         consume_pair_rows<C, OutT, LAYOUT, WRITE_OUT, WRITE_U8, true>(
             pr, g, j0, nrows, mis, sbase, lut_u32, ia, ib, has_a, has_b, xoa, xob, fxa, fxb,
-            fxa64, omfxa64, fxb64, omfxb64, E, out, out_u8);
+            fxa64, omfxa64, fxb64, omfxb64, E, out, out_u8, tile_a);
       else
         consume_pair_rows<C, OutT, LAYOUT, WRITE_OUT, WRITE_U8, false>(
             pr, g, j0, nrows, mis, sbase, lut_u32, ia, ib, has_a, has_b, xoa, xob, fxa, fxb,
-            fxa64, omfxa64, fxb64, omfxb64, E, out, out_u8);
+            fxa64, omfxa64, fxb64, omfxb64, E, out, out_u8, tile_a);
     }
     mbar_arrive(&hdr.empty[stage]);
     if (++stage == kStages) {

@@ -255,6 +255,18 @@ def main() -> None:
     meta["tokens_per_tile"] = {"512_16_4": tokens_per_tile(512, 16, 4),
                                "448_14_2": tokens_per_tile(448, 14, 2)}
 
+    # 7. pixel_unshuffle ------------------------------------------------------------
+    from vlmfp.tokenred import PatchGrid, pixel_unshuffle
+
+    ucases = [(4, 6, 3, 2, "float32", 1), (32, 32, 5, 2, "float32", 2), (8, 12, 7, 4, "int32", 3),
+              (6, 9, 2, 3, "float64", 4), (5, 5, 4, 1, "float32", 5)]
+    meta["unshuffle_cases"] = ucases
+    for i, (h, w, d, r, dt, seed) in enumerate(ucases):
+        data = np.random.default_rng(seed).standard_normal(h * w * d).astype(dt)
+        out = pixel_unshuffle(PatchGrid(h, w, d, data), r)
+        arrays[f"unshuffle_{i}"] = out.data
+        meta.setdefault("unshuffle_shapes", []).append([out.h, out.w, out.d])
+
     np.savez_compressed(OUT_NPZ, **arrays)
     OUT_JSON.write_text(json.dumps(meta, indent=1, sort_keys=True) + "\n")
     print(f"wrote {OUT_NPZ} ({OUT_NPZ.stat().st_size / 1e6:.2f} MB), {OUT_JSON}")

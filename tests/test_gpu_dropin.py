@@ -337,3 +337,48 @@ def test_assemble_contract_with_device_plans(vocab):
     bad = P.expand_and_mask([2, 4, 3], [plan.n_images + 1], 256, vocab)
     with pytest.raises(P.AssemblyError):
         P.assemble(bad, plan, tr)
+
+
+# ---------------------------------------------------------------------------
+# pixel_unshuffle (reference tests/test_tokenred.py:19-74)
+
+def test_pixel_unshuffle_golden(golden):
+    data, meta = golden
+    for i, (h, w, d, r, dt, seed) in enumerate(meta["unshuffle_cases"]):
+        flat = np.random.default_rng(seed).standard_normal(h * w * d).astype(dt)
+        out = P.pixel_unshuffle(P.PatchGrid(h, w, d, flat), r)
+        assert [out.h, out.w, out.d] == meta["unshuffle_shapes"][i]
+        assert out.data.dtype == flat.dtype
+        assert np.array_equal(out.data, data[f"unshuffle_{i}"])
+
+
+@settings(max_examples=30, deadline=None)
+@given(oh=st.integers(1, 9), ow=st.integers(1, 9), d=st.integers(1, 40), r=st.integers(1, 4),
+       dt=st.sampled_from(["float32", "float16", "int8", "float64"]), seed=st.integers(0, 2**31))
+def test_pixel_unshuffle_is_the_oracle_permutation(oh, ow, d, r, dt, seed):
+    h, w = oh * r, ow * r
+    flat = (np.random.default_rng(seed).standard_normal(h * w * d) * 50).astype(dt)
+    out = P.pixel_unshuffle(P.PatchGrid(h, w, d, flat), r)
+    want = O.pixel_unshuffle(flat.reshape(h, w, d), r)
+    assert np.array_equal(out.as_array(), want)
+    assert np.array_equal(np.sort(out.data.view(np.uint8)), np.sort(flat.view(np.uint8)))
+
+
+def test_pixel_unshuffle_errors_and_identity():
+    g = P.PatchGrid(4, 6, 2, np.arange(48, dtype=np.float32))
+    assert P.pixel_unshuffle(g, 1).data is g.data
+    with pytest.raises(P.DomainError):
+        P.pixel_unshuffle(g, 0)
+    with pytest.raises(P.ShapeError):
+        P.pixel_unshuffle(g, 4)
+    with pytest.raises(P.ShapeError):
+        P.PatchGrid(2, 2, 2, np.zeros(7, np.float32))
+
+
+def test_pixel_unshuffle_device_tensor():
+    import torch
+
+    t = torch.randn(32, 32, 1024, dtype=torch.bfloat16, device="cuda")
+    out = P.pixel_unshuffle_tensor(t, 2)
+    want = t.reshape(16, 2, 16, 2, 1024).permute(0, 2, 1, 3, 4).reshape(16, 16, 4096)
+    assert torch.equal(out, want)

@@ -175,3 +175,12 @@ def test_tiles_vs_live_reference(reference, h, w, seed, e, mt):
     plan = select_tile_plan(w, h, cfg)
     want = np.stack([t.data for t in tile_image(ImageBuffer.from_array(arr), plan, cfg)])
     assert np.array_equal(O.tiles_u8(arr, O.plan_float(w, h, e, mt)), want)
+
+
+def test_pixel_unshuffle_matches_golden(golden):
+    data, meta = golden
+    for i, (h, w, d, r, dt, seed) in enumerate(meta["unshuffle_cases"]):
+        grid = np.random.default_rng(seed).standard_normal(h * w * d).astype(dt).reshape(h, w, d)
+        got = O.pixel_unshuffle(grid, r)
+        assert list(got.shape) == meta["unshuffle_shapes"][i]
+        assert np.array_equal(got.reshape(-1), data[f"unshuffle_{i}"])
