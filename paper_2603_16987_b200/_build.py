@@ -56,19 +56,23 @@ def _stale(target: Path, deps: list[Path]) -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False, ptxas_info: bool = False) -> Path:
-    """Compile every csrc/*.cu for sm_100a and link libtileprep.so in-tree."""
+def build(verbose: bool = False, force: bool = False, ptxas_info: bool = False,
+          defines: tuple = (), lib_path: Path = None, build_dir: Path = None) -> Path:
+    """Compile every csrc/*.cu for sm_100a and link libtileprep.so in-tree.
+    `defines` (e.g. ("TP_K2_STAGES=4",)) and a separate lib/build dir give tuning variants."""
     nvcc = nvcc_path()
-    BUILD_DIR.mkdir(parents=True, exist_ok=True)
+    lib_out = Path(lib_path) if lib_path else LIB_PATH
+    bdir = Path(build_dir) if build_dir else BUILD_DIR
+    bdir.mkdir(parents=True, exist_ok=True)
     headers = _headers()
     objs: list[Path] = []
     jobs = []
     for src in sources():
-        obj = BUILD_DIR / (src.stem + ".o")
+        obj = bdir / (src.stem + ".o")
         objs.append(obj)
         if force or _stale(obj, [src, *headers]):
-            cmd = [nvcc, *ARCH_FLAGS, *NVCC_FLAGS, f"-I{INCLUDE}", f"-I{CSRC}", "-c", str(src),
-                   "-o", str(obj)]
+            cmd = [nvcc, *ARCH_FLAGS, *NVCC_FLAGS, *[f"-D{d}" for d in defines], f"-I{INCLUDE}",
+                   f"-I{CSRC}", "-c", str(src), "-o", str(obj)]
             if ptxas_info:
                 cmd += ["-Xptxas", "-v"]
             jobs.append(cmd)
@@ -86,11 +90,12 @@ def build(verbose: bool = False, force: bool = False, ptxas_info: bool = False) 
     with ThreadPoolExecutor(max_workers=min(8, max(1, len(jobs)))) as pool:
         list(pool.map(run, jobs))
 
-    if force or jobs or _stale(LIB_PATH, objs):
-        tmp = LIB_PATH.with_suffix(".so.tmp")
+    if force or jobs or _stale(lib_out, objs):
+        lib_out.parent.mkdir(parents=True, exist_ok=True)
+        tmp = lib_out.with_suffix(".so.tmp")
         run([nvcc, *ARCH_FLAGS, "-shared", "-o", str(tmp), *map(str, objs)])
-        os.replace(tmp, LIB_PATH)
-    return LIB_PATH
+        os.replace(tmp, lib_out)
+    return lib_out
 
 
 if __name__ == "__main__":

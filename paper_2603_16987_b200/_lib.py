@@ -11,7 +11,11 @@ import threading
 from ctypes import c_int32, c_int64, c_uint64, c_void_p, c_char_p, POINTER
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libtileprep.so"
+import os
+
+# TILEPREP_LIB points at an alternative build (tuning sweeps); default: the in-tree library
+LIB_PATH = Path(os.environ.get("TILEPREP_LIB") or
+                Path(__file__).resolve().parent / "libtileprep.so")
 
 TP_OK = 0
 TP_ERR_INVALID_ARGUMENT = 1

@@ -12,8 +12,8 @@
 // key is unimodal in c with its minimum at c ~ w r / h, so only
 // c = floor(w r / h) and c + 1 (clamped to [1, max_tiles / r]) can win.  The
 // per-lane winners are reduced across the warp with the exact comparator.
-// One CTA of 1024 threads walks the batch in chunks of 1024 images and
-// block-scans n_images into the output tile offsets.
+// One CTA (one warp per image, up to 1024 threads) walks the batch in chunks of
+// blockDim images and block-scans n_images into the output tile offsets.
 
 #include "tp_common.cuh"
 
@@ -94,12 +94,13 @@ __global__ void __launch_bounds__(kPlanThreads)
   const int lane = threadIdx.x & 31;
   if (threadIdx.x == 0) s_bad = 0;
   int64_t carry = 0;
-  for (int base = 0; base < n; base += kPlanThreads) {
-    const int chunk = min(kPlanThreads, n - base);
+  const int nthr = blockDim.x;  // sized to the batch (<= 1024): small batches, short syncs
+  for (int base = 0; base < n; base += nthr) {
+    const int chunk = min(nthr, n - base);
     s_cnt[threadIdx.x] = 0;
     __syncthreads();
-    // 32 warps x 32 images each
-    for (int j = warp; j < chunk; j += kPlanThreads / 32) {
+    // one warp per image (a block of 32 * n threads for n < 32 images)
+    for (int j = warp; j < chunk; j += nthr / 32) {
       const int k = base + j;
       const int w = wh[2 * k], h = wh[2 * k + 1];
       const bool ok = w >= 1 && h >= 1 && w <= TP_MAX_EDGE && h <= TP_MAX_EDGE;
@@ -151,7 +152,9 @@ extern "C" int tp_plan(const int32_t* d_wh, int32_t n, int32_t tile_edge, int32_
     return tp::set_error(TP_ERR_UNSUPPORTED, "tile_edge * max_tiles overflows int32");
   if (!d_tile_off || (n > 0 && (!d_wh || !d_plan || !d_n_img)))
     return tp::set_error(TP_ERR_INVALID_ARGUMENT, "tp_plan: null buffer");
-  tp::k_plan<<<1, tp::kPlanThreads, 0, tp::as_stream(stream)>>>(d_wh, n, tile_edge, max_tiles,
-                                                                d_plan, d_n_img, d_tile_off);
+  // one warp per image up to a full 1024-thread block (small batches: short block syncs)
+  const int threads = static_cast<int>(std::min<int64_t>(tp::kPlanThreads, 32LL * std::max(1, n)));
+  tp::k_plan<<<1, threads, 0, tp::as_stream(stream)>>>(d_wh, n, tile_edge, max_tiles, d_plan,
+                                                       d_n_img, d_tile_off);
   return tp::check_launch("tp_plan");
 }

@@ -29,13 +29,27 @@
 namespace tp {
 namespace {
 
-constexpr int kBand = 8;                 // output rows per work item
-constexpr int kStages = 3;
-constexpr int kArena = 23 * 1024;        // bytes of staged source rows per stage
-constexpr int kMaxThreads = 256;         // 1 producer warp + up to 7 consumer warps
-constexpr int kCtasPerSm = 3;
+// tuning knobs (overridable with -D for sweeps; defaults are the measured best)
+#ifndef TP_K2_BAND
+#define TP_K2_BAND 16
+#endif
+#ifndef TP_K2_STAGES
+#define TP_K2_STAGES 2
+#endif
+#ifndef TP_K2_ARENA_KB
+#define TP_K2_ARENA_KB 54
+#endif
+#ifndef TP_K2_CTAS_PER_SM
+#define TP_K2_CTAS_PER_SM 2
+#endif
+constexpr int kBand = TP_K2_BAND;              // output rows per work item
+constexpr int kStages = TP_K2_STAGES;
+constexpr int kArena = TP_K2_ARENA_KB * 1024;  // bytes of staged source rows per stage
+constexpr int kMaxThreads = 256;               // 1 producer warp + up to 7 consumer warps
+constexpr int kCtasPerSm = TP_K2_CTAS_PER_SM;
 constexpr int kRowSlack = 16;            // readable slack after each staged row
 constexpr int kTileCache = 16;           // per-image tile geometries kept in smem
+static_assert(kBand >= 2 && kBand <= 32, "a band is owned by the 32 lanes of the producer");
 
 struct __align__(16) Phase {
   // consumer header, read as int4 / double loads (keep the layout)
@@ -300,7 +314,7 @@ __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restri
                         const int64_t* __restrict__ src_off, const int32_t* __restrict__ wh,
                         int n, const int32_t* __restrict__ plan,
                         const int32_t* __restrict__ tile_off, int E, int64_t items, int bands,
-                        int cap_tiles) {
+                        int band, int cap_tiles) {
   const int lane = threadIdx.x & 31;
   int stage = 0;
   uint32_t parity = 0;
@@ -323,9 +337,9 @@ __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restri
     const int nimg = __ldg(tile_off + kimg + 1) - __ldg(tile_off + kimg);
     const int r = static_cast<int>(item - static_cast<int64_t>(__ldg(tile_off + kimg)) * bands);
     const int g = __ldg(tile_off + kimg) + r % nimg;
-    const int j0 = (r / nimg) * kBand;
+    const int j0 = (r / nimg) * band;
     if (g >= cap_tiles) continue;  // caller's buffers end before this tile
-    const int nrows = min(kBand, E - j0);
+    const int nrows = min(band, E - j0);
     if (kimg != cur_k) {  // new image: per-tile geometry, one lane per tile
       cur_k = kimg;
       W = __ldg(wh + 2 * kimg);
@@ -387,11 +401,13 @@ __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restri
         const int region = isnew ? ((delta + rb + 15) & ~15) + kRowSlack : 0;
         const int incl = warp_incl_sum(region, lane);
         // ---- how many output rows fit the stage (a prefix: incl is non-decreasing)
-        int last_e = contig ? (__shfl_sync(0xffffffffu, my_y1, min(jj + lane, 31)) - ymin)
-                            : (2 * lane + 1);
-        last_e = min(max(last_e, 0), 31);
+        // (a phase holds at most 32 entries: 16 rows when downscaling, fewer source rows
+        // than that when upscaling)
+        const int last_raw = contig ? (__shfl_sync(0xffffffffu, my_y1, min(jj + lane, 31)) - ymin)
+                                    : (2 * lane + 1);
+        const int last_e = min(max(last_raw, 0), 31);
         const int incl_at = __shfl_sync(0xffffffffu, incl, last_e);
-        const bool rfits = lane < nleft && incl_at <= kArena;
+        const bool rfits = lane < nleft && last_raw <= 31 && incl_at <= kArena;
         const int nr = max(1, __popc(__ballot_sync(0xffffffffu, rfits)));
         const int e_last = __shfl_sync(0xffffffffu, last_e, nr - 1);
         const bool staged = isnew && lane <= e_last;
@@ -767,10 +783,15 @@ __global__ void __launch_bounds__(kMaxThreads, kCtasPerSm)
   // above the output capacity are skipped
   const int all_tiles = __ldg(tile_off + n);
   const int cap_tiles = static_cast<int>(min(static_cast<int64_t>(all_tiles), cap));
-  const int bands = (E + kBand - 1) / kBand;
+  // band height: kBand rows, smaller when a small batch would leave SMs idle (batch-1
+  // latency); every CTA derives the same value from the device-side tile count
+  int band = kBand;
+  while (band > 2 && static_cast<int64_t>(all_tiles) * ((E + band - 1) / band) < 2 * gridDim.x)
+    band >>= 1;
+  const int bands = (E + band - 1) / band;
   const int64_t items = cap_tiles > 0 ? static_cast<int64_t>(all_tiles) * bands : 0;
   if (threadIdx.x < 32)
-    produce<C>(hdr, arena, src, src_off, wh, n, plan, tile_off, E, items, bands, cap_tiles);
+    produce<C>(hdr, arena, src, src_off, wh, n, plan, tile_off, E, items, bands, band, cap_tiles);
   else
     consume<C, OutT, LAYOUT, WRITE_OUT, WRITE_U8>(hdr, arena, s_lut, E, out, out_u8);
 }
