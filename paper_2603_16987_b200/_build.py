@@ -41,12 +41,12 @@ def nvcc_path() -> str:
     raise RuntimeError("nvcc not found; the CUDA toolkit is required to build libtileprep.so")
 
 
-def sources() -> list[Path]:
-    return sorted(CSRC.glob("*.cu"))
+def sources(csrc: Path = CSRC) -> list[Path]:
+    return sorted(Path(csrc).glob("*.cu"))
 
 
-def _headers() -> list[Path]:
-    return sorted(CSRC.glob("*.cuh")) + sorted(INCLUDE.glob("*.h"))
+def _headers(csrc: Path = CSRC) -> list[Path]:
+    return sorted(Path(csrc).glob("*.cuh")) + sorted(INCLUDE.glob("*.h"))
 
 
 def _stale(target: Path, deps: list[Path]) -> bool:
@@ -57,22 +57,24 @@ def _stale(target: Path, deps: list[Path]) -> bool:
 
 
 def build(verbose: bool = False, force: bool = False, ptxas_info: bool = False,
-          defines: tuple = (), lib_path: Path = None, build_dir: Path = None) -> Path:
+          defines: tuple = (), lib_path: Path = None, build_dir: Path = None,
+          csrc: Path = CSRC) -> Path:
     """Compile every csrc/*.cu for sm_100a and link libtileprep.so in-tree.
-    `defines` (e.g. ("TP_K2_STAGES=4",)) and a separate lib/build dir give tuning variants."""
+    `defines` (e.g. ("TP_K2_STAGES=4",)), another source dir and a separate lib/build dir
+    give tuning variants (tools/build_variants.py)."""
     nvcc = nvcc_path()
     lib_out = Path(lib_path) if lib_path else LIB_PATH
     bdir = Path(build_dir) if build_dir else BUILD_DIR
     bdir.mkdir(parents=True, exist_ok=True)
-    headers = _headers()
+    headers = _headers(csrc)
     objs: list[Path] = []
     jobs = []
-    for src in sources():
+    for src in sources(csrc):
         obj = bdir / (src.stem + ".o")
         objs.append(obj)
         if force or _stale(obj, [src, *headers]):
             cmd = [nvcc, *ARCH_FLAGS, *NVCC_FLAGS, *[f"-D{d}" for d in defines], f"-I{INCLUDE}",
-                   f"-I{CSRC}", "-c", str(src), "-o", str(obj)]
+                   f"-I{csrc}", "-c", str(src), "-o", str(obj)]
             if ptxas_info:
                 cmd += ["-Xptxas", "-v"]
             jobs.append(cmd)

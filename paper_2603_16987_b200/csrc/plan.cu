@@ -59,7 +59,7 @@ __device__ Cand warp_plan(uint32_t w, uint32_t h, int max_tiles) {
   for (int r = lane + 1; r <= max_tiles; r += 32) {
     const int cmax = max_tiles / r;
     // c* = floor(w r / h), candidates c*, c*+1 clamped to [1, cmax]
-    int c0 = static_cast<int>((static_cast<uint64_t>(w) * r) / h);
+    int c0 = static_cast<int>((w * static_cast<uint32_t>(r)) / h);  // w r <= 2^26
     c0 = max(1, min(c0, cmax));
     const int c1 = min(c0 + 1, cmax);
     Cand k0 = make_cand(w, h, r, c0);
@@ -92,6 +92,8 @@ __global__ void __launch_bounds__(kPlanThreads)
   __shared__ int s_bad;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  pdl_trigger();
+  pdl_wait();  // the previous K2 may still be reading plan / tile_off
   if (threadIdx.x == 0) s_bad = 0;
   int64_t carry = 0;
   const int nthr = blockDim.x;  // sized to the batch (<= 1024): small batches, short syncs
@@ -154,7 +156,8 @@ extern "C" int tp_plan(const int32_t* d_wh, int32_t n, int32_t tile_edge, int32_
     return tp::set_error(TP_ERR_INVALID_ARGUMENT, "tp_plan: null buffer");
   // one warp per image up to a full 1024-thread block (small batches: short block syncs)
   const int threads = static_cast<int>(std::min<int64_t>(tp::kPlanThreads, 32LL * std::max(1, n)));
-  tp::k_plan<<<1, threads, 0, tp::as_stream(stream)>>>(d_wh, n, tile_edge, max_tiles, d_plan,
-                                                       d_n_img, d_tile_off);
+  const cudaError_t err = tp::launch_pdl(tp::k_plan, dim3(1), dim3(threads), 0, tp::as_stream(stream),
+                                          d_wh, n, tile_edge, max_tiles, d_plan, d_n_img, d_tile_off);
+  if (err != cudaSuccess) return tp::set_error(TP_ERR_CUDA, "tp_plan: %s", cudaGetErrorString(err));
   return tp::check_launch("tp_plan");
 }

@@ -31,13 +31,22 @@ namespace {
 
 // tuning knobs (overridable with -D for sweeps; defaults are the measured best)
 #ifndef TP_K2_BAND
-#define TP_K2_BAND 16
+#define TP_K2_BAND 32
 #endif
 #ifndef TP_K2_STAGES
 #define TP_K2_STAGES 2
 #endif
 #ifndef TP_K2_ARENA_KB
 #define TP_K2_ARENA_KB 54
+#endif
+#ifndef TP_K2_PDL  // 0: plain launch; 1: PDL, successor released at start; 2: at the end
+#define TP_K2_PDL 2
+#endif
+#ifndef TP_K2_ROW_BALANCE
+#define TP_K2_ROW_BALANCE 1
+#endif
+#ifndef TP_K2_BATCHED_FALLBACK
+#define TP_K2_BATCHED_FALLBACK 0
 #endif
 #ifndef TP_K2_CTAS_PER_SM
 #define TP_K2_CTAS_PER_SM 2
@@ -102,16 +111,32 @@ __device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// Wait for the barrier phase.  The suspend-time hint parks the waiting warp until the
+// phase completes (SASS NANOSLEEP.SYNCS) instead of spinning: a bare try_wait loop
+// polled ~55 times per phase in the producer (12% of the kernel's issued instructions,
+// though with no measurable effect on its time).
+#ifndef TP_K2_WAIT_HINT_NS
+#define TP_K2_WAIT_HINT_NS 1000000
+#endif
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
   uint32_t done = 0;
   do {
+#if TP_K2_WAIT_HINT_NS > 0
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(a), "r"(parity), "n"(TP_K2_WAIT_HINT_NS)
+        : "memory");
+#else
     asm volatile(
         "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
         " selp.u32 %0, 1, 0, p;\n}\n"
         : "=r"(done)
         : "r"(a), "r"(parity)
         : "memory");
+#endif
   } while (!done);
 }
 
@@ -186,6 +211,10 @@ __device__ __forceinline__ float biased_byte(uint32_t g0, uint32_t g1, int k) {
 
 __device__ __forceinline__ uint32_t byte_of(uint32_t g0, uint32_t g1, int k) {
   return ((k < 4 ? g0 : g1) >> ((k & 3) * 8)) & 0xFFu;
+}
+// byte k (0..7, run-time) of (g0, g1), zero-extended: one select + one byte permute
+__device__ __forceinline__ uint32_t byte_dyn(uint32_t g0, uint32_t g1, int k) {
+  return __byte_perm(k < 4 ? g0 : g1, 0u, 0x4440u | static_cast<uint32_t>(k & 3));
 }
 
 // The fast path (consumer loop below) computes, per value, with biased taps
@@ -319,11 +348,22 @@ __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restri
   int stage = 0;
   uint32_t parity = 0;
 
-  // contiguous item range per CTA: consecutive bands of a tile stay on one SM,
-  // so per-tile geometry (and the consumers' column taps) are computed once
+  // contiguous range per CTA: consecutive bands of a tile stay on one SM, so per-tile
+  // geometry (and the consumers' column taps) are computed once.
+#if TP_K2_ROW_BALANCE
+  // The range is cut in output rows, not items: a CTA may start or end inside a band, so
+  // every CTA gets the same number of rows (+-1) whatever the band height (with whole
+  // items the last wave of a 2688-item launch left 10% of the SMs' time idle).
+  const int64_t vrows = items * band;
+  const int64_t v_begin = vrows * blockIdx.x / gridDim.x;
+  const int64_t v_end = vrows * (blockIdx.x + 1) / gridDim.x;
+  const int64_t it_begin = v_begin / band;
+  const int64_t it_end = (v_end + band - 1) / band;
+#else
   const int64_t per_cta = (items + gridDim.x - 1) / gridDim.x;
   const int64_t it_begin = min(items, static_cast<int64_t>(blockIdx.x) * per_cta);
   const int64_t it_end = min(items, it_begin + per_cta);
+#endif
   int cur_k = -1;
   const uint8_t* img = nullptr;
   int W = 1, H = 1;
@@ -337,9 +377,20 @@ __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restri
     const int nimg = __ldg(tile_off + kimg + 1) - __ldg(tile_off + kimg);
     const int r = static_cast<int>(item - static_cast<int64_t>(__ldg(tile_off + kimg)) * bands);
     const int g = __ldg(tile_off + kimg) + r % nimg;
+#if TP_K2_ROW_BALANCE
+    const int64_t vfirst = item * band;
+    const int64_t dlo = v_begin - vfirst, dhi = v_end - vfirst;
+    const int jlo = dlo > 0 ? static_cast<int>(dlo) : 0;
+    const int jhi = dhi < band ? static_cast<int>(dhi) : band;
+    const int j0 = (r / nimg) * band + jlo;
+    if (g >= cap_tiles) continue;  // caller's buffers end before this tile
+    const int nrows = min(jhi - jlo, E - j0);
+    if (nrows <= 0) continue;  // virtual rows past the end of a short last band
+#else
     const int j0 = (r / nimg) * band;
     if (g >= cap_tiles) continue;  // caller's buffers end before this tile
     const int nrows = min(band, E - j0);
+#endif
     if (kimg != cur_k) {  // new image: per-tile geometry, one lane per tile
       cur_k = kimg;
       W = __ldg(wh + 2 * kimg);
@@ -486,6 +537,9 @@ __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restri
     hdr.ph[stage].g = -1;
     mbar_arrive(&hdr.full[stage]);
   }
+#if TP_K2_PDL == 2
+  pdl_trigger();  // all of this CTA's copies are issued: let the next kernel be scheduled
+#endif
 }
 
 // ---------------------------------------------------------------------------
@@ -631,6 +685,33 @@ __device__ __forceinline__ void consume_pair_rows(
     if (worst < kAmbLimit) {  // recompute only the flagged values, exactly, in fp64
       const double fy64 = ldsd(pr.base + kPhFy64 + 8 * jj),
                    omfy64 = ldsd(pr.base + kPhOmfy64 + 8 * jj);
+#if TP_K2_BATCHED_FALLBACK
+      // Warp-cooperative: every lane with a flagged value recomputes one per pass (flags
+      // are rare, so one pass is the norm) instead of 2C divergent per-value branches.
+      uint32_t m = 0;
+#pragma unroll
+      for (int c = 0; c < C; ++c)
+        m |= (xa[c] < kAmbLimit ? 1u << c : 0u) | (xb[c] < kAmbLimit ? 1u << (C + c) : 0u);
+      while (m) {
+        const int idx = __ffs(m) - 1;
+        m &= m - 1;
+        const bool pb = idx >= C;
+        const int c = pb ? idx - C : idx;
+        const uint32_t g00 = pb ? b.r0w0 : a.r0w0, g01 = pb ? b.r0w1 : a.r0w1;
+        const uint32_t g10 = pb ? b.r1w0 : a.r1w0, g11 = pb ? b.r1w1 : a.r1w1;
+        const double fx64 = pb ? fxb64 : fxa64, omfx64 = pb ? omfxb64 : omfxa64;
+        const uint32_t k = kKrawBias + blend_exact_fast(byte_dyn(g00, g01, c),
+                                                        byte_dyn(g00, g01, C + c),
+                                                        byte_dyn(g10, g11, c),
+                                                        byte_dyn(g10, g11, C + c), fy64, omfy64,
+                                                        fx64, omfx64);
+#pragma unroll
+        for (int cc = 0; cc < C; ++cc) {
+          ka[cc] = idx == cc ? k : ka[cc];
+          kb[cc] = idx == C + cc ? k : kb[cc];
+        }
+      }
+#else
 #pragma unroll
       for (int c = 0; c < C; ++c) {
         if (xa[c] < kAmbLimit)
@@ -646,6 +727,7 @@ __device__ __forceinline__ void consume_pair_rows(
                                                byte_of(b.r1w0, b.r1w1, C + c), fy64, omfy64,
                                                fxb64, omfxb64);
       }
+#endif
     }
     const int64_t rowpix = static_cast<int64_t>(g) * EE + static_cast<int64_t>(j) * E;
     if (WRITE_U8) {
@@ -769,6 +851,9 @@ __global__ void __launch_bounds__(kMaxThreads, kCtasPerSm)
   OutT* s_lut = reinterpret_cast<OutT*>(smem + ((sizeof(SmemHeader) + 127) & ~size_t(127)));
   uint8_t* arena = smem + ((sizeof(SmemHeader) + 127) & ~size_t(127)) +
                    ((C * 256 * sizeof(OutT) + 127) & ~size_t(127));
+#if TP_K2_PDL == 1
+  pdl_trigger();
+#endif
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&hdr.full[s], 1);
@@ -776,6 +861,7 @@ __global__ void __launch_bounds__(kMaxThreads, kCtasPerSm)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  pdl_wait();  // K1 (plan, tile_off) and the LUT come from stream predecessors
   if (WRITE_OUT)
     for (int i = threadIdx.x; i < C * 256; i += blockDim.x) s_lut[i] = lut[i];
   __syncthreads();
@@ -823,9 +909,17 @@ int launch_variant(const uint8_t* src, const int64_t* src_off, const int32_t* wh
     cached_threads = threads;
   }
   const int grid = max(1, per_sm) * max(1, device_sm_count());
+#if TP_K2_PDL
+  const cudaError_t err =
+      launch_pdl(kern, dim3(grid), dim3(threads), smem, stream, src, src_off, wh, n, plan,
+                 tile_off, E, static_cast<const OutT*>(lut), static_cast<OutT*>(out), out_u8, cap);
+#else
   kern<<<grid, threads, smem, stream>>>(src, src_off, wh, n, plan, tile_off, E,
                                         static_cast<const OutT*>(lut), static_cast<OutT*>(out),
                                         out_u8, cap);
+  const cudaError_t err = cudaSuccess;
+#endif
+  if (err != cudaSuccess) return set_error(TP_ERR_CUDA, "tp_tile: %s", cudaGetErrorString(err));
   return check_launch("tp_tile(tma)");
 }
 
