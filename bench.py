@@ -39,7 +39,7 @@ UNIT = "images/s"
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=500)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--batch", type=int, default=64, help="images per GPU per step (C2: 64)")
@@ -102,47 +102,83 @@ class Dist:
 # clocks sampled during the timed region
 
 class ClockSampler:
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clock and throttle reasons sampled from a thread while the timed region runs.
+    In-process NVML (pynvml): no nvidia-smi fork inside the timed region, which used to
+    stall the launching thread for milliseconds.  Falls back to nvidia-smi."""
 
-    def __init__(self, gpu_index: int):
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))
+
+    def __init__(self, gpu_index: int, interval_s: float = 0.002):
         self.gpu = gpu_index
-        self.samples = []
+        self.interval = interval_s
+        self.samples = []  # (sm_mhz, max_mhz, [reason names])
         self._stop = threading.Event()
         self._thr = None
+        self._nvml = None
+        self._handle = None
+        try:
+            import pynvml
+            import torch
+
+            pynvml.nvmlInit()
+            handle = None
+            try:
+                prop = torch.cuda.get_device_properties(gpu_index)
+                bus = f"{prop.pci_domain_id:08x}:{prop.pci_bus_id:02x}:{prop.pci_device_id:02x}.0"
+                handle = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+            except Exception:
+                handle = pynvml.nvmlDeviceGetHandleByIndex(gpu_index)
+            self._nvml, self._handle = pynvml, handle
+        except Exception:
+            self._nvml = None
+
+    def _sample_nvml(self):
+        nv, h = self._nvml, self._handle
+        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        mask = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        names = [n for n, attr in self.REASONS if mask & getattr(nv, attr)]
+        self.samples.append((float(sm), float(mx), names))
+
+    def _sample_smi(self):
+        fields = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                  "clocks_event_reasons.hw_thermal_slowdown,"
+                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        out = subprocess.run(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={fields}",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                             timeout=5)
+        if out.returncode == 0 and out.stdout.strip():
+            v = [x.strip() for x in out.stdout.strip().split(",")]
+            names = [n for (n, _), x in zip(self.REASONS, v[2:]) if x.lower() == "active"]
+            self.samples.append((float(v[0]), float(v[1]), names))
 
     def start(self):
         self._thr = threading.Thread(target=self._run, daemon=True)
         self._thr.start()
 
     def _run(self):
-        while not self._stop.is_set():
+        while True:
             try:
-                out = subprocess.run(
-                    ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
-                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                if out.returncode == 0 and out.stdout.strip():
-                    self.samples.append([v.strip() for v in out.stdout.strip().split(",")])
+                self._sample_nvml() if self._nvml else self._sample_smi()
             except Exception:
                 pass
-            self._stop.wait(0.1)
+            if self._stop.wait(self.interval if self._nvml else 0.1):
+                break
 
     def stop(self) -> dict:
         self._stop.set()
         if self._thr:
             self._thr.join(timeout=10)
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"],
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clocks unavailable"],
                     "samples": 0}
-        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4)
-                          if len(s) > 5 + i and s[5 + i].lower() == "active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.samples)}
+        return {"sm_mhz": float(np.median([x[0] for x in self.samples])),
+                "sm_max_mhz": max(x[1] for x in self.samples),
+                "reasons": sorted({r for x in self.samples for r in x[2]}),
+                "samples": len(self.samples), "source": "nvml" if self._nvml else "nvidia-smi"}
 
 
 # ---------------------------------------------------------------------------

@@ -31,7 +31,7 @@ namespace {
 
 // tuning knobs (overridable with -D for sweeps; defaults are the measured best)
 #ifndef TP_K2_BAND
-#define TP_K2_BAND 32
+#define TP_K2_BAND 16
 #endif
 #ifndef TP_K2_STAGES
 #define TP_K2_STAGES 2
@@ -41,6 +41,10 @@ namespace {
 #endif
 #ifndef TP_K2_PDL  // 0: plain launch; 1: PDL, successor released at start; 2: at the end
 #define TP_K2_PDL 2
+#endif
+#ifndef TP_K2_L2  // 0: no hints; 1: streaming output stores; 2: + thumbnail reads evict_first;
+                   // 3: + tile reads evict_last
+#define TP_K2_L2 2
 #endif
 #ifndef TP_K2_ROW_BALANCE
 #define TP_K2_ROW_BALANCE 1
@@ -141,12 +145,38 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t pari
 }
 
 __device__ __forceinline__ void tma_row(void* dst, const void* src, uint32_t bytes,
-                                        unsigned long long* bar) {
+                                        unsigned long long* bar, uint64_t policy) {
+#if TP_K2_L2 >= 2
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+#else
+  (void)policy;
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
           "r"(smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+#endif
+}
+
+// L2 priorities.  A source row is read twice when an image has tiles and a thumbnail
+// (first by the tiles, then by the thumbnail of the same band): the tiles' reads are
+// kept (evict_last), the thumbnail's are the last use (evict_first), and the output
+// is written with streaming stores so it does not push the sources out of L2.
+__device__ __forceinline__ uint64_t l2_policy(bool last_use) {
+  uint64_t p;
+  if (last_use)
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  else
+#if TP_K2_L2 >= 3
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+#else
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+#endif
+  return p;
 }
 
 __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
@@ -369,14 +399,22 @@ __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restri
   int W = 1, H = 1;
   int64_t stride = 0;
   uintptr_t img_end = 0;
+  // image of the current item: one binary search for the first item, then a forward walk
+  // (the range is contiguous), so no chain of dependent global loads per item
+  int kimg = it_begin < it_end ? find_item_image(tile_off, n, it_begin, bands) : 0;
+  int toff0 = __ldg(tile_off + kimg), toff1 = __ldg(tile_off + kimg + 1);
   for (int64_t item = it_begin; item < it_end; ++item) {
     // item order: (image, band, tile): the tiles and the thumbnail of an image read
     // the same source rows within n_images consecutive items, so the second read
     // hits L2 instead of HBM
-    const int kimg = find_item_image(tile_off, n, item, bands);
-    const int nimg = __ldg(tile_off + kimg + 1) - __ldg(tile_off + kimg);
-    const int r = static_cast<int>(item - static_cast<int64_t>(__ldg(tile_off + kimg)) * bands);
-    const int g = __ldg(tile_off + kimg) + r % nimg;
+    while (static_cast<int64_t>(toff1) * bands <= item) {
+      ++kimg;
+      toff0 = toff1;
+      toff1 = __ldg(tile_off + kimg + 1);
+    }
+    const int nimg = toff1 - toff0;
+    const int r = static_cast<int>(item - static_cast<int64_t>(toff0) * bands);
+    const int g = toff0 + r % nimg;
 #if TP_K2_ROW_BALANCE
     const int64_t vfirst = item * band;
     const int64_t dlo = v_begin - vfirst, dhi = v_end - vfirst;
@@ -403,11 +441,12 @@ __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restri
         __syncwarp();
       }
     }
-    const int t = g - __ldg(tile_off + kimg);
+    const int t = g - toff0;
     const TileGeo geo = nimg <= kTileCache ? hdr.tg[t] : tile_geometry<C>(plan, kimg, t, W, H, E);
     const int RW = geo.RW, RH = geo.RH, oy0 = geo.oy0, ox0 = geo.ox0, cwid = geo.cwid;
     const bool contig = RH > H;
     const double sy = geo.sy, sx = geo.sx;
+    const uint64_t policy = l2_policy(t == nimg - 1);  // thumbnail (or only tile): last read
     // lane j owns output row j0 + j of the band
     int my_y0 = 0, my_y1 = 0;
     float my_fy = 0.f;
@@ -523,7 +562,7 @@ __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restri
         __syncwarp();
         if (bytes > 0)
           tma_row(base + (incl - region), reinterpret_cast<const void*>(start), bytes,
-                  &hdr.full[s]);
+                  &hdr.full[s], policy);
         jj += nr;
         if (++stage == kStages) {
           stage = 0;
@@ -561,7 +600,11 @@ struct LutLoad<__nv_bfloat16> {
     *reinterpret_cast<uint32_t*>(dst) = __byte_perm(a, b, 0x5410);
   }
   static __device__ __forceinline__ void store_one(__nv_bfloat16* dst, uint32_t a) {
+#if TP_K2_L2 >= 1
+    __stcs(reinterpret_cast<unsigned short*>(dst), static_cast<unsigned short>(a));
+#else
     *reinterpret_cast<unsigned short*>(dst) = static_cast<unsigned short>(a);
+#endif
   }
 };
 template <>
@@ -572,7 +615,11 @@ struct LutLoad<float> {
     *reinterpret_cast<uint2*>(dst) = make_uint2(a, b);
   }
   static __device__ __forceinline__ void store_one(float* dst, uint32_t a) {
+#if TP_K2_L2 >= 1
+    __stcs(reinterpret_cast<unsigned int*>(dst), a);
+#else
     *reinterpret_cast<uint32_t*>(dst) = a;
+#endif
   }
 };
 
