@@ -92,6 +92,20 @@ TP_API int tp_plan(const int32_t* d_wh, int32_t n, int32_t tile_edge, int32_t ma
 TP_API int tp_build_lut(int32_t channels, const float* mean, const float* std, int32_t dtype,
                  void* d_lut, void* stream);
 
+/* K0 with the affine form: the same table, followed by per-channel fp32 constants
+ * (a[c], b[c]) such that  fma((float)v, a[c], b[c])  rounds (bf16 RNE, or fp32 as is)
+ * to exactly lut[c][v] for all 256 values v.  The constants are searched and verified
+ * exhaustively on the host (IEEE fp32, the same arithmetic as the device table);
+ * *affine_ok (host, nullable) says whether such constants were found.  With the
+ * flag TP_TILE_NORM_AFFINE, tp_tile_ex normalizes with one fma per value instead
+ * of a table lookup -- identical results, no shared-memory gather.
+ *   d_lut  tp_lut_bytes(channels, dtype) bytes: [channels][256] table, then at byte
+ *          offset tp_lut_table_bytes(channels, dtype): float a[4], float b[4] */
+TP_API int64_t tp_lut_table_bytes(int32_t channels, int32_t dtype);
+TP_API int64_t tp_lut_bytes(int32_t channels, int32_t dtype);
+TP_API int tp_build_norm(int32_t channels, const float* mean, const float* std, int32_t dtype,
+                         void* d_lut, int32_t* affine_ok, void* stream);
+
 /* K2 — fused resample + crop + thumbnail + normalize + layout/cast.
  * Replaces tile_image/_tile_fused (imgproc.py:373-412, :449-465) followed by
  * normalize_tiles (imgproc.py:496-513), for a batch of images.
@@ -120,6 +134,9 @@ TP_API int tp_tile(const uint8_t* d_src, const int64_t* d_src_off, const int32_t
 #define TP_TILE_ALGO_AUTO 0
 #define TP_TILE_ALGO_FAST 1
 #define TP_TILE_ALGO_EXACT 2
+/* or-ed into algo: d_lut comes from tp_build_norm with *affine_ok == 1 (fast path,
+ * normalized outputs without uint8 tiles) */
+#define TP_TILE_NORM_AFFINE 256
 TP_API int tp_tile_ex(const uint8_t* d_src, const int64_t* d_src_off, const int32_t* d_wh,
                       int32_t n, int32_t channels, const int32_t* d_plan,
                       const int32_t* d_tile_off, int32_t tile_edge, const void* d_lut,

@@ -36,6 +36,7 @@ TP_EXPAND_ERR_OVERFLOW = 4
 TP_TILE_ALGO_AUTO = 0
 TP_TILE_ALGO_FAST = 1
 TP_TILE_ALGO_EXACT = 2
+TP_TILE_NORM_AFFINE = 256
 
 TP_PLAN_FIELDS = 6
 TP_MAX_EDGE = 65536
@@ -51,6 +52,10 @@ SIGNATURES = {
     "tp_plan": (c_int32, [c_void_p, c_int32, c_int32, c_int32, c_void_p, c_void_p, c_void_p,
                           c_void_p]),
     "tp_build_lut": (c_int32, [c_int32, _f32p, _f32p, c_int32, c_void_p, c_void_p]),
+    "tp_lut_table_bytes": (c_int64, [c_int32, c_int32]),
+    "tp_lut_bytes": (c_int64, [c_int32, c_int32]),
+    "tp_build_norm": (c_int32, [c_int32, _f32p, _f32p, c_int32, c_void_p, POINTER(c_int32),
+                                c_void_p]),
     "tp_tile": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_void_p,
                           c_int32, c_void_p, c_int32, c_int32, c_void_p, c_void_p, c_int64,
                           c_void_p]),

@@ -1,8 +1,10 @@
 // K0 (normalize LUT), K4 (LUT normalize of uint8 pixels), synthetic inputs,
 // and the C-ABI error plumbing.
 
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstring>
 
 #include "tp_common.cuh"
 
@@ -163,10 +165,95 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// the affine block after the table (tp_build_norm)
+__global__ void k_write_affine(float* blk, float a0, float a1, float a2, float b0, float b1,
+                               float b2) {
+  if (threadIdx.x == 0) {
+    blk[0] = a0; blk[1] = a1; blk[2] = a2; blk[3] = 0.f;
+    blk[4] = b0; blk[5] = b1; blk[6] = b2; blk[7] = 0.f;
+  }
+}
+
+// Host restatement of k_build_lut's value (IEEE fp32 on SSE: correctly rounded divide
+// and subtract, no contraction) and of the device's fp32 -> bf16 round-to-nearest-even.
+float host_lut_value(int v, float m, float s) {
+  volatile float q = static_cast<float>(v) / 255.0f;
+  volatile float d = q - m;
+  return d / s;
+}
+uint32_t host_bits(float f) {
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  return u;
+}
+uint32_t host_bf16(float f) {
+  const uint32_t u = host_bits(f);
+  return (u + 0x7FFFu + ((u >> 16) & 1u)) >> 16;  // values are finite
+}
+
+// fp32 (a, b) with round(fma(v, a, b)) == table[v] for all 256 v (round = bf16 RNE, or
+// the identity for fp32 output), searched around 1/(255 s), -m/s; false if none.
+bool find_affine(float m, float s, int dtype, float* a_out, float* b_out) {
+  float ref[256];
+  for (int v = 0; v < 256; ++v) ref[v] = host_lut_value(v, m, s);
+  const float a0 = static_cast<float>(1.0 / (255.0 * static_cast<double>(s)));
+  const float b0 = static_cast<float>(-static_cast<double>(m) / static_cast<double>(s));
+  auto step = [](float x, int k) {
+    for (; k > 0; --k) x = std::nextafterf(x, INFINITY);
+    for (; k < 0; ++k) x = std::nextafterf(x, -INFINITY);
+    return x;
+  };
+  constexpr int kRadius = 8;
+  for (int r = 0; r <= kRadius; ++r) {
+    for (int da = -r; da <= r; ++da) {
+      for (int db = -r; db <= r; ++db) {
+        if (std::max(std::abs(da), std::abs(db)) != r) continue;  // ring r only
+        const float a = step(a0, da), b = step(b0, db);
+        bool ok = true;
+        for (int v = 0; v < 256 && ok; ++v) {
+          const float y = std::fmaf(static_cast<float>(v), a, b);
+          ok = dtype == TP_DTYPE_BF16 ? host_bf16(y) == host_bf16(ref[v])
+                                      : host_bits(y) == host_bits(ref[v]);
+        }
+        if (ok) {
+          *a_out = a;
+          *b_out = b;
+          return true;
+        }
+      }
+    }
+  }
+  return false;
+}
+
 }  // namespace
 }  // namespace tp
 
 extern "C" int tp_abi_version(void) { return TP_ABI_VERSION; }
+
+extern "C" int64_t tp_lut_table_bytes(int32_t channels, int32_t dtype) {
+  const int64_t e = dtype == TP_DTYPE_F32 ? 4 : 2;
+  return (static_cast<int64_t>(channels) * 256 * e + 15) & ~int64_t(15);
+}
+
+extern "C" int64_t tp_lut_bytes(int32_t channels, int32_t dtype) {
+  return tp_lut_table_bytes(channels, dtype) + 8 * static_cast<int64_t>(sizeof(float));
+}
+
+extern "C" int tp_build_norm(int32_t channels, const float* mean, const float* std,
+                             int32_t dtype, void* d_lut, int32_t* affine_ok, void* stream) {
+  const int rc = tp_build_lut(channels, mean, std, dtype, d_lut, stream);
+  if (rc != TP_OK) return rc;
+  float a[3] = {0.f, 0.f, 0.f}, b[3] = {0.f, 0.f, 0.f};
+  bool ok = true;
+  for (int c = 0; c < channels && ok; ++c) ok = tp::find_affine(mean[c], std[c], dtype, &a[c], &b[c]);
+  if (!ok) a[0] = a[1] = a[2] = b[0] = b[1] = b[2] = 0.f;
+  float* blk = reinterpret_cast<float*>(static_cast<char*>(d_lut) +
+                                        tp_lut_table_bytes(channels, dtype));
+  tp::k_write_affine<<<1, 32, 0, tp::as_stream(stream)>>>(blk, a[0], a[1], a[2], b[0], b[1], b[2]);
+  if (affine_ok) *affine_ok = ok ? 1 : 0;
+  return tp::check_launch("tp_build_norm");
+}
 
 extern "C" const char* tp_last_error(void) { return tp::g_error; }
 

@@ -172,7 +172,7 @@ int launch_tile(const uint8_t* src, const int64_t* src_off, const int32_t* wh, i
                 uint8_t* out_u8, int64_t cap, int algo, cudaStream_t stream) {
   const int sms = max(1, device_sm_count());
   int per_sm = 0;
-  if (algo == TP_TILE_ALGO_EXACT) {
+  if ((algo & 0xFF) == TP_TILE_ALGO_EXACT) {
     auto kern = k_tile_exact<C, OutT, LAYOUT, WRITE_OUT>;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, 0);
     kern<<<max(1, per_sm) * sms, kThreads, 0, stream>>>(
@@ -181,7 +181,8 @@ int launch_tile(const uint8_t* src, const int64_t* src_off, const int32_t* wh, i
     return check_launch("tp_tile(exact)");
   }
   return launch_tile_tma<C, OutT, LAYOUT, WRITE_OUT>(src, src_off, wh, n, plan, tile_off, E, lut,
-                                                     out, out_u8, cap, stream);
+                                                     out, out_u8, cap,
+                                                     (algo & TP_TILE_NORM_AFFINE) != 0, stream);
 }
 
 template <int C>
@@ -223,7 +224,10 @@ extern "C" int tp_tile_ex(const uint8_t* d_src, const int64_t* d_src_off, const 
                           const int32_t* d_tile_off, int32_t tile_edge, const void* d_lut,
                           int32_t dtype, int32_t layout, void* d_out, uint8_t* d_out_u8,
                           int64_t out_capacity, int32_t algo, void* stream) {
-  if (algo != TP_TILE_ALGO_AUTO && algo != TP_TILE_ALGO_FAST && algo != TP_TILE_ALGO_EXACT)
+  const int base_algo = algo & 0xFF;
+  if ((base_algo != TP_TILE_ALGO_AUTO && base_algo != TP_TILE_ALGO_FAST &&
+       base_algo != TP_TILE_ALGO_EXACT) ||
+      (algo & ~(0xFF | TP_TILE_NORM_AFFINE)) != 0)
     return tp::set_error(TP_ERR_INVALID_ARGUMENT, "bad algo %d", algo);
   if (n < 0) return tp::set_error(TP_ERR_INVALID_ARGUMENT, "tp_tile: n must be >= 0");
   if (channels != 1 && channels != 3)

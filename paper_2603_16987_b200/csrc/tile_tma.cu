@@ -46,6 +46,15 @@ namespace {
                    // 3: + tile reads evict_last
 #define TP_K2_L2 2
 #endif
+#ifndef TP_K2_DEBUG_NOCONSUME
+#define TP_K2_DEBUG_NOCONSUME 0
+#endif
+#ifndef TP_K2_DEBUG_NOLOAD
+#define TP_K2_DEBUG_NOLOAD 0
+#endif
+#ifndef TP_K2_PAIR  // consumer rows in pairs (one basic block) instead of a row pipeline
+#define TP_K2_PAIR 0
+#endif
 #ifndef TP_K2_ROW_BALANCE
 #define TP_K2_ROW_BALANCE 1
 #endif
@@ -208,6 +217,11 @@ __device__ __forceinline__ void upk(f32x2 r, uint32_t& lo, uint32_t& hi) {
 __device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
   f32x2 d;
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ f32x2 add2(f32x2 a, f32x2 b) {
+  f32x2 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
   return d;
 }
 __device__ __forceinline__ f32x2 sub2(f32x2 a, f32x2 b) {
@@ -541,6 +555,9 @@ __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restri
             dst[b] = reinterpret_cast<const uint8_t*>(start)[b];
           bytes = body;
         }
+#if TP_K2_DEBUG_NOLOAD  // timing experiment only: consumers on whatever the stage holds
+        bytes = 0;
+#endif
         int tx = static_cast<int>(bytes);
 #pragma unroll
         for (int d = 16; d > 0; d >>= 1) tx += __shfl_xor_sync(0xffffffffu, tx, d);
@@ -680,17 +697,23 @@ __device__ __forceinline__ PixTaps fetch_pix(const PhaseRows& pr, int jj, uint32
 // consecutive pixels, which halves shared-memory bank conflicts versus adjacent
 // pairs), all output rows of the phase, all channels.  Math is packed f32x2
 // (lane 0: pixel a, lane 1: pixel b).
-template <int C, typename OutT, int LAYOUT, bool WRITE_OUT, bool WRITE_U8, bool UNIFORM>
+template <int C, typename OutT, int LAYOUT, bool WRITE_OUT, bool WRITE_U8, bool AFFINE,
+          bool UNIFORM>
 __device__ __forceinline__ void consume_pair_rows(
     const PhaseRows& pr, int g, int j0, int nrows, int mis_in, uint32_t sbase, uint32_t lut_u32,
     int ia, int ib, bool has_a, bool has_b, int xoa, int xob, float fxa, float fxb, double fxa64,
     double omfxa64, double fxb64, double omfxb64, int E, OutT* __restrict__ out,
-    uint8_t* __restrict__ out_u8, OutT* __restrict__ tile_a) {
+    uint8_t* __restrict__ out_u8, OutT* __restrict__ tile_a, const float (&aff_a)[C],
+    const float (&aff_b)[C]) {
   const int64_t EE = static_cast<int64_t>(E) * E;
   const f32x2 FX = pk(fxa, fxb);
-  const f32x2 KH = pk(8388607.5f, 8388607.5f);  // 2^23 - 0.5: biased byte -> byte + 0.5
+  const f32x2 KH = pk(8388608.0f, 8388608.0f);  // 2^23: biased byte -> byte
   const f32x2 S13 = pk(8192.0f, 8192.0f);
-  const f32x2 MAG = pk(12582912.0f, 12582912.0f);  // 1.5 * 2^23
+  const f32x2 MAG = pk(12587008.0f, 12587008.0f);  // 1.5 * 2^23 + 4096 (= the + 0.5)
+  const f32x2 MAGR = pk(12582912.0f, 12582912.0f);  // 1.5 * 2^23: round to integer
+  // affine normalize (TP_TILE_NORM_AFFINE): y = fma(k, a_c, b_c), verified at build time to
+  // round to the table entry for every k; only without uint8 tiles (those need k itself)
+  constexpr bool AFF = AFFINE && WRITE_OUT && !WRITE_U8;
   // uniform misalignment: word offsets and shift amounts are per-pixel constants
   const int mis = UNIFORM ? mis_in : 0;
   const uint32_t wa = static_cast<uint32_t>((mis + xoa) & ~3), wb = static_cast<uint32_t>((mis + xob) & ~3);
@@ -705,11 +728,11 @@ __device__ __forceinline__ void consume_pair_rows(
   for (int c = 1; c < C; ++c) oc[c] = oc[c - 1] + EE;
   const int ob_off = ib - ia;
   // one output row: taps (a, b) already fetched
-  auto row = [&](int jj, const PixTaps& a, const PixTaps& b) {
-    const int j = j0 + jj;
+  // fp32 fast path of output row jj: LUT codes (kKrawBias + value) and window flags
+  auto fast = [&](int jj, const PixTaps& a, const PixTaps& b, uint32_t (&ka)[C],
+                  uint32_t (&kb)[C], uint32_t (&xa)[C], uint32_t (&xb)[C]) -> uint32_t {
     const float fy = ldsf(pr.base + kPhFy + 4 * jj);
     const f32x2 FY = pk(fy, fy);
-    uint32_t ka[C], kb[C], xa[C], xb[C];
     uint32_t worst = 0xFFFFFFFFu;
 #pragma unroll
     for (int c = 0; c < C; ++c) {
@@ -718,18 +741,26 @@ __device__ __forceinline__ void consume_pair_rows(
       const f32x2 B = pk(biased_byte(a.r1w0, a.r1w1, c), biased_byte(b.r1w0, b.r1w1, c));
       const f32x2 Cc = pk(biased_byte(a.r0w0, a.r0w1, C + c), biased_byte(b.r0w0, b.r0w1, C + c));
       const f32x2 D = pk(biased_byte(a.r1w0, a.r1w1, C + c), biased_byte(b.r1w0, b.r1w1, C + c));
-      const f32x2 L = fma2(FY, sub2(B, A), sub2(A, KH));   // a + 0.5 + fy (b - a)
-      const f32x2 R = fma2(FY, sub2(D, Cc), sub2(Cc, KH));  // c + 0.5 + fy (d - c)
-      const f32x2 T = fma2(FX, sub2(R, L), L);              // ~ v + 0.5
+      const f32x2 L = fma2(FY, sub2(B, A), sub2(A, KH));   // a + fy (b - a)
+      const f32x2 R = fma2(FY, sub2(D, Cc), sub2(Cc, KH));  // c + fy (d - c)
+      const f32x2 T = fma2(FX, sub2(R, L), L);              // ~ v
       uint32_t na, nb;
-      upk(fma2(T, S13, MAG), na, nb);  // bits of 1.5*2^23 + round(8192 t)
-      ka[c] = __umulhi(na, 1u << 19);  // na >> 13 on the FMA pipe
-      kb[c] = __umulhi(nb, 1u << 19);
+      upk(fma2(T, S13, MAG), na, nb);  // bits of 1.5*2^23 + round(8192 (t + 0.5))
+      if (AFF) {
+        upk(add2(T, MAGR), ka[c], kb[c]);  // 1.5*2^23 + round(v): the exact value's float
+      } else {
+        ka[c] = __umulhi(na, 1u << 19);  // na >> 13 on the FMA pipe
+        kb[c] = __umulhi(nb, 1u << 19);
+      }
       xa[c] = na * (1u << 19) + (1u << 19);
       xb[c] = nb * (1u << 19) + (1u << 19);
       worst = min(worst, min(xa[c], xb[c]));
     }
-    if (worst < kAmbLimit) {  // recompute only the flagged values, exactly, in fp64
+    return worst;
+  };
+  // exact fp64 recomputation of the flagged values of row jj
+  auto fix = [&](int jj, const PixTaps& a, const PixTaps& b, uint32_t (&ka)[C],
+                 uint32_t (&kb)[C], const uint32_t (&xa)[C], const uint32_t (&xb)[C]) {
       const double fy64 = ldsd(pr.base + kPhFy64 + 8 * jj),
                    omfy64 = ldsd(pr.base + kPhOmfy64 + 8 * jj);
 #if TP_K2_BATCHED_FALLBACK
@@ -747,7 +778,7 @@ __device__ __forceinline__ void consume_pair_rows(
         const uint32_t g00 = pb ? b.r0w0 : a.r0w0, g01 = pb ? b.r0w1 : a.r0w1;
         const uint32_t g10 = pb ? b.r1w0 : a.r1w0, g11 = pb ? b.r1w1 : a.r1w1;
         const double fx64 = pb ? fxb64 : fxa64, omfx64 = pb ? omfxb64 : omfxa64;
-        const uint32_t k = kKrawBias + blend_exact_fast(byte_dyn(g00, g01, c),
+        const uint32_t k = (AFF ? 0x4B400000u : kKrawBias) + blend_exact_fast(byte_dyn(g00, g01, c),
                                                         byte_dyn(g00, g01, C + c),
                                                         byte_dyn(g10, g11, c),
                                                         byte_dyn(g10, g11, C + c), fy64, omfy64,
@@ -762,20 +793,23 @@ __device__ __forceinline__ void consume_pair_rows(
 #pragma unroll
       for (int c = 0; c < C; ++c) {
         if (xa[c] < kAmbLimit)
-          ka[c] = kKrawBias + blend_exact_fast(byte_of(a.r0w0, a.r0w1, c),
+          ka[c] = (AFF ? 0x4B400000u : kKrawBias) + blend_exact_fast(byte_of(a.r0w0, a.r0w1, c),
                                                byte_of(a.r0w0, a.r0w1, C + c),
                                                byte_of(a.r1w0, a.r1w1, c),
                                                byte_of(a.r1w0, a.r1w1, C + c), fy64, omfy64,
                                                fxa64, omfxa64);
         if (xb[c] < kAmbLimit)
-          kb[c] = kKrawBias + blend_exact_fast(byte_of(b.r0w0, b.r0w1, c),
+          kb[c] = (AFF ? 0x4B400000u : kKrawBias) + blend_exact_fast(byte_of(b.r0w0, b.r0w1, c),
                                                byte_of(b.r0w0, b.r0w1, C + c),
                                                byte_of(b.r1w0, b.r1w1, c),
                                                byte_of(b.r1w0, b.r1w1, C + c), fy64, omfy64,
                                                fxb64, omfxb64);
       }
 #endif
-    }
+      };
+  // LUT + stores of row jj (rows in order: the NCHW row pointers advance by one row)
+  auto emit = [&](int jj, const uint32_t (&ka)[C], const uint32_t (&kb)[C]) {
+    const int j = j0 + jj;
     const int64_t rowpix = static_cast<int64_t>(g) * EE + static_cast<int64_t>(j) * E;
     if (WRITE_U8) {
       uint8_t* ua = out_u8 + (rowpix + ia) * C;
@@ -786,7 +820,28 @@ __device__ __forceinline__ void consume_pair_rows(
         if (has_b) ub[c] = static_cast<uint8_t>(kb[c] - kKrawBias);
       }
     }
-    if (WRITE_OUT) {
+    if (AFF) {
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const f32x2 KF = sub2(pk(__uint_as_float(ka[c]), __uint_as_float(kb[c])), MAGR);
+        uint32_t va, vb;
+        upk(fma2(KF, pk(aff_a[c], aff_a[c]), pk(aff_b[c], aff_b[c])), va, vb);
+        if (sizeof(OutT) == 2) {  // fp32 -> bf16 RNE, both pixels in one conversion
+          const __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(va), __uint_as_float(vb));
+          const uint32_t hb = *reinterpret_cast<const uint32_t*>(&h);
+          va = hb & 0xFFFFu;
+          vb = hb >> 16;
+        }
+        if (LAYOUT == TP_LAYOUT_NCHW) {
+          if (has_a) LutLoad<OutT>::store_one(oc[c], va);
+          if (has_b) LutLoad<OutT>::store_one(oc[c] + ob_off, vb);
+          oc[c] += E;
+        } else {
+          if (has_a) LutLoad<OutT>::store_one(out + (rowpix + ia) * C + c, va);
+          if (has_b) LutLoad<OutT>::store_one(out + (rowpix + ib) * C + c, vb);
+        }
+      }
+    } else if (WRITE_OUT) {
 #pragma unroll
       for (int c = 0; c < C; ++c) {
         const uint32_t va = LutLoad<OutT>::load(lut0 + ka[c] * SZ + c * 256 * SZ);
@@ -802,6 +857,36 @@ __device__ __forceinline__ void consume_pair_rows(
       }
     }
   };
+  auto row = [&](int jj, const PixTaps& a, const PixTaps& b) {
+    uint32_t ka[C], kb[C], xa[C], xb[C];
+    if (fast(jj, a, b, ka, kb, xa, xb) < kAmbLimit) fix(jj, a, b, ka, kb, xa, xb);
+    emit(jj, ka, kb);
+  };
+#if TP_K2_PAIR
+  // rows in pairs: one basic block computes both rows (one window branch per pair), so
+  // the scheduler can overlap one row's LUT loads and stores with the other's math
+  int jj = 0;
+  for (; jj + 1 < nrows; jj += 2) {
+    const PixTaps a0 = fetch_pix<UNIFORM>(pr, jj, sbase, mis, xoa, wa, sha);
+    const PixTaps b0 = fetch_pix<UNIFORM>(pr, jj, sbase, mis, xob, wb, shb);
+    const PixTaps a1 = fetch_pix<UNIFORM>(pr, jj + 1, sbase, mis, xoa, wa, sha);
+    const PixTaps b1 = fetch_pix<UNIFORM>(pr, jj + 1, sbase, mis, xob, wb, shb);
+    uint32_t ka0[C], kb0[C], xa0[C], xb0[C], ka1[C], kb1[C], xa1[C], xb1[C];
+    const uint32_t w0 = fast(jj, a0, b0, ka0, kb0, xa0, xb0);
+    const uint32_t w1 = fast(jj + 1, a1, b1, ka1, kb1, xa1, xb1);
+    if (min(w0, w1) < kAmbLimit) {
+      if (w0 < kAmbLimit) fix(jj, a0, b0, ka0, kb0, xa0, xb0);
+      if (w1 < kAmbLimit) fix(jj + 1, a1, b1, ka1, kb1, xa1, xb1);
+    }
+    emit(jj, ka0, kb0);
+    emit(jj + 1, ka1, kb1);
+  }
+  if (jj < nrows) {
+    const PixTaps a0 = fetch_pix<UNIFORM>(pr, jj, sbase, mis, xoa, wa, sha);
+    const PixTaps b0 = fetch_pix<UNIFORM>(pr, jj, sbase, mis, xob, wb, shb);
+    row(jj, a0, b0);
+  }
+#else
   // software pipeline, unrolled by two so the prefetched taps need no register moves
   PixTaps a0 = fetch_pix<UNIFORM>(pr, 0, sbase, mis, xoa, wa, sha);
   PixTaps b0 = fetch_pix<UNIFORM>(pr, 0, sbase, mis, xob, wb, shb);
@@ -817,11 +902,13 @@ __device__ __forceinline__ void consume_pair_rows(
     row(jj + 1, a1, b1);
   }
   if (jj < nrows) row(jj, a0, b0);
+#endif
 }
 
-template <int C, typename OutT, int LAYOUT, bool WRITE_OUT, bool WRITE_U8>
+template <int C, typename OutT, int LAYOUT, bool WRITE_OUT, bool WRITE_U8, bool AFFINE>
 __device__ void consume(SmemHeader& hdr, const uint8_t* arena, const OutT* s_lut, int E,
-                        OutT* __restrict__ out, uint8_t* __restrict__ out_u8) {
+                        OutT* __restrict__ out, uint8_t* __restrict__ out_u8,
+                        const float* __restrict__ aff) {
   const int ctid = threadIdx.x - 32;
   const int ncons = blockDim.x - 32;
   const int lane = ctid & 31, cwarp = ctid >> 5;
@@ -836,6 +923,12 @@ __device__ void consume(SmemHeader& hdr, const uint8_t* arena, const OutT* s_lut
   double fxa64 = 0.0, omfxa64 = 1.0, fxb64 = 0.0, omfxb64 = 1.0;
   const int64_t EE = static_cast<int64_t>(E) * E;
   OutT* tile_a = out;
+  float aff_a[C], aff_b[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    aff_a[c] = AFFINE ? __ldg(aff + c) : 0.f;
+    aff_b[c] = AFFINE ? __ldg(aff + 4 + c) : 0.f;
+  }
   const uint32_t ph0 = smem_u32(&hdr.ph[0]);
   while (true) {
     mbar_wait(&hdr.full[stage], parity);
@@ -848,6 +941,16 @@ __device__ void consume(SmemHeader& hdr, const uint8_t* arena, const OutT* s_lut
     const int c0 = h1.x, cw = h1.y, xlo = h1.z, W = h1.w;
     const int segs = (cw + 63) >> 6;  // 64-pixel segments, one per consumer warp
     const uint32_t sbase = arena_u32 + stage * kArena;
+#if TP_K2_DEBUG_NOCONSUME  // timing experiment only: producer + TMA pipeline alone
+    if (segs > 0) {
+      mbar_arrive(&hdr.empty[stage]);
+      if (++stage == kStages) {
+        stage = 0;
+        parity ^= 1u;
+      }
+      continue;
+    }
+#endif
     for (int q = cwarp; q < segs; q += ncons >> 5) {
       const int la = 64 * q + lane, lb = la + 32;  // chunk-relative pixels
       const bool has_a = la < cw, has_b = lb < cw;
@@ -871,13 +974,13 @@ __device__ void consume(SmemHeader& hdr, const uint8_t* arena, const OutT* s_lut
         cache_q = q;
       }
       if (mis >= 0)
-        consume_pair_rows<C, OutT, LAYOUT, WRITE_OUT, WRITE_U8, true>(
+        consume_pair_rows<C, OutT, LAYOUT, WRITE_OUT, WRITE_U8, AFFINE, true>(
             pr, g, j0, nrows, mis, sbase, lut_u32, ia, ib, has_a, has_b, xoa, xob, fxa, fxb,
-            fxa64, omfxa64, fxb64, omfxb64, E, out, out_u8, tile_a);
+            fxa64, omfxa64, fxb64, omfxb64, E, out, out_u8, tile_a, aff_a, aff_b);
       else
-        consume_pair_rows<C, OutT, LAYOUT, WRITE_OUT, WRITE_U8, false>(
+        consume_pair_rows<C, OutT, LAYOUT, WRITE_OUT, WRITE_U8, AFFINE, false>(
             pr, g, j0, nrows, mis, sbase, lut_u32, ia, ib, has_a, has_b, xoa, xob, fxa, fxb,
-            fxa64, omfxa64, fxb64, omfxb64, E, out, out_u8, tile_a);
+            fxa64, omfxa64, fxb64, omfxb64, E, out, out_u8, tile_a, aff_a, aff_b);
     }
     mbar_arrive(&hdr.empty[stage]);
     if (++stage == kStages) {
@@ -887,12 +990,13 @@ __device__ void consume(SmemHeader& hdr, const uint8_t* arena, const OutT* s_lut
   }
 }
 
-template <int C, typename OutT, int LAYOUT, bool WRITE_OUT, bool WRITE_U8>
+template <int C, typename OutT, int LAYOUT, bool WRITE_OUT, bool WRITE_U8, bool AFFINE>
 __global__ void __launch_bounds__(kMaxThreads, kCtasPerSm)
     k_tile_tma(const uint8_t* __restrict__ src, const int64_t* __restrict__ src_off,
                const int32_t* __restrict__ wh, int n, const int32_t* __restrict__ plan,
                const int32_t* __restrict__ tile_off, int E, const OutT* __restrict__ lut,
-               OutT* __restrict__ out, uint8_t* __restrict__ out_u8, int64_t cap) {
+               const float* __restrict__ aff, OutT* __restrict__ out,
+               uint8_t* __restrict__ out_u8, int64_t cap) {
   extern __shared__ __align__(128) uint8_t smem[];
   SmemHeader& hdr = *reinterpret_cast<SmemHeader*>(smem);
   OutT* s_lut = reinterpret_cast<OutT*>(smem + ((sizeof(SmemHeader) + 127) & ~size_t(127)));
@@ -909,7 +1013,7 @@ __global__ void __launch_bounds__(kMaxThreads, kCtasPerSm)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   pdl_wait();  // K1 (plan, tile_off) and the LUT come from stream predecessors
-  if (WRITE_OUT)
+  if (WRITE_OUT && !(AFFINE && !WRITE_U8))
     for (int i = threadIdx.x; i < C * 256; i += blockDim.x) s_lut[i] = lut[i];
   __syncthreads();
   // every tile's items are enumerated (item order interleaves tiles); tiles at or
@@ -926,7 +1030,7 @@ __global__ void __launch_bounds__(kMaxThreads, kCtasPerSm)
   if (threadIdx.x < 32)
     produce<C>(hdr, arena, src, src_off, wh, n, plan, tile_off, E, items, bands, band, cap_tiles);
   else
-    consume<C, OutT, LAYOUT, WRITE_OUT, WRITE_U8>(hdr, arena, s_lut, E, out, out_u8);
+    consume<C, OutT, LAYOUT, WRITE_OUT, WRITE_U8, AFFINE>(hdr, arena, s_lut, E, out, out_u8, aff);
 }
 
 template <int C, typename OutT>
@@ -935,11 +1039,12 @@ size_t tma_smem_bytes() {
          ((C * 256 * sizeof(OutT) + 127) & ~size_t(127)) + kStages * kArena;
 }
 
-template <int C, typename OutT, int LAYOUT, bool WRITE_OUT, bool WRITE_U8>
+template <int C, typename OutT, int LAYOUT, bool WRITE_OUT, bool WRITE_U8, bool AFFINE>
 int launch_variant(const uint8_t* src, const int64_t* src_off, const int32_t* wh, int n,
                    const int32_t* plan, const int32_t* tile_off, int E, const void* lut,
-                   void* out, uint8_t* out_u8, int64_t cap, cudaStream_t stream) {
-  auto kern = k_tile_tma<C, OutT, LAYOUT, WRITE_OUT, WRITE_U8>;
+                   const float* aff, void* out, uint8_t* out_u8, int64_t cap,
+                   cudaStream_t stream) {
+  auto kern = k_tile_tma<C, OutT, LAYOUT, WRITE_OUT, WRITE_U8, AFFINE>;
   const size_t smem = tma_smem_bytes<C, OutT>();
   static bool configured = false;  // one per template instance
   static int per_sm = 0;
@@ -959,11 +1064,12 @@ int launch_variant(const uint8_t* src, const int64_t* src_off, const int32_t* wh
 #if TP_K2_PDL
   const cudaError_t err =
       launch_pdl(kern, dim3(grid), dim3(threads), smem, stream, src, src_off, wh, n, plan,
-                 tile_off, E, static_cast<const OutT*>(lut), static_cast<OutT*>(out), out_u8, cap);
+                 tile_off, E, static_cast<const OutT*>(lut), aff, static_cast<OutT*>(out),
+                 out_u8, cap);
 #else
   kern<<<grid, threads, smem, stream>>>(src, src_off, wh, n, plan, tile_off, E,
-                                        static_cast<const OutT*>(lut), static_cast<OutT*>(out),
-                                        out_u8, cap);
+                                        static_cast<const OutT*>(lut), aff,
+                                        static_cast<OutT*>(out), out_u8, cap);
   const cudaError_t err = cudaSuccess;
 #endif
   if (err != cudaSuccess) return set_error(TP_ERR_CUDA, "tp_tile: %s", cudaGetErrorString(err));
@@ -975,18 +1081,26 @@ int launch_variant(const uint8_t* src, const int64_t* src_off, const int32_t* wh
 template <int C, typename OutT, int LAYOUT, bool WRITE_OUT>
 int launch_tile_tma(const uint8_t* src, const int64_t* src_off, const int32_t* wh, int n,
                     const int32_t* plan, const int32_t* tile_off, int E, const void* lut,
-                    void* out, uint8_t* out_u8, int64_t cap, cudaStream_t stream) {
+                    void* out, uint8_t* out_u8, int64_t cap, bool affine, cudaStream_t stream) {
   if (out_u8)
-    return launch_variant<C, OutT, LAYOUT, WRITE_OUT, true>(src, src_off, wh, n, plan, tile_off,
-                                                            E, lut, out, out_u8, cap, stream);
-  return launch_variant<C, OutT, LAYOUT, WRITE_OUT, false>(src, src_off, wh, n, plan, tile_off, E,
-                                                           lut, out, out_u8, cap, stream);
+    return launch_variant<C, OutT, LAYOUT, WRITE_OUT, true, false>(
+        src, src_off, wh, n, plan, tile_off, E, lut, nullptr, out, out_u8, cap, stream);
+  if (WRITE_OUT && affine) {
+    // the affine block follows the table (tp_build_norm)
+    const float* aff = reinterpret_cast<const float*>(
+        static_cast<const char*>(lut) +
+        tp_lut_table_bytes(C, sizeof(OutT) == 4 ? TP_DTYPE_F32 : TP_DTYPE_BF16));
+    return launch_variant<C, OutT, LAYOUT, WRITE_OUT, false, true>(
+        src, src_off, wh, n, plan, tile_off, E, lut, aff, out, out_u8, cap, stream);
+  }
+  return launch_variant<C, OutT, LAYOUT, WRITE_OUT, false, false>(
+      src, src_off, wh, n, plan, tile_off, E, lut, nullptr, out, out_u8, cap, stream);
 }
 
 #define TP_INSTANTIATE(C, T, L, W)                                                             \
   template int launch_tile_tma<C, T, L, W>(const uint8_t*, const int64_t*, const int32_t*, int, \
                                            const int32_t*, const int32_t*, int, const void*,   \
-                                           void*, uint8_t*, int64_t, cudaStream_t);
+                                           void*, uint8_t*, int64_t, bool, cudaStream_t);
 TP_INSTANTIATE(1, float, TP_LAYOUT_NHWC, false)
 TP_INSTANTIATE(3, float, TP_LAYOUT_NHWC, false)
 TP_INSTANTIATE(1, float, TP_LAYOUT_NCHW, true)

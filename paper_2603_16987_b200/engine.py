@@ -22,7 +22,7 @@ import torch
 
 from . import _lib
 from .dtypes import FLOAT16_WIDE, FLOAT32
-from .runtime import dtype_code, normalize_lut, require_device, stream_handle, torch_dtype
+from .runtime import dtype_code, normalize_tables, require_device, stream_handle, torch_dtype
 
 IMAGE_ALIGN = 256
 
@@ -179,7 +179,7 @@ class TilePreprocessor:
         self.emit_uint8 = emit_uint8
         self.normalize = normalize
         self.dtype = dtype_code(cfg.effective_precision) if normalize else _lib.TP_DTYPE_NONE
-        self._luts: dict[int, torch.Tensor] = {}
+        self._luts: dict[int, tuple] = {}
 
     @property
     def tile_edge(self) -> int:
@@ -189,11 +189,15 @@ class TilePreprocessor:
         return n * (self.cfg.max_tiles + 1)
 
     def lut(self, channels: int) -> Optional[torch.Tensor]:
+        return self._norm(channels)[0]
+
+    def _norm(self, channels: int):
+        """(table, affine_ok) from K0; affine_ok lets K2 normalize by fma (same bits)."""
         if self.dtype == _lib.TP_DTYPE_NONE:
-            return None
+            return None, False
         if channels not in self._luts:
-            self._luts[channels] = normalize_lut(self.cfg.mean, self.cfg.std, channels,
-                                                 self.dtype, self.device)
+            self._luts[channels] = normalize_tables(self.cfg.mean, self.cfg.std, channels,
+                                                    self.dtype, self.device)
         return self._luts[channels]
 
     def alloc_plans(self, n: int) -> PlanBatch:
@@ -228,7 +232,8 @@ class TilePreprocessor:
     def tile(self, images: PackedImages, plans: PlanBatch, pixel_values=None, pixel_u8=None,
              stream: Optional[torch.cuda.Stream] = None) -> None:
         """K2 over a planned batch into caller-provided buffers."""
-        lut = self.lut(images.channels)
+        lut, affine = self._norm(images.channels)
+        algo = self.algo | (_lib.TP_TILE_NORM_AFFINE if affine else 0)
         caps = [t.shape[0] for t in (pixel_values, pixel_u8) if t is not None]
         if not caps:
             raise ValueError("no output buffer")
@@ -237,7 +242,7 @@ class TilePreprocessor:
                       _lib.ptr(images.wh), images.n, images.channels, _lib.ptr(plans.plan),
                       _lib.ptr(plans.tile_off), self.cfg.tile_edge, _lib.ptr(lut), self.dtype,
                       self.layout, _lib.ptr(pixel_values), _lib.ptr(pixel_u8), min(caps),
-                      self.algo, stream_handle(self.device, stream))
+                      algo, stream_handle(self.device, stream))
 
     def __call__(self, images: PackedImages, capacity: Optional[int] = None,
                  out: Optional[TileBatch] = None,

@@ -30,7 +30,8 @@ import torch
 from . import _lib
 from ._decode import decode_rgb
 from .dtypes import FLOAT16_WIDE, FLOAT32, UINT8, to_numpy
-from .runtime import dtype_code, normalize_lut, require_device, stream_handle, torch_dtype
+from .runtime import (dtype_code, normalize_lut, normalize_tables, require_device, stream_handle,
+                      torch_dtype)
 
 
 @dataclass
@@ -186,16 +187,18 @@ class _Run:
         self.wh = torch.tensor([[img.width, img.height]], dtype=torch.int32, device=self.device)
 
     def tile(self, plan_rec: torch.Tensor, tile_off: torch.Tensor, e: int, n_tiles: int,
-             lut: Optional[torch.Tensor], dtype: int, layout: int, want_u8: bool):
+             lut: Optional[torch.Tensor], dtype: int, layout: int, want_u8: bool,
+             affine: bool = False):
         c = self.img.channels
         out = None
         if dtype != _lib.TP_DTYPE_NONE:
             out = torch.empty((n_tiles, e, e, c), dtype=torch_dtype(dtype), device=self.device)
         u8 = torch.empty((n_tiles, e, e, c), dtype=torch.uint8, device=self.device) \
             if want_u8 else None
-        _lib.call("tp_tile", _lib.ptr(self.src), _lib.ptr(self.off), _lib.ptr(self.wh), 1, c,
+        algo = _lib.TP_TILE_ALGO_AUTO | (_lib.TP_TILE_NORM_AFFINE if affine else 0)
+        _lib.call("tp_tile_ex", _lib.ptr(self.src), _lib.ptr(self.off), _lib.ptr(self.wh), 1, c,
                   _lib.ptr(plan_rec), _lib.ptr(tile_off), e, _lib.ptr(lut), dtype, layout,
-                  _lib.ptr(out), _lib.ptr(u8), n_tiles, self.handle)
+                  _lib.ptr(out), _lib.ptr(u8), n_tiles, algo, self.handle)
         return out, u8
 
 
@@ -337,9 +340,9 @@ def preprocess(payload: bytes, cfg: PreprocessConfig, *,
         elem = UINT8
     else:
         dtype = dtype_code(cfg.effective_precision)
-        lut = normalize_lut(cfg.mean, cfg.std, img.channels, dtype, run.device)
+        lut, affine = normalize_tables(cfg.mean, cfg.std, img.channels, dtype, run.device)
         out, u8 = run.tile(rec, tile_off, cfg.tile_edge, cap, lut, dtype, _lib.TP_LAYOUT_NHWC,
-                           False)
+                           False, affine)
         elem = cfg.effective_precision
     ev[2].record(run.stream)
     plan = TilePlan.from_record(rec.cpu().numpy()[0])

@@ -7,6 +7,7 @@ computes pixels or ids on the host.
 
 from __future__ import annotations
 
+import ctypes
 import threading
 from typing import Optional, Sequence
 
@@ -17,7 +18,7 @@ from . import _lib
 from .errors import DeviceError
 
 _lut_lock = threading.Lock()
-_lut_cache: dict[tuple, torch.Tensor] = {}
+_lut_cache: dict[tuple, tuple] = {}
 
 
 def require_device(device=None) -> torch.device:
@@ -63,24 +64,38 @@ def fp32_constants(vals: Sequence[float], channels: int) -> tuple[float, ...]:
     return tuple(float(np.float32(v)) for v in tuple(vals)[:channels])
 
 
-def normalize_lut(mean, std, channels: int, dtype: int, device: torch.device) -> torch.Tensor:
-    """Device LUT [C,256] built by K0 (tp_build_lut); cached per constants."""
+def normalize_tables(mean, std, channels: int, dtype: int,
+                     device: torch.device) -> "tuple[torch.Tensor, bool]":
+    """K0 via tp_build_norm: the [C,256] table (a view of a buffer that also holds the
+    per-channel affine constants) and whether the affine form reproduces the table
+    exactly (then K2 may normalize with one fma per value, TP_TILE_NORM_AFFINE).
+    Cached per constants."""
     m = fp32_constants(mean, channels)
     s = fp32_constants(std, channels)
     if len(m) < channels or len(s) < channels:
         raise ValueError("mean/std need one entry per channel")
     key = (m, s, channels, dtype, device.index)
     with _lut_lock:
-        lut = _lut_cache.get(key)
-    if lut is not None:
-        return lut
-    lut = torch.empty((channels, 256), dtype=torch_dtype(dtype), device=device)
+        hit = _lut_cache.get(key)
+    if hit is not None:
+        return hit
+    lib = _lib.load()
+    nbytes = lib.tp_lut_bytes(channels, dtype)
+    buf = torch.empty((nbytes,), dtype=torch.uint8, device=device)
+    table = buf[: channels * 256 * torch_dtype(dtype).itemsize].view(torch_dtype(dtype))
+    ok = ctypes.c_int32(0)
     with torch.cuda.device(device):
-        _lib.call("tp_build_lut", channels, _lib.f32_array(m), _lib.f32_array(s), dtype,
-                  _lib.ptr(lut), stream_handle(device))
+        _lib.call("tp_build_norm", channels, _lib.f32_array(m), _lib.f32_array(s), dtype,
+                  _lib.ptr(buf), ctypes.byref(ok), stream_handle(device))
+    hit = (table.view(channels, 256), bool(ok.value))
     with _lut_lock:
-        _lut_cache[key] = lut
-    return lut
+        _lut_cache[key] = hit
+    return hit
+
+
+def normalize_lut(mean, std, channels: int, dtype: int, device: torch.device) -> torch.Tensor:
+    """Device LUT [C,256] built by K0 (tp_build_norm); cached per constants."""
+    return normalize_tables(mean, std, channels, dtype, device)[0]
 
 
 def to_device_i32(arr, device: torch.device, non_blocking: bool = False) -> torch.Tensor:

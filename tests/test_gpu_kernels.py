@@ -303,6 +303,78 @@ def test_fast_integer_scale_ties():
 
 
 # ---------------------------------------------------------------------------
+# affine normalize (TP_TILE_NORM_AFFINE): one fma per value instead of the table,
+# taken when no uint8 tiles are requested; must give the table's exact bits
+
+CLIP_MEAN = (0.48145466, 0.4578275, 0.40821073)
+CLIP_STD = (0.26862954, 0.26130258, 0.27577711)
+
+
+def _bf16_rne(x: np.ndarray) -> np.ndarray:
+    u = x.astype(np.float32).view(np.uint32).astype(np.uint64)
+    return ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
+
+
+@pytest.mark.parametrize("mean,std", [(IMAGENET_MEAN, IMAGENET_STD), ((0.5,) * 3, (0.5,) * 3),
+                                      (CLIP_MEAN, CLIP_STD)])
+def test_affine_block_reproduces_table(mean, std):
+    from paper_2603_16987_b200.runtime import normalize_tables
+
+    table, ok = normalize_tables(mean, std, 3, _lib.TP_DTYPE_BF16, torch.device(DEV))
+    assert ok
+    want = O.lut(mean, std, 3, True).view(np.uint16)
+    assert np.array_equal(table.cpu().view(torch.int16).numpy().view(np.uint16), want)
+    # the constants after the table: fma(v, a, b) (exact in float64, rounded once to fp32)
+    # must round to the table entry for every v
+    lib = _lib.load()
+    off = lib.tp_lut_table_bytes(3, _lib.TP_DTYPE_BF16)
+    full = torch.empty(0, dtype=torch.uint8, device=DEV).set_(table.untyped_storage())
+    assert full.numel() == lib.tp_lut_bytes(3, _lib.TP_DTYPE_BF16)
+    block = full[off: off + 32].clone()
+    ab = block.cpu().numpy().view(np.float32)
+    v = np.arange(256, dtype=np.float64)
+    for c in range(3):
+        y = (v * np.float64(ab[c]) + np.float64(ab[4 + c])).astype(np.float32)
+        assert np.array_equal(_bf16_rne(y), want[c]), c
+
+
+def _pixels(cfg, packed, layout, emit_uint8):
+    prep = TilePreprocessor(cfg, DEV, layout=layout, emit_uint8=emit_uint8)
+    out = prep(packed)
+    torch.cuda.synchronize()
+    return out
+
+
+@pytest.mark.parametrize("layout", ["NCHW", "NHWC"])
+@pytest.mark.parametrize("kind", [0, 1])
+def test_affine_normalize_equals_table_c4_slice(layout, kind):
+    from paper_2603_16987_b200.workloads import c4_shapes
+
+    wh = c4_shapes(192, start=2048 + 192 * kind)
+    packed = synth_packed(wh, 3, DEV, seed=7 + kind, kind=kind)
+    for mean, std in ((IMAGENET_MEAN, IMAGENET_STD), (CLIP_MEAN, CLIP_STD)):
+        cfg = PreprocessConfig(tile_edge=448, max_tiles=12, mean=mean, std=std,
+                               reduced_precision_normalize=True)
+        lut_path = _pixels(cfg, packed, layout, True)     # uint8 tiles: table lookups
+        aff_path = _pixels(cfg, packed, layout, False)    # affine fma
+        T = lut_path.num_tiles()
+        assert T == aff_path.num_tiles() > 192
+        assert torch.equal(lut_path.pixel_values[:T].view(torch.int16),
+                           aff_path.pixel_values[:T].view(torch.int16))
+
+
+@pytest.mark.parametrize("w,h,c", [(1920, 1080, 3), (333, 517, 3), (700, 300, 1)])
+def test_affine_normalize_vs_oracle(w, h, c):
+    arr = make_input(h, w, c, "random", w + h)
+    cfg = PreprocessConfig(tile_edge=448, max_tiles=12, mean=IMAGENET_MEAN, std=IMAGENET_STD,
+                           reduced_precision_normalize=True)
+    _, pv, _ = _run_engine([arr], cfg, layout="NCHW", emit_uint8=False)
+    want = O.tiles_u8(arr, O.plan_float(w, h, 448, 12))
+    wb = O.normalize(want, IMAGENET_MEAN, IMAGENET_STD, True).transpose(0, 3, 1, 2)
+    assert np.array_equal(pv.view(torch.int16).numpy().view(np.uint16), wb.view(np.uint16))
+
+
+# ---------------------------------------------------------------------------
 # K3 at C5 scale: 1024 ragged prompts, counts straight from K1's n_images
 
 def test_c5_expansion_batch_bit_exact(golden):
