@@ -697,14 +697,17 @@ __device__ __forceinline__ PixTaps fetch_pix(const PhaseRows& pr, int jj, uint32
 // consecutive pixels, which halves shared-memory bank conflicts versus adjacent
 // pairs), all output rows of the phase, all channels.  Math is packed f32x2
 // (lane 0: pixel a, lane 1: pixel b).
-template <int C, typename OutT, int LAYOUT, bool WRITE_OUT, bool WRITE_U8, bool AFFINE,
+template <int C, typename OutT, int LAYOUT, bool WRITE_OUT, bool WRITE_U8, bool AFFINE, int EK,
           bool UNIFORM>
 __device__ __forceinline__ void consume_pair_rows(
     const PhaseRows& pr, int g, int j0, int nrows, int mis_in, uint32_t sbase, uint32_t lut_u32,
     int ia, int ib, bool has_a, bool has_b, int xoa, int xob, float fxa, float fxb, double fxa64,
-    double omfxa64, double fxb64, double omfxb64, int E, OutT* __restrict__ out,
+    double omfxa64, double fxb64, double omfxb64, OutT* __restrict__ out,
     uint8_t* __restrict__ out_u8, OutT* __restrict__ tile_a, const float (&aff_a)[C],
-    const float (&aff_b)[C]) {
+    const float (&aff_b)[C], int E_rt) {
+  // EK > 0: the tile edge is a compile-time constant, so the channel planes of an NCHW
+  // row are immediate offsets from one row pointer (one 64-bit add per row, not C)
+  const int E = EK > 0 ? EK : E_rt;
   const int64_t EE = static_cast<int64_t>(E) * E;
   const f32x2 FX = pk(fxa, fxb);
   const f32x2 KH = pk(8388608.0f, 8388608.0f);  // 2^23: biased byte -> byte
@@ -725,7 +728,9 @@ __device__ __forceinline__ void consume_pair_rows(
   OutT* oc[C];  // tile_a = out + g*C*EE + ia, cached per (tile, column segment)
   oc[0] = tile_a + j0 * E;
 #pragma unroll
-  for (int c = 1; c < C; ++c) oc[c] = oc[c - 1] + EE;
+  for (int c = 1; c < C; ++c) oc[c] = EK > 0 ? oc[0] : oc[c - 1] + EE;
+  // plane c of the current row: oc[c] (run-time E) or oc[0] + c*EE (immediate offset)
+  auto plane = [&](int c) -> OutT* { return EK > 0 ? oc[0] + c * EE : oc[c]; };
   const int ob_off = ib - ia;
   // one output row: taps (a, b) already fetched
   // fp32 fast path of output row jj: LUT codes (kKrawBias + value) and window flags
@@ -833,28 +838,30 @@ __device__ __forceinline__ void consume_pair_rows(
           vb = hb >> 16;
         }
         if (LAYOUT == TP_LAYOUT_NCHW) {
-          if (has_a) LutLoad<OutT>::store_one(oc[c], va);
-          if (has_b) LutLoad<OutT>::store_one(oc[c] + ob_off, vb);
-          oc[c] += E;
+          if (has_a) LutLoad<OutT>::store_one(plane(c), va);
+          if (has_b) LutLoad<OutT>::store_one(plane(c) + ob_off, vb);
+          if (EK == 0) oc[c] += E;
         } else {
           if (has_a) LutLoad<OutT>::store_one(out + (rowpix + ia) * C + c, va);
           if (has_b) LutLoad<OutT>::store_one(out + (rowpix + ib) * C + c, vb);
         }
       }
+      if (EK > 0 && LAYOUT == TP_LAYOUT_NCHW) oc[0] += E;
     } else if (WRITE_OUT) {
 #pragma unroll
       for (int c = 0; c < C; ++c) {
         const uint32_t va = LutLoad<OutT>::load(lut0 + ka[c] * SZ + c * 256 * SZ);
         const uint32_t vb = LutLoad<OutT>::load(lut0 + kb[c] * SZ + c * 256 * SZ);
         if (LAYOUT == TP_LAYOUT_NCHW) {
-          if (has_a) LutLoad<OutT>::store_one(oc[c], va);
-          if (has_b) LutLoad<OutT>::store_one(oc[c] + ob_off, vb);
-          oc[c] += E;
+          if (has_a) LutLoad<OutT>::store_one(plane(c), va);
+          if (has_b) LutLoad<OutT>::store_one(plane(c) + ob_off, vb);
+          if (EK == 0) oc[c] += E;
         } else {
           if (has_a) LutLoad<OutT>::store_one(out + (rowpix + ia) * C + c, va);
           if (has_b) LutLoad<OutT>::store_one(out + (rowpix + ib) * C + c, vb);
         }
       }
+      if (EK > 0 && LAYOUT == TP_LAYOUT_NCHW) oc[0] += E;
     }
   };
   auto row = [&](int jj, const PixTaps& a, const PixTaps& b) {
@@ -905,7 +912,7 @@ __device__ __forceinline__ void consume_pair_rows(
 #endif
 }
 
-template <int C, typename OutT, int LAYOUT, bool WRITE_OUT, bool WRITE_U8, bool AFFINE>
+template <int C, typename OutT, int LAYOUT, bool WRITE_OUT, bool WRITE_U8, bool AFFINE, int EK>
 __device__ void consume(SmemHeader& hdr, const uint8_t* arena, const OutT* s_lut, int E,
                         OutT* __restrict__ out, uint8_t* __restrict__ out_u8,
                         const float* __restrict__ aff) {
@@ -974,13 +981,13 @@ __device__ void consume(SmemHeader& hdr, const uint8_t* arena, const OutT* s_lut
         cache_q = q;
       }
       if (mis >= 0)
-        consume_pair_rows<C, OutT, LAYOUT, WRITE_OUT, WRITE_U8, AFFINE, true>(
+        consume_pair_rows<C, OutT, LAYOUT, WRITE_OUT, WRITE_U8, AFFINE, EK, true>(
             pr, g, j0, nrows, mis, sbase, lut_u32, ia, ib, has_a, has_b, xoa, xob, fxa, fxb,
-            fxa64, omfxa64, fxb64, omfxb64, E, out, out_u8, tile_a, aff_a, aff_b);
+            fxa64, omfxa64, fxb64, omfxb64, out, out_u8, tile_a, aff_a, aff_b, E);
       else
-        consume_pair_rows<C, OutT, LAYOUT, WRITE_OUT, WRITE_U8, AFFINE, false>(
+        consume_pair_rows<C, OutT, LAYOUT, WRITE_OUT, WRITE_U8, AFFINE, EK, false>(
             pr, g, j0, nrows, mis, sbase, lut_u32, ia, ib, has_a, has_b, xoa, xob, fxa, fxb,
-            fxa64, omfxa64, fxb64, omfxb64, E, out, out_u8, tile_a, aff_a, aff_b);
+            fxa64, omfxa64, fxb64, omfxb64, out, out_u8, tile_a, aff_a, aff_b, E);
     }
     mbar_arrive(&hdr.empty[stage]);
     if (++stage == kStages) {
@@ -990,7 +997,7 @@ __device__ void consume(SmemHeader& hdr, const uint8_t* arena, const OutT* s_lut
   }
 }
 
-template <int C, typename OutT, int LAYOUT, bool WRITE_OUT, bool WRITE_U8, bool AFFINE>
+template <int C, typename OutT, int LAYOUT, bool WRITE_OUT, bool WRITE_U8, bool AFFINE, int EK>
 __global__ void __launch_bounds__(kMaxThreads, kCtasPerSm)
     k_tile_tma(const uint8_t* __restrict__ src, const int64_t* __restrict__ src_off,
                const int32_t* __restrict__ wh, int n, const int32_t* __restrict__ plan,
@@ -1030,7 +1037,8 @@ __global__ void __launch_bounds__(kMaxThreads, kCtasPerSm)
   if (threadIdx.x < 32)
     produce<C>(hdr, arena, src, src_off, wh, n, plan, tile_off, E, items, bands, band, cap_tiles);
   else
-    consume<C, OutT, LAYOUT, WRITE_OUT, WRITE_U8, AFFINE>(hdr, arena, s_lut, E, out, out_u8, aff);
+    consume<C, OutT, LAYOUT, WRITE_OUT, WRITE_U8, AFFINE, EK>(hdr, arena, s_lut, E, out, out_u8,
+                                                             aff);
 }
 
 template <int C, typename OutT>
@@ -1039,12 +1047,13 @@ size_t tma_smem_bytes() {
          ((C * 256 * sizeof(OutT) + 127) & ~size_t(127)) + kStages * kArena;
 }
 
-template <int C, typename OutT, int LAYOUT, bool WRITE_OUT, bool WRITE_U8, bool AFFINE>
+template <int C, typename OutT, int LAYOUT, bool WRITE_OUT, bool WRITE_U8, bool AFFINE,
+          int EK = 0>
 int launch_variant(const uint8_t* src, const int64_t* src_off, const int32_t* wh, int n,
                    const int32_t* plan, const int32_t* tile_off, int E, const void* lut,
                    const float* aff, void* out, uint8_t* out_u8, int64_t cap,
                    cudaStream_t stream) {
-  auto kern = k_tile_tma<C, OutT, LAYOUT, WRITE_OUT, WRITE_U8, AFFINE>;
+  auto kern = k_tile_tma<C, OutT, LAYOUT, WRITE_OUT, WRITE_U8, AFFINE, EK>;
   const size_t smem = tma_smem_bytes<C, OutT>();
   static bool configured = false;  // one per template instance
   static int per_sm = 0;
@@ -1090,6 +1099,9 @@ int launch_tile_tma(const uint8_t* src, const int64_t* src_off, const int32_t* w
     const float* aff = reinterpret_cast<const float*>(
         static_cast<const char*>(lut) +
         tp_lut_table_bytes(C, sizeof(OutT) == 4 ? TP_DTYPE_F32 : TP_DTYPE_BF16));
+    if (E == 448 && LAYOUT == TP_LAYOUT_NCHW)  // the InternVL / C2-C5 tile edge
+      return launch_variant<C, OutT, LAYOUT, WRITE_OUT, false, true, 448>(
+          src, src_off, wh, n, plan, tile_off, E, lut, aff, out, out_u8, cap, stream);
     return launch_variant<C, OutT, LAYOUT, WRITE_OUT, false, true>(
         src, src_off, wh, n, plan, tile_off, E, lut, aff, out, out_u8, cap, stream);
   }
