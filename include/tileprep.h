@@ -137,6 +137,11 @@ TP_API int tp_tile(const uint8_t* d_src, const int64_t* d_src_off, const int32_t
 /* or-ed into algo: d_lut comes from tp_build_norm with *affine_ok == 1 (fast path,
  * normalized outputs without uint8 tiles) */
 #define TP_TILE_NORM_AFFINE 256
+/* or-ed into algo: the immediately preceding operation on `stream` is the tp_plan
+ * that produced d_plan / d_tile_off, so K2 may be launched as its programmatic
+ * dependent (its launch and prologue overlap K1).  Without the flag K2 is a plain
+ * launch: a programmatic launch could start before a preceding copy had landed. */
+#define TP_TILE_AFTER_PLAN 512
 TP_API int tp_tile_ex(const uint8_t* d_src, const int64_t* d_src_off, const int32_t* d_wh,
                       int32_t n, int32_t channels, const int32_t* d_plan,
                       const int32_t* d_tile_off, int32_t tile_edge, const void* d_lut,

@@ -8,6 +8,7 @@ built libtileprep.so and a CUDA device and raise otherwise (no CPU fallback).
 
 from .dtypes import FLOAT16_WIDE, FLOAT32, INT32, UINT8
 from .errors import (
+    ArenaFullError,
     AssemblyError,
     ConfigError,
     DataError,
@@ -54,5 +55,23 @@ from .tokenred import (
 )
 from .backend import AssembledSequence, assemble
 from .engine import PackedImages, TileBatch, TilePreprocessor, pack_images, synth_packed
+from .transfer import (
+    DEFAULT_ALIGNMENT,
+    BatchEntry,
+    CostModel,
+    HostArena,
+    PipelinedPreprocessor,
+    Region,
+    StagedImages,
+    TransferBatch,
+    TransferResult,
+    pack,
+    payload_bytes,
+    stage_images,
+    stage_individually,
+    transfer,
+    unpack,
+    upload_images,
+)
 
 __version__ = "0.1.0"

@@ -37,6 +37,7 @@ TP_TILE_ALGO_AUTO = 0
 TP_TILE_ALGO_FAST = 1
 TP_TILE_ALGO_EXACT = 2
 TP_TILE_NORM_AFFINE = 256
+TP_TILE_AFTER_PLAN = 512
 
 TP_PLAN_FIELDS = 6
 TP_MAX_EDGE = 65536

@@ -17,6 +17,14 @@
 
 #include "tp_common.cuh"
 
+// K1 is a plain launch: a programmatic (PDL) launch may start before a preceding
+// non-kernel stream operation (an H2D copy of d_wh, an event wait) has completed,
+// which griddepcontrol.wait does not cover.  K1 still releases its dependent early
+// (pdl_trigger) so an engine-launched K2 overlaps K1's tail.
+#ifndef TP_K1_PDL
+#define TP_K1_PDL 0
+#endif
+
 namespace tp {
 namespace {
 
@@ -93,7 +101,7 @@ __global__ void __launch_bounds__(kPlanThreads)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   pdl_trigger();
-  pdl_wait();  // the previous K2 may still be reading plan / tile_off
+  pdl_wait();  // no-op unless launched as a programmatic dependent (TP_K1_PDL)
   if (threadIdx.x == 0) s_bad = 0;
   int64_t carry = 0;
   const int nthr = blockDim.x;  // sized to the batch (<= 1024): small batches, short syncs
@@ -156,8 +164,14 @@ extern "C" int tp_plan(const int32_t* d_wh, int32_t n, int32_t tile_edge, int32_
     return tp::set_error(TP_ERR_INVALID_ARGUMENT, "tp_plan: null buffer");
   // one warp per image up to a full 1024-thread block (small batches: short block syncs)
   const int threads = static_cast<int>(std::min<int64_t>(tp::kPlanThreads, 32LL * std::max(1, n)));
+#if TP_K1_PDL
   const cudaError_t err = tp::launch_pdl(tp::k_plan, dim3(1), dim3(threads), 0, tp::as_stream(stream),
                                           d_wh, n, tile_edge, max_tiles, d_plan, d_n_img, d_tile_off);
+#else
+  tp::k_plan<<<1, threads, 0, tp::as_stream(stream)>>>(d_wh, n, tile_edge, max_tiles, d_plan,
+                                                       d_n_img, d_tile_off);
+  const cudaError_t err = cudaSuccess;
+#endif
   if (err != cudaSuccess) return tp::set_error(TP_ERR_CUDA, "tp_plan: %s", cudaGetErrorString(err));
   return tp::check_launch("tp_plan");
 }

@@ -182,7 +182,8 @@ int launch_tile(const uint8_t* src, const int64_t* src_off, const int32_t* wh, i
   }
   return launch_tile_tma<C, OutT, LAYOUT, WRITE_OUT>(src, src_off, wh, n, plan, tile_off, E, lut,
                                                      out, out_u8, cap,
-                                                     (algo & TP_TILE_NORM_AFFINE) != 0, stream);
+                                                     (algo & TP_TILE_NORM_AFFINE) != 0,
+                                                     (algo & TP_TILE_AFTER_PLAN) != 0, stream);
 }
 
 template <int C>
@@ -227,7 +228,7 @@ extern "C" int tp_tile_ex(const uint8_t* d_src, const int64_t* d_src_off, const 
   const int base_algo = algo & 0xFF;
   if ((base_algo != TP_TILE_ALGO_AUTO && base_algo != TP_TILE_ALGO_FAST &&
        base_algo != TP_TILE_ALGO_EXACT) ||
-      (algo & ~(0xFF | TP_TILE_NORM_AFFINE)) != 0)
+      (algo & ~(0xFF | TP_TILE_NORM_AFFINE | TP_TILE_AFTER_PLAN)) != 0)
     return tp::set_error(TP_ERR_INVALID_ARGUMENT, "bad algo %d", algo);
   if (n < 0) return tp::set_error(TP_ERR_INVALID_ARGUMENT, "tp_tile: n must be >= 0");
   if (channels != 1 && channels != 3)

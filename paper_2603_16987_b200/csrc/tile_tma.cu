@@ -39,7 +39,8 @@ namespace {
 #ifndef TP_K2_ARENA_KB
 #define TP_K2_ARENA_KB 54
 #endif
-#ifndef TP_K2_PDL  // 0: plain launch; 1: PDL, successor released at start; 2: at the end
+#ifndef TP_K2_PDL  // 0: plain launch; 1: PDL, successor released at start; 2: at the end;
+                   // 3: PDL launch, successor never released early
 #define TP_K2_PDL 2
 #endif
 #ifndef TP_K2_L2  // 0: no hints; 1: streaming output stores; 2: + thumbnail reads evict_first;
@@ -54,6 +55,16 @@ namespace {
 #endif
 #ifndef TP_K2_PAIR  // consumer rows in pairs (one basic block) instead of a row pipeline
 #define TP_K2_PAIR 0
+#endif
+// loads of predecessor-written data: 1 = ld.global.cg (L2), 2 = ld.global.ca (L1+L2);
+// never the .nc path that plain loads through const __restrict__ pointers compile to
+#ifndef TP_K2_LDMODE
+#define TP_K2_LDMODE 2
+#endif
+#if TP_K2_LDMODE == 1
+#define TP_LD(p) __ldcg(p)
+#else
+#define TP_LD(p) __ldca(p)
 #endif
 #ifndef TP_K2_ROW_BALANCE
 #define TP_K2_ROW_BALANCE 1
@@ -274,7 +285,7 @@ __device__ __forceinline__ int find_item_image(const int32_t* __restrict__ tile_
   int lo = 0, hi = n;
   while (hi - lo > 1) {
     const int mid = (lo + hi) >> 1;
-    if (static_cast<int64_t>(__ldg(tile_off + mid)) * bands <= item) lo = mid; else hi = mid;
+    if (static_cast<int64_t>(TP_LD(tile_off + mid)) * bands <= item) lo = mid; else hi = mid;
   }
   return lo;
 }
@@ -284,7 +295,7 @@ __device__ __forceinline__ int find_tile_image(const int32_t* __restrict__ tile_
   int lo = 0, hi = n;
   while (hi - lo > 1) {
     const int mid = (lo + hi) >> 1;
-    if (__ldg(tile_off + mid) <= g) lo = mid; else hi = mid;
+    if (TP_LD(tile_off + mid) <= g) lo = mid; else hi = mid;
   }
   return lo;
 }
@@ -332,11 +343,11 @@ template <int C>
 __device__ TileGeo tile_geometry(const int32_t* __restrict__ plan, int k, int t, int W, int H,
                                  int E) {
   const int32_t* p = plan + static_cast<int64_t>(k) * TP_PLAN_FIELDS;
-  const int rows = __ldg(p + TP_PLAN_ROWS), cols = __ldg(p + TP_PLAN_COLS);
+  const int rows = TP_LD(p + TP_PLAN_ROWS), cols = TP_LD(p + TP_PLAN_COLS);
   TileGeo q;
   if (t < rows * cols) {
-    q.RW = __ldg(p + TP_PLAN_RESIZED_W);
-    q.RH = __ldg(p + TP_PLAN_RESIZED_H);
+    q.RW = TP_LD(p + TP_PLAN_RESIZED_W);
+    q.RH = TP_LD(p + TP_PLAN_RESIZED_H);
     q.oy0 = (t / cols) * E;
     q.ox0 = (t % cols) * E;
   } else {
@@ -416,7 +427,7 @@ __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restri
   // image of the current item: one binary search for the first item, then a forward walk
   // (the range is contiguous), so no chain of dependent global loads per item
   int kimg = it_begin < it_end ? find_item_image(tile_off, n, it_begin, bands) : 0;
-  int toff0 = __ldg(tile_off + kimg), toff1 = __ldg(tile_off + kimg + 1);
+  int toff0 = TP_LD(tile_off + kimg), toff1 = TP_LD(tile_off + kimg + 1);
   for (int64_t item = it_begin; item < it_end; ++item) {
     // item order: (image, band, tile): the tiles and the thumbnail of an image read
     // the same source rows within n_images consecutive items, so the second read
@@ -424,7 +435,7 @@ __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restri
     while (static_cast<int64_t>(toff1) * bands <= item) {
       ++kimg;
       toff0 = toff1;
-      toff1 = __ldg(tile_off + kimg + 1);
+      toff1 = TP_LD(tile_off + kimg + 1);
     }
     const int nimg = toff1 - toff0;
     const int r = static_cast<int>(item - static_cast<int64_t>(toff0) * bands);
@@ -445,9 +456,9 @@ __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restri
 #endif
     if (kimg != cur_k) {  // new image: per-tile geometry, one lane per tile
       cur_k = kimg;
-      W = __ldg(wh + 2 * kimg);
-      H = __ldg(wh + 2 * kimg + 1);
-      img = src + __ldg(src_off + kimg);
+      W = TP_LD(wh + 2 * kimg);
+      H = TP_LD(wh + 2 * kimg + 1);
+      img = src + TP_LD(src_off + kimg);
       stride = static_cast<int64_t>(W) * C;
       img_end = reinterpret_cast<uintptr_t>(img) + static_cast<uintptr_t>(stride) * H;
       if (nimg <= kTileCache) {
@@ -933,8 +944,8 @@ __device__ void consume(SmemHeader& hdr, const uint8_t* arena, const OutT* s_lut
   float aff_a[C], aff_b[C];
 #pragma unroll
   for (int c = 0; c < C; ++c) {
-    aff_a[c] = AFFINE ? __ldg(aff + c) : 0.f;
-    aff_b[c] = AFFINE ? __ldg(aff + 4 + c) : 0.f;
+    aff_a[c] = AFFINE ? TP_LD(aff + c) : 0.f;
+    aff_b[c] = AFFINE ? TP_LD(aff + 4 + c) : 0.f;
   }
   const uint32_t ph0 = smem_u32(&hdr.ph[0]);
   while (true) {
@@ -1020,12 +1031,16 @@ __global__ void __launch_bounds__(kMaxThreads, kCtasPerSm)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   pdl_wait();  // K1 (plan, tile_off) and the LUT come from stream predecessors
+  // Everything a predecessor wrote is read with coherent loads (TP_LD), never through
+  // the non-coherent path: under a programmatic launch this grid starts while K1 is
+  // still writing, and .nc loads require data that is read-only for the kernel's whole
+  // lifetime (with __ldg here, plans read stale and K2 faulted under PDL).
   if (WRITE_OUT && !(AFFINE && !WRITE_U8))
-    for (int i = threadIdx.x; i < C * 256; i += blockDim.x) s_lut[i] = lut[i];
+    for (int i = threadIdx.x; i < C * 256; i += blockDim.x) s_lut[i] = TP_LD(lut + i);
   __syncthreads();
   // every tile's items are enumerated (item order interleaves tiles); tiles at or
   // above the output capacity are skipped
-  const int all_tiles = __ldg(tile_off + n);
+  const int all_tiles = TP_LD(tile_off + n);
   const int cap_tiles = static_cast<int>(min(static_cast<int64_t>(all_tiles), cap));
   // band height: kBand rows, smaller when a small batch would leave SMs idle (batch-1
   // latency); every CTA derives the same value from the device-side tile count
@@ -1051,7 +1066,7 @@ template <int C, typename OutT, int LAYOUT, bool WRITE_OUT, bool WRITE_U8, bool 
           int EK = 0>
 int launch_variant(const uint8_t* src, const int64_t* src_off, const int32_t* wh, int n,
                    const int32_t* plan, const int32_t* tile_off, int E, const void* lut,
-                   const float* aff, void* out, uint8_t* out_u8, int64_t cap,
+                   const float* aff, void* out, uint8_t* out_u8, int64_t cap, bool pdl,
                    cudaStream_t stream) {
   auto kern = k_tile_tma<C, OutT, LAYOUT, WRITE_OUT, WRITE_U8, AFFINE, EK>;
   const size_t smem = tma_smem_bytes<C, OutT>();
@@ -1070,17 +1085,16 @@ int launch_variant(const uint8_t* src, const int64_t* src_off, const int32_t* wh
     cached_threads = threads;
   }
   const int grid = max(1, per_sm) * max(1, device_sm_count());
-#if TP_K2_PDL
-  const cudaError_t err =
-      launch_pdl(kern, dim3(grid), dim3(threads), smem, stream, src, src_off, wh, n, plan,
-                 tile_off, E, static_cast<const OutT*>(lut), aff, static_cast<OutT*>(out),
-                 out_u8, cap);
-#else
-  kern<<<grid, threads, smem, stream>>>(src, src_off, wh, n, plan, tile_off, E,
-                                        static_cast<const OutT*>(lut), aff,
-                                        static_cast<OutT*>(out), out_u8, cap);
-  const cudaError_t err = cudaSuccess;
-#endif
+  cudaError_t err = cudaSuccess;
+  if (TP_K2_PDL && pdl) {  // programmatic dependent of the K1 right before it
+    err = launch_pdl(kern, dim3(grid), dim3(threads), smem, stream, src, src_off, wh, n, plan,
+                     tile_off, E, static_cast<const OutT*>(lut), aff, static_cast<OutT*>(out),
+                     out_u8, cap);
+  } else {
+    kern<<<grid, threads, smem, stream>>>(src, src_off, wh, n, plan, tile_off, E,
+                                          static_cast<const OutT*>(lut), aff,
+                                          static_cast<OutT*>(out), out_u8, cap);
+  }
   if (err != cudaSuccess) return set_error(TP_ERR_CUDA, "tp_tile: %s", cudaGetErrorString(err));
   return check_launch("tp_tile(tma)");
 }
@@ -1090,10 +1104,11 @@ int launch_variant(const uint8_t* src, const int64_t* src_off, const int32_t* wh
 template <int C, typename OutT, int LAYOUT, bool WRITE_OUT>
 int launch_tile_tma(const uint8_t* src, const int64_t* src_off, const int32_t* wh, int n,
                     const int32_t* plan, const int32_t* tile_off, int E, const void* lut,
-                    void* out, uint8_t* out_u8, int64_t cap, bool affine, cudaStream_t stream) {
+                    void* out, uint8_t* out_u8, int64_t cap, bool affine, bool after_plan,
+                    cudaStream_t stream) {
   if (out_u8)
     return launch_variant<C, OutT, LAYOUT, WRITE_OUT, true, false>(
-        src, src_off, wh, n, plan, tile_off, E, lut, nullptr, out, out_u8, cap, stream);
+        src, src_off, wh, n, plan, tile_off, E, lut, nullptr, out, out_u8, cap, after_plan, stream);
   if (WRITE_OUT && affine) {
     // the affine block follows the table (tp_build_norm)
     const float* aff = reinterpret_cast<const float*>(
@@ -1101,18 +1116,18 @@ int launch_tile_tma(const uint8_t* src, const int64_t* src_off, const int32_t* w
         tp_lut_table_bytes(C, sizeof(OutT) == 4 ? TP_DTYPE_F32 : TP_DTYPE_BF16));
     if (E == 448 && LAYOUT == TP_LAYOUT_NCHW)  // the InternVL / C2-C5 tile edge
       return launch_variant<C, OutT, LAYOUT, WRITE_OUT, false, true, 448>(
-          src, src_off, wh, n, plan, tile_off, E, lut, aff, out, out_u8, cap, stream);
+          src, src_off, wh, n, plan, tile_off, E, lut, aff, out, out_u8, cap, after_plan, stream);
     return launch_variant<C, OutT, LAYOUT, WRITE_OUT, false, true>(
-        src, src_off, wh, n, plan, tile_off, E, lut, aff, out, out_u8, cap, stream);
+        src, src_off, wh, n, plan, tile_off, E, lut, aff, out, out_u8, cap, after_plan, stream);
   }
   return launch_variant<C, OutT, LAYOUT, WRITE_OUT, false, false>(
-      src, src_off, wh, n, plan, tile_off, E, lut, nullptr, out, out_u8, cap, stream);
+      src, src_off, wh, n, plan, tile_off, E, lut, nullptr, out, out_u8, cap, after_plan, stream);
 }
 
 #define TP_INSTANTIATE(C, T, L, W)                                                             \
   template int launch_tile_tma<C, T, L, W>(const uint8_t*, const int64_t*, const int32_t*, int, \
                                            const int32_t*, const int32_t*, int, const void*,   \
-                                           void*, uint8_t*, int64_t, bool, cudaStream_t);
+                                           void*, uint8_t*, int64_t, bool, bool, cudaStream_t);
 TP_INSTANTIATE(1, float, TP_LAYOUT_NHWC, false)
 TP_INSTANTIATE(3, float, TP_LAYOUT_NHWC, false)
 TP_INSTANTIATE(1, float, TP_LAYOUT_NCHW, true)

@@ -149,6 +149,7 @@ __device__ __forceinline__ T block_exclusive_scan(T v, T* scratch, T* total) {
 template <int C, typename OutT, int LAYOUT, bool WRITE_OUT>
 int launch_tile_tma(const uint8_t* src, const int64_t* src_off, const int32_t* wh, int n,
                     const int32_t* plan, const int32_t* tile_off, int E, const void* lut,
-                    void* out, uint8_t* out_u8, int64_t cap, bool affine, cudaStream_t stream);
+                    void* out, uint8_t* out_u8, int64_t cap, bool affine, bool after_plan,
+                    cudaStream_t stream);
 
 }  // namespace tp

@@ -230,10 +230,13 @@ class TilePreprocessor:
         return out
 
     def tile(self, images: PackedImages, plans: PlanBatch, pixel_values=None, pixel_u8=None,
-             stream: Optional[torch.cuda.Stream] = None) -> None:
-        """K2 over a planned batch into caller-provided buffers."""
+             stream: Optional[torch.cuda.Stream] = None, after_plan: bool = False) -> None:
+        """K2 over a planned batch into caller-provided buffers.  ``after_plan``: the
+        last operation enqueued on ``stream`` is the plan() of this batch, so K2 may be
+        launched as K1's programmatic dependent."""
         lut, affine = self._norm(images.channels)
-        algo = self.algo | (_lib.TP_TILE_NORM_AFFINE if affine else 0)
+        algo = self.algo | (_lib.TP_TILE_NORM_AFFINE if affine else 0) | (
+            _lib.TP_TILE_AFTER_PLAN if after_plan else 0)
         caps = [t.shape[0] for t in (pixel_values, pixel_u8) if t is not None]
         if not caps:
             raise ValueError("no output buffer")
@@ -253,8 +256,9 @@ class TilePreprocessor:
             cap = capacity if capacity is not None else self.capacity_for(images.n)
             pv, u8 = self.alloc_outputs(images.channels, cap)
             out = TileBatch(self.alloc_plans(images.n), pv, u8)
+        self._norm(images.channels)  # K0 (first use only) before K1, so K2 follows K1 directly
         self.plan(images, out.plans, stream)
-        self.tile(images, out.plans, out.pixel_values, out.pixel_u8, stream)
+        self.tile(images, out.plans, out.pixel_values, out.pixel_u8, stream, after_plan=True)
         return out
 
 
