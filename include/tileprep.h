@@ -188,6 +188,29 @@ TP_API int tp_expand(const int32_t* d_ids, const int32_t* d_seq_off, int32_t n_s
 TP_API int tp_supervision_mask(const int32_t* d_ids, int64_t n, int64_t first_asst,
                                int32_t asst_id, uint8_t* d_mask, void* stream);
 
+/* K6 — greedy longest-match tokenizer, batched (replaces tokenize, tokenizer.py:135-158).
+ * The vocabulary is an open-addressing hash table built on the HOST by tp_vocab_build
+ * into a caller buffer of tp_vocab_table_bytes(n_tokens) bytes; the caller copies it
+ * to the device.  Tokens are 1..16 bytes (longer: TP_ERR_UNSUPPORTED); byte_ids[256]
+ * holds the byte-fallback token of each byte value, -1 when the vocabulary has none.
+ *   tok_bytes / tok_off[n+1] / tok_id   the non-byte tokens (UTF-8), their ids
+ * tp_tokenize: texts are concatenated UTF-8 bytes, text t = d_text[off[t] .. off[t+1]).
+ *   d_out_ids  capacity total_bytes (a text of B bytes gives at most B ids)
+ *   d_out_off  [n+1] exclusive prefix of the id counts (text t's ids at
+ *              d_out_ids[out_off[t] .. out_off[t+1]])
+ *   d_err      [n]: 0, or 0x100 | byte for a byte with neither a token nor a fallback
+ *              (the reference raises DataError there; that text gets 0 ids)
+ *   d_workspace tp_tokenize_workspace_bytes(total_bytes, n) bytes */
+TP_API int64_t tp_vocab_table_bytes(int32_t n_tokens);
+TP_API int tp_vocab_build(const uint8_t* tok_bytes, const int32_t* tok_off, const int32_t* tok_id,
+                          int32_t n_tokens, const int32_t* byte_ids, void* host_table,
+                          int64_t table_bytes);
+TP_API int64_t tp_tokenize_workspace_bytes(int64_t total_bytes, int32_t n_texts);
+TP_API int tp_tokenize(const void* d_vocab, const uint8_t* d_text, const int64_t* d_text_off,
+                       int32_t n_texts, int64_t total_bytes, int32_t* d_out_ids,
+                       int32_t* d_out_off, int32_t* d_err, void* d_workspace,
+                       int64_t workspace_bytes, void* stream);
+
 /* pixel_unshuffle (tokenred.py:80-103): [h][w][d] patch grid of elem_bytes-sized
  * elements -> [h/r][w/r][d*r*r], output cell (i, j) = input cells (i*r+a, j*r+b) with
  * a outer, b inner.  A pure permutation (bit-exact for any element type). */

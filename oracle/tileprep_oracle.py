@@ -286,3 +286,50 @@ def preprocess_image(arr: np.ndarray, tile_edge: int, max_tiles: int, mean, std,
     plan = plan_float(w, h, tile_edge, max_tiles)
     tiles = tiles_u8(arr, plan)
     return plan, normalize(tiles, mean, std, bf16)
+
+
+# ---------------------------------------------------------------------------
+# greedy tokenizer (tokenizer.py:72-158)
+
+def parse_vocab(text: str):
+    """(id_to_token, byte_ids[256], match_table {bytes: id}, max_token_bytes) of a vocab
+    file's contents: JSON header line, then one token per line, id = line index
+    (tokenizer.py:72-129; validation lives in the product's load_vocab)."""
+    import re
+
+    lines = text.split("\n")
+    if lines and lines[-1] == "":
+        lines.pop()
+    toks = lines[1:]
+    byte_ids = [-1] * 256
+    table = {}
+    max_len = 1
+    for i, tok in enumerate(toks):
+        m = re.match(r"^<0x([0-9A-F]{2})>$", tok)
+        if m:
+            byte_ids[int(m.group(1), 16)] = i
+        else:
+            b = tok.encode("utf-8")
+            table[b] = i
+            max_len = max(max_len, len(b))
+    return toks, byte_ids, table, max_len
+
+
+def tokenize(text: str, byte_ids, table, max_len: int) -> list:
+    """Greedy longest match, byte fallback (tokenizer.py:135-158)."""
+    data = text.encode("utf-8")
+    out, pos, n = [], 0, len(data)
+    while pos < n:
+        for stop in range(min(pos + max_len, n), pos, -1):
+            tid = table.get(data[pos:stop])
+            if tid is not None:
+                out.append(tid)
+                pos = stop
+                break
+        else:
+            bid = byte_ids[data[pos]]
+            if bid < 0:
+                raise ValueError(f"no token or byte fallback for byte 0x{data[pos]:02X}")
+            out.append(bid)
+            pos += 1
+    return out

@@ -37,6 +37,12 @@ from .imgproc import (
     tile_image,
 )
 from .tokenizer import (
+    TokenizedBatch,
+    Vocab,
+    detokenize,
+    load_vocab,
+    tokenize,
+    tokenize_batch,
     PlaceholderExpander,
     SpecialIds,
     TokenSequence,

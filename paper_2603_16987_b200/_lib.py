@@ -74,6 +74,12 @@ SIGNATURES = {
     "tp_supervision_mask": (c_int32, [c_void_p, c_int64, c_int64, c_int32, c_void_p, c_void_p]),
     "tp_pixel_unshuffle": (c_int32, [c_void_p, c_int32, c_int32, c_int64, c_int32, c_int32,
                                      c_void_p, c_void_p]),
+    "tp_vocab_table_bytes": (c_int64, [c_int32]),
+    "tp_vocab_build": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_void_p, c_void_p,
+                                 c_int64]),
+    "tp_tokenize_workspace_bytes": (c_int64, [c_int64, c_int32]),
+    "tp_tokenize": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_int64, c_void_p,
+                              c_void_p, c_void_p, c_void_p, c_int64, c_void_p]),
     "tp_synth": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_uint64, c_int32,
                            c_int64, c_void_p]),
 }

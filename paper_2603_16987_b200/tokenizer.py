@@ -9,16 +9,21 @@ assistant index and mask are computed by tp_expand / tp_supervision_mask.
 whole batch in one launch pair, with the per-marker tile counts taken straight
 from the planner's ``n_images`` tensor (no host round trip).
 
-Vocabulary loading and greedy tokenization stay out of scope (SURVEY.md §2);
-any vocab object with a ``specials`` attribute naming ``image_marker``,
-``image_context`` and ``assistant_header`` ids works (the reference ``Vocab``
-does), and ``load_specials`` reads those ids from a vocab file.
+Greedy tokenization is K6 (tp_tokenize): ``load_vocab``
+parses a vocab file with the reference's validation (tokenizer.py:72-129), the
+vocabulary becomes a device hash table, and ``tokenize`` / ``tokenize_batch`` run
+the longest-match walk on the GPU (tokenizer.py:135-158); ``detokenize`` is host
+string work.  Any vocab object with a ``specials`` attribute naming ``image_marker``,
+``image_context`` and ``assistant_header`` ids works for the expansion (the reference
+``Vocab`` does), and ``load_specials`` reads those ids from a vocab file.
 """
 
 from __future__ import annotations
 
 import json
-from dataclasses import dataclass
+import re
+import threading
+from dataclasses import dataclass, field
 from pathlib import Path
 from typing import Optional, Sequence, Union
 
@@ -79,6 +84,160 @@ def load_specials(path: Union[str, Path]) -> SpecialVocab:
     if len(set(ids.values())) != len(ids):
         raise DataError(f"{path}: special ids must be distinct")
     return SpecialVocab(SpecialIds(**ids))
+
+
+_BYTE_TOKEN = re.compile(r"^<0x([0-9A-F]{2})>$")
+
+
+@dataclass
+class Vocab:
+    """Immutable token table: line number (after the JSON header) = id (tokenizer.py:54-69).
+    ``device_table`` caches the K6 hash table per device."""
+
+    id_to_token: list
+    token_to_id: dict
+    specials: SpecialIds
+    byte_ids: list  # byte value -> fallback token id, -1 when absent
+    match_table: dict
+    max_token_bytes: int
+    _tables: dict = field(default_factory=dict, repr=False, compare=False)
+    _lock: threading.Lock = field(default_factory=threading.Lock, repr=False, compare=False)
+
+    def special_token(self, name: str) -> str:
+        return self.id_to_token[getattr(self.specials, name)]
+
+    def __len__(self) -> int:
+        return len(self.id_to_token)
+
+    def host_table(self) -> np.ndarray:
+        """The K6 hash table (tp_vocab_build) as host bytes."""
+        lib = _lib.load()
+        items = sorted(self.match_table.items(), key=lambda kv: kv[1])
+        blob = b"".join(k for k, _ in items)
+        off = np.zeros(len(items) + 1, dtype=np.int32)
+        off[1:] = np.cumsum([len(k) for k, _ in items])
+        ids = np.asarray([i for _, i in items], dtype=np.int32)
+        bids = np.asarray(self.byte_ids, dtype=np.int32)
+        nbytes = lib.tp_vocab_table_bytes(len(items))
+        table = np.zeros(nbytes, dtype=np.uint8)
+        tok = np.frombuffer(blob, dtype=np.uint8) if blob else np.zeros(1, np.uint8)
+        _lib.call("tp_vocab_build", tok.ctypes.data, off.ctypes.data, ids.ctypes.data,
+                  len(items), bids.ctypes.data, table.ctypes.data, nbytes)
+        return table
+
+    def device_table(self, device) -> torch.Tensor:
+        device = torch.device(device)
+        with self._lock:
+            t = self._tables.get(device.index)
+            if t is None:
+                t = torch.from_numpy(self.host_table()).to(device)
+                self._tables[device.index] = t
+        return t
+
+
+def load_vocab(path: Union[str, Path]) -> Vocab:
+    """Parse a vocab file: one JSON header line naming the special tokens, then one
+    token per line, UTF-8, ids assigned in file order (tokenizer.py:72-129; same
+    checks and DataError messages)."""
+    raw = Path(path).read_text(encoding="utf-8")
+    lines = raw.split("\n")
+    if lines and lines[-1] == "":
+        lines.pop()
+    if not lines:
+        raise DataError(f"{path}: empty vocab file")
+    try:
+        header = json.loads(lines[0])
+    except json.JSONDecodeError as exc:
+        raise DataError(f"{path}: bad JSON header: {exc}") from exc
+    if not isinstance(header, dict) or "specials" not in header:
+        raise DataError(f"{path}: header must be an object with a 'specials' map")
+    id_to_token = lines[1:]
+    token_to_id: dict = {}
+    for i, tok in enumerate(id_to_token):
+        if tok == "":
+            raise DataError(f"{path}: empty token at id {i}")
+        if tok in token_to_id:
+            raise DataError(f"{path}: duplicate token {tok!r} at ids {token_to_id[tok]} and {i}")
+        token_to_id[tok] = i
+    byte_ids = [-1] * 256
+    match_table: dict = {}
+    max_len = 1
+    for tok, i in token_to_id.items():
+        m = _BYTE_TOKEN.match(tok)
+        if m:
+            byte_ids[int(m.group(1), 16)] = i
+        else:
+            b = tok.encode("utf-8")
+            match_table[b] = i
+            max_len = max(max_len, len(b))
+    spec_map = header["specials"]
+    missing = [n for n in _SPECIAL_NAMES if n not in spec_map]
+    if missing:
+        raise DataError(f"{path}: header missing specials {missing}")
+    ids = {}
+    for name in _SPECIAL_NAMES:
+        tok = spec_map[name]
+        if tok not in token_to_id:
+            raise DataError(f"{path}: special {name}={tok!r} has no token line")
+        ids[name] = token_to_id[tok]
+    if len(set(ids.values())) != len(ids):
+        raise DataError(f"{path}: special ids must be distinct")
+    return Vocab(id_to_token=id_to_token, token_to_id=token_to_id, specials=SpecialIds(**ids),
+                 byte_ids=byte_ids, match_table=match_table, max_token_bytes=max_len)
+
+
+@dataclass
+class TokenizedBatch:
+    """Device result of tokenize_batch (int32): text t's ids are
+    ids[off[t]:off[t+1]]; err[t] = 0x100 | byte when a byte has no token."""
+
+    ids: torch.Tensor
+    off: torch.Tensor
+    err: torch.Tensor
+
+
+def tokenize_batch(texts: Sequence, vocab: Vocab, device=None,
+                   stream: Optional[torch.cuda.Stream] = None) -> TokenizedBatch:
+    """K6 over a batch of texts (str or UTF-8 bytes); one H2D copy of the bytes."""
+    device = require_device(device)
+    blobs = [t.encode("utf-8") if isinstance(t, str) else bytes(t) for t in texts]
+    n = len(blobs)
+    off = np.zeros(n + 1, dtype=np.int64)
+    off[1:] = np.cumsum([len(b) for b in blobs])
+    total = int(off[-1])
+    data = np.frombuffer(b"".join(blobs), dtype=np.uint8) if total else np.zeros(1, np.uint8)
+    lib = _lib.load()
+    ws_bytes = lib.tp_tokenize_workspace_bytes(total, n)
+    d_text = torch.from_numpy(data.copy()).to(device, non_blocking=False)
+    d_off = torch.from_numpy(off).to(device)
+    out_ids = torch.empty(max(total, 1), dtype=torch.int32, device=device)
+    out_off = torch.empty(n + 1, dtype=torch.int32, device=device)
+    err = torch.empty(max(n, 1), dtype=torch.int32, device=device)
+    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=device)
+    table = vocab.device_table(device)
+    with torch.cuda.device(device):
+        _lib.call("tp_tokenize", _lib.ptr(table), _lib.ptr(d_text), _lib.ptr(d_off), n, total,
+                  _lib.ptr(out_ids), _lib.ptr(out_off), _lib.ptr(err), _lib.ptr(ws), ws_bytes,
+                  stream_handle(device, stream))
+    return TokenizedBatch(out_ids, out_off, err[:n])
+
+
+def tokenize(text: str, vocab: Vocab) -> list:
+    """Greedy longest-match over the vocabulary, byte fallback for gaps
+    (tokenizer.py:135-158), on the GPU."""
+    res = tokenize_batch([text], vocab)
+    off = res.off.cpu().numpy()
+    e = int(res.err.cpu()[0])
+    if e:
+        raise DataError(f"no token or byte fallback for byte 0x{e & 0xFF:02X}")
+    return res.ids[off[0]: off[1]].cpu().tolist()
+
+
+def detokenize(ids: list, vocab: Vocab) -> str:
+    """Inverse of tokenize (tokenizer.py:161-169); host string work."""
+    byte_of = {i: bytes([b]) for b, i in enumerate(vocab.byte_ids) if i >= 0}
+    chunks = [byte_of[t] if t in byte_of else vocab.id_to_token[t].encode("utf-8") for t in ids]
+    return b"".join(chunks).decode("utf-8")
 
 
 @dataclass

@@ -267,6 +267,23 @@ def main() -> None:
         arrays[f"unshuffle_{i}"] = out.data
         meta.setdefault("unshuffle_shapes", []).append([out.h, out.w, out.d])
 
+    # 8. greedy tokenizer ------------------------------------------------------------
+    # the reference vocabulary file (a data fixture: the GPU box has no /root/reference)
+    vocab_path = Path(args.ref) / "vlmfp" / "data" / "base_vocab.txt"
+    meta["vocab_file"] = vocab_path.read_text(encoding="utf-8")
+    rng = np.random.default_rng(777)
+    alphabet = list("abcdefghijklmnopqrstuvwxyz ABCXYZ0123456789.,;:!?'\"()[]{}<>|_-+=/\\\n\t") + [
+        "\u00e9", "\u00fc", "\u4e2d", "\u6587", "\u2603", "\U0001F600", "<|user|>", "<|image|>",
+        "<IMG_CONTEXT>", "<|assistant|>", "<|bos|>", "<|eos|>", "<|pad|>", "<|", "|>", "describe",
+        "image", "the ", " of ", "\x00", "\x7f"]
+    texts = ["", "a", " ", "<|user|><|image|>describe the image<|assistant|>", "\u2603" * 5,
+             "<<|||>>", "<|assistant|" * 3, "x" * 3000]
+    for _ in range(300):
+        k = int(rng.integers(0, 60))
+        texts.append("".join(str(alphabet[int(j)]) for j in rng.integers(0, len(alphabet), k)))
+    meta["tok_texts"] = texts
+    meta["tok_ids"] = [T.tokenize(t, vocab) for t in texts]
+
     np.savez_compressed(OUT_NPZ, **arrays)
     OUT_JSON.write_text(json.dumps(meta, indent=1, sort_keys=True) + "\n")
     print(f"wrote {OUT_NPZ} ({OUT_NPZ.stat().st_size / 1e6:.2f} MB), {OUT_JSON}")
