@@ -519,7 +519,7 @@ def run_sweep(args, dist, device):
     from paper_2603_16987_b200.engine import TilePreprocessor, synth_packed
     from paper_2603_16987_b200.imgproc import PreprocessConfig
     from paper_2603_16987_b200.sharding import shard
-    from paper_2603_16987_b200.tokenizer import PlaceholderExpander, SpecialIds, SpecialVocab
+    from paper_2603_16987_b200.tokenizer import PlaceholderExpander
     from paper_2603_16987_b200.workloads import Workload, c4, workload_bytes
 
     total = 8192 if args.workload == "c4" else 1024
@@ -538,22 +538,31 @@ def run_sweep(args, dist, device):
     torch.cuda.synchronize(device)
     with_expand = args.workload == "c5"
     if with_expand:
-        vocab = SpecialVocab(SpecialIds(0, 1, 2, 3, 4, 5, 6))
-        prompt = [2, 4, 100, 101, 102, 103, 104, 105, 3]  # <|user|><|image|>...<|assistant|>
+        # rendered prompts tokenized on the device (K6), then expanded with the tile
+        # counts straight from K1 (K3): ids never leave the GPU
+        from paper_2603_16987_b200.tokenizer import DeviceTokenizer, parse_vocab
+        from paper_2603_16987_b200.workloads import c5_texts, synthetic_vocab_text
+
+        vocab = parse_vocab(synthetic_vocab_text(), "synthetic")
         n = len(idx)
-        ids = torch.tensor(prompt * n, dtype=torch.int32, device=device)
-        seq_off = torch.arange(0, len(prompt) * n + 1, len(prompt), dtype=torch.int32,
-                               device=device)
+        tok = DeviceTokenizer(vocab, device)
+        texts = tok.upload(c5_texts(n, wl_all.seed))
+        toks = tok(texts)
         count_off = torch.arange(0, n + 1, dtype=torch.int32, device=device)
         exp = PlaceholderExpander(vocab, 256, device)
-        cap = n * (len(prompt) + 13 * 256)
-        ex = exp(ids, seq_off, outs.plans.n_images, count_off, cap)
+        cap = texts.total + n * 13 * 256
+        ex = exp(toks.ids, toks.off, outs.plans.n_images, count_off, cap)
+        torch.cuda.synchronize(device)
+        assert int(toks.err[:n].abs().sum()) == 0 and int(ex.out_off[-1]) > 0
 
     def step(i=None):
         for ch in chunks:
+            if with_expand:
+                tok(texts, out=toks, stream=stream)
             prep(ch, out=outs, stream=stream)
             if with_expand:
-                exp(ids, seq_off, outs.plans.n_images, count_off, cap, out=ex, stream=stream)
+                exp(toks.ids, toks.off, outs.plans.n_images, count_off, cap, out=ex,
+                    stream=stream)
 
     ms, clk = _timed(step, args.steps, args.warmup, stream, device, dist)
     ms_step = ms / args.steps
@@ -570,14 +579,15 @@ def run_sweep(args, dist, device):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "u8 in, fp32/fp64-exact resample, bf16 out", "data": "synthetic",
             "config": {"workload": ("C4: " if not with_expand else "C5: ") + wl_all.description
-                       + (" + image-token expansion (256 tokens/tile)" if with_expand else ""),
+                       + (" + device tokenization of rendered prompts (K6) and image-token"
+                          " expansion (256 tokens/tile)" if with_expand else ""),
                        "images_total": total, "images_rank0": len(idx),
                        "l2": "inputs larger than L2", "parallelism": f"dp{dist.world} LPT shards"},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak[0],
                          "unit": "GB/s", "frac": round(achieved / peak[0], 4), "traffic": None,
                          "bytes_per_step_rank0": wb["total"],
-                         "note": "whole step (K1+K2" + ("+K3" if with_expand else "") + ")"},
-            "gpu_launches": args.steps * len(chunks) * (4 if with_expand else 2),
+                         "note": "whole step (K1+K2" + ("+K6+K3" if with_expand else "") + ")"},
+            "gpu_launches": args.steps * len(chunks) * (8 if with_expand else 2),
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)

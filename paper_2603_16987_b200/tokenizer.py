@@ -139,7 +139,11 @@ def load_vocab(path: Union[str, Path]) -> Vocab:
     """Parse a vocab file: one JSON header line naming the special tokens, then one
     token per line, UTF-8, ids assigned in file order (tokenizer.py:72-129; same
     checks and DataError messages)."""
-    raw = Path(path).read_text(encoding="utf-8")
+    return parse_vocab(Path(path).read_text(encoding="utf-8"), str(path))
+
+
+def parse_vocab(raw: str, path: str = "<vocab>") -> Vocab:
+    """load_vocab on the file's contents."""
     lines = raw.split("\n")
     if lines and lines[-1] == "":
         lines.pop()
@@ -196,30 +200,62 @@ class TokenizedBatch:
     err: torch.Tensor
 
 
+@dataclass
+class DeviceTexts:
+    """Ragged UTF-8 texts in device memory: text t = data[off[t]:off[t+1]] (int64 off)."""
+
+    data: torch.Tensor  # uint8 [max(total, 1)]
+    off: torch.Tensor  # int64 [n + 1]
+    n: int
+    total: int
+
+
+class DeviceTokenizer:
+    """K6 with device-resident texts and reusable outputs (serving / bench path):
+    ``upload`` once, then ``__call__`` enqueues the four K6 launches on a stream."""
+
+    def __init__(self, vocab: Vocab, device=None):
+        self.vocab = vocab
+        self.device = require_device(device)
+        self.table = vocab.device_table(self.device)
+        self._ws: Optional[torch.Tensor] = None
+
+    def upload(self, texts: Sequence) -> DeviceTexts:
+        blobs = [t.encode("utf-8") if isinstance(t, str) else bytes(t) for t in texts]
+        off = np.zeros(len(blobs) + 1, dtype=np.int64)
+        off[1:] = np.cumsum([len(b) for b in blobs])
+        total = int(off[-1])
+        data = np.frombuffer(b"".join(blobs), dtype=np.uint8) if total else np.zeros(1, np.uint8)
+        return DeviceTexts(torch.from_numpy(data.copy()).to(self.device),
+                           torch.from_numpy(off).to(self.device), len(blobs), total)
+
+    def alloc(self, texts: DeviceTexts) -> TokenizedBatch:
+        d = self.device
+        return TokenizedBatch(torch.empty(max(texts.total, 1), dtype=torch.int32, device=d),
+                              torch.empty(texts.n + 1, dtype=torch.int32, device=d),
+                              torch.empty(max(texts.n, 1), dtype=torch.int32, device=d))
+
+    def __call__(self, texts: DeviceTexts, out: Optional[TokenizedBatch] = None,
+                 stream: Optional[torch.cuda.Stream] = None) -> TokenizedBatch:
+        out = out or self.alloc(texts)
+        ws_bytes = int(_lib.load().tp_tokenize_workspace_bytes(texts.total, texts.n))
+        if self._ws is None or self._ws.numel() < ws_bytes:
+            self._ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=self.device)
+        with torch.cuda.device(self.device):
+            _lib.call("tp_tokenize", _lib.ptr(self.table), _lib.ptr(texts.data),
+                      _lib.ptr(texts.off), texts.n, texts.total, _lib.ptr(out.ids),
+                      _lib.ptr(out.off), _lib.ptr(out.err), _lib.ptr(self._ws), ws_bytes,
+                      stream_handle(self.device, stream))
+        return out
+
+
 def tokenize_batch(texts: Sequence, vocab: Vocab, device=None,
                    stream: Optional[torch.cuda.Stream] = None) -> TokenizedBatch:
     """K6 over a batch of texts (str or UTF-8 bytes); one H2D copy of the bytes."""
-    device = require_device(device)
-    blobs = [t.encode("utf-8") if isinstance(t, str) else bytes(t) for t in texts]
-    n = len(blobs)
-    off = np.zeros(n + 1, dtype=np.int64)
-    off[1:] = np.cumsum([len(b) for b in blobs])
-    total = int(off[-1])
-    data = np.frombuffer(b"".join(blobs), dtype=np.uint8) if total else np.zeros(1, np.uint8)
-    lib = _lib.load()
-    ws_bytes = lib.tp_tokenize_workspace_bytes(total, n)
-    d_text = torch.from_numpy(data.copy()).to(device, non_blocking=False)
-    d_off = torch.from_numpy(off).to(device)
-    out_ids = torch.empty(max(total, 1), dtype=torch.int32, device=device)
-    out_off = torch.empty(n + 1, dtype=torch.int32, device=device)
-    err = torch.empty(max(n, 1), dtype=torch.int32, device=device)
-    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=device)
-    table = vocab.device_table(device)
-    with torch.cuda.device(device):
-        _lib.call("tp_tokenize", _lib.ptr(table), _lib.ptr(d_text), _lib.ptr(d_off), n, total,
-                  _lib.ptr(out_ids), _lib.ptr(out_off), _lib.ptr(err), _lib.ptr(ws), ws_bytes,
-                  stream_handle(device, stream))
-    return TokenizedBatch(out_ids, out_off, err[:n])
+    tok = DeviceTokenizer(vocab, device)
+    dt = tok.upload(texts)
+    res = tok(dt, stream=stream)
+    return TokenizedBatch(res.ids, res.off, res.err[: dt.n])
 
 
 def tokenize(text: str, vocab: Vocab) -> list:

@@ -129,3 +129,48 @@ def workload_bytes(wl: Workload, with_u8: bool = False) -> dict:
             tot[k] += cache[key][k]
     tot["total"] = tot["read"] + tot["write"]
     return tot
+
+
+# ---------------------------------------------------------------------------
+# C5 prompts: rendered chat prompts tokenized on the device (K6)
+
+C5_PROMPTS = [
+    "describe the image",
+    "what is in the picture?",
+    "count the objects in the scene",
+    "describe every region with a caption",
+    "what color is the car on the left?",
+    "read the text in the image",
+    "is there a person in this photo? answer yes or no",
+    "list the objects from left to right",
+    "where was this picture taken?",
+    "summarize the chart in one sentence",
+    "what is unusual about this image?",
+    "give a detailed description of the scene, including the background",
+]
+
+_C5_WORDS = ["describe", "the", "image", "picture", "what", "count", "objects", "scene",
+             "every", "region", "caption", "color", "left", "right", "text", "person",
+             "photo", "answer", "where", "chart", "sentence", "unusual", "detailed", " the ",
+             " of ", " in ", "ing", "tion"]
+
+
+def synthetic_vocab_text() -> str:
+    """A vocab file in the reference format (JSON header naming the specials, one token
+    per line): the specials, all 256 byte-fallback tokens, printable ASCII and a few
+    words. Synthetic (the reference vocabulary does not travel to the GPU box)."""
+    specials = {"bos": "<|bos|>", "eos": "<|eos|>", "user_header": "<|user|>",
+                "assistant_header": "<|assistant|>", "image_marker": "<|image|>",
+                "image_context": "<IMG_CONTEXT>", "pad": "<|pad|>"}
+    import json as _json
+
+    toks = list(specials.values()) + [f"<0x{b:02X}>" for b in range(256)]
+    toks += [chr(c) for c in range(32, 127)] + _C5_WORDS
+    return _json.dumps({"specials": specials}) + "\n" + "\n".join(toks) + "\n"
+
+
+def c5_texts(n: int, seed: int = 20261018) -> list:
+    """n rendered prompts: "<|user|><|image|>" + prompt + "<|assistant|>"."""
+    rng = np.random.default_rng(seed)
+    return ["<|user|><|image|>" + C5_PROMPTS[int(rng.integers(len(C5_PROMPTS)))] + "<|assistant|>"
+            for _ in range(n)]
