@@ -440,3 +440,29 @@ def test_expand_errors_and_capacity_flags():
     small = exp(ids[:3], seq_off[:2], counts[:1], count_off[:2], capacity=5)
     torch.cuda.synchronize()
     assert int(small.out_off[-1]) == -1  # capacity overflow is flagged, nothing written
+
+
+# ---------------------------------------------------------------------------
+# geometry extremes: rows wider than a shared-memory stage (column chunks), very tall
+# images, more tiles per image than the per-image tile cache, large tile edges
+
+@pytest.mark.parametrize("w,h,e,mt", [(30000, 40, 448, 12), (40, 30000, 448, 12),
+                                      (9000, 700, 256, 40), (1500, 1500, 1024, 4),
+                                      (2000, 1200, 96, 64)])
+def test_fast_equals_exact_geometry_extremes(w, h, e, mt):
+    cfg = PreprocessConfig(tile_edge=e, max_tiles=mt, mean=IMAGENET_MEAN, std=IMAGENET_STD,
+                           reduced_precision_normalize=True)
+    wh = np.array([[w, h], [h, w]])
+    T = _fast_vs_exact(wh, 31, 0, cfg)
+    assert T >= 2
+    T = _fast_vs_exact(wh, 32, 1, cfg, layout="NHWC")
+
+
+def test_many_tiles_per_image_vs_oracle():
+    # 17+ tiles per image exceeds the producer's per-image tile cache (16)
+    arr = make_input(300, 1700, 3, "random", 77)
+    cfg = PreprocessConfig(tile_edge=64, max_tiles=40)
+    _, pv, u8 = _run_engine([arr], cfg)
+    plan = O.plan_float(1700, 300, 64, 40)
+    assert plan[0] * plan[1] + plan[3] > 16
+    assert np.array_equal(u8, O.tiles_u8(arr, plan))
