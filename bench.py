@@ -481,10 +481,24 @@ def batch1_latency(cfg, device, iters: int):
 
     p50, p99 = timed(dev_only)
     h50, h99 = timed(with_h2d)
+    f50, _ = timed(_empty_graph(device, s))
     return {"p50_ms": round(p50, 4), "p99_ms": round(p99, 4), "h2d_p50_ms": round(h50, 4),
             "h2d_p99_ms": round(h99, 4), "iters": iters,
+            "graph_floor_p50_ms": round(f50, 4),
             "workload": "1 x 1920x1080, E=448 InternVL3-2B tiling, bf16 NCHW; CUDA graph "
                         "(K1+K2); h2d_* add the 6.2 MB pinned upload"}
+
+
+def _empty_graph(device, stream):
+    """Replay of a one-tiny-kernel CUDA graph: the launch + event floor under which no
+    batch-1 latency measured this way can go (reported beside p50)."""
+    import torch
+
+    x = torch.zeros(1, device=device)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        x.add_(1)
+    return g.replay
 
 
 def _timed(fn, steps: int, warmup: int, stream, device, dist, events_per_step=None):
@@ -629,6 +643,16 @@ def run_single(args, dist, device):
             if k >= 50:
                 sink.append(a.elapsed_time(b))
     ts, th = np.array(ts), np.array(th)
+    floor_fn, tf = _empty_graph(device, s), []
+    for k in range(550):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        with torch.cuda.stream(s):
+            floor_fn()
+        b.record(s)
+        b.synchronize()
+        if k >= 50:
+            tf.append(a.elapsed_time(b))
     wb = workload_bytes(wl)
     if dist.rank == 0:
         line = {
@@ -641,6 +665,7 @@ def run_single(args, dist, device):
             "p99_ms": round(float(np.percentile(ts, 99)), 4),
             "h2d_p50_ms": round(float(np.percentile(th, 50)), 4),
             "h2d_p99_ms": round(float(np.percentile(th, 99)), 4),
+            "graph_floor_p50_ms": round(float(np.median(tf)), 4),
             "algorithmic_bytes": wb["total"],
         }
         print(json.dumps(line), flush=True)
