@@ -66,6 +66,9 @@ namespace {
 #else
 #define TP_LD(p) __ldca(p)
 #endif
+#ifndef TP_K2_MIN_ITEMS  // small batches: halve the band until items >= this x CTAs
+#define TP_K2_MIN_ITEMS 2
+#endif
 #ifndef TP_K2_ROW_BALANCE
 #define TP_K2_ROW_BALANCE 1
 #endif
@@ -1045,7 +1048,8 @@ __global__ void __launch_bounds__(kMaxThreads, kCtasPerSm)
   // band height: kBand rows, smaller when a small batch would leave SMs idle (batch-1
   // latency); every CTA derives the same value from the device-side tile count
   int band = kBand;
-  while (band > 2 && static_cast<int64_t>(all_tiles) * ((E + band - 1) / band) < 2 * gridDim.x)
+  while (band > 2 &&
+         static_cast<int64_t>(all_tiles) * ((E + band - 1) / band) < TP_K2_MIN_ITEMS * gridDim.x)
     band >>= 1;
   const int bands = (E + band - 1) / band;
   const int64_t items = cap_tiles > 0 ? static_cast<int64_t>(all_tiles) * bands : 0;

@@ -1,0 +1,4 @@
+for v in build/variants/*/; do
+  name=$(basename $v)
+  TILEPREP_LIB=$PWD/$v/libtileprep.so timeout 300 python tools/latency_breakdown.py > gpurun_out/lat_${name}.log 2>&1
+done
