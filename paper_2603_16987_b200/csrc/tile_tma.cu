@@ -1074,19 +1074,23 @@ int launch_variant(const uint8_t* src, const int64_t* src_off, const int32_t* wh
                    cudaStream_t stream) {
   auto kern = k_tile_tma<C, OutT, LAYOUT, WRITE_OUT, WRITE_U8, AFFINE, EK>;
   const size_t smem = tma_smem_bytes<C, OutT>();
-  static bool configured = false;  // one per template instance
-  static int per_sm = 0;
+  // per device and template instance: the shared-memory opt-in and the occupancy for
+  // each block size (idempotent, so concurrent first calls are harmless)
+  constexpr int kDevs = 64;
+  static int per_sm_of[kDevs][(kMaxThreads / 32) + 1];  // 0 = not yet configured
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kDevs)
+    return set_error(TP_ERR_CUDA, "tp_tile: no usable current device");
   const int segs = (E + 63) / 64;  // 64-pixel segments: one consumer warp each
-  const int threads = 32 + 32 * min((kMaxThreads - 32) / 32, max(1, segs));
-  static int cached_threads = -1;
-  if (!configured) {
+  const int warps = 1 + min((kMaxThreads - 32) / 32, max(1, segs));
+  const int threads = 32 * warps;
+  int per_sm = per_sm_of[dev][warps];
+  if (per_sm == 0) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));
-    configured = true;
-  }
-  if (threads != cached_threads) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
-    cached_threads = threads;
+    if (per_sm <= 0) return set_error(TP_ERR_CUDA, "tp_tile: kernel does not fit an SM");
+    per_sm_of[dev][warps] = per_sm;
   }
   const int grid = max(1, per_sm) * max(1, device_sm_count());
   cudaError_t err = cudaSuccess;
