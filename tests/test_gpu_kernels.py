@@ -466,3 +466,43 @@ def test_many_tiles_per_image_vs_oracle():
     plan = O.plan_float(1700, 300, 64, 40)
     assert plan[0] * plan[1] + plan[3] > 16
     assert np.array_equal(u8, O.tiles_u8(arr, plan))
+
+
+# ---------------------------------------------------------------------------
+# randomized configurations: every dtype/layout/side-output/normalize-form combination
+# on random sizes and tile edges, checked image by image against the oracle
+
+def test_randomized_configs_vs_oracle():
+    rng = np.random.default_rng(2026)
+    means = [((0.5,) * 3, (0.5,) * 3), (IMAGENET_MEAN, IMAGENET_STD),
+             ((0.48145466, 0.4578275, 0.40821073), (0.26862954, 0.26130258, 0.27577711))]
+    for case in range(40):
+        c = 3 if case % 5 else 1
+        n = int(rng.integers(1, 6))
+        e = int(rng.choice([7, 16, 33, 64, 100, 448]))
+        mt = int(rng.integers(1, 14))
+        arrs = [make_input(int(rng.integers(1, 300)), int(rng.integers(1, 300)), c,
+                           "random" if rng.random() < 0.5 else "smooth", 1000 * case + i)
+                for i in range(n)]
+        mean, std = means[case % 3]
+        bf16 = bool(case % 2)
+        cfg = PreprocessConfig(tile_edge=e, max_tiles=mt, mean=mean[:c], std=std[:c],
+                               reduced_precision_normalize=bf16)
+        layout = "NCHW" if case % 4 < 2 else "NHWC"
+        emit = bool((case // 2) % 2)
+        out, pv, u8 = _run_engine(arrs, cfg, layout=layout, emit_uint8=emit)
+        off = out.plans.tile_off.cpu().numpy()
+        for k, a in enumerate(arrs):
+            plan = O.plan_float(a.shape[1], a.shape[0], e, mt)
+            want = O.tiles_u8(a, plan)
+            if emit:
+                assert np.array_equal(u8[off[k]: off[k + 1]], want), (case, k)
+            wn = O.normalize(want, mean[:c], std[:c], bf16)
+            got = pv[off[k]: off[k + 1]]
+            if layout == "NCHW":
+                wn = wn.transpose(0, 3, 1, 2)
+            if bf16:
+                assert np.array_equal(got.view(torch.int16).numpy().view(np.uint16),
+                                      wn.view(np.uint16)), (case, k)
+            else:
+                assert np.array_equal(got.numpy(), wn), (case, k)
