@@ -53,9 +53,6 @@ namespace {
 #ifndef TP_K2_DEBUG_NOLOAD
 #define TP_K2_DEBUG_NOLOAD 0
 #endif
-#ifndef TP_K2_PAIR  // consumer rows in pairs (one basic block) instead of a row pipeline
-#define TP_K2_PAIR 0
-#endif
 // loads of predecessor-written data: 1 = ld.global.cg (L2), 2 = ld.global.ca (L1+L2);
 // never the .nc path that plain loads through const __restrict__ pointers compile to
 #ifndef TP_K2_LDMODE
@@ -71,9 +68,6 @@ namespace {
 #endif
 #ifndef TP_K2_ROW_BALANCE
 #define TP_K2_ROW_BALANCE 1
-#endif
-#ifndef TP_K2_BATCHED_FALLBACK
-#define TP_K2_BATCHED_FALLBACK 0
 #endif
 #ifndef TP_K2_CTAS_PER_SM
 #define TP_K2_CTAS_PER_SM 2
@@ -269,10 +263,6 @@ __device__ __forceinline__ float biased_byte(uint32_t g0, uint32_t g1, int k) {
 
 __device__ __forceinline__ uint32_t byte_of(uint32_t g0, uint32_t g1, int k) {
   return ((k < 4 ? g0 : g1) >> ((k & 3) * 8)) & 0xFFu;
-}
-// byte k (0..7, run-time) of (g0, g1), zero-extended: one select + one byte permute
-__device__ __forceinline__ uint32_t byte_dyn(uint32_t g0, uint32_t g1, int k) {
-  return __byte_perm(k < 4 ? g0 : g1, 0u, 0x4440u | static_cast<uint32_t>(k & 3));
 }
 
 // The fast path (consumer loop below) computes, per value, with biased taps
@@ -780,52 +770,21 @@ __device__ __forceinline__ void consume_pair_rows(
   // exact fp64 recomputation of the flagged values of row jj
   auto fix = [&](int jj, const PixTaps& a, const PixTaps& b, uint32_t (&ka)[C],
                  uint32_t (&kb)[C], const uint32_t (&xa)[C], const uint32_t (&xb)[C]) {
-      const double fy64 = ldsd(pr.base + kPhFy64 + 8 * jj),
-                   omfy64 = ldsd(pr.base + kPhOmfy64 + 8 * jj);
-#if TP_K2_BATCHED_FALLBACK
-      // Warp-cooperative: every lane with a flagged value recomputes one per pass (flags
-      // are rare, so one pass is the norm) instead of 2C divergent per-value branches.
-      uint32_t m = 0;
+    const double fy64 = ldsd(pr.base + kPhFy64 + 8 * jj),
+                 omfy64 = ldsd(pr.base + kPhOmfy64 + 8 * jj);
+    constexpr uint32_t kOut = AFF ? 0x4B400000u : kKrawBias;  // code of value 0
 #pragma unroll
-      for (int c = 0; c < C; ++c)
-        m |= (xa[c] < kAmbLimit ? 1u << c : 0u) | (xb[c] < kAmbLimit ? 1u << (C + c) : 0u);
-      while (m) {
-        const int idx = __ffs(m) - 1;
-        m &= m - 1;
-        const bool pb = idx >= C;
-        const int c = pb ? idx - C : idx;
-        const uint32_t g00 = pb ? b.r0w0 : a.r0w0, g01 = pb ? b.r0w1 : a.r0w1;
-        const uint32_t g10 = pb ? b.r1w0 : a.r1w0, g11 = pb ? b.r1w1 : a.r1w1;
-        const double fx64 = pb ? fxb64 : fxa64, omfx64 = pb ? omfxb64 : omfxa64;
-        const uint32_t k = (AFF ? 0x4B400000u : kKrawBias) + blend_exact_fast(byte_dyn(g00, g01, c),
-                                                        byte_dyn(g00, g01, C + c),
-                                                        byte_dyn(g10, g11, c),
-                                                        byte_dyn(g10, g11, C + c), fy64, omfy64,
-                                                        fx64, omfx64);
-#pragma unroll
-        for (int cc = 0; cc < C; ++cc) {
-          ka[cc] = idx == cc ? k : ka[cc];
-          kb[cc] = idx == C + cc ? k : kb[cc];
-        }
-      }
-#else
-#pragma unroll
-      for (int c = 0; c < C; ++c) {
-        if (xa[c] < kAmbLimit)
-          ka[c] = (AFF ? 0x4B400000u : kKrawBias) + blend_exact_fast(byte_of(a.r0w0, a.r0w1, c),
-                                               byte_of(a.r0w0, a.r0w1, C + c),
-                                               byte_of(a.r1w0, a.r1w1, c),
-                                               byte_of(a.r1w0, a.r1w1, C + c), fy64, omfy64,
-                                               fxa64, omfxa64);
-        if (xb[c] < kAmbLimit)
-          kb[c] = (AFF ? 0x4B400000u : kKrawBias) + blend_exact_fast(byte_of(b.r0w0, b.r0w1, c),
-                                               byte_of(b.r0w0, b.r0w1, C + c),
-                                               byte_of(b.r1w0, b.r1w1, c),
-                                               byte_of(b.r1w0, b.r1w1, C + c), fy64, omfy64,
-                                               fxb64, omfxb64);
-      }
-#endif
-      };
+    for (int c = 0; c < C; ++c) {
+      if (xa[c] < kAmbLimit)
+        ka[c] = kOut + blend_exact_fast(byte_of(a.r0w0, a.r0w1, c), byte_of(a.r0w0, a.r0w1, C + c),
+                                        byte_of(a.r1w0, a.r1w1, c), byte_of(a.r1w0, a.r1w1, C + c),
+                                        fy64, omfy64, fxa64, omfxa64);
+      if (xb[c] < kAmbLimit)
+        kb[c] = kOut + blend_exact_fast(byte_of(b.r0w0, b.r0w1, c), byte_of(b.r0w0, b.r0w1, C + c),
+                                        byte_of(b.r1w0, b.r1w1, c), byte_of(b.r1w0, b.r1w1, C + c),
+                                        fy64, omfy64, fxb64, omfxb64);
+    }
+  };
   // LUT + stores of row jj (rows in order: the NCHW row pointers advance by one row)
   auto emit = [&](int jj, const uint32_t (&ka)[C], const uint32_t (&kb)[C]) {
     const int j = j0 + jj;
@@ -883,31 +842,6 @@ __device__ __forceinline__ void consume_pair_rows(
     if (fast(jj, a, b, ka, kb, xa, xb) < kAmbLimit) fix(jj, a, b, ka, kb, xa, xb);
     emit(jj, ka, kb);
   };
-#if TP_K2_PAIR
-  // rows in pairs: one basic block computes both rows (one window branch per pair), so
-  // the scheduler can overlap one row's LUT loads and stores with the other's math
-  int jj = 0;
-  for (; jj + 1 < nrows; jj += 2) {
-    const PixTaps a0 = fetch_pix<UNIFORM>(pr, jj, sbase, mis, xoa, wa, sha);
-    const PixTaps b0 = fetch_pix<UNIFORM>(pr, jj, sbase, mis, xob, wb, shb);
-    const PixTaps a1 = fetch_pix<UNIFORM>(pr, jj + 1, sbase, mis, xoa, wa, sha);
-    const PixTaps b1 = fetch_pix<UNIFORM>(pr, jj + 1, sbase, mis, xob, wb, shb);
-    uint32_t ka0[C], kb0[C], xa0[C], xb0[C], ka1[C], kb1[C], xa1[C], xb1[C];
-    const uint32_t w0 = fast(jj, a0, b0, ka0, kb0, xa0, xb0);
-    const uint32_t w1 = fast(jj + 1, a1, b1, ka1, kb1, xa1, xb1);
-    if (min(w0, w1) < kAmbLimit) {
-      if (w0 < kAmbLimit) fix(jj, a0, b0, ka0, kb0, xa0, xb0);
-      if (w1 < kAmbLimit) fix(jj + 1, a1, b1, ka1, kb1, xa1, xb1);
-    }
-    emit(jj, ka0, kb0);
-    emit(jj + 1, ka1, kb1);
-  }
-  if (jj < nrows) {
-    const PixTaps a0 = fetch_pix<UNIFORM>(pr, jj, sbase, mis, xoa, wa, sha);
-    const PixTaps b0 = fetch_pix<UNIFORM>(pr, jj, sbase, mis, xob, wb, shb);
-    row(jj, a0, b0);
-  }
-#else
   // software pipeline, unrolled by two so the prefetched taps need no register moves
   PixTaps a0 = fetch_pix<UNIFORM>(pr, 0, sbase, mis, xoa, wa, sha);
   PixTaps b0 = fetch_pix<UNIFORM>(pr, 0, sbase, mis, xob, wb, shb);
@@ -923,7 +857,6 @@ __device__ __forceinline__ void consume_pair_rows(
     row(jj + 1, a1, b1);
   }
   if (jj < nrows) row(jj, a0, b0);
-#endif
 }
 
 template <int C, typename OutT, int LAYOUT, bool WRITE_OUT, bool WRITE_U8, bool AFFINE, int EK>
