@@ -15,18 +15,30 @@ ROOT = Path(__file__).resolve().parent.parent
 
 CHILD = r"""
 import json, sys, torch
+import numpy as np
 sys.path.insert(0, %(root)r)
 from paper_2603_16987_b200.engine import TilePreprocessor, synth_packed
 from paper_2603_16987_b200.imgproc import PreprocessConfig
-from paper_2603_16987_b200.workloads import c2, c4
+from paper_2603_16987_b200.workloads import Workload, c2, c3, c4, workload_bytes
 dev = torch.device("cuda:0")
 res = {}
-for name, wl, n in (("c2", c2(), 200), ("c4k", c4(1024), 20)):
+w3 = c3()
+c3b = Workload("C3x32", "32 x 4K", np.repeat(w3.wh, 32, axis=0), w3.tile_edge, w3.max_tiles,
+               w3.mean, w3.std, w3.bf16, w3.seed)
+up = Workload("UP", "64 x 640x480 (3x4 upscaled)", np.repeat(np.array([[640, 480]], np.int32), 64, axis=0),
+              448, 12, w3.mean, w3.std, True, 5)
+tall = Workload("TALL", "64 x 1080x1920 portrait", np.repeat(np.array([[1080, 1920]], np.int32), 64, axis=0),
+                448, 12, w3.mean, w3.std, True, 6)
+import os
+sel = os.environ.get("ABW", "c2,c4k,c3x32").split(",")
+for name, wl, n in [x for x in (("c2", c2(), 200), ("c4k", c4(1024), 20), ("c3x32", c3b, 100),
+                                ("up", up, 50), ("tall", tall, 100)) if x[0] in sel]:
     cfg = PreprocessConfig(tile_edge=wl.tile_edge, max_tiles=wl.max_tiles, mean=wl.mean,
                            std=wl.std, reduced_precision_normalize=wl.bf16)
     imgs = synth_packed(wl.wh, 3, dev, seed=wl.seed, kind=0)
     prep = TilePreprocessor(cfg, dev)
     out = prep(imgs)
+    torch.cuda.synchronize()  # synth + K1 ran on the default stream; the loops use s
     s = torch.cuda.Stream(dev)
     for _ in range(5):
         prep.tile(imgs, out.plans, out.pixel_values, None, s)
@@ -38,6 +50,7 @@ for name, wl, n in (("c2", c2(), 200), ("c4k", c4(1024), 20)):
     b.record(s)
     torch.cuda.synchronize()
     res[name + "_us"] = round(a.elapsed_time(b) / n * 1e3, 2)
+    res[name + "_frac"] = round(workload_bytes(wl)["total"] / (res[name + "_us"] * 1e-6) / 6545.3e9, 4)
     a.record(s)
     for _ in range(n):
         prep.plan(imgs, out.plans, s)
@@ -52,6 +65,7 @@ print(json.dumps(res))
 
 def main():
     rounds = int(sys.argv[1]) if len(sys.argv) > 1 else 3
+    # ABW=c2,c4k,c3x32,up,tall selects the workloads (default: c2,c4k,c3x32)
     variants = sorted(p for p in (ROOT / "build" / "variants").glob("*/libtileprep.so"))
     results = {p.parent.name: [] for p in variants}
     for r in range(rounds):
