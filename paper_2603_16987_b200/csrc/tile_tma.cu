@@ -106,6 +106,27 @@ struct TileGeo {
   int RW, RH, oy0, ox0, cwid, pad;
 };
 
+#ifndef TP_K2_TRACE  // diagnostic build: per-phase clock64 stamps of producer and consumer
+#define TP_K2_TRACE 0
+#endif
+#if TP_K2_TRACE
+constexpr int kTraceCtas = 296, kTracePhases = 96;
+// [cta][phase]: item-start flag, plan start, copies issued, consumer wait start,
+// consumer data ready, consumer phase done
+__device__ unsigned long long g_k2_trace[kTraceCtas][kTracePhases][6];
+__device__ unsigned long long g_k2_cta[kTraceCtas][3];  // smid, globaltimer start, end
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned long long clk() {
+  unsigned long long c;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+  return c;
+}
+#endif
+
 struct __align__(16) SmemHeader {
   Phase ph[kStages];
   TileGeo tg[kTileCache];  // producer: tiles of the current image
@@ -421,7 +442,20 @@ __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restri
   // (the range is contiguous), so no chain of dependent global loads per item
   int kimg = it_begin < it_end ? find_item_image(tile_off, n, it_begin, bands) : 0;
   int toff0 = TP_LD(tile_off + kimg), toff1 = TP_LD(tile_off + kimg + 1);
+#if TP_K2_TRACE
+  int tr_phase = 0;
+  unsigned long long tr_item = 0;
+  if (lane == 0 && blockIdx.x < kTraceCtas) {
+    unsigned int smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_k2_cta[blockIdx.x][0] = smid;
+    g_k2_cta[blockIdx.x][1] = gtime();
+  }
+#endif
   for (int64_t item = it_begin; item < it_end; ++item) {
+#if TP_K2_TRACE
+    tr_item = clk();
+#endif
     // item order: (image, band, tile): the tiles and the thumbnail of an image read
     // the same source rows within n_images consecutive items, so the second read
     // hits L2 instead of HBM
@@ -483,6 +517,9 @@ __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restri
       const int rb = (axis_tap(ox0 + c0 + cw - 1, W, sx).i1 - xlo + 1) * C;
       int jj = 0;
       while (jj < nrows) {
+#if TP_K2_TRACE
+        const unsigned long long tr_plan = jj == 0 && c0 == 0 ? tr_item : clk();
+#endif
         const int s = stage;
         const int nleft = nrows - jj;
         // ---- entries
@@ -579,6 +616,16 @@ __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restri
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
+#if TP_K2_TRACE
+        if (lane == 0 && blockIdx.x < kTraceCtas && tr_phase < kTracePhases) {
+          g_k2_trace[blockIdx.x][tr_phase][0] = ((jj == 0 && c0 == 0) ? 1 : 0) |
+                                                (t == nimg - 1 && nimg > 1 ? 2 : 0) |
+                                                (static_cast<unsigned long long>(nr) << 8);
+          g_k2_trace[blockIdx.x][tr_phase][1] = tr_plan;
+          g_k2_trace[blockIdx.x][tr_phase][2] = clk();
+        }
+        ++tr_phase;
+#endif
         if (lane == 0) mbar_arrive_expect_tx(&hdr.full[s], static_cast<uint32_t>(tx));
         __syncwarp();
         if (bytes > 0)
@@ -884,8 +931,17 @@ __device__ void consume(SmemHeader& hdr, const uint8_t* arena, const OutT* s_lut
     aff_b[c] = AFFINE ? TP_LD(aff + 4 + c) : 0.f;
   }
   const uint32_t ph0 = smem_u32(&hdr.ph[0]);
+#if TP_K2_TRACE
+  int tr_phase = 0;
+#endif
   while (true) {
+#if TP_K2_TRACE
+    const unsigned long long tr_w0 = clk();
+#endif
     mbar_wait(&hdr.full[stage], parity);
+#if TP_K2_TRACE
+    const unsigned long long tr_w1 = clk();
+#endif
     PhaseRows pr;
     pr.base = ph0 + stage * static_cast<uint32_t>(sizeof(Phase));
     const int4 h0 = lds128(pr.base), h1 = lds128(pr.base + 16);
@@ -936,6 +992,15 @@ __device__ void consume(SmemHeader& hdr, const uint8_t* arena, const OutT* s_lut
             pr, g, j0, nrows, mis, sbase, lut_u32, ia, ib, has_a, has_b, xoa, xob, fxa, fxb,
             fxa64, omfxa64, fxb64, omfxb64, out, out_u8, tile_a, aff_a, aff_b, E);
     }
+#if TP_K2_TRACE
+    if (cwarp == 0 && lane == 0 && blockIdx.x < kTraceCtas && tr_phase < kTracePhases) {
+      g_k2_trace[blockIdx.x][tr_phase][3] = tr_w0;
+      g_k2_trace[blockIdx.x][tr_phase][4] = tr_w1;
+      g_k2_trace[blockIdx.x][tr_phase][5] = clk();
+      g_k2_cta[blockIdx.x][2] = gtime();
+    }
+    ++tr_phase;
+#endif
     mbar_arrive(&hdr.empty[stage]);
     if (++stage == kStages) {
       stage = 0;
@@ -1082,3 +1147,19 @@ TP_INSTANTIATE(3, __nv_bfloat16, TP_LAYOUT_NHWC, true)
 #undef TP_INSTANTIATE
 
 }  // namespace tp
+
+#if TP_K2_TRACE
+// diagnostic export (trace builds only; not part of include/tileprep.h)
+extern "C" __attribute__((visibility("default"))) int tp_debug_k2_trace(void* host, int64_t bytes) {
+  if (bytes < static_cast<int64_t>(sizeof(tp::g_k2_trace))) return -1;
+  return cudaMemcpyFromSymbol(host, tp::g_k2_trace, sizeof(tp::g_k2_trace)) == cudaSuccess ? 0 : -2;
+}
+extern "C" __attribute__((visibility("default"))) int tp_debug_k2_cta(void* host, int64_t bytes) {
+  if (bytes < static_cast<int64_t>(sizeof(tp::g_k2_cta))) return -1;
+  return cudaMemcpyFromSymbol(host, tp::g_k2_cta, sizeof(tp::g_k2_cta)) == cudaSuccess ? 0 : -2;
+}
+extern "C" __attribute__((visibility("default"))) int tp_debug_k2_trace_clear() {
+  static unsigned long long zeros[tp::kTraceCtas][tp::kTracePhases][6];
+  return cudaMemcpyToSymbol(tp::g_k2_trace, zeros, sizeof(zeros)) == cudaSuccess ? 0 : -2;
+}
+#endif
