@@ -4,6 +4,8 @@ reference itself (tests/golden/make_golden.py), plus live cross-checks when
 
 from __future__ import annotations
 
+from pathlib import Path
+
 import numpy as np
 import pytest
 from hypothesis import given, settings, strategies as st
@@ -184,3 +186,14 @@ def test_pixel_unshuffle_matches_golden(golden):
         got = O.pixel_unshuffle(grid, r)
         assert list(got.shape) == meta["unshuffle_shapes"][i]
         assert np.array_equal(got.reshape(-1), data[f"unshuffle_{i}"])
+
+
+@pytest.mark.reference
+@settings(max_examples=400, deadline=None)
+@given(text=st.text(max_size=80))
+def test_tokenize_vs_live_reference(reference, text):
+    from vlmfp import tokenizer as T
+
+    vocab = T.load_vocab(Path("/root/reference/pkg/src/vlmfp/data/base_vocab.txt"))
+    want = T.tokenize(text, vocab)
+    assert O.tokenize(text, vocab.byte_ids, vocab.match_table, vocab.max_token_bytes) == want
