@@ -159,6 +159,15 @@ class ClockSampler:
         self._thr = threading.Thread(target=self._run, daemon=True)
         self._thr.start()
 
+    def sample_now(self):
+        """One sample from the calling thread: called right after the timed steps are
+        enqueued, while the GPU is still executing them, so even a short timed region
+        has a sample taken under load."""
+        try:
+            self._sample_nvml() if self._nvml else self._sample_smi()
+        except Exception:
+            pass
+
     def _run(self):
         while True:
             try:
@@ -320,6 +329,7 @@ def main():
     for i in range(args.steps):
         step(i)
     stop.record(stream)
+    clocks.sample_now()
     torch.cuda.synchronize(device)
     dist.barrier(device)
     clk = clocks.stop()
@@ -538,6 +548,7 @@ def _timed(fn, steps: int, warmup: int, stream, device, dist, events_per_step=No
         for i in range(steps):
             fn(i)
     b.record(stream)
+    clocks.sample_now()
     torch.cuda.synchronize(device)
     dist.barrier(device)
     clk = clocks.stop()
