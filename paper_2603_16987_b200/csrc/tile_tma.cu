@@ -66,6 +66,10 @@ namespace {
 #ifndef TP_K2_MIN_ITEMS  // small batches: halve the band until items >= this x CTAs
 #define TP_K2_MIN_ITEMS 2
 #endif
+#ifndef TP_K2_L2PF  // bulk L2 prefetch of a phase's rows before waiting for its stage (1: all
+                    // items, 2: not thumbnails, whose rows the tiles just read): C4 -3%, C2 +0.4%
+#define TP_K2_L2PF 2
+#endif
 #ifndef TP_K2_ROW_BALANCE
 #define TP_K2_ROW_BALANCE 1
 #endif
@@ -571,6 +575,19 @@ __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restri
         const int e1 = contig ? ry1 - ymin : 2 * lane + 1;
         const int off0 = __shfl_sync(0xffffffffu, ent_off, min(max(e0, 0), 31));
         const int off1 = __shfl_sync(0xffffffffu, ent_off, min(max(e1, 0), 31));
+#if TP_K2_L2PF
+        // warm L2 with this phase's rows while the stage is still busy: the bulk copy
+        // issued after the wait then reads L2 instead of waiting on DRAM
+        if (staged && (TP_K2_L2PF == 1 || !(t == nimg - 1 && nimg > 1))) {  // 2: not thumbnails
+          const uintptr_t pstart = gs - delta;
+          uint32_t pbytes = static_cast<uint32_t>((delta + rb + 15) & ~15);
+          if (pstart + pbytes > img_end)
+            pbytes = static_cast<uint32_t>((img_end - pstart) & ~uintptr_t(15));
+          if (pbytes > 0)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pstart), "r"(pbytes)
+                         : "memory");
+        }
+#endif
         // the plan above needs no stage: only now wait until the consumers release it
         if (lane == 0) mbar_wait(&hdr.empty[s], parity ^ 1u);
         __syncwarp();
