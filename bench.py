@@ -436,7 +436,10 @@ def main():
                          "kernel": "tp_tile (K2)", "kernel_ms": round(k2_ms, 4),
                          "kernel_timing": "CUDA events around K back-to-back K2 launches, "
                                           "same stream and inputs, after the timed steps",
-                         "bytes_per_launch": bytes_per_launch},
+                         "bytes_per_launch": bytes_per_launch,
+                         "bytes_full_image": int(wb["read_full"] + wb["write"]),
+                         "peak_nominal_gbs": 8000.0,
+                         "frac_of_nominal": round(achieved / 8000.0, 4)},
             "cpu_baseline": cpu,
             "e2e": {"value": round(dist.world * n / (e2e_ms / 1e3), 2), "unit": UNIT,
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
