@@ -71,6 +71,16 @@ def test_argument_errors_return_codes_without_touching_the_gpu():
     assert lib.tp_expand(None, None, -1, None, None, 4, 1, 2, 3, 1, None, 0, None, None, None,
                          None, None, None, None) == _lib.TP_ERR_INVALID_ARGUMENT
     assert lib.tp_supervision_mask(None, 3, 9, 3, None, None) == _lib.TP_ERR_INVALID_ARGUMENT
+    # unknown algo flag bits, tokenizer and norm-table argument checks
+    assert lib.tp_tile_ex(None, None, None, 1, 3, None, None, 448, None, 1, 0, None, None, 1,
+                          1 << 12, None) == _lib.TP_ERR_INVALID_ARGUMENT
+    assert lib.tp_tokenize(None, None, None, 1, 10, None, None, None, None, 0,
+                           None) == _lib.TP_ERR_INVALID_ARGUMENT
+    assert lib.tp_tokenize_workspace_bytes(-1, 1) == -1
+    assert lib.tp_vocab_table_bytes(-1) == -1
+    assert lib.tp_build_norm(3, zero, bad, 2, None, None, None) == _lib.TP_ERR_INVALID_ARGUMENT
+    assert lib.tp_lut_bytes(3, _lib.TP_DTYPE_BF16) == lib.tp_lut_table_bytes(3, 2) + 32
+    assert lib.tp_lut_table_bytes(3, _lib.TP_DTYPE_F32) == 3 * 256 * 4
     with pytest.raises(ValueError):
         _lib.check(_lib.TP_ERR_INVALID_ARGUMENT, "x")
     with pytest.raises(P.DeviceError):
