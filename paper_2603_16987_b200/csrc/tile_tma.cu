@@ -293,7 +293,7 @@ __device__ __forceinline__ uint32_t byte_of(uint32_t g0, uint32_t g1, int k) {
 // The fast path (consumer loop below) computes, per value, with biased taps
 // s' = 2^23 + s:  L = fma(fy, b'-a', a'-(2^23-0.5)), R = fma(fy, d'-c', c'-(2^23-0.5)),
 // t = fma(fx, R-L, L) ~ v + 0.5, and N = round(8192 t) via one fma against
-// 1.5*2^23.  |t - (v_ref + 0.5)| <= 3.8e-5, so when N mod 8192 is in
+// 1.5*2^23.  |t - (v_ref + 0.5)| <= 6.9e-5, so when N mod 8192 is in
 // [2, 8190] the value floor(t) = N >> 13 equals the reference's floor(v64 + 0.5);
 // otherwise (exact k + 0.5 ties included) the pixel pair is recomputed in fp64.
 
