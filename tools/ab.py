@@ -32,10 +32,11 @@ tall = Workload("TALL", "64 x 1080x1920 portrait", np.repeat(np.array([[1080, 19
 import os
 sel = os.environ.get("ABW", "c2,c4k,c3x32").split(",")
 for name, wl, n in [x for x in (("c2", c2(), 200), ("c4k", c4(1024), 20), ("c3x32", c3b, 100),
-                                ("up", up, 50), ("tall", tall, 100)) if x[0] in sel]:
+                                ("up", up, 50), ("tall", tall, 100), ("c2s", c2(), 200))
+                     if x[0] in sel]:
     cfg = PreprocessConfig(tile_edge=wl.tile_edge, max_tiles=wl.max_tiles, mean=wl.mean,
                            std=wl.std, reduced_precision_normalize=wl.bf16)
-    imgs = synth_packed(wl.wh, 3, dev, seed=wl.seed, kind=0)
+    imgs = synth_packed(wl.wh, 3, dev, seed=wl.seed, kind=1 if name.endswith("s") else 0)
     prep = TilePreprocessor(cfg, dev)
     out = prep(imgs)
     torch.cuda.synchronize()  # synth + K1 ran on the default stream; the loops use s
@@ -65,7 +66,8 @@ print(json.dumps(res))
 
 def main():
     rounds = int(sys.argv[1]) if len(sys.argv) > 1 else 3
-    # ABW=c2,c4k,c3x32,up,tall selects the workloads (default: c2,c4k,c3x32)
+    # ABW=c2,c4k,c3x32,up,tall,c2s selects the workloads (default: c2,c4k,c3x32);
+    # c2s is C2 on smooth synthetic content (kind 1), which flags more exact ties
     variants = sorted(p for p in (ROOT / "build" / "variants").glob("*/libtileprep.so"))
     results = {p.parent.name: [] for p in variants}
     for r in range(rounds):
