@@ -314,7 +314,8 @@ def main():
     def step(i=None):
         # K1 then K2; K2 is a programmatic dependent launch of K1 (and the next K1 of K2),
         # so no event is recorded between them inside the timed steps
-        prep.plan(images, out.plans, stream)
+        # steady state: the previous step's K2 is the last kernel on the stream
+        prep.plan(images, out.plans, stream, after_kernel=True)
         prep.tile(images, out.plans, out.pixel_values, None, stream, after_plan=True)
 
     with torch.cuda.stream(stream):

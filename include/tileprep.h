@@ -83,6 +83,15 @@ TP_API int tp_device_sm_count(void);
 TP_API int tp_plan(const int32_t* d_wh, int32_t n, int32_t tile_edge, int32_t max_tiles,
             int32_t* d_plan, int32_t* d_n_img, int32_t* d_tile_off, void* stream);
 
+/* tp_plan with flags.  TP_PLAN_AFTER_KERNEL: the last operation on `stream` is a kernel
+ * launch (e.g. the previous batch's tp_tile), not a copy or an event wait, so K1 may be
+ * launched as its programmatic dependent (K1 waits for that kernel before writing; d_wh
+ * must have been written before that kernel). */
+#define TP_PLAN_AFTER_KERNEL 1
+TP_API int tp_plan_ex(const int32_t* d_wh, int32_t n, int32_t tile_edge, int32_t max_tiles,
+                      int32_t* d_plan, int32_t* d_n_img, int32_t* d_tile_off, int32_t flags,
+                      void* stream);
+
 /* K0 — normalize lookup table: lut[c][v] = ((float)v / 255.f - mean[c]) / std[c]
  * in IEEE fp32 (true divides), optionally rounded to bf16 RNE.
  * Replaces the arithmetic of _normalize_array (imgproc.py:471-478).

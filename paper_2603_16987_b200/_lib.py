@@ -38,6 +38,7 @@ TP_TILE_ALGO_FAST = 1
 TP_TILE_ALGO_EXACT = 2
 TP_TILE_NORM_AFFINE = 256
 TP_TILE_AFTER_PLAN = 512
+TP_PLAN_AFTER_KERNEL = 1
 
 TP_PLAN_FIELDS = 6
 TP_MAX_EDGE = 65536
@@ -52,6 +53,8 @@ SIGNATURES = {
     "tp_device_sm_count": (c_int32, []),
     "tp_plan": (c_int32, [c_void_p, c_int32, c_int32, c_int32, c_void_p, c_void_p, c_void_p,
                           c_void_p]),
+    "tp_plan_ex": (c_int32, [c_void_p, c_int32, c_int32, c_int32, c_void_p, c_void_p, c_void_p,
+                             c_int32, c_void_p]),
     "tp_build_lut": (c_int32, [c_int32, _f32p, _f32p, c_int32, c_void_p, c_void_p]),
     "tp_lut_table_bytes": (c_int64, [c_int32, c_int32]),
     "tp_lut_bytes": (c_int64, [c_int32, c_int32]),

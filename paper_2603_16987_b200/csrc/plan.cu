@@ -152,6 +152,12 @@ __global__ void __launch_bounds__(kPlanThreads)
 
 extern "C" int tp_plan(const int32_t* d_wh, int32_t n, int32_t tile_edge, int32_t max_tiles,
                        int32_t* d_plan, int32_t* d_n_img, int32_t* d_tile_off, void* stream) {
+  return tp_plan_ex(d_wh, n, tile_edge, max_tiles, d_plan, d_n_img, d_tile_off, 0, stream);
+}
+
+extern "C" int tp_plan_ex(const int32_t* d_wh, int32_t n, int32_t tile_edge, int32_t max_tiles,
+                          int32_t* d_plan, int32_t* d_n_img, int32_t* d_tile_off, int32_t flags,
+                          void* stream) {
   if (n < 0) return tp::set_error(TP_ERR_INVALID_ARGUMENT, "tp_plan: n must be >= 0");
   if (tile_edge < 1) return tp::set_error(TP_ERR_INVALID_ARGUMENT, "tile_edge must be positive");
   if (max_tiles < 1) return tp::set_error(TP_ERR_INVALID_ARGUMENT, "max_tiles must be >= 1");
@@ -160,18 +166,22 @@ extern "C" int tp_plan(const int32_t* d_wh, int32_t n, int32_t tile_edge, int32_
                          max_tiles, TP_MAX_TILES_LIMIT);
   if (static_cast<int64_t>(tile_edge) * max_tiles > INT32_MAX)
     return tp::set_error(TP_ERR_UNSUPPORTED, "tile_edge * max_tiles overflows int32");
+  if (flags & ~TP_PLAN_AFTER_KERNEL)
+    return tp::set_error(TP_ERR_INVALID_ARGUMENT, "tp_plan_ex: bad flags %d", flags);
   if (!d_tile_off || (n > 0 && (!d_wh || !d_plan || !d_n_img)))
     return tp::set_error(TP_ERR_INVALID_ARGUMENT, "tp_plan: null buffer");
   // one warp per image up to a full 1024-thread block (small batches: short block syncs)
   const int threads = static_cast<int>(std::min<int64_t>(tp::kPlanThreads, 32LL * std::max(1, n)));
-#if TP_K1_PDL
-  const cudaError_t err = tp::launch_pdl(tp::k_plan, dim3(1), dim3(threads), 0, tp::as_stream(stream),
-                                          d_wh, n, tile_edge, max_tiles, d_plan, d_n_img, d_tile_off);
-#else
-  tp::k_plan<<<1, threads, 0, tp::as_stream(stream)>>>(d_wh, n, tile_edge, max_tiles, d_plan,
-                                                       d_n_img, d_tile_off);
-  const cudaError_t err = cudaSuccess;
-#endif
+  cudaError_t err = cudaSuccess;
+  if (TP_K1_PDL || (flags & TP_PLAN_AFTER_KERNEL)) {
+    // programmatic dependent of the kernel before it (the previous batch's K2): K1's
+    // launch overlaps that kernel's tail; k_plan waits for it before writing anything
+    err = tp::launch_pdl(tp::k_plan, dim3(1), dim3(threads), 0, tp::as_stream(stream), d_wh, n,
+                         tile_edge, max_tiles, d_plan, d_n_img, d_tile_off);
+  } else {
+    tp::k_plan<<<1, threads, 0, tp::as_stream(stream)>>>(d_wh, n, tile_edge, max_tiles, d_plan,
+                                                         d_n_img, d_tile_off);
+  }
   if (err != cudaSuccess) return tp::set_error(TP_ERR_CUDA, "tp_plan: %s", cudaGetErrorString(err));
   return tp::check_launch("tp_plan");
 }

@@ -221,12 +221,16 @@ class TilePreprocessor:
         return pv, u8
 
     def plan(self, images: PackedImages, out: Optional[PlanBatch] = None,
-             stream: Optional[torch.cuda.Stream] = None) -> PlanBatch:
+             stream: Optional[torch.cuda.Stream] = None, after_kernel: bool = False) -> PlanBatch:
+        """K1.  ``after_kernel``: the last operation enqueued on ``stream`` is a kernel
+        (e.g. the previous batch's tile()), so K1 may start under its tail."""
         out = out or self.alloc_plans(images.n)
         with torch.cuda.device(self.device):
-            _lib.call("tp_plan", _lib.ptr(images.wh), images.n, self.cfg.tile_edge,
+            _lib.call("tp_plan_ex", _lib.ptr(images.wh), images.n, self.cfg.tile_edge,
                       self.cfg.max_tiles, _lib.ptr(out.plan), _lib.ptr(out.n_images),
-                      _lib.ptr(out.tile_off), stream_handle(self.device, stream))
+                      _lib.ptr(out.tile_off),
+                      _lib.TP_PLAN_AFTER_KERNEL if after_kernel else 0,
+                      stream_handle(self.device, stream))
         return out
 
     def tile(self, images: PackedImages, plans: PlanBatch, pixel_values=None, pixel_u8=None,

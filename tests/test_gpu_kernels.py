@@ -506,3 +506,27 @@ def test_randomized_configs_vs_oracle():
                                       wn.view(np.uint16)), (case, k)
             else:
                 assert np.array_equal(got.numpy(), wn), (case, k)
+
+
+def test_plan_after_kernel_steady_state():
+    # the bench loop: plan (programmatic dependent of the previous tile) -> tile -> ...
+    from paper_2603_16987_b200.workloads import c4_shapes
+
+    wh = c4_shapes(64, start=300)
+    packed = synth_packed(wh, 3, DEV, seed=9, kind=0)
+    cfg = PreprocessConfig(tile_edge=448, max_tiles=12, mean=IMAGENET_MEAN, std=IMAGENET_STD,
+                           reduced_precision_normalize=True)
+    prep = TilePreprocessor(cfg, DEV)
+    ref = prep(packed)
+    torch.cuda.synchronize()
+    want_plan = ref.plans.plan.clone()
+    want_pv = ref.pixel_values.clone()
+    T = ref.num_tiles()
+    s = torch.cuda.Stream(DEV)
+    with torch.cuda.stream(s):
+        for _ in range(20):
+            prep.plan(packed, ref.plans, s, after_kernel=True)
+            prep.tile(packed, ref.plans, ref.pixel_values, None, s, after_plan=True)
+    torch.cuda.synchronize()
+    assert torch.equal(ref.plans.plan, want_plan)
+    assert torch.equal(ref.pixel_values[:T].view(torch.int16), want_pv[:T].view(torch.int16))
