@@ -31,7 +31,7 @@ namespace {
 
 // tuning knobs (overridable with -D for sweeps; defaults are the measured best)
 #ifndef TP_K2_BAND
-#define TP_K2_BAND 16
+#define TP_K2_BAND 32
 #endif
 #ifndef TP_K2_STAGES
 #define TP_K2_STAGES 2
@@ -69,6 +69,9 @@ namespace {
 #ifndef TP_K2_L2PF  // bulk L2 prefetch of a phase's rows before waiting for its stage (1: all
                     // items, 2: not thumbnails, whose rows the tiles just read): C4 -3%, C2 +0.4%
 #define TP_K2_L2PF 2
+#endif
+#ifndef TP_K2_BAND_ADAPT  // with TP_K2_BAND 32: use 16 when tiles per image <= 4
+#define TP_K2_BAND_ADAPT 1
 #endif
 #ifndef TP_K2_ROW_BALANCE
 #define TP_K2_ROW_BALANCE 1
@@ -1063,6 +1066,12 @@ __global__ void __launch_bounds__(kMaxThreads, kCtasPerSm)
   // band height: kBand rows, smaller when a small batch would leave SMs idle (batch-1
   // latency); every CTA derives the same value from the device-side tile count
   int band = kBand;
+#if TP_K2_BAND_ADAPT
+  // many tiles per image (multi-row grids): the thumbnail rarely re-reads the rows the
+  // tiles just read, so the larger band's lower per-item cost wins; few tiles per image
+  // (1-row grids, C2): band 16 keeps the tile/thumbnail L2 reuse
+  if (kBand > 16 && static_cast<int64_t>(all_tiles) <= 4LL * n) band = 16;
+#endif
   while (band > 2 &&
          static_cast<int64_t>(all_tiles) * ((E + band - 1) / band) < TP_K2_MIN_ITEMS * gridDim.x)
     band >>= 1;
