@@ -95,7 +95,10 @@ __global__ void __launch_bounds__(kPlanThreads)
     k_plan(const int32_t* __restrict__ wh, int32_t n, int32_t tile_edge, int32_t max_tiles,
            int32_t* __restrict__ plan, int32_t* __restrict__ n_img,
            int32_t* __restrict__ tile_off) {
-  __shared__ int32_t s_cnt[kPlanThreads];
+  // per-image counts, blockDim.x entries of dynamic shared memory: a batch-1 plan takes
+  // ~0.4 KB, so it shares an SM with two K2 CTAs (the SM K1 runs on would otherwise
+  // start its second K2 CTA only after K1 exits: +1 us on batch-1 latency)
+  extern __shared__ int32_t s_cnt[];
   __shared__ int64_t s_scan[33];
   __shared__ int s_bad;
   const int warp = threadIdx.x >> 5;
@@ -172,14 +175,15 @@ extern "C" int tp_plan_ex(const int32_t* d_wh, int32_t n, int32_t tile_edge, int
     return tp::set_error(TP_ERR_INVALID_ARGUMENT, "tp_plan: null buffer");
   // one warp per image up to a full 1024-thread block (small batches: short block syncs)
   const int threads = static_cast<int>(std::min<int64_t>(tp::kPlanThreads, 32LL * std::max(1, n)));
+  const size_t smem = sizeof(int32_t) * threads;
   cudaError_t err = cudaSuccess;
   if (TP_K1_PDL || (flags & TP_PLAN_AFTER_KERNEL)) {
     // programmatic dependent of the kernel before it (the previous batch's K2): K1's
     // launch overlaps that kernel's tail; k_plan waits for it before writing anything
-    err = tp::launch_pdl(tp::k_plan, dim3(1), dim3(threads), 0, tp::as_stream(stream), d_wh, n,
+    err = tp::launch_pdl(tp::k_plan, dim3(1), dim3(threads), smem, tp::as_stream(stream), d_wh, n,
                          tile_edge, max_tiles, d_plan, d_n_img, d_tile_off);
   } else {
-    tp::k_plan<<<1, threads, 0, tp::as_stream(stream)>>>(d_wh, n, tile_edge, max_tiles, d_plan,
+    tp::k_plan<<<1, threads, smem, tp::as_stream(stream)>>>(d_wh, n, tile_edge, max_tiles, d_plan,
                                                          d_n_img, d_tile_off);
   }
   if (err != cudaSuccess) return tp::set_error(TP_ERR_CUDA, "tp_plan: %s", cudaGetErrorString(err));

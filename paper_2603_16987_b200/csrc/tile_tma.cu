@@ -102,11 +102,10 @@ struct __align__(16) Phase {
   double pad3;
   int off0[kBand], off1[kBand];  // arena byte offset of column xlo in rows y0 / y1
   float fy[kBand];
-  double fy64[kBand], omfy64[kBand];  // exact row weights for the fp64 fallback
+  double fy64[kBand];  // exact row weights for the fp64 fallback (1 - fy64 is recomputed)
 };
 constexpr uint32_t kPhOff0 = offsetof(Phase, off0), kPhOff1 = offsetof(Phase, off1),
-                   kPhFy = offsetof(Phase, fy), kPhFy64 = offsetof(Phase, fy64),
-                   kPhOmfy64 = offsetof(Phase, omfy64);
+                   kPhFy = offsetof(Phase, fy), kPhFy64 = offsetof(Phase, fy64);
 
 struct TileGeo {
   double sx, sy;
@@ -140,6 +139,20 @@ struct __align__(16) SmemHeader {
   unsigned long long full[kStages];
   unsigned long long empty[kStages];
 };
+
+// Bytes of one stage for an instance: TP_K2_ARENA_KB, trimmed (128-byte steps) so that
+// kCtasPerSm CTAs of header + LUT + stages fit the SM's 228 KB (1 KB reserved per CTA)
+// next to a small-batch K1 (kK1Room: its CTA plus reserve, for the PDL overlap).
+// Without the trim the fp32 instances at band 32 need 2.5 KB too much and drop to one
+// CTA per SM (batch-1 latency +1.2 us).
+constexpr int kK1Room = 2048;
+template <int C, typename OutT>
+__host__ __device__ constexpr int arena_bytes() {
+  constexpr int fixed = static_cast<int>(((sizeof(SmemHeader) + 127) & ~size_t(127)) +
+                                         ((C * 256 * sizeof(OutT) + 127) & ~size_t(127)));
+  constexpr int fit = (((228 * 1024 - kK1Room) / kCtasPerSm - 1024 - fixed) / kStages) & ~127;
+  return fit < kArena ? fit : kArena;
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -360,7 +373,7 @@ __device__ __forceinline__ void store2<__nv_bfloat16>(__nv_bfloat16* dst, __nv_b
 
 // geometry of tile t of image k (tile t < rows*cols: window of the virtual resize;
 // t == rows*cols: the thumbnail) and its column-chunk width
-template <int C>
+template <int C, int ARENA>
 __device__ TileGeo tile_geometry(const int32_t* __restrict__ plan, int k, int t, int W, int H,
                                  int E) {
   const int32_t* p = plan + static_cast<int64_t>(k) * TP_PLAN_FIELDS;
@@ -391,7 +404,7 @@ __device__ TileGeo tile_geometry(const int32_t* __restrict__ plan, int k, int t,
       worst = max(worst, bts);
     }
     q.cwid = cwid;
-    if (2 * (worst + 15 + 16 + kRowSlack) <= kArena || cwid <= 2) break;
+    if (2 * (worst + 15 + 16 + kRowSlack) <= ARENA || cwid <= 2) break;
   }
   return q;
 }
@@ -414,7 +427,7 @@ __device__ __forceinline__ int warp_incl_max(int v, int lane) {
   return v;
 }
 
-template <int C>
+template <int C, int ARENA>
 __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restrict__ src,
                         const int64_t* __restrict__ src_off, const int32_t* __restrict__ wh,
                         int n, const int32_t* __restrict__ plan,
@@ -496,12 +509,12 @@ __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restri
       stride = static_cast<int64_t>(W) * C;
       img_end = reinterpret_cast<uintptr_t>(img) + static_cast<uintptr_t>(stride) * H;
       if (nimg <= kTileCache) {
-        if (lane < nimg) hdr.tg[lane] = tile_geometry<C>(plan, kimg, lane, W, H, E);
+        if (lane < nimg) hdr.tg[lane] = tile_geometry<C, ARENA>(plan, kimg, lane, W, H, E);
         __syncwarp();
       }
     }
     const int t = g - toff0;
-    const TileGeo geo = nimg <= kTileCache ? hdr.tg[t] : tile_geometry<C>(plan, kimg, t, W, H, E);
+    const TileGeo geo = nimg <= kTileCache ? hdr.tg[t] : tile_geometry<C, ARENA>(plan, kimg, t, W, H, E);
     const int RW = geo.RW, RH = geo.RH, oy0 = geo.oy0, ox0 = geo.ox0, cwid = geo.cwid;
     const bool contig = RH > H;
     const double sy = geo.sy, sx = geo.sx;
@@ -509,14 +522,13 @@ __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restri
     // lane j owns output row j0 + j of the band
     int my_y0 = 0, my_y1 = 0;
     float my_fy = 0.f;
-    double my_fy64 = 0.0, my_omf64 = 1.0;
+    double my_fy64 = 0.0;
     if (lane < nrows) {
       const AxisTap ty = axis_tap(oy0 + j0 + lane, H, sy);
       my_y0 = ty.i0;
       my_y1 = ty.i1;
       my_fy = __double2float_rn(ty.f);
       my_fy64 = ty.f;
-      my_omf64 = ty.omf;
     }
     for (int c0 = 0; c0 < E; c0 += cwid) {
       const int cw = min(cwid, E - c0);
@@ -559,7 +571,7 @@ __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restri
                                     : (2 * lane + 1);
         const int last_e = min(max(last_raw, 0), 31);
         const int incl_at = __shfl_sync(0xffffffffu, incl, last_e);
-        const bool rfits = lane < nleft && last_raw <= 31 && incl_at <= kArena;
+        const bool rfits = lane < nleft && last_raw <= 31 && incl_at <= ARENA;
         const int nr = max(1, __popc(__ballot_sync(0xffffffffu, rfits)));
         const int e_last = __shfl_sync(0xffffffffu, last_e, nr - 1);
         const bool staged = isnew && lane <= e_last;
@@ -573,7 +585,6 @@ __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restri
         const int ry1 = __shfl_sync(0xffffffffu, my_y1, rsrc);
         const float rfy = __shfl_sync(0xffffffffu, my_fy, rsrc);
         const double rfy64 = __shfl_sync(0xffffffffu, my_fy64, rsrc);
-        const double romf64 = __shfl_sync(0xffffffffu, my_omf64, rsrc);
         const int e0 = contig ? ry0 - ymin : 2 * lane;
         const int e1 = contig ? ry1 - ymin : 2 * lane + 1;
         const int off0 = __shfl_sync(0xffffffffu, ent_off, min(max(e0, 0), 31));
@@ -603,10 +614,9 @@ __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restri
           ph.off1[lane] = off1;
           ph.fy[lane] = rfy;
           ph.fy64[lane] = rfy64;
-          ph.omfy64[lane] = romf64;
         }
         // ---- copies: bulk for the 16-byte-aligned body; never read past the image
-        uint8_t* base = arena + s * kArena;
+        uint8_t* base = arena + s * ARENA;
         const uintptr_t start = gs - delta;
         uint32_t bytes = staged ? static_cast<uint32_t>((delta + rb + 15) & ~15) : 0u;
         if (staged && start + bytes > img_end) {
@@ -837,8 +847,7 @@ __device__ __forceinline__ void consume_pair_rows(
   // exact fp64 recomputation of the flagged values of row jj
   auto fix = [&](int jj, const PixTaps& a, const PixTaps& b, uint32_t (&ka)[C],
                  uint32_t (&kb)[C], const uint32_t (&xa)[C], const uint32_t (&xb)[C]) {
-    const double fy64 = ldsd(pr.base + kPhFy64 + 8 * jj),
-                 omfy64 = ldsd(pr.base + kPhOmfy64 + 8 * jj);
+    const double fy64 = ldsd(pr.base + kPhFy64 + 8 * jj), omfy64 = __dsub_rn(1.0, fy64);
     constexpr uint32_t kOut = AFF ? 0x4B400000u : kKrawBias;  // code of value 0
 #pragma unroll
     for (int c = 0; c < C; ++c) {
@@ -970,7 +979,7 @@ __device__ void consume(SmemHeader& hdr, const uint8_t* arena, const OutT* s_lut
     const int j0 = h0.y, nrows = h0.z, mis = h0.w;
     const int c0 = h1.x, cw = h1.y, xlo = h1.z, W = h1.w;
     const int segs = (cw + 63) >> 6;  // 64-pixel segments, one per consumer warp
-    const uint32_t sbase = arena_u32 + stage * kArena;
+    const uint32_t sbase = arena_u32 + stage * arena_bytes<C, OutT>();
 #if TP_K2_DEBUG_NOCONSUME  // timing experiment only: producer + TMA pipeline alone
     if (segs > 0) {
       mbar_arrive(&hdr.empty[stage]);
@@ -1078,7 +1087,7 @@ __global__ void __launch_bounds__(kMaxThreads, kCtasPerSm)
   const int bands = (E + band - 1) / band;
   const int64_t items = cap_tiles > 0 ? static_cast<int64_t>(all_tiles) * bands : 0;
   if (threadIdx.x < 32)
-    produce<C>(hdr, arena, src, src_off, wh, n, plan, tile_off, E, items, bands, band, cap_tiles);
+    produce<C, arena_bytes<C, OutT>()>(hdr, arena, src, src_off, wh, n, plan, tile_off, E, items, bands, band, cap_tiles);
   else
     consume<C, OutT, LAYOUT, WRITE_OUT, WRITE_U8, AFFINE, EK>(hdr, arena, s_lut, E, out, out_u8,
                                                              aff);
@@ -1087,7 +1096,7 @@ __global__ void __launch_bounds__(kMaxThreads, kCtasPerSm)
 template <int C, typename OutT>
 size_t tma_smem_bytes() {
   return ((sizeof(SmemHeader) + 127) & ~size_t(127)) +
-         ((C * 256 * sizeof(OutT) + 127) & ~size_t(127)) + kStages * kArena;
+         ((C * 256 * sizeof(OutT) + 127) & ~size_t(127)) + kStages * arena_bytes<C, OutT>();
 }
 
 template <int C, typename OutT, int LAYOUT, bool WRITE_OUT, bool WRITE_U8, bool AFFINE,
