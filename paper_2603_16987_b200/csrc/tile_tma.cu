@@ -70,6 +70,9 @@ namespace {
                     // items, 2: not thumbnails, whose rows the tiles just read): C4 -3%, C2 +0.4%
 #define TP_K2_L2PF 2
 #endif
+#ifndef TP_K2_FIXMODE  // fp64 fallback: 1 = conversions folded into fma (S w - 2^52 w), PRMT bytes
+#define TP_K2_FIXMODE 1
+#endif
 #ifndef TP_K2_BAND_ADAPT  // with TP_K2_BAND 32: use 16 when tiles per image <= 4
 #define TP_K2_BAND_ADAPT 1
 #endif
@@ -295,6 +298,26 @@ __device__ __forceinline__ uint32_t blend_exact_fast(uint32_t s00, uint32_t s01,
   const uint32_t k = static_cast<uint32_t>(__double2loint(__dadd_rd(t, 4503599627370496.0)));
   return min(k, 255u);  // t >= 0.5 > 0, so no lower clip is needed
 }
+// The same with the conversions folded into the products: for S = 2^52 + s (the byte in
+// the low word of 2^52's bit pattern) fma(S, w, -2^52 w) = round(s w) exactly, because
+// -2^52 w is exact (power-of-two scale) and the fma rounds S w - 2^52 w = s w once.
+// nw0 = -2^52 (1 - fy), nw1 = -2^52 fy, per output row.
+__device__ __forceinline__ double byte_f64_biased(uint32_t b) {
+  return __hiloint2double(0x43300000, static_cast<int>(b));
+}
+__device__ __forceinline__ uint32_t blend_exact_fma(uint32_t s00, uint32_t s01, uint32_t s10,
+                                                    uint32_t s11, double fy, double omfy,
+                                                    double nw1, double nw0, double fx,
+                                                    double omfx) {
+  const double l = __dadd_rn(__fma_rn(byte_f64_biased(s00), omfy, nw0),
+                             __fma_rn(byte_f64_biased(s10), fy, nw1));
+  const double r = __dadd_rn(__fma_rn(byte_f64_biased(s01), omfy, nw0),
+                             __fma_rn(byte_f64_biased(s11), fy, nw1));
+  const double v = __dadd_rn(__dmul_rn(l, omfx), __dmul_rn(r, fx));
+  const double t = __dadd_rn(v, 0.5);
+  const uint32_t k = static_cast<uint32_t>(__double2loint(__dadd_rd(t, 4503599627370496.0)));
+  return min(k, 255u);
+}
 
 // byte k (0..7) of (g0, g1) as the float 2^23 + byte (exact)
 __device__ __forceinline__ float biased_byte(uint32_t g0, uint32_t g1, int k) {
@@ -303,7 +326,11 @@ __device__ __forceinline__ float biased_byte(uint32_t g0, uint32_t g1, int k) {
 }
 
 __device__ __forceinline__ uint32_t byte_of(uint32_t g0, uint32_t g1, int k) {
+#if TP_K2_FIXMODE >= 1
+  return __byte_perm(k < 4 ? g0 : g1, 0u, 0x4440u | static_cast<uint32_t>(k & 3));  // one PRMT
+#else
   return ((k < 4 ? g0 : g1) >> ((k & 3) * 8)) & 0xFFu;
+#endif
 }
 
 // The fast path (consumer loop below) computes, per value, with biased taps
@@ -849,17 +876,27 @@ __device__ __forceinline__ void consume_pair_rows(
                  uint32_t (&kb)[C], const uint32_t (&xa)[C], const uint32_t (&xb)[C]) {
     const double fy64 = ldsd(pr.base + kPhFy64 + 8 * jj), omfy64 = __dsub_rn(1.0, fy64);
     constexpr uint32_t kOut = AFF ? 0x4B400000u : kKrawBias;  // code of value 0
+#if TP_K2_FIXMODE >= 1
+    const double nw1 = __dmul_rn(fy64, -4503599627370496.0),
+                 nw0 = __dmul_rn(omfy64, -4503599627370496.0);
+#define TP_BLEND(s00, s01, s10, s11, fx, omfx) \
+  blend_exact_fma(s00, s01, s10, s11, fy64, omfy64, nw1, nw0, fx, omfx)
+#else
+#define TP_BLEND(s00, s01, s10, s11, fx, omfx) \
+  blend_exact_fast(s00, s01, s10, s11, fy64, omfy64, fx, omfx)
+#endif
 #pragma unroll
     for (int c = 0; c < C; ++c) {
       if (xa[c] < kAmbLimit)
-        ka[c] = kOut + blend_exact_fast(byte_of(a.r0w0, a.r0w1, c), byte_of(a.r0w0, a.r0w1, C + c),
-                                        byte_of(a.r1w0, a.r1w1, c), byte_of(a.r1w0, a.r1w1, C + c),
-                                        fy64, omfy64, fxa64, omfxa64);
+        ka[c] = kOut + TP_BLEND(byte_of(a.r0w0, a.r0w1, c), byte_of(a.r0w0, a.r0w1, C + c),
+                                byte_of(a.r1w0, a.r1w1, c), byte_of(a.r1w0, a.r1w1, C + c),
+                                fxa64, omfxa64);
       if (xb[c] < kAmbLimit)
-        kb[c] = kOut + blend_exact_fast(byte_of(b.r0w0, b.r0w1, c), byte_of(b.r0w0, b.r0w1, C + c),
-                                        byte_of(b.r1w0, b.r1w1, c), byte_of(b.r1w0, b.r1w1, C + c),
-                                        fy64, omfy64, fxb64, omfxb64);
+        kb[c] = kOut + TP_BLEND(byte_of(b.r0w0, b.r0w1, c), byte_of(b.r0w0, b.r0w1, C + c),
+                                byte_of(b.r1w0, b.r1w1, c), byte_of(b.r1w0, b.r1w1, C + c),
+                                fxb64, omfxb64);
     }
+#undef TP_BLEND
   };
   // LUT + stores of row jj (rows in order: the NCHW row pointers advance by one row)
   auto emit = [&](int jj, const uint32_t (&ka)[C], const uint32_t (&kb)[C]) {
