@@ -73,6 +73,9 @@ namespace {
 #ifndef TP_K2_FIXMODE  // fp64 fallback: 1 = conversions folded into fma (S w - 2^52 w), PRMT bytes
 #define TP_K2_FIXMODE 1
 #endif
+#ifndef TP_K2_DWIN  // affine path: window test on d = T - round(T) instead of N = round(8192 t)
+#define TP_K2_DWIN 1
+#endif
 #ifndef TP_K2_BAND_ADAPT  // with TP_K2_BAND 32: use 16 when tiles per image <= 4
 #define TP_K2_BAND_ADAPT 1
 #endif
@@ -753,6 +756,7 @@ struct LutLoad<float> {
 // flagged iff N mod 8192 is 8191, 0 or 1 (within 1.83e-4 of a rounding boundary).
 constexpr uint32_t kKrawBias = 0x4B400000u >> 13;  // 0x25A00
 constexpr uint32_t kAmbLimit = 3u << 19;
+constexpr float kDwinThr = 8189.0f / 16384.0f;  // 1/2 - 3/16384 (= 1.5/8192 below 1/2)
 
 // Taps of one pixel in the two staged rows of output row jj: (row, word) pairs.
 struct PixTaps {
@@ -842,11 +846,20 @@ __device__ __forceinline__ void consume_pair_rows(
   const int ob_off = ib - ia;
   // one output row: taps (a, b) already fetched
   // fp32 fast path of output row jj: LUT codes (kKrawBias + value) and window flags
+  // AFF with TP_K2_DWIN: ka/kb hold round(T) as a float and xa/xb the distance
+  // d = T - round(T) (exact); a value is flagged when |d| >= 1/2 - 3/16384, the same
+  // 1.83e-4 window around the rounding boundary as the N test below.  Saves the N fma,
+  // the integer window test and emit's unbias per channel.
+  constexpr bool DW = AFF && TP_K2_DWIN;
+  auto flagged = [&](uint32_t x) -> bool {
+    return DW ? fabsf(__uint_as_float(x)) >= kDwinThr : x < kAmbLimit;
+  };
   auto fast = [&](int jj, const PixTaps& a, const PixTaps& b, uint32_t (&ka)[C],
-                  uint32_t (&kb)[C], uint32_t (&xa)[C], uint32_t (&xb)[C]) -> uint32_t {
+                  uint32_t (&kb)[C], uint32_t (&xa)[C], uint32_t (&xb)[C]) -> bool {
     const float fy = ldsf(pr.base + kPhFy + 4 * jj);
     const f32x2 FY = pk(fy, fy);
     uint32_t worst = 0xFFFFFFFFu;
+    float dmax = 0.f;
 #pragma unroll
     for (int c = 0; c < C; ++c) {
       // lanes: (pixel a, pixel b); taps s00, s10, s01, s11 as 2^23 + byte
@@ -857,6 +870,13 @@ __device__ __forceinline__ void consume_pair_rows(
       const f32x2 L = fma2(FY, sub2(B, A), sub2(A, KH));   // a + fy (b - a)
       const f32x2 R = fma2(FY, sub2(D, Cc), sub2(Cc, KH));  // c + fy (d - c)
       const f32x2 T = fma2(FX, sub2(R, L), L);              // ~ v
+      if (DW) {
+        const f32x2 KF = sub2(add2(T, MAGR), MAGR);  // round(T), exact
+        upk(KF, ka[c], kb[c]);
+        upk(sub2(T, KF), xa[c], xb[c]);
+        dmax = fmaxf(dmax, fmaxf(fabsf(__uint_as_float(xa[c])), fabsf(__uint_as_float(xb[c]))));
+        continue;
+      }
       uint32_t na, nb;
       upk(fma2(T, S13, MAG), na, nb);  // bits of 1.5*2^23 + round(8192 (t + 0.5))
       if (AFF) {
@@ -869,13 +889,17 @@ __device__ __forceinline__ void consume_pair_rows(
       xb[c] = nb * (1u << 19) + (1u << 19);
       worst = min(worst, min(xa[c], xb[c]));
     }
-    return worst;
+    return DW ? dmax >= kDwinThr : worst < kAmbLimit;
   };
   // exact fp64 recomputation of the flagged values of row jj
   auto fix = [&](int jj, const PixTaps& a, const PixTaps& b, uint32_t (&ka)[C],
                  uint32_t (&kb)[C], const uint32_t (&xa)[C], const uint32_t (&xb)[C]) {
     const double fy64 = ldsd(pr.base + kPhFy64 + 8 * jj), omfy64 = __dsub_rn(1.0, fy64);
-    constexpr uint32_t kOut = AFF ? 0x4B400000u : kKrawBias;  // code of value 0
+    constexpr uint32_t kOut = DW ? 0x4B000000u : AFF ? 0x4B400000u : kKrawBias;  // value 0
+    // DW codes are the float k itself: (2^23 + k) - 2^23
+    auto code = [&](uint32_t k) -> uint32_t {
+      return DW ? __float_as_uint(__uint_as_float(kOut + k) - 8388608.0f) : kOut + k;
+    };
 #if TP_K2_FIXMODE >= 1
     const double nw1 = __dmul_rn(fy64, -4503599627370496.0),
                  nw0 = __dmul_rn(omfy64, -4503599627370496.0);
@@ -887,14 +911,14 @@ __device__ __forceinline__ void consume_pair_rows(
 #endif
 #pragma unroll
     for (int c = 0; c < C; ++c) {
-      if (xa[c] < kAmbLimit)
-        ka[c] = kOut + TP_BLEND(byte_of(a.r0w0, a.r0w1, c), byte_of(a.r0w0, a.r0w1, C + c),
-                                byte_of(a.r1w0, a.r1w1, c), byte_of(a.r1w0, a.r1w1, C + c),
-                                fxa64, omfxa64);
-      if (xb[c] < kAmbLimit)
-        kb[c] = kOut + TP_BLEND(byte_of(b.r0w0, b.r0w1, c), byte_of(b.r0w0, b.r0w1, C + c),
-                                byte_of(b.r1w0, b.r1w1, c), byte_of(b.r1w0, b.r1w1, C + c),
-                                fxb64, omfxb64);
+      if (flagged(xa[c]))
+        ka[c] = code(TP_BLEND(byte_of(a.r0w0, a.r0w1, c), byte_of(a.r0w0, a.r0w1, C + c),
+                              byte_of(a.r1w0, a.r1w1, c), byte_of(a.r1w0, a.r1w1, C + c),
+                              fxa64, omfxa64));
+      if (flagged(xb[c]))
+        kb[c] = code(TP_BLEND(byte_of(b.r0w0, b.r0w1, c), byte_of(b.r0w0, b.r0w1, C + c),
+                              byte_of(b.r1w0, b.r1w1, c), byte_of(b.r1w0, b.r1w1, C + c),
+                              fxb64, omfxb64));
     }
 #undef TP_BLEND
   };
@@ -914,7 +938,8 @@ __device__ __forceinline__ void consume_pair_rows(
     if (AFF) {
 #pragma unroll
       for (int c = 0; c < C; ++c) {
-        const f32x2 KF = sub2(pk(__uint_as_float(ka[c]), __uint_as_float(kb[c])), MAGR);
+        const f32x2 KR = pk(__uint_as_float(ka[c]), __uint_as_float(kb[c]));
+        const f32x2 KF = DW ? KR : sub2(KR, MAGR);
         uint32_t va, vb;
         upk(fma2(KF, pk(aff_a[c], aff_a[c]), pk(aff_b[c], aff_b[c])), va, vb);
         if (sizeof(OutT) == 2) {  // fp32 -> bf16 RNE, both pixels in one conversion
@@ -952,7 +977,7 @@ __device__ __forceinline__ void consume_pair_rows(
   };
   auto row = [&](int jj, const PixTaps& a, const PixTaps& b) {
     uint32_t ka[C], kb[C], xa[C], xb[C];
-    if (fast(jj, a, b, ka, kb, xa, xb) < kAmbLimit) fix(jj, a, b, ka, kb, xa, xb);
+    if (fast(jj, a, b, ka, kb, xa, xb)) fix(jj, a, b, ka, kb, xa, xb);
     emit(jj, ka, kb);
   };
   // software pipeline, unrolled by two so the prefetched taps need no register moves

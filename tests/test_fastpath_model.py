@@ -4,7 +4,10 @@ Emulates the packed-fp32 arithmetic in numpy (fp32 rounding after every operatio
 fma as an fp64 product-sum rounded once to fp32, exact for these magnitudes) and checks
 the two facts bit-exactness rests on, against the oracle's fp64 reference values:
   * |T' - v| <= 6.9e-5 for every value;
-  * whenever the window test does not flag a value, round(T') is the reference byte.
+  * whenever the window test does not flag a value, round(T') is the reference byte;
+  * the affine path's form of the test (|T' - round(T')| >= 1/2 - 3/16384, TP_K2_DWIN)
+    flags nearly the same values (the window edges differ by < 1/16384) and is
+    sufficient on its own.
 """
 
 from __future__ import annotations
@@ -67,6 +70,14 @@ def test_fast_path_error_bound_and_window(h, w, oh, ow, kind):
     fast_byte = np.floor(T.astype(np.float64) + 0.5).clip(0, 255).astype(np.uint8)
     ok = ~flagged
     assert np.array_equal(fast_byte[ok], ref[ok])
+    # affine path (TP_K2_DWIN): d = T - rint(T) exact in fp32, flagged when |d| >= 8189/16384
+    kf = (T + F32(12582912.0)).astype(F32) - F32(12582912.0)
+    d = (T - kf).astype(F32)
+    flagged_d = np.abs(d) >= F32(8189.0 / 16384.0)
+    ok_d = ~flagged_d
+    assert np.array_equal(kf[ok_d].astype(np.int64), ref[ok_d].astype(np.int64))
+    # the same window up to its edges: N = round(8192 t) moves the edge by < 1/16384
+    assert int(flagged_d.sum()) <= 1.1 * int(flagged.sum()) + 8
     # on random content the flagged share stays small except on exact-tie grids
     # (smooth content with rational weights hits exact k + 1/2 more often: 2.4% here)
     if kind == "random" and (h, w) != (128, 128):
