@@ -157,6 +157,18 @@ TP_API int tp_tile_ex(const uint8_t* d_src, const int64_t* d_src_off, const int3
                       int32_t dtype, int32_t layout, void* d_out, uint8_t* d_out_u8,
                       int64_t out_capacity, int32_t algo, void* stream);
 
+/* K1 + K2 in one launch for small batches (n <= TP_PLAN_TILE_MAX_IMAGES; batch-1
+ * latency): every CTA of the K2 grid plans the batch with K1's rule itself, CTA 0
+ * writes d_plan / d_n_img / d_tile_off exactly as tp_plan would, and the tiles are
+ * written as by tp_tile_ex.  Fast algorithm only (AUTO / FAST, optionally
+ * TP_TILE_NORM_AFFINE); TP_ERR_UNSUPPORTED for larger batches. */
+#define TP_PLAN_TILE_MAX_IMAGES 4
+TP_API int tp_plan_tile(const uint8_t* d_src, const int64_t* d_src_off, const int32_t* d_wh,
+                        int32_t n, int32_t channels, int32_t tile_edge, int32_t max_tiles,
+                        int32_t* d_plan, int32_t* d_n_img, int32_t* d_tile_off,
+                        const void* d_lut, int32_t dtype, int32_t layout, void* d_out,
+                        uint8_t* d_out_u8, int64_t out_capacity, int32_t algo, void* stream);
+
 /* K2 variant for resize_bilinear / _resize_array (imgproc.py:352-367): one
  * full-frame half-pixel bilinear resize, uint8 HWC -> uint8 HWC. */
 TP_API int tp_resize(const uint8_t* d_src, int32_t width, int32_t height, int32_t channels,

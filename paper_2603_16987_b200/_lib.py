@@ -39,6 +39,7 @@ TP_TILE_ALGO_EXACT = 2
 TP_TILE_NORM_AFFINE = 256
 TP_TILE_AFTER_PLAN = 512
 TP_PLAN_AFTER_KERNEL = 1
+TP_PLAN_TILE_MAX_IMAGES = 4
 
 TP_PLAN_FIELDS = 6
 TP_MAX_EDGE = 65536
@@ -66,6 +67,9 @@ SIGNATURES = {
     "tp_tile_ex": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_void_p,
                              c_int32, c_void_p, c_int32, c_int32, c_void_p, c_void_p, c_int64,
                              c_int32, c_void_p]),
+    "tp_plan_tile": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_int32,
+                               c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_int32,
+                               c_int32, c_void_p, c_void_p, c_int64, c_int32, c_void_p]),
     "tp_resize": (c_int32, [c_void_p, c_int32, c_int32, c_int32, c_int32, c_int32, c_void_p,
                             c_void_p]),
     "tp_normalize": (c_int32, [c_void_p, c_int64, c_int64, c_int32, c_void_p, c_int32,

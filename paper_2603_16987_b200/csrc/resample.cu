@@ -169,7 +169,8 @@ __global__ void __launch_bounds__(kThreads)
 template <int C, typename OutT, int LAYOUT, bool WRITE_OUT>
 int launch_tile(const uint8_t* src, const int64_t* src_off, const int32_t* wh, int n,
                 const int32_t* plan, const int32_t* tile_off, int E, const void* lut, void* out,
-                uint8_t* out_u8, int64_t cap, int algo, cudaStream_t stream) {
+                uint8_t* out_u8, int64_t cap, int algo, cudaStream_t stream,
+                FusePlan fuse = FusePlan{}) {
   const int sms = max(1, device_sm_count());
   int per_sm = 0;
   if ((algo & 0xFF) == TP_TILE_ALGO_EXACT) {
@@ -183,29 +184,57 @@ int launch_tile(const uint8_t* src, const int64_t* src_off, const int32_t* wh, i
   return launch_tile_tma<C, OutT, LAYOUT, WRITE_OUT>(src, src_off, wh, n, plan, tile_off, E, lut,
                                                      out, out_u8, cap,
                                                      (algo & TP_TILE_NORM_AFFINE) != 0,
-                                                     (algo & TP_TILE_AFTER_PLAN) != 0, stream);
+                                                     (algo & TP_TILE_AFTER_PLAN) != 0, stream,
+                                                     fuse);
 }
 
 template <int C>
 int dispatch_tile(const uint8_t* src, const int64_t* src_off, const int32_t* wh, int n,
                   const int32_t* plan, const int32_t* tile_off, int E, const void* lut,
                   int dtype, int layout, void* out, uint8_t* out_u8, int64_t cap, int algo,
-                  cudaStream_t s) {
+                  cudaStream_t s, FusePlan fuse = FusePlan{}) {
   if (dtype == TP_DTYPE_NONE)
     return launch_tile<C, float, TP_LAYOUT_NHWC, false>(src, src_off, wh, n, plan, tile_off, E,
-                                                        lut, out, out_u8, cap, algo, s);
+                                                        lut, out, out_u8, cap, algo, s, fuse);
   if (dtype == TP_DTYPE_F32) {
     if (layout == TP_LAYOUT_NCHW)
       return launch_tile<C, float, TP_LAYOUT_NCHW, true>(src, src_off, wh, n, plan, tile_off,
-                                                         E, lut, out, out_u8, cap, algo, s);
+                                                         E, lut, out, out_u8, cap, algo, s, fuse);
     return launch_tile<C, float, TP_LAYOUT_NHWC, true>(src, src_off, wh, n, plan, tile_off, E,
-                                                       lut, out, out_u8, cap, algo, s);
+                                                       lut, out, out_u8, cap, algo, s, fuse);
   }
   if (layout == TP_LAYOUT_NCHW)
     return launch_tile<C, __nv_bfloat16, TP_LAYOUT_NCHW, true>(src, src_off, wh, n, plan,
-                                                               tile_off, E, lut, out, out_u8, cap, algo, s);
+                                                               tile_off, E, lut, out, out_u8, cap, algo, s, fuse);
   return launch_tile<C, __nv_bfloat16, TP_LAYOUT_NHWC, true>(src, src_off, wh, n, plan,
-                                                             tile_off, E, lut, out, out_u8, cap, algo, s);
+                                                             tile_off, E, lut, out, out_u8, cap, algo, s, fuse);
+}
+
+// argument checks shared by tp_tile_ex and tp_plan_tile (plans and offsets apart)
+int check_tile_args(const uint8_t* src, const int64_t* src_off, const int32_t* wh, int n,
+                    int channels, int tile_edge, const void* lut, int dtype, int layout,
+                    const void* out, const uint8_t* out_u8, int64_t cap, int algo) {
+  const int base_algo = algo & 0xFF;
+  if ((base_algo != TP_TILE_ALGO_AUTO && base_algo != TP_TILE_ALGO_FAST &&
+       base_algo != TP_TILE_ALGO_EXACT) ||
+      (algo & ~(0xFF | TP_TILE_NORM_AFFINE | TP_TILE_AFTER_PLAN)) != 0)
+    return set_error(TP_ERR_INVALID_ARGUMENT, "bad algo %d", algo);
+  if (n < 0) return set_error(TP_ERR_INVALID_ARGUMENT, "tp_tile: n must be >= 0");
+  if (channels != 1 && channels != 3)
+    return set_error(TP_ERR_INVALID_ARGUMENT, "channels must be 1 or 3, got %d", channels);
+  if (tile_edge < 1) return set_error(TP_ERR_INVALID_ARGUMENT, "tile_edge must be positive");
+  if (dtype != TP_DTYPE_NONE && dtype != TP_DTYPE_F32 && dtype != TP_DTYPE_BF16)
+    return set_error(TP_ERR_INVALID_ARGUMENT, "bad dtype %d", dtype);
+  if (layout != TP_LAYOUT_NCHW && layout != TP_LAYOUT_NHWC)
+    return set_error(TP_ERR_INVALID_ARGUMENT, "bad layout %d", layout);
+  if (dtype != TP_DTYPE_NONE && (!out || !lut))
+    return set_error(TP_ERR_INVALID_ARGUMENT, "tp_tile: normalized output needs out and lut");
+  if (dtype == TP_DTYPE_NONE && !out_u8)
+    return set_error(TP_ERR_INVALID_ARGUMENT, "tp_tile: nothing to write");
+  if (cap < 0) return set_error(TP_ERR_INVALID_ARGUMENT, "bad out_capacity");
+  if (n > 0 && cap > 0 && (!src || !src_off || !wh))
+    return set_error(TP_ERR_INVALID_ARGUMENT, "tp_tile: null buffer");
+  return TP_OK;
 }
 
 }  // namespace
@@ -220,32 +249,51 @@ extern "C" int tp_tile(const uint8_t* d_src, const int64_t* d_src_off, const int
                     dtype, layout, d_out, d_out_u8, out_capacity, TP_TILE_ALGO_AUTO, stream);
 }
 
+extern "C" int tp_plan_tile(const uint8_t* d_src, const int64_t* d_src_off, const int32_t* d_wh,
+                            int32_t n, int32_t channels, int32_t tile_edge, int32_t max_tiles,
+                            int32_t* d_plan, int32_t* d_n_img, int32_t* d_tile_off,
+                            const void* d_lut, int32_t dtype, int32_t layout, void* d_out,
+                            uint8_t* d_out_u8, int64_t out_capacity, int32_t algo,
+                            void* stream) {
+  if (n < 0 || n > TP_PLAN_TILE_MAX_IMAGES)
+    return tp::set_error(TP_ERR_UNSUPPORTED, "tp_plan_tile: n = %d outside [0, %d] (use tp_plan + tp_tile_ex)",
+                         n, TP_PLAN_TILE_MAX_IMAGES);
+  if ((algo & 0xFF) == TP_TILE_ALGO_EXACT || (algo & TP_TILE_AFTER_PLAN))
+    return tp::set_error(TP_ERR_INVALID_ARGUMENT, "tp_plan_tile: fast algorithm only, no AFTER_PLAN");
+  if (max_tiles < 1) return tp::set_error(TP_ERR_INVALID_ARGUMENT, "max_tiles must be >= 1");
+  if (max_tiles > TP_MAX_TILES_LIMIT)
+    return tp::set_error(TP_ERR_UNSUPPORTED, "max_tiles %d above the exact-planner limit %d",
+                         max_tiles, TP_MAX_TILES_LIMIT);
+  if (tile_edge >= 1 && static_cast<int64_t>(tile_edge) * max_tiles > INT32_MAX)
+    return tp::set_error(TP_ERR_UNSUPPORTED, "tile_edge * max_tiles overflows int32");
+  if (!d_tile_off || (n > 0 && (!d_wh || !d_plan || !d_n_img)))
+    return tp::set_error(TP_ERR_INVALID_ARGUMENT, "tp_plan_tile: null plan buffer");
+  int rc = tp::check_tile_args(d_src, d_src_off, d_wh, n, channels, tile_edge, d_lut, dtype,
+                               layout, d_out, d_out_u8, out_capacity, algo);
+  if (rc != TP_OK) return rc;
+  cudaStream_t s = tp::as_stream(stream);
+  if (n == 0 || out_capacity == 0)  // nothing to tile: the plans alone (K1)
+    return tp_plan(d_wh, n, tile_edge, max_tiles, d_plan, d_n_img, d_tile_off, stream);
+  tp::FusePlan fuse;
+  fuse.max_tiles = max_tiles;
+  fuse.n_img = d_n_img;
+  if (channels == 3)
+    return tp::dispatch_tile<3>(d_src, d_src_off, d_wh, n, d_plan, d_tile_off, tile_edge, d_lut,
+                                dtype, layout, d_out, d_out_u8, out_capacity, algo, s, fuse);
+  return tp::dispatch_tile<1>(d_src, d_src_off, d_wh, n, d_plan, d_tile_off, tile_edge, d_lut,
+                              dtype, layout, d_out, d_out_u8, out_capacity, algo, s, fuse);
+}
+
 extern "C" int tp_tile_ex(const uint8_t* d_src, const int64_t* d_src_off, const int32_t* d_wh,
                           int32_t n, int32_t channels, const int32_t* d_plan,
                           const int32_t* d_tile_off, int32_t tile_edge, const void* d_lut,
                           int32_t dtype, int32_t layout, void* d_out, uint8_t* d_out_u8,
                           int64_t out_capacity, int32_t algo, void* stream) {
-  const int base_algo = algo & 0xFF;
-  if ((base_algo != TP_TILE_ALGO_AUTO && base_algo != TP_TILE_ALGO_FAST &&
-       base_algo != TP_TILE_ALGO_EXACT) ||
-      (algo & ~(0xFF | TP_TILE_NORM_AFFINE | TP_TILE_AFTER_PLAN)) != 0)
-    return tp::set_error(TP_ERR_INVALID_ARGUMENT, "bad algo %d", algo);
-  if (n < 0) return tp::set_error(TP_ERR_INVALID_ARGUMENT, "tp_tile: n must be >= 0");
-  if (channels != 1 && channels != 3)
-    return tp::set_error(TP_ERR_INVALID_ARGUMENT, "channels must be 1 or 3, got %d", channels);
-  if (tile_edge < 1) return tp::set_error(TP_ERR_INVALID_ARGUMENT, "tile_edge must be positive");
-  if (dtype != TP_DTYPE_NONE && dtype != TP_DTYPE_F32 && dtype != TP_DTYPE_BF16)
-    return tp::set_error(TP_ERR_INVALID_ARGUMENT, "bad dtype %d", dtype);
-  if (layout != TP_LAYOUT_NCHW && layout != TP_LAYOUT_NHWC)
-    return tp::set_error(TP_ERR_INVALID_ARGUMENT, "bad layout %d", layout);
-  if (dtype != TP_DTYPE_NONE && (!d_out || !d_lut))
-    return tp::set_error(TP_ERR_INVALID_ARGUMENT, "tp_tile: normalized output needs out and lut");
-  if (dtype == TP_DTYPE_NONE && !d_out_u8)
-    return tp::set_error(TP_ERR_INVALID_ARGUMENT, "tp_tile: nothing to write");
-  if (out_capacity < 0) return tp::set_error(TP_ERR_INVALID_ARGUMENT, "bad out_capacity");
+  const int rc = tp::check_tile_args(d_src, d_src_off, d_wh, n, channels, tile_edge, d_lut, dtype,
+                                     layout, d_out, d_out_u8, out_capacity, algo);
+  if (rc != TP_OK) return rc;
   if (n == 0 || out_capacity == 0) return TP_OK;
-  if (!d_src || !d_src_off || !d_wh || !d_plan || !d_tile_off)
-    return tp::set_error(TP_ERR_INVALID_ARGUMENT, "tp_tile: null buffer");
+  if (!d_plan || !d_tile_off) return tp::set_error(TP_ERR_INVALID_ARGUMENT, "tp_tile: null buffer");
   cudaStream_t s = tp::as_stream(stream);
   if (channels == 3)
     return tp::dispatch_tile<3>(d_src, d_src_off, d_wh, n, d_plan, d_tile_off, tile_edge, d_lut,

@@ -25,6 +25,7 @@
 #include <cstddef>
 
 #include "tp_common.cuh"
+#include "plan_core.cuh"
 
 namespace tp {
 namespace {
@@ -144,7 +145,16 @@ struct __align__(16) SmemHeader {
   TileGeo tg[kTileCache];  // producer: tiles of the current image
   unsigned long long full[kStages];
   unsigned long long empty[kStages];
+  // fused small-batch mode: this CTA's own plans and tile offsets (FusePlan)
+  int fplan[kFuseMaxImages][TP_PLAN_FIELDS];
+  int ftoff[kFuseMaxImages + 1];
 };
+
+// plans / tile offsets: K1's output in global memory (coherent loads, see TP_LD) or,
+// in the fused mode, the CTA's own copy in shared memory
+__device__ __forceinline__ int ld_plan(const int32_t* p, bool in_smem) {
+  return in_smem ? *p : TP_LD(p);
+}
 
 // Bytes of one stage for an instance: TP_K2_ARENA_KB, trimmed (128-byte steps) so that
 // kCtasPerSm CTAs of header + LUT + stages fit the SM's 228 KB (1 KB reserved per CTA)
@@ -344,12 +354,12 @@ __device__ __forceinline__ uint32_t byte_of(uint32_t g0, uint32_t g1, int k) {
 // otherwise (exact k + 0.5 ties included) the pixel pair is recomputed in fp64.
 
 // image whose items contain `item` (items of image k start at tile_off[k] * bands)
-__device__ __forceinline__ int find_item_image(const int32_t* __restrict__ tile_off, int n,
+__device__ __forceinline__ int find_item_image(const int32_t* __restrict__ tile_off, bool psm, int n,
                                                int64_t item, int bands) {
   int lo = 0, hi = n;
   while (hi - lo > 1) {
     const int mid = (lo + hi) >> 1;
-    if (static_cast<int64_t>(TP_LD(tile_off + mid)) * bands <= item) lo = mid; else hi = mid;
+    if (static_cast<int64_t>(ld_plan(tile_off + mid, psm)) * bands <= item) lo = mid; else hi = mid;
   }
   return lo;
 }
@@ -404,14 +414,14 @@ __device__ __forceinline__ void store2<__nv_bfloat16>(__nv_bfloat16* dst, __nv_b
 // geometry of tile t of image k (tile t < rows*cols: window of the virtual resize;
 // t == rows*cols: the thumbnail) and its column-chunk width
 template <int C, int ARENA>
-__device__ TileGeo tile_geometry(const int32_t* __restrict__ plan, int k, int t, int W, int H,
-                                 int E) {
+__device__ TileGeo tile_geometry(const int32_t* __restrict__ plan, bool psm, int k, int t, int W,
+                                 int H, int E) {
   const int32_t* p = plan + static_cast<int64_t>(k) * TP_PLAN_FIELDS;
-  const int rows = TP_LD(p + TP_PLAN_ROWS), cols = TP_LD(p + TP_PLAN_COLS);
+  const int rows = ld_plan(p + TP_PLAN_ROWS, psm), cols = ld_plan(p + TP_PLAN_COLS, psm);
   TileGeo q;
   if (t < rows * cols) {
-    q.RW = TP_LD(p + TP_PLAN_RESIZED_W);
-    q.RH = TP_LD(p + TP_PLAN_RESIZED_H);
+    q.RW = ld_plan(p + TP_PLAN_RESIZED_W, psm);
+    q.RH = ld_plan(p + TP_PLAN_RESIZED_H, psm);
     q.oy0 = (t / cols) * E;
     q.ox0 = (t % cols) * E;
   } else {
@@ -461,8 +471,8 @@ template <int C, int ARENA>
 __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restrict__ src,
                         const int64_t* __restrict__ src_off, const int32_t* __restrict__ wh,
                         int n, const int32_t* __restrict__ plan,
-                        const int32_t* __restrict__ tile_off, int E, int64_t items, int bands,
-                        int band, int cap_tiles) {
+                        const int32_t* __restrict__ tile_off, bool psm, int E, int64_t items,
+                        int bands, int band, int cap_tiles) {
   const int lane = threadIdx.x & 31;
   int stage = 0;
   uint32_t parity = 0;
@@ -490,8 +500,8 @@ __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restri
   uintptr_t img_end = 0;
   // image of the current item: one binary search for the first item, then a forward walk
   // (the range is contiguous), so no chain of dependent global loads per item
-  int kimg = it_begin < it_end ? find_item_image(tile_off, n, it_begin, bands) : 0;
-  int toff0 = TP_LD(tile_off + kimg), toff1 = TP_LD(tile_off + kimg + 1);
+  int kimg = it_begin < it_end ? find_item_image(tile_off, psm, n, it_begin, bands) : 0;
+  int toff0 = ld_plan(tile_off + kimg, psm), toff1 = ld_plan(tile_off + kimg + 1, psm);
 #if TP_K2_TRACE
   int tr_phase = 0;
   unsigned long long tr_item = 0;
@@ -512,7 +522,7 @@ __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restri
     while (static_cast<int64_t>(toff1) * bands <= item) {
       ++kimg;
       toff0 = toff1;
-      toff1 = TP_LD(tile_off + kimg + 1);
+      toff1 = ld_plan(tile_off + kimg + 1, psm);
     }
     const int nimg = toff1 - toff0;
     const int r = static_cast<int>(item - static_cast<int64_t>(toff0) * bands);
@@ -539,12 +549,12 @@ __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restri
       stride = static_cast<int64_t>(W) * C;
       img_end = reinterpret_cast<uintptr_t>(img) + static_cast<uintptr_t>(stride) * H;
       if (nimg <= kTileCache) {
-        if (lane < nimg) hdr.tg[lane] = tile_geometry<C, ARENA>(plan, kimg, lane, W, H, E);
+        if (lane < nimg) hdr.tg[lane] = tile_geometry<C, ARENA>(plan, psm, kimg, lane, W, H, E);
         __syncwarp();
       }
     }
     const int t = g - toff0;
-    const TileGeo geo = nimg <= kTileCache ? hdr.tg[t] : tile_geometry<C, ARENA>(plan, kimg, t, W, H, E);
+    const TileGeo geo = nimg <= kTileCache ? hdr.tg[t] : tile_geometry<C, ARENA>(plan, psm, kimg, t, W, H, E);
     const int RW = geo.RW, RH = geo.RH, oy0 = geo.oy0, ox0 = geo.ox0, cwid = geo.cwid;
     const bool contig = RH > H;
     const double sy = geo.sy, sx = geo.sx;
@@ -1106,7 +1116,7 @@ __global__ void __launch_bounds__(kMaxThreads, kCtasPerSm)
                const int32_t* __restrict__ wh, int n, const int32_t* __restrict__ plan,
                const int32_t* __restrict__ tile_off, int E, const OutT* __restrict__ lut,
                const float* __restrict__ aff, OutT* __restrict__ out,
-               uint8_t* __restrict__ out_u8, int64_t cap) {
+               uint8_t* __restrict__ out_u8, int64_t cap, FusePlan fp) {
   extern __shared__ __align__(128) uint8_t smem[];
   SmemHeader& hdr = *reinterpret_cast<SmemHeader*>(smem);
   OutT* s_lut = reinterpret_cast<OutT*>(smem + ((sizeof(SmemHeader) + 127) & ~size_t(127)));
@@ -1129,10 +1139,55 @@ __global__ void __launch_bounds__(kMaxThreads, kCtasPerSm)
   // lifetime (with __ldg here, plans read stale and K2 faulted under PDL).
   if (WRITE_OUT && !(AFFINE && !WRITE_U8))
     for (int i = threadIdx.x; i < C * 256; i += blockDim.x) s_lut[i] = TP_LD(lut + i);
+  // fused small-batch mode (tp_plan_tile): warp 0 plans the batch with K1's rule into
+  // shared memory (every CTA, n <= kFuseMaxImages: a few hundred cycles) and CTA 0
+  // publishes the plans; the batch-1 critical path loses K1's launch and completion
+  const bool fused = fp.max_tiles > 0;
+  if (fused && threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    int acc = 0;
+    bool bad = false;
+    for (int k = 0; k < n; ++k) {
+      const int w = TP_LD(wh + 2 * k), h = TP_LD(wh + 2 * k + 1);
+      const bool ok = w >= 1 && h >= 1 && w <= TP_MAX_EDGE && h <= TP_MAX_EDGE;
+      Cand best;
+      best.rows = 0;
+      best.cols = 0;
+      if (ok) best = warp_plan(static_cast<uint32_t>(w), static_cast<uint32_t>(h), fp.max_tiles);
+      const int tiles = best.rows * best.cols, thumb = tiles > 1 ? 1 : 0;
+      if (lane == 0) {
+        int* q = hdr.fplan[k];
+        q[TP_PLAN_ROWS] = best.rows;
+        q[TP_PLAN_COLS] = best.cols;
+        q[TP_PLAN_TILE_EDGE] = E;
+        q[TP_PLAN_THUMB] = thumb;
+        q[TP_PLAN_RESIZED_W] = best.cols * E;
+        q[TP_PLAN_RESIZED_H] = best.rows * E;
+        hdr.ftoff[k] = acc;
+      }
+      bad = bad || !ok;
+      acc += tiles + thumb;
+    }
+    if (lane == 0) hdr.ftoff[n] = bad ? -1 : acc;
+    __syncwarp();
+    if (blockIdx.x == 0) {  // the caller's plan / n_img / tile_off buffers (K1's outputs)
+      int32_t* gplan = const_cast<int32_t*>(plan);
+      int32_t* gtoff = const_cast<int32_t*>(tile_off);
+      for (int i = lane; i < n * TP_PLAN_FIELDS; i += 32)
+        gplan[i] = hdr.fplan[i / TP_PLAN_FIELDS][i % TP_PLAN_FIELDS];
+      if (lane < n) {
+        const int* q = hdr.fplan[lane];
+        fp.n_img[lane] = q[TP_PLAN_ROWS] * q[TP_PLAN_COLS] + q[TP_PLAN_THUMB];
+      }
+      if (lane <= n) gtoff[lane] = hdr.ftoff[lane];
+    }
+  }
   __syncthreads();
+  const int32_t* plan_r = fused ? &hdr.fplan[0][0] : plan;
+  const int32_t* toff_r = fused ? hdr.ftoff : tile_off;
   // every tile's items are enumerated (item order interleaves tiles); tiles at or
   // above the output capacity are skipped
-  const int all_tiles = TP_LD(tile_off + n);
+  const int all_tiles = ld_plan(toff_r + n, fused);
   const int cap_tiles = static_cast<int>(min(static_cast<int64_t>(all_tiles), cap));
   // band height: kBand rows, smaller when a small batch would leave SMs idle (batch-1
   // latency); every CTA derives the same value from the device-side tile count
@@ -1149,7 +1204,8 @@ __global__ void __launch_bounds__(kMaxThreads, kCtasPerSm)
   const int bands = (E + band - 1) / band;
   const int64_t items = cap_tiles > 0 ? static_cast<int64_t>(all_tiles) * bands : 0;
   if (threadIdx.x < 32)
-    produce<C, arena_bytes<C, OutT>()>(hdr, arena, src, src_off, wh, n, plan, tile_off, E, items, bands, band, cap_tiles);
+    produce<C, arena_bytes<C, OutT>()>(hdr, arena, src, src_off, wh, n, plan_r, toff_r, fused,
+                                       E, items, bands, band, cap_tiles);
   else
     consume<C, OutT, LAYOUT, WRITE_OUT, WRITE_U8, AFFINE, EK>(hdr, arena, s_lut, E, out, out_u8,
                                                              aff);
@@ -1166,7 +1222,7 @@ template <int C, typename OutT, int LAYOUT, bool WRITE_OUT, bool WRITE_U8, bool 
 int launch_variant(const uint8_t* src, const int64_t* src_off, const int32_t* wh, int n,
                    const int32_t* plan, const int32_t* tile_off, int E, const void* lut,
                    const float* aff, void* out, uint8_t* out_u8, int64_t cap, bool pdl,
-                   cudaStream_t stream) {
+                   cudaStream_t stream, FusePlan fuse) {
   auto kern = k_tile_tma<C, OutT, LAYOUT, WRITE_OUT, WRITE_U8, AFFINE, EK>;
   const size_t smem = tma_smem_bytes<C, OutT>();
   // per device and template instance: the shared-memory opt-in and the occupancy for
@@ -1192,11 +1248,11 @@ int launch_variant(const uint8_t* src, const int64_t* src_off, const int32_t* wh
   if (TP_K2_PDL && pdl) {  // programmatic dependent of the K1 right before it
     err = launch_pdl(kern, dim3(grid), dim3(threads), smem, stream, src, src_off, wh, n, plan,
                      tile_off, E, static_cast<const OutT*>(lut), aff, static_cast<OutT*>(out),
-                     out_u8, cap);
+                     out_u8, cap, fuse);
   } else {
     kern<<<grid, threads, smem, stream>>>(src, src_off, wh, n, plan, tile_off, E,
                                           static_cast<const OutT*>(lut), aff,
-                                          static_cast<OutT*>(out), out_u8, cap);
+                                          static_cast<OutT*>(out), out_u8, cap, fuse);
   }
   if (err != cudaSuccess) return set_error(TP_ERR_CUDA, "tp_tile: %s", cudaGetErrorString(err));
   return check_launch("tp_tile(tma)");
@@ -1208,10 +1264,10 @@ template <int C, typename OutT, int LAYOUT, bool WRITE_OUT>
 int launch_tile_tma(const uint8_t* src, const int64_t* src_off, const int32_t* wh, int n,
                     const int32_t* plan, const int32_t* tile_off, int E, const void* lut,
                     void* out, uint8_t* out_u8, int64_t cap, bool affine, bool after_plan,
-                    cudaStream_t stream) {
+                    cudaStream_t stream, FusePlan fuse) {
   if (out_u8)
     return launch_variant<C, OutT, LAYOUT, WRITE_OUT, true, false>(
-        src, src_off, wh, n, plan, tile_off, E, lut, nullptr, out, out_u8, cap, after_plan, stream);
+        src, src_off, wh, n, plan, tile_off, E, lut, nullptr, out, out_u8, cap, after_plan, stream, fuse);
   if (WRITE_OUT && affine) {
     // the affine block follows the table (tp_build_norm)
     const float* aff = reinterpret_cast<const float*>(
@@ -1219,18 +1275,19 @@ int launch_tile_tma(const uint8_t* src, const int64_t* src_off, const int32_t* w
         tp_lut_table_bytes(C, sizeof(OutT) == 4 ? TP_DTYPE_F32 : TP_DTYPE_BF16));
     if (E == 448 && LAYOUT == TP_LAYOUT_NCHW)  // the InternVL / C2-C5 tile edge
       return launch_variant<C, OutT, LAYOUT, WRITE_OUT, false, true, 448>(
-          src, src_off, wh, n, plan, tile_off, E, lut, aff, out, out_u8, cap, after_plan, stream);
+          src, src_off, wh, n, plan, tile_off, E, lut, aff, out, out_u8, cap, after_plan, stream, fuse);
     return launch_variant<C, OutT, LAYOUT, WRITE_OUT, false, true>(
-        src, src_off, wh, n, plan, tile_off, E, lut, aff, out, out_u8, cap, after_plan, stream);
+        src, src_off, wh, n, plan, tile_off, E, lut, aff, out, out_u8, cap, after_plan, stream, fuse);
   }
   return launch_variant<C, OutT, LAYOUT, WRITE_OUT, false, false>(
-      src, src_off, wh, n, plan, tile_off, E, lut, nullptr, out, out_u8, cap, after_plan, stream);
+      src, src_off, wh, n, plan, tile_off, E, lut, nullptr, out, out_u8, cap, after_plan, stream, fuse);
 }
 
 #define TP_INSTANTIATE(C, T, L, W)                                                             \
   template int launch_tile_tma<C, T, L, W>(const uint8_t*, const int64_t*, const int32_t*, int, \
                                            const int32_t*, const int32_t*, int, const void*,   \
-                                           void*, uint8_t*, int64_t, bool, bool, cudaStream_t);
+                                           void*, uint8_t*, int64_t, bool, bool, cudaStream_t, \
+                                           FusePlan);
 TP_INSTANTIATE(1, float, TP_LAYOUT_NHWC, false)
 TP_INSTANTIATE(3, float, TP_LAYOUT_NHWC, false)
 TP_INSTANTIATE(1, float, TP_LAYOUT_NCHW, true)

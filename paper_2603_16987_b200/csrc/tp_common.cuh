@@ -145,11 +145,20 @@ __device__ __forceinline__ T block_exclusive_scan(T v, T* scratch, T* total) {
   return res;
 }
 
+// K2's fused small-batch mode (tp_plan_tile): max_tiles > 0 makes every CTA plan the
+// batch itself (K1's rule, plan_core.cuh) instead of reading K1's output; CTA 0 writes
+// the plans, per-image counts and tile offsets to these buffers for the caller.
+constexpr int kFuseMaxImages = TP_PLAN_TILE_MAX_IMAGES;
+struct FusePlan {
+  int max_tiles = 0;  // 0: plans come from a preceding tp_plan
+  int32_t* n_img = nullptr;
+};
+
 // K2 fast path (tile_tma.cu): TMA-staged fp32 kernel with exact fallback
 template <int C, typename OutT, int LAYOUT, bool WRITE_OUT>
 int launch_tile_tma(const uint8_t* src, const int64_t* src_off, const int32_t* wh, int n,
                     const int32_t* plan, const int32_t* tile_off, int E, const void* lut,
                     void* out, uint8_t* out_u8, int64_t cap, bool affine, bool after_plan,
-                    cudaStream_t stream);
+                    cudaStream_t stream, FusePlan fuse = FusePlan{});
 
 }  // namespace tp

@@ -160,11 +160,14 @@ class TilePreprocessor:
     layout         "NCHW" (vision-encoder input) or "NHWC" (reference layout)
     emit_uint8     also write the uint8 HWC tiles (deferred-normalize payload)
     normalize      write normalized tiles (False = uint8 tiles only)
+    fuse_small     batches of <= TP_PLAN_TILE_MAX_IMAGES images run K1 inside K2
+                   (tp_plan_tile: one launch, same plans and tiles; batch-1 latency)
     """
 
     def __init__(self, cfg, device=None, layout: str = "NCHW", emit_uint8: bool = False,
-                 normalize: bool = True, algo: str = "auto"):
+                 normalize: bool = True, algo: str = "auto", fuse_small: bool = True):
         self.cfg = cfg
+        self.fuse_small = fuse_small
         algos = {"auto": _lib.TP_TILE_ALGO_AUTO, "fast": _lib.TP_TILE_ALGO_FAST,
                  "exact": _lib.TP_TILE_ALGO_EXACT}
         if algo not in algos:
@@ -261,9 +264,31 @@ class TilePreprocessor:
             pv, u8 = self.alloc_outputs(images.channels, cap)
             out = TileBatch(self.alloc_plans(images.n), pv, u8)
         self._norm(images.channels)  # K0 (first use only) before K1, so K2 follows K1 directly
+        if (self.fuse_small and 0 < images.n <= _lib.TP_PLAN_TILE_MAX_IMAGES
+                and self.algo != _lib.TP_TILE_ALGO_EXACT):
+            self.plan_tile(images, out, stream)
+            return out
         self.plan(images, out.plans, stream)
         self.tile(images, out.plans, out.pixel_values, out.pixel_u8, stream, after_plan=True)
         return out
+
+    def plan_tile(self, images: PackedImages, out: TileBatch,
+                  stream: Optional[torch.cuda.Stream] = None) -> None:
+        """K1 + K2 as one launch (tp_plan_tile) for a batch of at most
+        TP_PLAN_TILE_MAX_IMAGES images: the same plans, counts, offsets and tiles."""
+        lut, affine = self._norm(images.channels)
+        algo = self.algo | (_lib.TP_TILE_NORM_AFFINE if affine else 0)
+        caps = [t.shape[0] for t in (out.pixel_values, out.pixel_u8) if t is not None]
+        if not caps:
+            raise ValueError("no output buffer")
+        p = out.plans
+        with torch.cuda.device(self.device):
+            _lib.call("tp_plan_tile", _lib.ptr(images.data), _lib.ptr(images.offsets),
+                      _lib.ptr(images.wh), images.n, images.channels, self.cfg.tile_edge,
+                      self.cfg.max_tiles, _lib.ptr(p.plan), _lib.ptr(p.n_images),
+                      _lib.ptr(p.tile_off), _lib.ptr(lut), self.dtype, self.layout,
+                      _lib.ptr(out.pixel_values), _lib.ptr(out.pixel_u8), min(caps), algo,
+                      stream_handle(self.device, stream))
 
 
 __all__ = [
