@@ -1,4 +1,4 @@
-"""Per-phase timing of K2 on C2 from a TP_K2_TRACE=1 build (clock64 stamps, same SM):
+"""Per-phase timing of K2 on C2 (or C3: K2_TRACE_WL=c3) from a TP_K2_TRACE=1 build (clock64 stamps, same SM):
 how long consumers wait for data, whether waits cluster at item starts, producer
 planning time.  TILEPREP_LIB must point at the trace build."""
 import ctypes
@@ -14,10 +14,10 @@ import torch  # noqa: E402
 from paper_2603_16987_b200 import _lib  # noqa: E402
 from paper_2603_16987_b200.engine import TilePreprocessor, synth_packed  # noqa: E402
 from paper_2603_16987_b200.imgproc import PreprocessConfig  # noqa: E402
-from paper_2603_16987_b200.workloads import c2  # noqa: E402
+from paper_2603_16987_b200.workloads import c2, c3  # noqa: E402
 
 lib = _lib.load()
-wl = c2()
+wl = c3() if os.environ.get("K2_TRACE_WL") == "c3" else c2()
 cfg = PreprocessConfig(tile_edge=wl.tile_edge, max_tiles=wl.max_tiles, mean=wl.mean, std=wl.std,
                        reduced_precision_normalize=wl.bf16)
 imgs = synth_packed(wl.wh, 3, "cuda:0", seed=wl.seed, kind=0)
@@ -41,8 +41,9 @@ plan = (t[:, :, 2] - t[:, :, 1])[valid]
 wait = (t[:, :, 4] - t[:, :, 3])[valid]
 work = (t[:, :, 5] - t[:, :, 4])[valid]
 start = t[:, 0, 3]
-end = np.array([t[c, valid[c], 5].max() for c in range(296)])
+end = np.array([t[c, valid[c], 5].max() if valid[c].any() else t[c, 0, 3] for c in range(296)])
 res = {
+    "workload": wl.name,
     "phases": int(valid.sum()),
     "cycles_per_cta_p50": float(np.median(end - start)),
     "cta_span_min_max": [float((end - start).min()), float((end - start).max())],
