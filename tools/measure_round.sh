@@ -1,5 +1,6 @@
 set -x
 timeout 900 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print(\"smoke ok\")" > gpurun_out/smoke.log 2>&1
 timeout 600 python bench.py > gpurun_out/bench_default.log 2>gpurun_out/bench_default.err
 timeout 600 python bench.py --impl reference --steps 5 --warmup 1 > gpurun_out/bench_reference.log 2>&1
 timeout 600 python bench.py --workload c4 --steps 3 --warmup 2 > gpurun_out/bench_c4.log 2>&1
