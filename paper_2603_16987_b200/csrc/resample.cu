@@ -75,17 +75,6 @@ __device__ __forceinline__ void store_norm(OutT* out, int64_t idx, const OutT* l
   out[idx] = lut[c * 256 + u];
 }
 
-__device__ __forceinline__ void store_pair(float* dst, float a, float b) {
-  *reinterpret_cast<float2*>(dst) = make_float2(a, b);
-}
-__device__ __forceinline__ void store_pair(__nv_bfloat16* dst, __nv_bfloat16 a,
-                                           __nv_bfloat16 b) {
-  __nv_bfloat162 v;
-  v.x = a;
-  v.y = b;
-  *reinterpret_cast<__nv_bfloat162*>(dst) = v;
-}
-
 // One output row segment [0, OW) of row `oy` of the window, exact fp64.
 template <int C, typename OutT, int LAYOUT, bool WRITE_OUT>
 __device__ __forceinline__ void exact_row(const TileGeom& q, int j, int E, double sy,

@@ -71,9 +71,6 @@ namespace {
                     // items, 2: not thumbnails, whose rows the tiles just read): C4 -3%, C2 +0.4%
 #define TP_K2_L2PF 2
 #endif
-#ifndef TP_K2_FIXMODE  // fp64 fallback: 1 = conversions folded into fma (S w - 2^52 w), PRMT bytes
-#define TP_K2_FIXMODE 1
-#endif
 #ifndef TP_K2_DWIN  // affine path: window test on d = T - round(T) instead of N = round(8192 t)
 #define TP_K2_DWIN 1
 #endif
@@ -295,24 +292,9 @@ __device__ __forceinline__ f32x2 sub2(f32x2 a, f32x2 b) {
   return d;
 }
 
-// exact reference-order fp64 sample (imgproc.py:309-349) with cheap conversions:
-// byte -> double as (2^52 + b) - 2^52, floor(t) as the low word of t + 2^52
-// rounded toward -inf (0 <= t < 2^32).  No FMA contraction (explicit _rn ops).
-__device__ __forceinline__ double u8_to_f64(uint32_t b) {
-  return __dsub_rn(__hiloint2double(0x43300000, static_cast<int>(b)), 4503599627370496.0);
-}
-__device__ __forceinline__ uint32_t blend_exact_fast(uint32_t s00, uint32_t s01, uint32_t s10,
-                                                     uint32_t s11, double fy, double omfy,
-                                                     double fx, double omfx) {
-  const double l = __dadd_rn(__dmul_rn(u8_to_f64(s00), omfy), __dmul_rn(u8_to_f64(s10), fy));
-  const double r = __dadd_rn(__dmul_rn(u8_to_f64(s01), omfy), __dmul_rn(u8_to_f64(s11), fy));
-  const double v = __dadd_rn(__dmul_rn(l, omfx), __dmul_rn(r, fx));
-  const double t = __dadd_rn(v, 0.5);
-  const uint32_t k = static_cast<uint32_t>(__double2loint(__dadd_rd(t, 4503599627370496.0)));
-  return min(k, 255u);  // t >= 0.5 > 0, so no lower clip is needed
-}
-// The same with the conversions folded into the products: for S = 2^52 + s (the byte in
-// the low word of 2^52's bit pattern) fma(S, w, -2^52 w) = round(s w) exactly, because
+// Exact reference-order fp64 sample (imgproc.py:309-349, uncontracted products and
+// sums), with the byte conversions folded into the products: for S = 2^52 + s (the byte
+// in the low word of 2^52's bit pattern) fma(S, w, -2^52 w) = round(s w) exactly, because
 // -2^52 w is exact (power-of-two scale) and the fma rounds S w - 2^52 w = s w once.
 // nw0 = -2^52 (1 - fy), nw1 = -2^52 fy, per output row.
 __device__ __forceinline__ double byte_f64_biased(uint32_t b) {
@@ -329,7 +311,7 @@ __device__ __forceinline__ uint32_t blend_exact_fma(uint32_t s00, uint32_t s01, 
   const double v = __dadd_rn(__dmul_rn(l, omfx), __dmul_rn(r, fx));
   const double t = __dadd_rn(v, 0.5);
   const uint32_t k = static_cast<uint32_t>(__double2loint(__dadd_rd(t, 4503599627370496.0)));
-  return min(k, 255u);
+  return min(k, 255u);  // t >= 0.5 > 0, so no lower clip is needed
 }
 
 // byte k (0..7) of (g0, g1) as the float 2^23 + byte (exact)
@@ -339,11 +321,7 @@ __device__ __forceinline__ float biased_byte(uint32_t g0, uint32_t g1, int k) {
 }
 
 __device__ __forceinline__ uint32_t byte_of(uint32_t g0, uint32_t g1, int k) {
-#if TP_K2_FIXMODE >= 1
   return __byte_perm(k < 4 ? g0 : g1, 0u, 0x4440u | static_cast<uint32_t>(k & 3));  // one PRMT
-#else
-  return ((k < 4 ? g0 : g1) >> ((k & 3) * 8)) & 0xFFu;
-#endif
 }
 
 // The fast path (consumer loop below) computes, per value, with biased taps
@@ -362,42 +340,6 @@ __device__ __forceinline__ int find_item_image(const int32_t* __restrict__ tile_
     if (static_cast<int64_t>(ld_plan(tile_off + mid, psm)) * bands <= item) lo = mid; else hi = mid;
   }
   return lo;
-}
-
-__device__ __forceinline__ int find_tile_image(const int32_t* __restrict__ tile_off, int n,
-                                               int g) {
-  int lo = 0, hi = n;
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (TP_LD(tile_off + mid) <= g) lo = mid; else hi = mid;
-  }
-  return lo;
-}
-
-template <typename OutT>
-__device__ __forceinline__ void store2(OutT* dst, OutT a, OutT b, bool pair_ok, bool has_b);
-template <>
-__device__ __forceinline__ void store2<float>(float* dst, float a, float b, bool pair_ok,
-                                              bool has_b) {
-  if (pair_ok) {
-    *reinterpret_cast<float2*>(dst) = make_float2(a, b);
-  } else {
-    dst[0] = a;
-    if (has_b) dst[1] = b;
-  }
-}
-template <>
-__device__ __forceinline__ void store2<__nv_bfloat16>(__nv_bfloat16* dst, __nv_bfloat16 a,
-                                                      __nv_bfloat16 b, bool pair_ok, bool has_b) {
-  if (pair_ok) {
-    __nv_bfloat162 v;
-    v.x = a;
-    v.y = b;
-    *reinterpret_cast<__nv_bfloat162*>(dst) = v;
-  } else {
-    dst[0] = a;
-    if (has_b) dst[1] = b;
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -555,7 +497,7 @@ __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restri
     }
     const int t = g - toff0;
     const TileGeo geo = nimg <= kTileCache ? hdr.tg[t] : tile_geometry<C, ARENA>(plan, psm, kimg, t, W, H, E);
-    const int RW = geo.RW, RH = geo.RH, oy0 = geo.oy0, ox0 = geo.ox0, cwid = geo.cwid;
+    const int RH = geo.RH, oy0 = geo.oy0, ox0 = geo.ox0, cwid = geo.cwid;
     const bool contig = RH > H;
     const double sy = geo.sy, sx = geo.sx;
     const uint64_t policy = l2_policy(t == nimg - 1);  // thumbnail (or only tile): last read
@@ -910,15 +852,10 @@ __device__ __forceinline__ void consume_pair_rows(
     auto code = [&](uint32_t k) -> uint32_t {
       return DW ? __float_as_uint(__uint_as_float(kOut + k) - 8388608.0f) : kOut + k;
     };
-#if TP_K2_FIXMODE >= 1
     const double nw1 = __dmul_rn(fy64, -4503599627370496.0),
                  nw0 = __dmul_rn(omfy64, -4503599627370496.0);
 #define TP_BLEND(s00, s01, s10, s11, fx, omfx) \
   blend_exact_fma(s00, s01, s10, s11, fy64, omfy64, nw1, nw0, fx, omfx)
-#else
-#define TP_BLEND(s00, s01, s10, s11, fx, omfx) \
-  blend_exact_fast(s00, s01, s10, s11, fy64, omfy64, fx, omfx)
-#endif
 #pragma unroll
     for (int c = 0; c < C; ++c) {
       if (flagged(xa[c]))
