@@ -169,6 +169,28 @@ TP_API int tp_plan_tile(const uint8_t* d_src, const int64_t* d_src_off, const in
                         const void* d_lut, int32_t dtype, int32_t layout, void* d_out,
                         uint8_t* d_out_u8, int64_t out_capacity, int32_t algo, void* stream);
 
+/* Touched-row staging.  K2 reads only the source rows its 2-tap stencil touches
+ * (tiles: H -> rows*E, thumbnail: H -> E), so an uploader can send just those rows.
+ *   tp_plan_host     K1's exact planner on the host for one image (plan[6])
+ *   tp_touched_rows  row map of one image: row_map[0] = n touched rows,
+ *                    row_map[1 + y] = compact index of source row y or -1 (h + 1 ints);
+ *                    returns n (or a negative error code)
+ *   tp_tile_rows     tp_tile_ex over images whose pixel blocks hold only the touched
+ *                    rows (compact index order, each a full row of w*channels bytes):
+ *                    d_row_map holds every image's map, d_row_map_off[k] the int32
+ *                    index of image k's map.  Fast algorithm only.  Same output as
+ *                    tp_tile_ex on the full images. */
+TP_API int tp_plan_host(int32_t width, int32_t height, int32_t tile_edge, int32_t max_tiles,
+                        int32_t* plan);
+TP_API int64_t tp_touched_rows(int32_t width, int32_t height, const int32_t* plan,
+                               int32_t* row_map);
+TP_API int tp_tile_rows(const uint8_t* d_src, const int64_t* d_src_off, const int32_t* d_wh,
+                        int32_t n, int32_t channels, const int32_t* d_plan,
+                        const int32_t* d_tile_off, int32_t tile_edge, const void* d_lut,
+                        int32_t dtype, int32_t layout, void* d_out, uint8_t* d_out_u8,
+                        int64_t out_capacity, int32_t algo, const int32_t* d_row_map,
+                        const int64_t* d_row_map_off, void* stream);
+
 /* K2 variant for resize_bilinear / _resize_array (imgproc.py:352-367): one
  * full-frame half-pixel bilinear resize, uint8 HWC -> uint8 HWC. */
 TP_API int tp_resize(const uint8_t* d_src, int32_t width, int32_t height, int32_t channels,

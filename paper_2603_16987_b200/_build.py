@@ -30,6 +30,8 @@ NVCC_FLAGS = [
     "-fPIC",
     "-Xcompiler",
     "-fvisibility=hidden",
+    "-Xcompiler",
+    "-ffp-contract=off",  # host fp64 (rows_host.cu) must round like the device's _rn ops
     "--expt-relaxed-constexpr",
 ]
 

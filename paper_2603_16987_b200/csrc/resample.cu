@@ -159,7 +159,7 @@ template <int C, typename OutT, int LAYOUT, bool WRITE_OUT>
 int launch_tile(const uint8_t* src, const int64_t* src_off, const int32_t* wh, int n,
                 const int32_t* plan, const int32_t* tile_off, int E, const void* lut, void* out,
                 uint8_t* out_u8, int64_t cap, int algo, cudaStream_t stream,
-                FusePlan fuse = FusePlan{}) {
+                K2Options fuse = K2Options{}) {
   const int sms = max(1, device_sm_count());
   int per_sm = 0;
   if ((algo & 0xFF) == TP_TILE_ALGO_EXACT) {
@@ -181,7 +181,7 @@ template <int C>
 int dispatch_tile(const uint8_t* src, const int64_t* src_off, const int32_t* wh, int n,
                   const int32_t* plan, const int32_t* tile_off, int E, const void* lut,
                   int dtype, int layout, void* out, uint8_t* out_u8, int64_t cap, int algo,
-                  cudaStream_t s, FusePlan fuse = FusePlan{}) {
+                  cudaStream_t s, K2Options fuse = K2Options{}) {
   if (dtype == TP_DTYPE_NONE)
     return launch_tile<C, float, TP_LAYOUT_NHWC, false>(src, src_off, wh, n, plan, tile_off, E,
                                                         lut, out, out_u8, cap, algo, s, fuse);
@@ -263,7 +263,7 @@ extern "C" int tp_plan_tile(const uint8_t* d_src, const int64_t* d_src_off, cons
   cudaStream_t s = tp::as_stream(stream);
   if (n == 0 || out_capacity == 0)  // nothing to tile: the plans alone (K1)
     return tp_plan(d_wh, n, tile_edge, max_tiles, d_plan, d_n_img, d_tile_off, stream);
-  tp::FusePlan fuse;
+  tp::K2Options fuse;
   fuse.max_tiles = max_tiles;
   fuse.n_img = d_n_img;
   if (channels == 3)
@@ -271,6 +271,31 @@ extern "C" int tp_plan_tile(const uint8_t* d_src, const int64_t* d_src_off, cons
                                 dtype, layout, d_out, d_out_u8, out_capacity, algo, s, fuse);
   return tp::dispatch_tile<1>(d_src, d_src_off, d_wh, n, d_plan, d_tile_off, tile_edge, d_lut,
                               dtype, layout, d_out, d_out_u8, out_capacity, algo, s, fuse);
+}
+
+extern "C" int tp_tile_rows(const uint8_t* d_src, const int64_t* d_src_off, const int32_t* d_wh,
+                            int32_t n, int32_t channels, const int32_t* d_plan,
+                            const int32_t* d_tile_off, int32_t tile_edge, const void* d_lut,
+                            int32_t dtype, int32_t layout, void* d_out, uint8_t* d_out_u8,
+                            int64_t out_capacity, int32_t algo, const int32_t* d_row_map,
+                            const int64_t* d_row_map_off, void* stream) {
+  if ((algo & 0xFF) == TP_TILE_ALGO_EXACT)
+    return tp::set_error(TP_ERR_INVALID_ARGUMENT, "tp_tile_rows: fast algorithm only");
+  const int rc = tp::check_tile_args(d_src, d_src_off, d_wh, n, channels, tile_edge, d_lut, dtype,
+                                     layout, d_out, d_out_u8, out_capacity, algo);
+  if (rc != TP_OK) return rc;
+  if (n == 0 || out_capacity == 0) return TP_OK;
+  if (!d_plan || !d_tile_off || !d_row_map || !d_row_map_off)
+    return tp::set_error(TP_ERR_INVALID_ARGUMENT, "tp_tile_rows: null buffer");
+  tp::K2Options opt;
+  opt.row_map = d_row_map;
+  opt.row_map_off = d_row_map_off;
+  cudaStream_t s = tp::as_stream(stream);
+  if (channels == 3)
+    return tp::dispatch_tile<3>(d_src, d_src_off, d_wh, n, d_plan, d_tile_off, tile_edge, d_lut,
+                                dtype, layout, d_out, d_out_u8, out_capacity, algo, s, opt);
+  return tp::dispatch_tile<1>(d_src, d_src_off, d_wh, n, d_plan, d_tile_off, tile_edge, d_lut,
+                              dtype, layout, d_out, d_out_u8, out_capacity, algo, s, opt);
 }
 
 extern "C" int tp_tile_ex(const uint8_t* d_src, const int64_t* d_src_off, const int32_t* d_wh,

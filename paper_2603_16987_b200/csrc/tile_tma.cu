@@ -142,7 +142,7 @@ struct __align__(16) SmemHeader {
   TileGeo tg[kTileCache];  // producer: tiles of the current image
   unsigned long long full[kStages];
   unsigned long long empty[kStages];
-  // fused small-batch mode: this CTA's own plans and tile offsets (FusePlan)
+  // fused small-batch mode: this CTA's own plans and tile offsets (K2Options)
   int fplan[kFuseMaxImages][TP_PLAN_FIELDS];
   int ftoff[kFuseMaxImages + 1];
 };
@@ -414,7 +414,8 @@ __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restri
                         const int64_t* __restrict__ src_off, const int32_t* __restrict__ wh,
                         int n, const int32_t* __restrict__ plan,
                         const int32_t* __restrict__ tile_off, bool psm, int E, int64_t items,
-                        int bands, int band, int cap_tiles) {
+                        int bands, int band, int cap_tiles, const int32_t* __restrict__ row_map,
+                        const int64_t* __restrict__ row_map_off) {
   const int lane = threadIdx.x & 31;
   int stage = 0;
   uint32_t parity = 0;
@@ -440,6 +441,7 @@ __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restri
   int W = 1, H = 1;
   int64_t stride = 0;
   uintptr_t img_end = 0;
+  const int32_t* rmap = nullptr;  // touched-row input: compact index of each source row
   // image of the current item: one binary search for the first item, then a forward walk
   // (the range is contiguous), so no chain of dependent global loads per item
   int kimg = it_begin < it_end ? find_item_image(tile_off, psm, n, it_begin, bands) : 0;
@@ -489,7 +491,13 @@ __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restri
       H = TP_LD(wh + 2 * kimg + 1);
       img = src + TP_LD(src_off + kimg);
       stride = static_cast<int64_t>(W) * C;
-      img_end = reinterpret_cast<uintptr_t>(img) + static_cast<uintptr_t>(stride) * H;
+      int rows_held = H;
+      if (row_map) {  // touched-row input: the block holds row_map's rows only
+        rmap = row_map + TP_LD(row_map_off + kimg);
+        rows_held = TP_LD(rmap);
+        ++rmap;
+      }
+      img_end = reinterpret_cast<uintptr_t>(img) + static_cast<uintptr_t>(stride) * rows_held;
       if (nimg <= kTileCache) {
         if (lane < nimg) hdr.tg[lane] = tile_geometry<C, ARENA>(plan, psm, kimg, lane, W, H, E);
         __syncwarp();
@@ -542,7 +550,9 @@ __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restri
           isnew = valid && (lane == 0 || y_e != yp);
         }
         const uintptr_t gs =
-            valid ? reinterpret_cast<uintptr_t>(img + y_e * stride + xlo * C) : uintptr_t(0);
+            valid ? reinterpret_cast<uintptr_t>(img + (row_map ? TP_LD(rmap + y_e) : y_e) * stride +
+                                                xlo * C)
+                  : uintptr_t(0);
         const int delta = static_cast<int>(gs & 15u);
         const int region = isnew ? ((delta + rb + 15) & ~15) + kRowSlack : 0;
         const int incl = warp_incl_sum(region, lane);
@@ -1053,7 +1063,7 @@ __global__ void __launch_bounds__(kMaxThreads, kCtasPerSm)
                const int32_t* __restrict__ wh, int n, const int32_t* __restrict__ plan,
                const int32_t* __restrict__ tile_off, int E, const OutT* __restrict__ lut,
                const float* __restrict__ aff, OutT* __restrict__ out,
-               uint8_t* __restrict__ out_u8, int64_t cap, FusePlan fp) {
+               uint8_t* __restrict__ out_u8, int64_t cap, K2Options fp) {
   extern __shared__ __align__(128) uint8_t smem[];
   SmemHeader& hdr = *reinterpret_cast<SmemHeader*>(smem);
   OutT* s_lut = reinterpret_cast<OutT*>(smem + ((sizeof(SmemHeader) + 127) & ~size_t(127)));
@@ -1142,7 +1152,8 @@ __global__ void __launch_bounds__(kMaxThreads, kCtasPerSm)
   const int64_t items = cap_tiles > 0 ? static_cast<int64_t>(all_tiles) * bands : 0;
   if (threadIdx.x < 32)
     produce<C, arena_bytes<C, OutT>()>(hdr, arena, src, src_off, wh, n, plan_r, toff_r, fused,
-                                       E, items, bands, band, cap_tiles);
+                                       E, items, bands, band, cap_tiles, fp.row_map,
+                                       fp.row_map_off);
   else
     consume<C, OutT, LAYOUT, WRITE_OUT, WRITE_U8, AFFINE, EK>(hdr, arena, s_lut, E, out, out_u8,
                                                              aff);
@@ -1159,7 +1170,7 @@ template <int C, typename OutT, int LAYOUT, bool WRITE_OUT, bool WRITE_U8, bool 
 int launch_variant(const uint8_t* src, const int64_t* src_off, const int32_t* wh, int n,
                    const int32_t* plan, const int32_t* tile_off, int E, const void* lut,
                    const float* aff, void* out, uint8_t* out_u8, int64_t cap, bool pdl,
-                   cudaStream_t stream, FusePlan fuse) {
+                   cudaStream_t stream, K2Options fuse) {
   auto kern = k_tile_tma<C, OutT, LAYOUT, WRITE_OUT, WRITE_U8, AFFINE, EK>;
   const size_t smem = tma_smem_bytes<C, OutT>();
   // per device and template instance: the shared-memory opt-in and the occupancy for
@@ -1201,7 +1212,7 @@ template <int C, typename OutT, int LAYOUT, bool WRITE_OUT>
 int launch_tile_tma(const uint8_t* src, const int64_t* src_off, const int32_t* wh, int n,
                     const int32_t* plan, const int32_t* tile_off, int E, const void* lut,
                     void* out, uint8_t* out_u8, int64_t cap, bool affine, bool after_plan,
-                    cudaStream_t stream, FusePlan fuse) {
+                    cudaStream_t stream, K2Options fuse) {
   if (out_u8)
     return launch_variant<C, OutT, LAYOUT, WRITE_OUT, true, false>(
         src, src_off, wh, n, plan, tile_off, E, lut, nullptr, out, out_u8, cap, after_plan, stream, fuse);
@@ -1224,7 +1235,7 @@ int launch_tile_tma(const uint8_t* src, const int64_t* src_off, const int32_t* w
   template int launch_tile_tma<C, T, L, W>(const uint8_t*, const int64_t*, const int32_t*, int, \
                                            const int32_t*, const int32_t*, int, const void*,   \
                                            void*, uint8_t*, int64_t, bool, bool, cudaStream_t, \
-                                           FusePlan);
+                                           K2Options);
 TP_INSTANTIATE(1, float, TP_LAYOUT_NHWC, false)
 TP_INSTANTIATE(3, float, TP_LAYOUT_NHWC, false)
 TP_INSTANTIATE(1, float, TP_LAYOUT_NCHW, true)

@@ -145,13 +145,19 @@ __device__ __forceinline__ T block_exclusive_scan(T v, T* scratch, T* total) {
   return res;
 }
 
-// K2's fused small-batch mode (tp_plan_tile): max_tiles > 0 makes every CTA plan the
-// batch itself (K1's rule, plan_core.cuh) instead of reading K1's output; CTA 0 writes
-// the plans, per-image counts and tile offsets to these buffers for the caller.
+// K2 launch options beyond tp_tile_ex's arguments.
+//  * fused small-batch mode (tp_plan_tile): max_tiles > 0 makes every CTA plan the
+//    batch itself (K1's rule, plan_core.cuh) instead of reading K1's output; CTA 0
+//    writes the plans, per-image counts (n_img) and tile offsets for the caller;
+//  * touched-row input (tp_tile_rows): row_map != nullptr means image k's pixel block
+//    holds only its touched rows; row y is at compact index
+//    row_map[row_map_off[k] + 1 + y] (tp_touched_rows).
 constexpr int kFuseMaxImages = TP_PLAN_TILE_MAX_IMAGES;
-struct FusePlan {
+struct K2Options {
   int max_tiles = 0;  // 0: plans come from a preceding tp_plan
   int32_t* n_img = nullptr;
+  const int32_t* row_map = nullptr;
+  const int64_t* row_map_off = nullptr;
 };
 
 // K2 fast path (tile_tma.cu): TMA-staged fp32 kernel with exact fallback
@@ -159,6 +165,6 @@ template <int C, typename OutT, int LAYOUT, bool WRITE_OUT>
 int launch_tile_tma(const uint8_t* src, const int64_t* src_off, const int32_t* wh, int n,
                     const int32_t* plan, const int32_t* tile_off, int E, const void* lut,
                     void* out, uint8_t* out_u8, int64_t cap, bool affine, bool after_plan,
-                    cudaStream_t stream, FusePlan fuse = FusePlan{});
+                    cudaStream_t stream, K2Options fuse = K2Options{});
 
 }  // namespace tp

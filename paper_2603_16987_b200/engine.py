@@ -40,6 +40,10 @@ class PackedImages:
     channels: int
     wh_host: np.ndarray  # int32 [n, 2]
     offsets_host: np.ndarray  # int64 [n]
+    # touched-row input (transfer.stage_images(touched=...)): each image block holds only
+    # the source rows K2 reads; row_map / row_map_off as tp_tile_rows takes them
+    row_map: Optional[torch.Tensor] = None  # int32
+    row_map_off: Optional[torch.Tensor] = None  # int64 [n]
 
     @property
     def n(self) -> int:
@@ -61,6 +65,10 @@ class PackedImages:
             channels=self.channels,
             wh_host=self.wh_host,
             offsets_host=self.offsets_host,
+            row_map=None if self.row_map is None else self.row_map.to(
+                device, non_blocking=non_blocking),
+            row_map_off=None if self.row_map_off is None else self.row_map_off.to(
+                device, non_blocking=non_blocking),
         )
 
     def copy_from_(self, other: "PackedImages", non_blocking: bool = True) -> "PackedImages":
@@ -247,12 +255,16 @@ class TilePreprocessor:
         caps = [t.shape[0] for t in (pixel_values, pixel_u8) if t is not None]
         if not caps:
             raise ValueError("no output buffer")
+        args = (_lib.ptr(images.data), _lib.ptr(images.offsets), _lib.ptr(images.wh), images.n,
+                images.channels, _lib.ptr(plans.plan), _lib.ptr(plans.tile_off),
+                self.cfg.tile_edge, _lib.ptr(lut), self.dtype, self.layout,
+                _lib.ptr(pixel_values), _lib.ptr(pixel_u8), min(caps), algo)
         with torch.cuda.device(self.device):
-            _lib.call("tp_tile_ex", _lib.ptr(images.data), _lib.ptr(images.offsets),
-                      _lib.ptr(images.wh), images.n, images.channels, _lib.ptr(plans.plan),
-                      _lib.ptr(plans.tile_off), self.cfg.tile_edge, _lib.ptr(lut), self.dtype,
-                      self.layout, _lib.ptr(pixel_values), _lib.ptr(pixel_u8), min(caps),
-                      algo, stream_handle(self.device, stream))
+            if images.row_map is not None:  # touched rows only (transfer.stage_images)
+                _lib.call("tp_tile_rows", *args, _lib.ptr(images.row_map),
+                          _lib.ptr(images.row_map_off), stream_handle(self.device, stream))
+            else:
+                _lib.call("tp_tile_ex", *args, stream_handle(self.device, stream))
 
     def __call__(self, images: PackedImages, capacity: Optional[int] = None,
                  out: Optional[TileBatch] = None,
@@ -265,7 +277,7 @@ class TilePreprocessor:
             out = TileBatch(self.alloc_plans(images.n), pv, u8)
         self._norm(images.channels)  # K0 (first use only) before K1, so K2 follows K1 directly
         if (self.fuse_small and 0 < images.n <= _lib.TP_PLAN_TILE_MAX_IMAGES
-                and self.algo != _lib.TP_TILE_ALGO_EXACT):
+                and self.algo != _lib.TP_TILE_ALGO_EXACT and images.row_map is None):
             self.plan_tile(images, out, stream)
             return out
         self.plan(images, out.plans, stream)

@@ -64,6 +64,31 @@ def test_staged_upload_feeds_k2_bit_exact():
     assert torch.equal(out.pixel_values[:T].view(torch.int16), ref.pixel_values[:T].view(torch.int16))
 
 
+@pytest.mark.parametrize("seed,n,e,mt,emit_uint8", [(4, 6, 448, 12, False), (5, 3, 448, 12, True),
+                                                    (6, 9, 512, 6, True), (7, 2, 224, 1, True)])
+def test_touched_row_upload_equals_full(seed, n, e, mt, emit_uint8):
+    """Only the rows K2 reads go over the link (tp_tile_rows): same plans and tile bytes."""
+    imgs = _batch(seed, n)
+    cfg = PreprocessConfig(tile_edge=e, max_tiles=mt, mean=IMAGENET_MEAN, std=IMAGENET_STD,
+                           reduced_precision_normalize=True)
+    nbytes = staged_bytes(imgs, touched=(e, mt))
+    staged = stage_images(imgs, HostArena(capacity=nbytes, alignment=256), touched=(e, mt))
+    assert len(staged.batch.payload) == nbytes <= staged_bytes(imgs)
+    dest = torch.empty(nbytes, dtype=torch.uint8, device=DEV)
+    packed, done = upload_images(staged, dest)
+    assert packed.row_map is not None
+    prep = TilePreprocessor(cfg, DEV, emit_uint8=emit_uint8)
+    out = prep(packed)
+    ref = prep(pack_images(imgs).to(DEV))
+    torch.cuda.synchronize()
+    T = ref.num_tiles()
+    assert out.num_tiles() == T
+    assert torch.equal(out.plans.plan, ref.plans.plan)
+    assert torch.equal(out.pixel_values[:T].view(torch.int16), ref.pixel_values[:T].view(torch.int16))
+    if emit_uint8:
+        assert torch.equal(out.pixel_u8[:T], ref.pixel_u8[:T])
+
+
 def test_pipeline_matches_direct_calls():
     batches = [_batch(10 + i, 4 + i % 3) for i in range(5)]
     slab = max(staged_bytes(b) for b in batches)

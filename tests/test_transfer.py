@@ -206,3 +206,26 @@ def test_stage_images_layout_and_round_trip():
         assert np.array_equal(got, want)
     with pytest.raises(DataError):
         stage_images([np.zeros((2, 2, 3), np.uint8), np.zeros((2, 2, 1), np.uint8)], arena)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_touched_row_maps_match_oracle_taps(seed):
+    """tp_plan_host + tp_touched_rows (host C) mark exactly the rows of the oracle's
+    axis taps for the oracle's plan: tiles H -> rows*E and the thumbnail H -> E."""
+    from oracle import tileprep_oracle as O
+    from paper_2603_16987_b200.transfer import touched_row_maps
+
+    rng = np.random.default_rng(seed)
+    wh = np.stack([rng.integers(1, 5000, 40), rng.integers(1, 5000, 40)], axis=1).astype(np.int32)
+    e, mt = [(448, 12), (512, 6), (224, 1), (33, 40), (448, 12), (336, 9)][seed]
+    maps = touched_row_maps(wh, e, mt)
+    for (w, h), m in zip(wh, maps):
+        rows, cols, _, thumb, _, rh = O.plan_float(int(w), int(h), e, mt)
+        want = set()
+        for out in ([rh, e] if thumb else [rh]):
+            y0, y1, _ = O.axis_weights(int(h), out)
+            want |= set(y0.tolist()) | set(y1.tolist())
+        got = np.nonzero(m[1:] >= 0)[0]
+        assert m[0] == len(want) and set(got.tolist()) == want
+        assert np.array_equal(m[1:][got], np.arange(len(got)))
+
