@@ -474,12 +474,14 @@ class PipelinedPreprocessor:
     K1+K2 on batch i, the host packs batch i+1 into the next pinned slab and the copy
     stream moves it to the next device slab; the compute stream waits only on that
     batch's copy event.  A pinned slab is reused after its copy has completed, a
-    device slab after the K2 that read it has completed."""
+    device slab after the K2 that read it has completed.  ``touched`` stages only the
+    source rows the preprocessor's tiling reads (stage_images(touched=...))."""
 
-    def __init__(self, prep, slab_bytes: int, depth: int = 2):
+    def __init__(self, prep, slab_bytes: int, depth: int = 2, touched: bool = False):
         if depth < 2:
             raise DomainError("depth must be >= 2 for overlap")
         self.prep = prep
+        self.touched = (prep.cfg.tile_edge, prep.cfg.max_tiles) if touched else None
         self.device = prep.device
         self.depth = depth
         self.slab_bytes = _round_up(int(slab_bytes), IMAGE_ALIGNMENT)
@@ -500,7 +502,7 @@ class PipelinedPreprocessor:
             if self._copied[k] is not None:
                 self._copied[k].synchronize()  # host slab k free again
             self.host[k].reset()
-            staged = stage_images(images, self.host[k])
+            staged = stage_images(images, self.host[k], touched=self.touched)
             if self._consumed[k] is not None:
                 self.copy_stream.wait_event(self._consumed[k])  # device slab k free again
             packed, copied = upload_images(staged, self.dev[k], self.copy_stream)

@@ -89,11 +89,12 @@ def test_touched_row_upload_equals_full(seed, n, e, mt, emit_uint8):
         assert torch.equal(out.pixel_u8[:T], ref.pixel_u8[:T])
 
 
-def test_pipeline_matches_direct_calls():
+@pytest.mark.parametrize("touched", [False, True])
+def test_pipeline_matches_direct_calls(touched):
     batches = [_batch(10 + i, 4 + i % 3) for i in range(5)]
     slab = max(staged_bytes(b) for b in batches)
     prep = TilePreprocessor(CFG, DEV)
-    pipe = PipelinedPreprocessor(prep, slab, depth=2)
+    pipe = PipelinedPreprocessor(prep, slab, depth=2, touched=touched)
     outs = pipe.run(batches)
     pipe.synchronize()
     for b, out in zip(batches, outs):
