@@ -316,3 +316,22 @@ def test_pack_images_roundtrip():
     assert packed.wh_host.tolist() == [[4, 3], [1, 10], [5, 5]]
     with pytest.raises(ValueError):
         pack_images([np.zeros((2, 2, 3), np.uint8), np.zeros((2, 2, 1), np.uint8)], pin=False)
+
+
+def test_host_planner_matches_reference_rule():
+    """tp_plan_host (host C, used for touched-row staging) is K1's exact rule: equal to
+    the reference's float-log planner (oracle restatement, imgproc.py:266-292)."""
+    from oracle import tileprep_oracle as O
+
+    lib = _lib.load()
+    rng = np.random.default_rng(17)
+    plan = np.zeros(_lib.TP_PLAN_FIELDS, dtype=np.int32)
+    cases = [(1, 1, 448, 12), (900, 450, 448, 12), (800, 600, 448, 12), (65536, 1, 448, 12)]
+    cases += [(int(w), int(h), int(e), int(m)) for w, h, e, m in zip(
+        rng.integers(1, 8192, 400), rng.integers(1, 8192, 400),
+        rng.choice([224, 336, 448, 512], 400), rng.integers(1, 13, 400))]
+    for w, h, e, m in cases:
+        assert lib.tp_plan_host(w, h, e, m, plan.ctypes.data) == _lib.TP_OK
+        assert tuple(plan.tolist()) == O.plan_float(w, h, e, m), (w, h, e, m)
+    assert lib.tp_plan_host(0, 5, 448, 12, plan.ctypes.data) == _lib.TP_ERR_INVALID_ARGUMENT
+    assert lib.tp_plan_host(5, 5, 448, 0, plan.ctypes.data) == _lib.TP_ERR_INVALID_ARGUMENT
