@@ -157,7 +157,7 @@ def _check_plan_args(width: int, height: int, cfg: PreprocessConfig) -> None:
 
 
 def _upload(arr: np.ndarray, device: torch.device) -> torch.Tensor:
-    host = torch.from_numpy(np.ascontiguousarray(arr))
+    host = torch.from_numpy(np.require(arr, requirements=("C", "W")))  # copies read-only views
     return host.to(device, non_blocking=False)
 
 

@@ -104,3 +104,23 @@ def test_pipeline_matches_direct_calls(touched):
         assert out.num_tiles() == T
         assert torch.equal(out.pixel_values[:T].view(torch.int16),
                            ref.pixel_values[:T].view(torch.int16))
+
+
+@pytest.mark.parametrize("layout,bf16", [("NHWC", False), ("NCHW", True)])
+def test_touched_rows_grayscale_and_extremes(layout, bf16):
+    sizes = [(1, 1), (2, 4000), (4000, 3), (333, 517), (1080, 1920), (64, 64)]
+    imgs = [make_input(h, w, 1, "random", 40 + i) for i, (h, w) in enumerate(sizes)]
+    cfg = PreprocessConfig(tile_edge=336, max_tiles=9, mean=(0.5,), std=(0.25,),
+                           reduced_precision_normalize=bf16)
+    nbytes = staged_bytes(imgs, touched=(336, 9))
+    staged = stage_images(imgs, HostArena(capacity=nbytes, alignment=256), touched=(336, 9))
+    dest = torch.empty(nbytes, dtype=torch.uint8, device=DEV)
+    packed, _ = upload_images(staged, dest)
+    prep = TilePreprocessor(cfg, DEV, layout=layout, emit_uint8=True)
+    out = prep(packed)
+    ref = prep(pack_images(imgs).to(DEV))
+    torch.cuda.synchronize()
+    T = ref.num_tiles()
+    assert out.num_tiles() == T
+    assert torch.equal(out.pixel_u8[:T], ref.pixel_u8[:T])
+    assert torch.equal(out.pixel_values[:T].view(torch.uint8), ref.pixel_values[:T].view(torch.uint8))
