@@ -44,6 +44,7 @@ class PackedImages:
     # the source rows K2 reads; row_map / row_map_off as tp_tile_rows takes them
     row_map: Optional[torch.Tensor] = None  # int32
     row_map_off: Optional[torch.Tensor] = None  # int64 [n]
+    touched_for: Optional[tuple] = None  # (tile_edge, max_tiles) the rows were chosen for
 
     @property
     def n(self) -> int:
@@ -69,6 +70,7 @@ class PackedImages:
                 device, non_blocking=non_blocking),
             row_map_off=None if self.row_map_off is None else self.row_map_off.to(
                 device, non_blocking=non_blocking),
+            touched_for=self.touched_for,
         )
 
     def copy_from_(self, other: "PackedImages", non_blocking: bool = True) -> "PackedImages":
@@ -261,6 +263,10 @@ class TilePreprocessor:
                 _lib.ptr(pixel_values), _lib.ptr(pixel_u8), min(caps), algo)
         with torch.cuda.device(self.device):
             if images.row_map is not None:  # touched rows only (transfer.stage_images)
+                if images.touched_for != (self.cfg.tile_edge, self.cfg.max_tiles):
+                    raise ValueError(f"images were staged with the rows of tiling "
+                                     f"{images.touched_for}, preprocessor tiles with "
+                                     f"{(self.cfg.tile_edge, self.cfg.max_tiles)}")
                 _lib.call("tp_tile_rows", *args, _lib.ptr(images.row_map),
                           _lib.ptr(images.row_map_off), stream_handle(self.device, stream))
             else:

@@ -316,6 +316,7 @@ class StagedImages:
     row_map_at: Optional[int] = None
     row_map_len: int = 0
     row_map_off_at: Optional[int] = None
+    touched_for: Optional[tuple] = None  # (tile_edge, max_tiles)
 
 
 def _image_layout(wh: np.ndarray, channels: int):
@@ -425,7 +426,7 @@ def _stage_touched(arrs, wh, channels, arena, tile_edge: int, max_tiles: int) ->
     batch = TransferBatch(payload=view[:total], entries=tuple(entries), copies=((0, total),),
                           slab=arena.tensor, base=region.offset)
     return StagedImages(batch, n, channels, wh, offs, wh_at, offsets_at, map_at,
-                        int(maps_all.size), map_off_at)
+                        int(maps_all.size), map_off_at, (int(tile_edge), int(max_tiles)))
 
 
 def upload_images(staged: StagedImages, dest: torch.Tensor,
@@ -444,6 +445,7 @@ def upload_images(staged: StagedImages, dest: torch.Tensor,
             torch.int32)
         packed.row_map_off = dest[staged.row_map_off_at: staged.row_map_off_at + 8 * n].view(
             torch.int64)
+        packed.touched_for = staged.touched_for
     return packed, res.done
 
 

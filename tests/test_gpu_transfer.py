@@ -87,6 +87,9 @@ def test_touched_row_upload_equals_full(seed, n, e, mt, emit_uint8):
     assert torch.equal(out.pixel_values[:T].view(torch.int16), ref.pixel_values[:T].view(torch.int16))
     if emit_uint8:
         assert torch.equal(out.pixel_u8[:T], ref.pixel_u8[:T])
+    other = TilePreprocessor(PreprocessConfig(tile_edge=e + 16, max_tiles=mt), DEV)
+    with pytest.raises(ValueError):
+        other(packed)  # rows staged for another tiling
 
 
 @pytest.mark.parametrize("touched", [False, True])
