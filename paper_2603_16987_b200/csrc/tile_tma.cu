@@ -80,13 +80,24 @@ namespace {
 #ifndef TP_K2_ROW_BALANCE
 #define TP_K2_ROW_BALANCE 1
 #endif
+// Producer/consumer groups per CTA.  2 (default): one CTA per SM holding two groups
+// (each a producer warp, up to 7 consumer warps and its own 2-stage ring) that claim
+// the CTA's items one at a time from a shared-memory counter.  With two CTAs per SM the
+// warp scheduler favours the older CTA: on C2 one CTA of each SM finished ~15 us
+// before the other (141 vs 157 us, the same CTAs on every run and every input), and the
+// SM then ran on half its warps.  Claiming items dynamically removes that tail:
+// C2 163.7 -> 153.8 us, C4 chunk 5.14 -> 4.86 ms.  (Trace builds assume 1.)
+#ifndef TP_K2_GROUPS
+#define TP_K2_GROUPS 2
+#endif
 #ifndef TP_K2_CTAS_PER_SM
-#define TP_K2_CTAS_PER_SM 2
+#define TP_K2_CTAS_PER_SM (2 / TP_K2_GROUPS)
 #endif
 constexpr int kBand = TP_K2_BAND;              // output rows per work item
 constexpr int kStages = TP_K2_STAGES;
 constexpr int kArena = TP_K2_ARENA_KB * 1024;  // bytes of staged source rows per stage
-constexpr int kMaxThreads = 256;               // 1 producer warp + up to 7 consumer warps
+constexpr int kGroups = TP_K2_GROUPS;
+constexpr int kMaxThreads = 256 * kGroups;     // per group: 1 producer warp + up to 7 consumer warps
 constexpr int kCtasPerSm = TP_K2_CTAS_PER_SM;
 constexpr int kRowSlack = 16;            // readable slack after each staged row
 constexpr int kTileCache = 16;           // per-image tile geometries kept in smem
@@ -145,6 +156,7 @@ struct __align__(16) SmemHeader {
   // fused small-batch mode: this CTA's own plans and tile offsets (K2Options)
   int fplan[kFuseMaxImages][TP_PLAN_FIELDS];
   int ftoff[kFuseMaxImages + 1];
+  unsigned next_item;  // kGroups > 1: the CTA's next unclaimed item (group 0's header)
 };
 
 // plans / tile offsets: K1's output in global memory (coherent loads, see TP_LD) or,
@@ -161,9 +173,10 @@ __device__ __forceinline__ int ld_plan(const int32_t* p, bool in_smem) {
 constexpr int kK1Room = 2048;
 template <int C, typename OutT>
 __host__ __device__ constexpr int arena_bytes() {
-  constexpr int fixed = static_cast<int>(((sizeof(SmemHeader) + 127) & ~size_t(127)) +
+  constexpr int fixed = static_cast<int>(kGroups * ((sizeof(SmemHeader) + 127) & ~size_t(127)) +
                                          ((C * 256 * sizeof(OutT) + 127) & ~size_t(127)));
-  constexpr int fit = (((228 * 1024 - kK1Room) / kCtasPerSm - 1024 - fixed) / kStages) & ~127;
+  constexpr int fit =
+      (((228 * 1024 - kK1Room) / kCtasPerSm - 1024 - fixed) / (kStages * kGroups)) & ~127;
   return fit < kArena ? fit : kArena;
 }
 
@@ -415,7 +428,7 @@ __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restri
                         int n, const int32_t* __restrict__ plan,
                         const int32_t* __restrict__ tile_off, bool psm, int E, int64_t items,
                         int bands, int band, int cap_tiles, const int32_t* __restrict__ row_map,
-                        const int64_t* __restrict__ row_map_off) {
+                        const int64_t* __restrict__ row_map_off, unsigned* next_item) {
   const int lane = threadIdx.x & 31;
   int stage = 0;
   uint32_t parity = 0;
@@ -456,7 +469,16 @@ __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restri
     g_k2_cta[blockIdx.x][1] = gtime();
   }
 #endif
-  for (int64_t item = it_begin; item < it_end; ++item) {
+  int64_t item = it_begin - 1;
+  while (true) {
+    if (kGroups > 1) {  // the CTA's groups claim the range's items in order, one at a time
+      unsigned k = 0;
+      if (lane == 0) k = atomicAdd(next_item, 1u);
+      item = it_begin + __shfl_sync(0xffffffffu, k, 0);
+    } else {
+      ++item;
+    }
+    if (item >= it_end) break;
 #if TP_K2_TRACE
     tr_item = clk();
 #endif
@@ -957,9 +979,9 @@ __device__ __forceinline__ void consume_pair_rows(
 template <int C, typename OutT, int LAYOUT, bool WRITE_OUT, bool WRITE_U8, bool AFFINE, int EK>
 __device__ void consume(SmemHeader& hdr, const uint8_t* arena, const OutT* s_lut, int E,
                         OutT* __restrict__ out, uint8_t* __restrict__ out_u8,
-                        const float* __restrict__ aff) {
-  const int ctid = threadIdx.x - 32;
-  const int ncons = blockDim.x - 32;
+                        const float* __restrict__ aff, int gtid, int gthreads) {
+  const int ctid = gtid - 32;
+  const int ncons = gthreads - 32;
   const int lane = ctid & 31, cwarp = ctid >> 5;
   const uint32_t arena_u32 = smem_u32(arena);
   const uint32_t lut_u32 = smem_u32(s_lut);
@@ -1065,18 +1087,24 @@ __global__ void __launch_bounds__(kMaxThreads, kCtasPerSm)
                const float* __restrict__ aff, OutT* __restrict__ out,
                uint8_t* __restrict__ out_u8, int64_t cap, K2Options fp) {
   extern __shared__ __align__(128) uint8_t smem[];
-  SmemHeader& hdr = *reinterpret_cast<SmemHeader*>(smem);
-  OutT* s_lut = reinterpret_cast<OutT*>(smem + ((sizeof(SmemHeader) + 127) & ~size_t(127)));
-  uint8_t* arena = smem + ((sizeof(SmemHeader) + 127) & ~size_t(127)) +
-                   ((C * 256 * sizeof(OutT) + 127) & ~size_t(127));
+  constexpr size_t kHdrBytes = (sizeof(SmemHeader) + 127) & ~size_t(127);
+  const int gthreads = blockDim.x / kGroups;  // threads of one producer/consumer group
+  const int group = kGroups > 1 ? static_cast<int>(threadIdx.x) / gthreads : 0;
+  const int gtid = static_cast<int>(threadIdx.x) - group * gthreads;
+  SmemHeader& hdr0 = *reinterpret_cast<SmemHeader*>(smem);
+  SmemHeader& hdr = *reinterpret_cast<SmemHeader*>(smem + group * kHdrBytes);
+  OutT* s_lut = reinterpret_cast<OutT*>(smem + kGroups * kHdrBytes);
+  uint8_t* arena = smem + kGroups * kHdrBytes + ((C * 256 * sizeof(OutT) + 127) & ~size_t(127)) +
+                   static_cast<size_t>(group) * kStages * arena_bytes<C, OutT>();
 #if TP_K2_PDL == 1
   pdl_trigger();
 #endif
-  if (threadIdx.x == 0) {
+  if (gtid == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&hdr.full[s], 1);
-      mbar_init(&hdr.empty[s], blockDim.x - 32);
+      mbar_init(&hdr.empty[s], gthreads - 32);
     }
+    if (group == 0) hdr0.next_item = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   pdl_wait();  // K1 (plan, tile_off) and the LUT come from stream predecessors
@@ -1103,35 +1131,35 @@ __global__ void __launch_bounds__(kMaxThreads, kCtasPerSm)
       if (ok) best = warp_plan(static_cast<uint32_t>(w), static_cast<uint32_t>(h), fp.max_tiles);
       const int tiles = best.rows * best.cols, thumb = tiles > 1 ? 1 : 0;
       if (lane == 0) {
-        int* q = hdr.fplan[k];
+        int* q = hdr0.fplan[k];
         q[TP_PLAN_ROWS] = best.rows;
         q[TP_PLAN_COLS] = best.cols;
         q[TP_PLAN_TILE_EDGE] = E;
         q[TP_PLAN_THUMB] = thumb;
         q[TP_PLAN_RESIZED_W] = best.cols * E;
         q[TP_PLAN_RESIZED_H] = best.rows * E;
-        hdr.ftoff[k] = acc;
+        hdr0.ftoff[k] = acc;
       }
       bad = bad || !ok;
       acc += tiles + thumb;
     }
-    if (lane == 0) hdr.ftoff[n] = bad ? -1 : acc;
+    if (lane == 0) hdr0.ftoff[n] = bad ? -1 : acc;
     __syncwarp();
     if (blockIdx.x == 0) {  // the caller's plan / n_img / tile_off buffers (K1's outputs)
       int32_t* gplan = const_cast<int32_t*>(plan);
       int32_t* gtoff = const_cast<int32_t*>(tile_off);
       for (int i = lane; i < n * TP_PLAN_FIELDS; i += 32)
-        gplan[i] = hdr.fplan[i / TP_PLAN_FIELDS][i % TP_PLAN_FIELDS];
+        gplan[i] = hdr0.fplan[i / TP_PLAN_FIELDS][i % TP_PLAN_FIELDS];
       if (lane < n) {
-        const int* q = hdr.fplan[lane];
+        const int* q = hdr0.fplan[lane];
         fp.n_img[lane] = q[TP_PLAN_ROWS] * q[TP_PLAN_COLS] + q[TP_PLAN_THUMB];
       }
-      if (lane <= n) gtoff[lane] = hdr.ftoff[lane];
+      if (lane <= n) gtoff[lane] = hdr0.ftoff[lane];
     }
   }
   __syncthreads();
-  const int32_t* plan_r = fused ? &hdr.fplan[0][0] : plan;
-  const int32_t* toff_r = fused ? hdr.ftoff : tile_off;
+  const int32_t* plan_r = fused ? &hdr0.fplan[0][0] : plan;
+  const int32_t* toff_r = fused ? hdr0.ftoff : tile_off;
   // every tile's items are enumerated (item order interleaves tiles); tiles at or
   // above the output capacity are skipped
   const int all_tiles = ld_plan(toff_r + n, fused);
@@ -1150,19 +1178,20 @@ __global__ void __launch_bounds__(kMaxThreads, kCtasPerSm)
     band >>= 1;
   const int bands = (E + band - 1) / band;
   const int64_t items = cap_tiles > 0 ? static_cast<int64_t>(all_tiles) * bands : 0;
-  if (threadIdx.x < 32)
+  if (gtid < 32)
     produce<C, arena_bytes<C, OutT>()>(hdr, arena, src, src_off, wh, n, plan_r, toff_r, fused,
                                        E, items, bands, band, cap_tiles, fp.row_map,
-                                       fp.row_map_off);
+                                       fp.row_map_off, &hdr0.next_item);
   else
     consume<C, OutT, LAYOUT, WRITE_OUT, WRITE_U8, AFFINE, EK>(hdr, arena, s_lut, E, out, out_u8,
-                                                             aff);
+                                                             aff, gtid, gthreads);
 }
 
 template <int C, typename OutT>
 size_t tma_smem_bytes() {
-  return ((sizeof(SmemHeader) + 127) & ~size_t(127)) +
-         ((C * 256 * sizeof(OutT) + 127) & ~size_t(127)) + kStages * arena_bytes<C, OutT>();
+  return kGroups * ((sizeof(SmemHeader) + 127) & ~size_t(127)) +
+         ((C * 256 * sizeof(OutT) + 127) & ~size_t(127)) +
+         kGroups * kStages * arena_bytes<C, OutT>();
 }
 
 template <int C, typename OutT, int LAYOUT, bool WRITE_OUT, bool WRITE_U8, bool AFFINE,
@@ -1181,8 +1210,8 @@ int launch_variant(const uint8_t* src, const int64_t* src_off, const int32_t* wh
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kDevs)
     return set_error(TP_ERR_CUDA, "tp_tile: no usable current device");
   const int segs = (E + 63) / 64;  // 64-pixel segments: one consumer warp each
-  const int warps = 1 + min((kMaxThreads - 32) / 32, max(1, segs));
-  const int threads = 32 * warps;
+  const int warps = 1 + min((kMaxThreads / kGroups - 32) / 32, max(1, segs));  // per group
+  const int threads = 32 * warps * kGroups;
   int per_sm = per_sm_of[dev][warps];
   if (per_sm == 0) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
