@@ -86,9 +86,12 @@ namespace {
 // warp scheduler favours the older CTA: on C2 one CTA of each SM finished ~15 us
 // before the other (141 vs 157 us, the same CTAs on every run and every input), and the
 // SM then ran on half its warps.  Claiming items dynamically removes that tail:
-// C2 163.7 -> 153.8 us, C4 chunk 5.14 -> 4.86 ms.  (Trace builds assume 1.)
+// C2 163.7 -> 153.8 us, C4 chunk 5.14 -> 4.86 ms.  (Trace builds use 1.)
+#ifndef TP_K2_TRACE  // diagnostic build: per-phase clock64 stamps of producer and consumer
+#define TP_K2_TRACE 0
+#endif
 #ifndef TP_K2_GROUPS
-#define TP_K2_GROUPS 2
+#define TP_K2_GROUPS (TP_K2_TRACE ? 1 : 2)  // the trace slots are per CTA
 #endif
 #ifndef TP_K2_CTAS_PER_SM
 #define TP_K2_CTAS_PER_SM (2 / TP_K2_GROUPS)
@@ -127,9 +130,6 @@ struct TileGeo {
   int RW, RH, oy0, ox0, cwid, pad;
 };
 
-#ifndef TP_K2_TRACE  // diagnostic build: per-phase clock64 stamps of producer and consumer
-#define TP_K2_TRACE 0
-#endif
 #if TP_K2_TRACE
 constexpr int kTraceCtas = 296, kTracePhases = 96;
 // [cta][phase]: item-start flag, plan start, copies issued, consumer wait start,
