@@ -449,7 +449,7 @@ def main():
             "e2e": {"value": round(dist.world * n / (e2e_ms / 1e3), 2), "unit": UNIT,
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                     "ms_per_step": round(e2e_ms, 4),
-                    "path": "page-locked staged batch (touched source rows + row maps) -> "
+                    "path": "page-locked staged batch (touched source rows and columns + maps) -> "
                             "one H2D copy (copy stream) -> TilePreprocessor K1+K2 "
                             "(compute stream, K2 reads rows through the maps) -> D2H "
                             "plans/offsets; two device buffers, so step i+1's upload "

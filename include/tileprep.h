@@ -175,15 +175,20 @@ TP_API int tp_plan_tile(const uint8_t* d_src, const int64_t* d_src_off, const in
  *   tp_touched_rows  row map of one image: row_map[0] = n touched rows,
  *                    row_map[1 + y] = compact index of source row y or -1 (h + 1 ints);
  *                    returns n (or a negative error code)
+ *   tp_touched_cols  the same for columns (tiles: W -> cols*E, thumbnail: W -> E):
+ *                    col_map[0] = n touched columns, col_map[1 + x] = index or -1
  *   tp_tile_rows     tp_tile_ex over images whose pixel blocks hold only the touched
- *                    rows (compact index order, each a full row of w*channels bytes):
- *                    d_row_map holds every image's map, d_row_map_off[k] the int32
- *                    index of image k's map.  Fast algorithm only.  Same output as
- *                    tp_tile_ex on the full images. */
+ *                    rows, each holding only the touched columns (compact order, rows
+ *                    of n_cols*channels bytes): d_row_map holds, per image, the row map
+ *                    (h + 1 ints) followed by the column map (w + 1 ints);
+ *                    d_row_map_off[k] is the int32 index of image k's maps.  Fast
+ *                    algorithm only.  Same output as tp_tile_ex on the full images. */
 TP_API int tp_plan_host(int32_t width, int32_t height, int32_t tile_edge, int32_t max_tiles,
                         int32_t* plan);
 TP_API int64_t tp_touched_rows(int32_t width, int32_t height, const int32_t* plan,
                                int32_t* row_map);
+TP_API int64_t tp_touched_cols(int32_t width, int32_t height, const int32_t* plan,
+                               int32_t* col_map);
 TP_API int tp_tile_rows(const uint8_t* d_src, const int64_t* d_src_off, const int32_t* d_wh,
                         int32_t n, int32_t channels, const int32_t* d_plan,
                         const int32_t* d_tile_off, int32_t tile_edge, const void* d_lut,

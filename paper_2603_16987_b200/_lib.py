@@ -72,6 +72,7 @@ SIGNATURES = {
                                c_int32, c_void_p, c_void_p, c_int64, c_int32, c_void_p]),
     "tp_plan_host": (c_int32, [c_int32, c_int32, c_int32, c_int32, c_void_p]),
     "tp_touched_rows": (c_int64, [c_int32, c_int32, c_void_p, c_void_p]),
+    "tp_touched_cols": (c_int64, [c_int32, c_int32, c_void_p, c_void_p]),
     "tp_tile_rows": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_void_p,
                                c_void_p, c_int32, c_void_p, c_int32, c_int32, c_void_p,
                                c_void_p, c_int64, c_int32, c_void_p, c_void_p, c_void_p]),

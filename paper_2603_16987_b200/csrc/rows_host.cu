@@ -109,3 +109,20 @@ extern "C" int64_t tp_touched_rows(int32_t width, int32_t height, const int32_t*
   row_map[0] = n;
   return n;
 }
+
+extern "C" int64_t tp_touched_cols(int32_t width, int32_t height, const int32_t* plan,
+                                   int32_t* col_map) {
+  if (!plan || !col_map || width < 1 || height < 1 || width > TP_MAX_EDGE)
+    return tp::set_error(TP_ERR_INVALID_ARGUMENT, "tp_touched_cols: bad arguments");
+  const int E = plan[TP_PLAN_TILE_EDGE], RW = plan[TP_PLAN_RESIZED_W];
+  if (E < 1 || RW < 1) return tp::set_error(TP_ERR_INVALID_ARGUMENT, "tp_touched_cols: bad plan");
+  int32_t* map = col_map + 1;
+  for (int x = 0; x < width; ++x) map[x] = 0;
+  mark_axis(width, RW, map);                          // tiles: W -> cols * E
+  if (plan[TP_PLAN_THUMB]) mark_axis(width, E, map);  // thumbnail: W -> E
+  int32_t n = 0;
+  for (int x = 0; x < width; ++x) map[x] = map[x] ? n++ : -1;
+  col_map[0] = n;
+  return n;
+}
+

@@ -117,13 +117,14 @@ struct __align__(16) Phase {
   int W;
   int ox0, pad0, pad1, pad2;
   double sx;  // W / RW (column taps)
-  double pad3;
+  const int32_t* cmap;  // touched-column input: compact index of each source column, else null
   int off0[kBand], off1[kBand];  // arena byte offset of column xlo in rows y0 / y1
   float fy[kBand];
   double fy64[kBand];  // exact row weights for the fp64 fallback (1 - fy64 is recomputed)
 };
 constexpr uint32_t kPhOff0 = offsetof(Phase, off0), kPhOff1 = offsetof(Phase, off1),
-                   kPhFy = offsetof(Phase, fy), kPhFy64 = offsetof(Phase, fy64);
+                   kPhFy = offsetof(Phase, fy), kPhFy64 = offsetof(Phase, fy64),
+                   kPhCmap = offsetof(Phase, cmap);
 
 struct TileGeo {
   double sx, sy;
@@ -455,6 +456,7 @@ __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restri
   int64_t stride = 0;
   uintptr_t img_end = 0;
   const int32_t* rmap = nullptr;  // touched-row input: compact index of each source row
+  const int32_t* cmap = nullptr;  // ... and of each source column
   // image of the current item: one binary search for the first item, then a forward walk
   // (the range is contiguous), so no chain of dependent global loads per item
   int kimg = it_begin < it_end ? find_item_image(tile_off, psm, n, it_begin, bands) : 0;
@@ -514,10 +516,12 @@ __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restri
       img = src + TP_LD(src_off + kimg);
       stride = static_cast<int64_t>(W) * C;
       int rows_held = H;
-      if (row_map) {  // touched-row input: the block holds row_map's rows only
+      if (row_map) {  // touched input: the block holds only the mapped rows and columns
         rmap = row_map + TP_LD(row_map_off + kimg);
         rows_held = TP_LD(rmap);
         ++rmap;
+        cmap = rmap + H + 1;
+        stride = static_cast<int64_t>(TP_LD(cmap - 1)) * C;
       }
       img_end = reinterpret_cast<uintptr_t>(img) + static_cast<uintptr_t>(stride) * rows_held;
       if (nimg <= kTileCache) {
@@ -544,8 +548,13 @@ __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restri
     }
     for (int c0 = 0; c0 < E; c0 += cwid) {
       const int cw = min(cwid, E - c0);
-      const int xlo = axis_tap(ox0 + c0, W, sx).i0;
-      const int rb = (axis_tap(ox0 + c0 + cw - 1, W, sx).i1 - xlo + 1) * C;
+      int xlo = axis_tap(ox0 + c0, W, sx).i0;
+      int xhi = axis_tap(ox0 + c0 + cw - 1, W, sx).i1;
+      if (cmap) {  // compact column space (touched columns only)
+        xlo = TP_LD(cmap + xlo);
+        xhi = TP_LD(cmap + xhi);
+      }
+      const int rb = (xhi - xlo + 1) * C;
       int jj = 0;
       while (jj < nrows) {
 #if TP_K2_TRACE
@@ -657,6 +666,7 @@ __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restri
           ph.W = W;
           ph.ox0 = ox0;
           ph.sx = sx;
+          ph.cmap = cmap;
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
@@ -1038,10 +1048,12 @@ __device__ void consume(SmemHeader& hdr, const uint8_t* arena, const OutT* s_lut
       if (g != cache_g || c0 != cache_c0 || q != cache_q) {
         const int ox0 = lds32(pr.base + 32);
         const double sx = ldsd(pr.base + 48);
+        const int32_t* cm = reinterpret_cast<const int32_t*>(
+            __double_as_longlong(ldsd(pr.base + kPhCmap)));
         const AxisTap ta = axis_tap(ox0 + min(ia, c0 + cw - 1), W, sx);
         const AxisTap tb = axis_tap(ox0 + min(ib, c0 + cw - 1), W, sx);
-        xoa = (ta.i0 - xlo) * C;
-        xob = (tb.i0 - xlo) * C;
+        xoa = ((cm ? TP_LD(cm + ta.i0) : ta.i0) - xlo) * C;
+        xob = ((cm ? TP_LD(cm + tb.i0) : tb.i0) - xlo) * C;
         fxa = __double2float_rn(ta.f);
         fxb = __double2float_rn(tb.f);
         fxa64 = ta.f;

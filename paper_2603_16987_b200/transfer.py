@@ -332,31 +332,40 @@ def _image_layout(wh: np.ndarray, channels: int):
 
 
 def touched_row_maps(wh: np.ndarray, tile_edge: int, max_tiles: int):
-    """Per image, the source rows K2's stencil reads under its plan (tp_plan_host +
-    tp_touched_rows, host C code with the device's arithmetic): a list of int32 maps
-    [n_rows, idx(y) for each y] (idx -1 = not read)."""
+    """Per image, the source rows and columns K2's stencil reads under its plan
+    (tp_plan_host + tp_touched_rows / tp_touched_cols, host C code with the device's
+    arithmetic): a list of int32 maps [n_rows, idx(y) for each y, n_cols, idx(x) for
+    each x] (idx -1 = not read), the layout tp_tile_rows reads."""
     lib = _lib.load()
     maps = []
     plan = np.zeros(_lib.TP_PLAN_FIELDS, dtype=np.int32)
     for w, h in np.asarray(wh, dtype=np.int64).reshape(-1, 2):
         _lib.check(lib.tp_plan_host(int(w), int(h), tile_edge, max_tiles, plan.ctypes.data),
                    "tp_plan_host")
-        m = np.empty(int(h) + 1, dtype=np.int32)
-        n = lib.tp_touched_rows(int(w), int(h), plan.ctypes.data, m.ctypes.data)
-        if n < 0:
-            _lib.check(int(n), "tp_touched_rows")
+        m = np.empty(int(h) + int(w) + 2, dtype=np.int32)
+        rows = m[: int(h) + 1]
+        cols = m[int(h) + 1:]
+        for fn, part in (("tp_touched_rows", rows), ("tp_touched_cols", cols)):
+            n = getattr(lib, fn)(int(w), int(h), plan.ctypes.data, part.ctypes.data)
+            if n < 0:
+                _lib.check(int(n), fn)
         maps.append(m)
     return maps
+
+
+def _touched_dims(m: np.ndarray, h: int) -> tuple:
+    """(n_rows, n_cols) of a touched map."""
+    return int(m[0]), int(m[h + 1])
 
 
 def stage_images(images: Sequence[np.ndarray], arena: HostArena,
                  touched: Optional[tuple] = None) -> StagedImages:
     """Pack HWC uint8 images and their sizes/offsets into one arena region.
 
-    ``touched=(tile_edge, max_tiles)`` stages only the source rows K2 will read for
-    that tiling (every tile row and thumbnail row's two taps; 83% of a 1080p image at
-    E=448, 41% of a 4K one) plus the row maps K2 reads them through (tp_tile_rows):
-    fewer bytes on the H2D link, the same tiles."""
+    ``touched=(tile_edge, max_tiles)`` stages only the source rows and columns K2 will
+    read for that tiling (every tile and thumbnail output's two taps per axis; 80% of a
+    1080p image at E=448, 29% of a 4K one) plus the maps K2 reads them through
+    (tp_tile_rows): fewer bytes on the H2D link, the same tiles."""
     if not images:
         raise DataError("no images to stage")
     arrs = [a[:, :, None] if a.ndim == 2 else a for a in images]
@@ -402,7 +411,8 @@ def _stage_touched(arrs, wh, channels, arena, tile_edge: int, max_tiles: int) ->
     offs = np.empty(n, dtype=np.int64)
     for k in range(n):
         offs[k] = mark
-        mark = _round_up(mark + int(maps[k][0]) * int(wh[k, 0]) * channels, IMAGE_ALIGNMENT)
+        nr, nc = _touched_dims(maps[k], int(wh[k, 1]))
+        mark = _round_up(mark + nr * nc * channels, IMAGE_ALIGNMENT)
     total = max(mark, IMAGE_ALIGNMENT)
     if arena.alignment % IMAGE_ALIGNMENT and IMAGE_ALIGNMENT % arena.alignment:
         raise DomainError("arena alignment must divide or be a multiple of 256")
@@ -419,10 +429,13 @@ def _stage_touched(arrs, wh, channels, arena, tile_edge: int, max_tiles: int) ->
                BatchEntry(map_off_at, map_off.nbytes, "int64", map_off.shape),
                BatchEntry(map_at, maps_all.nbytes, "int32", maps_all.shape)]
     for a, m, off in zip(arrs, maps, offs):
-        rows = np.nonzero(m[1:] >= 0)[0]
-        block = a[rows].reshape(-1)  # touched rows in source order = compact index order
+        h = a.shape[0]
+        rows = np.nonzero(m[1: h + 1] >= 0)[0]
+        cols = np.nonzero(m[h + 2:] >= 0)[0]
+        block = a[rows][:, cols].reshape(-1)  # source order = compact index order
         view[off: off + block.size] = block
-        entries.append(BatchEntry(int(off), int(block.size), "uint8", (len(rows),) + a.shape[1:]))
+        entries.append(BatchEntry(int(off), int(block.size), "uint8",
+                                  (len(rows), len(cols), a.shape[2])))
     batch = TransferBatch(payload=view[:total], entries=tuple(entries), copies=((0, total),),
                           slab=arena.tensor, base=region.offset)
     return StagedImages(batch, n, channels, wh, offs, wh_at, offsets_at, map_at,
@@ -463,8 +476,9 @@ def staged_bytes(images: Sequence[np.ndarray], touched: Optional[tuple] = None) 
     n = len(arrs)
     mark = _round_up(_round_up(8 * n, 8) + 16 * n + 4 * sum(m.size for m in maps),
                      IMAGE_ALIGNMENT)
-    for (w, _), m in zip(wh, maps):
-        mark = _round_up(mark + int(m[0]) * int(w) * channels, IMAGE_ALIGNMENT)
+    for (_, h), m in zip(wh, maps):
+        nr, nc = _touched_dims(m, int(h))
+        mark = _round_up(mark + nr * nc * channels, IMAGE_ALIGNMENT)
     return max(mark, IMAGE_ALIGNMENT)
 
 

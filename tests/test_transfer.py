@@ -210,8 +210,9 @@ def test_stage_images_layout_and_round_trip():
 
 @pytest.mark.parametrize("seed", range(6))
 def test_touched_row_maps_match_oracle_taps(seed):
-    """tp_plan_host + tp_touched_rows (host C) mark exactly the rows of the oracle's
-    axis taps for the oracle's plan: tiles H -> rows*E and the thumbnail H -> E."""
+    """tp_plan_host + tp_touched_rows / _cols (host C) mark exactly the rows and columns
+    of the oracle's axis taps for the oracle's plan: tiles H -> rows*E, W -> cols*E and
+    the thumbnail H -> E, W -> E."""
     from oracle import tileprep_oracle as O
     from paper_2603_16987_b200.transfer import touched_row_maps
 
@@ -220,12 +221,14 @@ def test_touched_row_maps_match_oracle_taps(seed):
     e, mt = [(448, 12), (512, 6), (224, 1), (33, 40), (448, 12), (336, 9)][seed]
     maps = touched_row_maps(wh, e, mt)
     for (w, h), m in zip(wh, maps):
-        rows, cols, _, thumb, _, rh = O.plan_float(int(w), int(h), e, mt)
-        want = set()
-        for out in ([rh, e] if thumb else [rh]):
-            y0, y1, _ = O.axis_weights(int(h), out)
-            want |= set(y0.tolist()) | set(y1.tolist())
-        got = np.nonzero(m[1:] >= 0)[0]
-        assert m[0] == len(want) and set(got.tolist()) == want
-        assert np.array_equal(m[1:][got], np.arange(len(got)))
+        rows, cols, _, thumb, rw, rh = O.plan_float(int(w), int(h), e, mt)
+        for src, outs, part in ((int(h), [rh, e] if thumb else [rh], m[: h + 1]),
+                                (int(w), [rw, e] if thumb else [rw], m[h + 1:])):
+            want = set()
+            for out in outs:
+                i0, i1, _ = O.axis_weights(src, out)
+                want |= set(i0.tolist()) | set(i1.tolist())
+            got = np.nonzero(part[1:] >= 0)[0]
+            assert part[0] == len(want) and set(got.tolist()) == want
+            assert np.array_equal(part[1:][got], np.arange(len(got)))
 
