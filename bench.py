@@ -63,20 +63,33 @@ class Dist:
         self.rank = int(os.environ.get("RANK", "0"))
         self.local_rank = int(os.environ.get("LOCAL_RANK", "0"))
         self.pg = False
+        self.backend = None
+        # dry run of the N-rank path on fewer GPUs (ranks share devices, gloo barrier):
+        # checks that the sharded bench runs end to end; its numbers are not scaling data
+        self.shared_gpu = os.environ.get("TP_BENCH_SHARED_GPU_DRYRUN") == "1"
+
+    def tag(self, line: dict) -> dict:
+        if self.shared_gpu and self.world > 1:
+            line["dryrun"] = "ranks shared GPUs (TP_BENCH_SHARED_GPU_DRYRUN): not a scaling number"
+        return line
+
+    def device_index(self, n_devices: int) -> int:
+        return self.local_rank % n_devices if self.shared_gpu else self.local_rank
 
     def init(self, backend: str):
         if self.world > 1:
             import torch.distributed as dist
 
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            dist.init_process_group(backend=backend)
+            self.backend = "gloo" if self.shared_gpu else backend
+            dist.init_process_group(backend=self.backend)
             self.pg = True
 
     def barrier(self, device=None):
         if self.pg:
             import torch.distributed as dist
 
-            if device is not None:
+            if device is not None and self.backend == "nccl":
                 dist.barrier(device_ids=[device.index])
             else:
                 dist.barrier()
@@ -87,7 +100,8 @@ class Dist:
         import torch
         import torch.distributed as dist
 
-        t = torch.tensor([value], dtype=torch.float64, device=device)
+        t = torch.tensor([value], dtype=torch.float64,
+                         device=device if self.backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -262,7 +276,7 @@ def run_reference(args, dist: Dist):
         "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    print(json.dumps(dist.tag(line)), flush=True)
 
 
 # ---------------------------------------------------------------------------
@@ -284,8 +298,9 @@ def main():
 
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA device")
-    torch.cuda.set_device(dist.local_rank)
-    device = torch.device("cuda", dist.local_rank)
+    dev_index = dist.device_index(torch.cuda.device_count())
+    torch.cuda.set_device(dev_index)
+    device = torch.device("cuda", dev_index)
     dist.init("nccl")
     if args.workload in ("c4", "c5"):
         run_sweep(args, dist, device)
@@ -322,7 +337,7 @@ def main():
         for _ in range(max(3, args.warmup)):
             step()
     torch.cuda.synchronize(device)
-    clocks = ClockSampler(dist.local_rank)
+    clocks = ClockSampler(dev_index)
     clocks.start()
     dist.barrier(device)
     torch.cuda.synchronize(device)
@@ -458,7 +473,7 @@ def main():
             "gpu_launches": 2 * args.steps,
             "clocks": clk,
         }
-        print(json.dumps(line), flush=True)
+        print(json.dumps(dist.tag(line)), flush=True)
     dist.close()
 
 
@@ -689,7 +704,7 @@ def run_sweep(args, dist, device):
             "gpu_launches": args.steps * len(chunks) * (8 if with_expand else 2),
             "clocks": clk,
         }
-        print(json.dumps(line), flush=True)
+        print(json.dumps(dist.tag(line)), flush=True)
 
 
 def run_single(args, dist, device):
@@ -756,7 +771,7 @@ def run_single(args, dist, device):
             "h2d_touched_bytes": tbytes, "h2d_full_bytes": int(host.data.numel()),
             "algorithmic_bytes": wb["total"],
         }
-        print(json.dumps(line), flush=True)
+        print(json.dumps(dist.tag(line)), flush=True)
 
 
 if __name__ == "__main__":
