@@ -87,3 +87,21 @@ def test_two_rank_gloo_sharding_and_timing():
         flat = sorted(i for part in sizes for i in part)
         assert flat == list(range(300))
         assert not set(sizes[0]) & set(sizes[1])
+
+
+def test_shared_gpu_dryrun_maps_ranks_and_tags_lines(monkeypatch):
+    """TP_BENCH_SHARED_GPU_DRYRUN: ranks fold onto the devices present, the barrier backend
+    is gloo and every JSON line says it is not a scaling number."""
+    sys.path.insert(0, str(REPO))
+    import bench
+
+    monkeypatch.setenv("WORLD_SIZE", "4")
+    monkeypatch.setenv("LOCAL_RANK", "3")
+    monkeypatch.setenv("TP_BENCH_SHARED_GPU_DRYRUN", "1")
+    d = bench.Dist()
+    assert d.device_index(1) == 0 and d.device_index(2) == 1
+    assert "dryrun" in d.tag({"value": 1.0})
+    monkeypatch.delenv("TP_BENCH_SHARED_GPU_DRYRUN")
+    d = bench.Dist()
+    assert d.device_index(8) == 3
+    assert "dryrun" not in d.tag({"value": 1.0})
