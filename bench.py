@@ -236,6 +236,58 @@ def cpu_throughput(n_images: int, cores: int, seed: int = 20260817):
     return cores / float(per.mean()), float(np.median(per)) * 1e3, float(per.sum())
 
 
+def _cpu_wl_one(args):
+    """One image of a workload through the oracle path (input generated off the clock)."""
+    seed, k, w, h, e, max_tiles, mean, std, bf16 = args
+    from oracle import tileprep_oracle as O
+
+    arr = O.synth_image(seed, k, w, h, 3, 0)
+    t0 = time.perf_counter()
+    O.preprocess_image(arr, e, max_tiles, mean, std, bf16)
+    return time.perf_counter() - t0
+
+
+def _wl_jobs(wl, n: int):
+    return [(wl.seed, k, int(wl.wh[k % len(wl.wh)][0]), int(wl.wh[k % len(wl.wh)][1]),
+             wl.tile_edge, wl.max_tiles, tuple(wl.mean), tuple(wl.std), bool(wl.bf16))
+            for k in range(n)]
+
+
+def cpu_latency(wl, runs: int = 15) -> dict:
+    """Batch-1 latency of the oracle path on one host core (one process,
+    OMP/OPENBLAS_NUM_THREADS=1, p50/p99 over >= 15 runs), as a cpu_baseline object."""
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    job = _wl_jobs(wl, 1)[0]
+    _cpu_wl_one(job)  # warm-up
+    t = np.array([_cpu_wl_one(job) for _ in range(runs)]) * 1e3
+    p50 = float(np.percentile(t, 50))
+    return {"value": round(1e3 / p50, 3), "unit": UNIT, "cores": 1, "kind": "port",
+            "p50_ms": round(p50, 2), "p99_ms": round(float(np.percentile(t, 99)), 2),
+            "sample": f"{runs} runs of 1 x {job[2]}x{job[3]} through oracle/tileprep_oracle "
+                      "(numpy restatement of the vlmfp fused path), one process, one thread; "
+                      "value = 1 / p50"}
+
+
+def cpu_throughput_wl(wl, cores: int, cpu_seconds: float) -> dict:
+    """images/s of the oracle path on a prefix of the workload's images, one process per
+    core (all busy at once), sized to about `cpu_seconds` of CPU work."""
+    import multiprocessing as mp
+
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores) as pool:
+        cal = np.array(pool.map(_cpu_wl_one, _wl_jobs(wl, cores), chunksize=1))
+        n = int(max(cores, min(len(wl.wh), cpu_seconds / max(float(cal.mean()), 1e-3))))
+        per = np.array(pool.map(_cpu_wl_one, _wl_jobs(wl, n), chunksize=1))
+    return {"value": round(cores / float(per.mean()), 3), "unit": UNIT, "cores": cores,
+            "kind": "port",
+            "sample": f"first {n} of the {len(wl.wh)} {wl.name} images through "
+                      f"oracle/tileprep_oracle, one process per core, {per.sum():.1f} CPU-s; "
+                      f"per-image p50 {np.median(per) * 1e3:.1f} ms"}
+
+
 def host_cores() -> int:
     try:
         return len(os.sched_getaffinity(0))
@@ -704,6 +756,8 @@ def run_sweep(args, dist, device):
             "gpu_launches": args.steps * len(chunks) * (8 if with_expand else 2),
             "clocks": clk,
         }
+        if dist.world == 1 and not args.no_cpu_baseline and not with_expand:
+            line["cpu_baseline"] = cpu_throughput_wl(wl_all, host_cores(), args.cpu_seconds)
         print(json.dumps(dist.tag(line)), flush=True)
 
 
@@ -771,6 +825,8 @@ def run_single(args, dist, device):
             "h2d_touched_bytes": tbytes, "h2d_full_bytes": int(host.data.numel()),
             "algorithmic_bytes": wb["total"],
         }
+        if not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_latency(wl)
         print(json.dumps(dist.tag(line)), flush=True)
 
 
