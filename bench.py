@@ -236,20 +236,45 @@ def cpu_throughput(n_images: int, cores: int, seed: int = 20260817):
     return cores / float(per.mean()), float(np.median(per)) * 1e3, float(per.sum())
 
 
+_CPU_VOCAB = None
+
+
+def _cpu_vocab():
+    """(byte_ids, table, max_len, marker, ctx, asst) of the synthetic C5 vocab, per worker."""
+    global _CPU_VOCAB
+    if _CPU_VOCAB is None:
+        from oracle import tileprep_oracle as O
+        from paper_2603_16987_b200.workloads import synthetic_vocab_text
+
+        toks, byte_ids, table, max_len = O.parse_vocab(synthetic_vocab_text())
+        _CPU_VOCAB = (byte_ids, table, max_len, toks.index("<|image|>"),
+                      toks.index("<IMG_CONTEXT>"), toks.index("<|assistant|>"))
+    return _CPU_VOCAB
+
+
 def _cpu_wl_one(args):
-    """One image of a workload through the oracle path (input generated off the clock)."""
-    seed, k, w, h, e, max_tiles, mean, std, bf16 = args
+    """One image of a workload through the oracle path (input generated off the clock);
+    with a prompt (C5) also its tokenization, image-token expansion (256 tokens per tile)
+    and supervision mask."""
+    seed, k, w, h, e, max_tiles, mean, std, bf16, text = args
     from oracle import tileprep_oracle as O
 
     arr = O.synth_image(seed, k, w, h, 3, 0)
+    voc = _cpu_vocab() if text is not None else None
     t0 = time.perf_counter()
-    O.preprocess_image(arr, e, max_tiles, mean, std, bf16)
+    plan, _ = O.preprocess_image(arr, e, max_tiles, mean, std, bf16)
+    if voc is not None:
+        byte_ids, table, max_len, marker, ctx, asst = voc
+        ids = O.tokenize(text, byte_ids, table, max_len)
+        out, _, t = O.expand(ids, [O.n_images(plan)], 256, marker, ctx, asst)
+        O.supervision_mask(out, t, asst)
     return time.perf_counter() - t0
 
 
-def _wl_jobs(wl, n: int):
+def _wl_jobs(wl, n: int, texts=None):
     return [(wl.seed, k, int(wl.wh[k % len(wl.wh)][0]), int(wl.wh[k % len(wl.wh)][1]),
-             wl.tile_edge, wl.max_tiles, tuple(wl.mean), tuple(wl.std), bool(wl.bf16))
+             wl.tile_edge, wl.max_tiles, tuple(wl.mean), tuple(wl.std), bool(wl.bf16),
+             None if texts is None else texts[k])
             for k in range(n)]
 
 
@@ -269,22 +294,24 @@ def cpu_latency(wl, runs: int = 15) -> dict:
                       "value = 1 / p50"}
 
 
-def cpu_throughput_wl(wl, cores: int, cpu_seconds: float) -> dict:
-    """images/s of the oracle path on a prefix of the workload's images, one process per
-    core (all busy at once), sized to about `cpu_seconds` of CPU work."""
+def cpu_throughput_wl(wl, cores: int, cpu_seconds: float, texts=None) -> dict:
+    """images/s of the oracle path on a prefix of the workload's images (and prompts),
+    one process per core (all busy at once), sized to about `cpu_seconds` of CPU work."""
     import multiprocessing as mp
 
     os.environ.setdefault("OMP_NUM_THREADS", "1")
     os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
     ctx = mp.get_context("fork")
     with ctx.Pool(cores) as pool:
-        cal = np.array(pool.map(_cpu_wl_one, _wl_jobs(wl, cores), chunksize=1))
+        cal = np.array(pool.map(_cpu_wl_one, _wl_jobs(wl, cores, texts), chunksize=1))
         n = int(max(cores, min(len(wl.wh), cpu_seconds / max(float(cal.mean()), 1e-3))))
-        per = np.array(pool.map(_cpu_wl_one, _wl_jobs(wl, n), chunksize=1))
+        per = np.array(pool.map(_cpu_wl_one, _wl_jobs(wl, n, texts), chunksize=1))
     return {"value": round(cores / float(per.mean()), 3), "unit": UNIT, "cores": cores,
             "kind": "port",
-            "sample": f"first {n} of the {len(wl.wh)} {wl.name} images through "
-                      f"oracle/tileprep_oracle, one process per core, {per.sum():.1f} CPU-s; "
+            "sample": f"first {n} of the {len(wl.wh)} {wl.name} images"
+                      + (" and prompts (tokenize + expand + mask)" if texts else "")
+                      + f" through oracle/tileprep_oracle, one process per core, "
+                      f"{per.sum():.1f} CPU-s; "
                       f"per-image p50 {np.median(per) * 1e3:.1f} ms"}
 
 
@@ -756,8 +783,13 @@ def run_sweep(args, dist, device):
             "gpu_launches": args.steps * len(chunks) * (8 if with_expand else 2),
             "clocks": clk,
         }
-        if dist.world == 1 and not args.no_cpu_baseline and not with_expand:
-            line["cpu_baseline"] = cpu_throughput_wl(wl_all, host_cores(), args.cpu_seconds)
+        if dist.world == 1 and not args.no_cpu_baseline:
+            cpu_texts = None
+            if with_expand:
+                from paper_2603_16987_b200.workloads import c5_texts
+                cpu_texts = c5_texts(total, wl_all.seed)
+            line["cpu_baseline"] = cpu_throughput_wl(wl_all, host_cores(), args.cpu_seconds,
+                                                     cpu_texts)
         print(json.dumps(dist.tag(line)), flush=True)
 
 
