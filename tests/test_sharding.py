@@ -105,3 +105,19 @@ def test_shared_gpu_dryrun_maps_ranks_and_tags_lines(monkeypatch):
     d = bench.Dist()
     assert d.device_index(8) == 3
     assert "dryrun" not in d.tag({"value": 1.0})
+
+
+def test_bench_cpu_baselines_on_a_tiny_workload():
+    """bench.py's cpu_baseline helpers (batch-1 latency and the per-core pool, with and
+    without the C5 prompt leg) return well-formed objects; sizes kept tiny for the CPU suite."""
+    sys.path.insert(0, str(REPO))
+    import bench
+    from paper_2603_16987_b200.workloads import IMAGENET_MEAN, IMAGENET_STD, Workload, c5_texts
+
+    wl = Workload("T", "tiny", np.array([[96, 64], [64, 96]], np.int32), 32, 6,
+                  IMAGENET_MEAN, IMAGENET_STD, True, 7)
+    lat = bench.cpu_latency(wl, runs=2)
+    assert lat["cores"] == 1 and lat["kind"] == "port" and lat["value"] > 0
+    assert lat["p99_ms"] >= lat["p50_ms"] > 0
+    thr = bench.cpu_throughput_wl(wl, 2, 0.01, c5_texts(2, 7))
+    assert thr["cores"] == 2 and thr["value"] > 0 and "prompts" in thr["sample"]
