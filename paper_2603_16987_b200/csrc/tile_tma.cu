@@ -102,6 +102,8 @@ constexpr int kArena = TP_K2_ARENA_KB * 1024;  // bytes of staged source rows pe
 constexpr int kGroups = TP_K2_GROUPS;
 constexpr int kMaxThreads = 256 * kGroups;     // per group: 1 producer warp + up to 7 consumer warps
 constexpr int kCtasPerSm = TP_K2_CTAS_PER_SM;
+static_assert(kGroups >= 1 && kGroups <= 4, "1..4 producer/consumer groups per CTA");
+static_assert(kCtasPerSm >= 1, "TP_K2_CTAS_PER_SM must be >= 1 (set it for GROUPS > 2 builds)");
 constexpr int kRowSlack = 16;            // readable slack after each staged row
 constexpr int kTileCache = 16;           // per-image tile geometries kept in smem
 static_assert(kBand >= 2 && kBand <= 32, "a band is owned by the 32 lanes of the producer");
@@ -158,6 +160,7 @@ struct __align__(16) SmemHeader {
   int fplan[kFuseMaxImages][TP_PLAN_FIELDS];
   int ftoff[kFuseMaxImages + 1];
   unsigned next_item;  // kGroups > 1: the CTA's next unclaimed item (group 0's header)
+  unsigned producers_done;  // producers that issued their last copy (group 0's header)
 };
 
 // plans / tile offsets: K1's output in global memory (coherent loads, see TP_LD) or,
@@ -429,7 +432,8 @@ __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restri
                         int n, const int32_t* __restrict__ plan,
                         const int32_t* __restrict__ tile_off, bool psm, int E, int64_t items,
                         int bands, int band, int cap_tiles, const int32_t* __restrict__ row_map,
-                        const int64_t* __restrict__ row_map_off, unsigned* next_item) {
+                        const int64_t* __restrict__ row_map_off, unsigned* next_item,
+                        unsigned* producers_done) {
   const int lane = threadIdx.x & 31;
   int stage = 0;
   uint32_t parity = 0;
@@ -699,7 +703,13 @@ __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restri
     mbar_arrive(&hdr.full[stage]);
   }
 #if TP_K2_PDL == 2
-  pdl_trigger();  // all of this CTA's copies are issued: let the next kernel be scheduled
+  // the trigger is per CTA (any thread's counts for the whole CTA): only the last of the
+  // CTA's producers to finish issuing copies fires it, so no group still reading plans
+  // or issuing bulk copies is overtaken by the dependent grid's launch
+  if (lane == 0 && atomicAdd(producers_done, 1u) == static_cast<unsigned>(kGroups - 1))
+    pdl_trigger();
+#else
+  (void)producers_done;
 #endif
 }
 
@@ -1116,7 +1126,10 @@ __global__ void __launch_bounds__(kMaxThreads, kCtasPerSm)
       mbar_init(&hdr.full[s], 1);
       mbar_init(&hdr.empty[s], gthreads - 32);
     }
-    if (group == 0) hdr0.next_item = 0;
+    if (group == 0) {
+      hdr0.next_item = 0;
+      hdr0.producers_done = 0;
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   pdl_wait();  // K1 (plan, tile_off) and the LUT come from stream predecessors
@@ -1193,7 +1206,7 @@ __global__ void __launch_bounds__(kMaxThreads, kCtasPerSm)
   if (gtid < 32)
     produce<C, arena_bytes<C, OutT>()>(hdr, arena, src, src_off, wh, n, plan_r, toff_r, fused,
                                        E, items, bands, band, cap_tiles, fp.row_map,
-                                       fp.row_map_off, &hdr0.next_item);
+                                       fp.row_map_off, &hdr0.next_item, &hdr0.producers_done);
   else
     consume<C, OutT, LAYOUT, WRITE_OUT, WRITE_U8, AFFINE, EK>(hdr, arena, s_lut, E, out, out_u8,
                                                              aff, gtid, gthreads);

@@ -74,10 +74,27 @@ class PackedImages:
         )
 
     def copy_from_(self, other: "PackedImages", non_blocking: bool = True) -> "PackedImages":
-        """In-place refill (same layout) — the per-step H2D of a serving loop."""
+        """In-place refill (same layout) — the per-step H2D of a serving loop.  A
+        touched-row batch (row maps) refills only a touched-row batch of the same tiling
+        and map size, a whole-image batch only a whole-image one: K2 would otherwise read
+        one layout as the other."""
+        if (self.row_map is None) != (other.row_map is None):
+            raise ValueError("copy_from_: one batch is touched-row staged and the other is not")
+        if self.row_map is not None:
+            if self.touched_for != other.touched_for:
+                raise ValueError(f"copy_from_: batches staged for tilings {self.touched_for} "
+                                 f"and {other.touched_for}")
+            if (self.row_map.numel() != other.row_map.numel()
+                    or self.row_map_off.numel() != other.row_map_off.numel()):
+                raise ValueError("copy_from_: row maps differ in size")
         self.data.copy_(other.data, non_blocking=non_blocking)
         self.offsets.copy_(other.offsets, non_blocking=non_blocking)
         self.wh.copy_(other.wh, non_blocking=non_blocking)
+        if self.row_map is not None:
+            self.row_map.copy_(other.row_map, non_blocking=non_blocking)
+            self.row_map_off.copy_(other.row_map_off, non_blocking=non_blocking)
+        self.wh_host = other.wh_host
+        self.offsets_host = other.offsets_host
         return self
 
 
@@ -294,6 +311,12 @@ class TilePreprocessor:
                   stream: Optional[torch.cuda.Stream] = None) -> None:
         """K1 + K2 as one launch (tp_plan_tile) for a batch of at most
         TP_PLAN_TILE_MAX_IMAGES images: the same plans, counts, offsets and tiles."""
+        if images.row_map is not None:
+            # a touched-row block is not a W*H*C image: tp_plan_tile would read it as one
+            # (wrong tiles, and past the slab for the last image); plan() + tile() route
+            # through tp_tile_rows
+            raise ValueError("plan_tile takes whole-image batches; touched-row batches "
+                             "(stage_images(touched=...)) go through plan() + tile()")
         lut, affine = self._norm(images.channels)
         algo = self.algo | (_lib.TP_TILE_NORM_AFFINE if affine else 0)
         caps = [t.shape[0] for t in (out.pixel_values, out.pixel_u8) if t is not None]

@@ -335,3 +335,43 @@ def test_host_planner_matches_reference_rule():
         assert tuple(plan.tolist()) == O.plan_float(w, h, e, m), (w, h, e, m)
     assert lib.tp_plan_host(0, 5, 448, 12, plan.ctypes.data) == _lib.TP_ERR_INVALID_ARGUMENT
     assert lib.tp_plan_host(5, 5, 448, 0, plan.ctypes.data) == _lib.TP_ERR_INVALID_ARGUMENT
+
+
+# ---------------------------------------------------------------------------
+# layout guards of the batch engine (touched-row vs whole-image batches)
+
+def _cpu_packed(touched: bool, tiling=(448, 12), map_len=8):
+    from paper_2603_16987_b200.engine import PackedImages
+
+    wh = np.array([[4, 3]], dtype=np.int32)
+    p = PackedImages(torch.zeros(256, dtype=torch.uint8), torch.zeros(1, dtype=torch.int64),
+                     torch.from_numpy(wh.copy()), 3, wh, np.zeros(1, dtype=np.int64))
+    if touched:
+        p.row_map = torch.arange(map_len, dtype=torch.int32)
+        p.row_map_off = torch.zeros(1, dtype=torch.int64)
+        p.touched_for = tiling
+    return p
+
+
+def test_copy_from_carries_row_maps_and_rejects_layout_mismatch():
+    a, b = _cpu_packed(True), _cpu_packed(True)
+    b.row_map += 100
+    b.data += 7
+    a.copy_from_(b, non_blocking=False)
+    assert torch.equal(a.row_map, b.row_map) and torch.equal(a.data, b.data)
+    with pytest.raises(ValueError, match="touched-row"):
+        _cpu_packed(False).copy_from_(_cpu_packed(True))
+    with pytest.raises(ValueError, match="touched-row"):
+        _cpu_packed(True).copy_from_(_cpu_packed(False))
+    with pytest.raises(ValueError, match="tilings"):
+        _cpu_packed(True).copy_from_(_cpu_packed(True, tiling=(512, 12)))
+    with pytest.raises(ValueError, match="differ in size"):
+        _cpu_packed(True).copy_from_(_cpu_packed(True, map_len=9))
+
+
+def test_plan_tile_rejects_touched_row_batches():
+    from paper_2603_16987_b200.engine import TilePreprocessor
+
+    prep = object.__new__(TilePreprocessor)  # no device needed: the guard comes first
+    with pytest.raises(ValueError, match="whole-image"):
+        prep.plan_tile(_cpu_packed(True), out=None)
