@@ -7,13 +7,28 @@ One step = one pass of the hot path over one batch: K1 (plan) + K2 (fused
 resample/crop/thumbnail/normalize -> bf16 NCHW) over BASELINE configs[1]
 (C2: 64 synthetic 1920x1080 RGB images, InternVL3-2B tiling, E=448, max 12 +
 thumbnail, ImageNet mean/std).  Inputs (398 MB) are larger than L2 (126 MB).
-Under torchrun each rank runs its own 64-image batch on its own GPU (weak
-scaling, no data-path collective); the barrier + max-over-ranks timing are
-the only cross-rank operations.
+Each rank runs its own 64-image batch on its own GPU (weak scaling, no
+data-path collective); the barrier + max-over-ranks timing are the only
+cross-rank operations.  `--gpus N` without a torchrun environment re-launches
+this script under torch.distributed.run with N ranks.
 
-`--impl reference` times the reference algorithm on the host cores (the
-oracle port of vlmfp's fused/contiguous path, oracle/tileprep_oracle.py) on a
-bounded sample of the same workload; rank 0 only.
+The JSON line also carries, as sub-blocks measured in the same run:
+  e2e      the C2 batch end to end from the caller's numpy HWC arrays through the
+           public pipeline (native host packing + one pinned H2D + K1 + K2 + D2H of
+           the plans), host wall clock, packing inside the timed loop
+  latency  batch-1 1080p (C2 tiling) p50/p99
+  c3       BASELINE configs[2]: batch-1 4K p50/p99 (>= 1000 CUDA-graph launches)
+  c1       BASELINE configs[0]: batch-1 1080p, E=512, fp32
+  c4       BASELINE configs[3]: the 8192-image mixed sweep, LPT-sharded over the N
+           ranks (strong scaling), per-GPU roofline
+  c5       BASELINE configs[4]: 1024 images + device tokenization + expansion
+each with its own clock record and CPU baseline.
+
+`--impl reference` times the reference's own CPU implementation (vlmfp, installed
+unmodified into baseline/_ref; its fastest recipe path: fused_transform,
+contiguous_tensor_path, avoid_per_item_split, skip_pixel_mask) on all host cores,
+rank 0 only, on the C2 batch.  Without baseline/_ref it falls back to the numpy
+port in oracle/ (kind "port").
 """
 
 from __future__ import annotations
@@ -21,6 +36,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -34,28 +50,58 @@ sys.path.insert(0, str(REPO))
 
 METRIC = "preprocessed images/sec and p50 per-image preprocess latency (ms); % of HBM roofline"
 UNIT = "images/s"
+DTYPE = "u8 in, fp32 + fp64-exact resample, bf16 out"
+REF_DIR = REPO / "baseline" / "_ref"
 
 
-def parse_args():
+def parse_args(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=500)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--batch", type=int, default=64, help="images per GPU per step (C2: 64)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0,
-                    help="target CPU time of the cpu_baseline sample")
-    ap.add_argument("--latency-iters", type=int, default=300)
+                    help="target CPU time of each cpu_baseline sample")
+    ap.add_argument("--latency-iters", type=int, default=1000)
+    ap.add_argument("--e2e-steps", type=int, default=30)
+    ap.add_argument("--no-sub", action="store_true",
+                    help="skip the c1/c3/c4/c5 sub-blocks of the default line")
     ap.add_argument("--workload", choices=["c2", "c4", "c5", "c1", "c3"], default="c2",
-                    help="c2 (default, the BASELINE metric config); c4 = 8192-image "
-                         "mixed-aspect sweep (sharded, strong scaling); c5 = 1024 images + "
-                         "placeholder expansion; c1/c3 = single-image latency configs")
-    return ap.parse_args()
+                    help="c2 (default, the BASELINE metric config, with the other configs "
+                         "as sub-blocks); c1/c3/c4/c5 alone as the line's workload")
+    return ap.parse_args(argv)
 
 
 # ---------------------------------------------------------------------------
 # distributed plumbing
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def spawn_command(args_gpus: int, argv) -> list:
+    """torch.distributed.run command line that re-runs this script with N ranks."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+            f"--nproc-per-node={args_gpus}", "--master-addr=127.0.0.1",
+            f"--master-port={_free_port()}", str(Path(__file__).resolve()), *argv]
+
+
+def maybe_spawn(args, argv) -> int | None:
+    """`--gpus N` (N > 1) outside torchrun: run N ranks under torch.distributed.run and
+    return its exit code; inside torchrun: check WORLD_SIZE == N.  None = run here."""
+    world = os.environ.get("WORLD_SIZE")
+    if world is None:
+        if args.gpus > 1:
+            return subprocess.call(spawn_command(args.gpus, argv))
+        return None
+    if int(world) != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    return None
+
 
 class Dist:
     def __init__(self):
@@ -172,6 +218,7 @@ class ClockSampler:
     def start(self):
         self._thr = threading.Thread(target=self._run, daemon=True)
         self._thr.start()
+        return self
 
     def sample_now(self):
         """One sample from the calling thread: called right after the timed steps are
@@ -205,81 +252,147 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# CPU side: the reference algorithm on host cores (oracle port)
+# CPU side: the reference's own implementation (vlmfp from baseline/_ref), else the port
 
-def _cpu_one(args):
-    """One image through the oracle path; the synthetic input is generated before
-    the clock starts, so only the preprocessing itself is timed."""
-    seed, k, w, h = args
+_VLMFP = None
+
+
+def reference_module():
+    """vlmfp as installed unmodified into baseline/_ref (pip --target), or None.
+    TP_BENCH_CPU_IMPL=port forces the oracle port."""
+    global _VLMFP
+    if _VLMFP is None:
+        _VLMFP = False
+        if os.environ.get("TP_BENCH_CPU_IMPL") != "port" and (REF_DIR / "vlmfp").is_dir():
+            if str(REF_DIR) not in sys.path:
+                sys.path.insert(0, str(REF_DIR))
+            try:
+                import vlmfp
+
+                _VLMFP = vlmfp
+            except Exception:  # pragma: no cover - missing PIL / ml_dtypes
+                _VLMFP = False
+    return _VLMFP or None
+
+
+def cpu_kind() -> str:
+    return "reference" if reference_module() is not None else "port"
+
+
+def cpu_impl_name() -> str:
+    return ("vlmfp (the reference, baseline/_ref) select_tile_plan -> tile_image -> "
+            "normalize_tiles with fused_transform, contiguous_tensor_path, "
+            "avoid_per_item_split, skip_pixel_mask"
+            if reference_module() is not None else
+            "oracle/tileprep_oracle (numpy port of vlmfp's fused path, band-shared "
+            "vertical blend, in-place ops)")
+
+
+def cpu_preprocess(arr, e, max_tiles, mean, std, bf16):
+    """One image through the CPU path; returns the plan's n_images."""
+    V = reference_module()
+    if V is not None:
+        cfg = V.PreprocessConfig(tile_edge=e, max_tiles=max_tiles, mean=tuple(mean),
+                                 std=tuple(std), reduced_precision_normalize=bf16,
+                                 fused_transform=True, contiguous_tensor_path=True,
+                                 avoid_per_item_split=True, skip_pixel_mask=True)
+        img = V.ImageBuffer.from_array(arr)
+        plan = V.select_tile_plan(img.width, img.height, cfg)
+        V.normalize_tiles(V.tile_image(img, plan, cfg), cfg)
+        return plan.n_images
     from oracle import tileprep_oracle as O
-    from paper_2603_16987_b200.workloads import IMAGENET_MEAN, IMAGENET_STD
 
-    arr = O.synth_image(seed, k, w, h, 3, 0)
-    t0 = time.perf_counter()
-    O.preprocess_image(arr, 448, 12, IMAGENET_MEAN, IMAGENET_STD, True)
-    return time.perf_counter() - t0
-
-
-def cpu_throughput(n_images: int, cores: int, seed: int = 20260817):
-    """images/s of the oracle path with `cores` worker processes busy at once:
-    cores / mean per-image time (each time measured while all workers run, so
-    memory-bandwidth contention is included).  Returns (images/s, p50 ms, CPU-s)."""
-    import multiprocessing as mp
-
-    os.environ.setdefault("OMP_NUM_THREADS", "1")
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
-    jobs = [(seed, k, 1920, 1080) for k in range(n_images)]
-    ctx = mp.get_context("fork")
-    with ctx.Pool(cores) as pool:
-        pool.map(_cpu_one, jobs[:cores])  # warm the workers
-        per = np.array(pool.map(_cpu_one, jobs, chunksize=1))
-    return cores / float(per.mean()), float(np.median(per)) * 1e3, float(per.sum())
+    plan, _ = O.preprocess_image(arr, e, max_tiles, mean, std, bf16)
+    return O.n_images(plan)
 
 
 _CPU_VOCAB = None
 
 
 def _cpu_vocab():
-    """(byte_ids, table, max_len, marker, ctx, asst) of the synthetic C5 vocab, per worker."""
+    """(tokenize, expand+mask) closures over the synthetic C5 vocab, per worker."""
     global _CPU_VOCAB
     if _CPU_VOCAB is None:
-        from oracle import tileprep_oracle as O
         from paper_2603_16987_b200.workloads import synthetic_vocab_text
 
-        toks, byte_ids, table, max_len = O.parse_vocab(synthetic_vocab_text())
-        _CPU_VOCAB = (byte_ids, table, max_len, toks.index("<|image|>"),
-                      toks.index("<IMG_CONTEXT>"), toks.index("<|assistant|>"))
+        V = reference_module()
+        if V is not None:
+            import tempfile
+
+            with tempfile.NamedTemporaryFile("w", suffix=".txt", delete=False,
+                                             encoding="utf-8") as f:
+                f.write(synthetic_vocab_text())
+            vocab = V.load_vocab(f.name)
+            os.unlink(f.name)
+
+            def tok(text):
+                return V.tokenize(text, vocab)
+
+            def expand(ids, n_img):
+                seq = V.expand_image_placeholders(ids, [n_img], 256, vocab)
+                return V.build_supervision_mask(seq, vocab)
+        else:
+            from oracle import tileprep_oracle as O
+
+            toks, byte_ids, table, max_len = O.parse_vocab(synthetic_vocab_text())
+            marker, ctx, asst = (toks.index("<|image|>"), toks.index("<IMG_CONTEXT>"),
+                                 toks.index("<|assistant|>"))
+
+            def tok(text):
+                return O.tokenize(text, byte_ids, table, max_len)
+
+            def expand(ids, n_img):
+                out, _, t = O.expand(ids, [n_img], 256, marker, ctx, asst)
+                return O.supervision_mask(out, t, asst)
+        _CPU_VOCAB = (tok, expand)
     return _CPU_VOCAB
 
 
 def _cpu_wl_one(args):
-    """One image of a workload through the oracle path (input generated off the clock);
-    with a prompt (C5) also its tokenization, image-token expansion (256 tokens per tile)
-    and supervision mask."""
+    """One image of a workload through the CPU path (input generated off the clock);
+    with a prompt (C5) also its tokenization, image-token expansion (256 tokens per
+    tile) and supervision mask.  Returns seconds."""
     seed, k, w, h, e, max_tiles, mean, std, bf16, text = args
     from oracle import tileprep_oracle as O
 
-    arr = O.synth_image(seed, k, w, h, 3, 0)
+    arr = _CPU_IMAGES.get((seed, k, w, h)) if _CPU_IMAGES else None
+    if arr is None:
+        arr = O.synth_image(seed, k, w, h, 3, 0)
     voc = _cpu_vocab() if text is not None else None
     t0 = time.perf_counter()
-    plan, _ = O.preprocess_image(arr, e, max_tiles, mean, std, bf16)
+    n_img = cpu_preprocess(arr, e, max_tiles, mean, std, bf16)
     if voc is not None:
-        byte_ids, table, max_len, marker, ctx, asst = voc
-        ids = O.tokenize(text, byte_ids, table, max_len)
-        out, _, t = O.expand(ids, [O.n_images(plan)], 256, marker, ctx, asst)
-        O.supervision_mask(out, t, asst)
+        voc[1](voc[0](text), n_img)
     return time.perf_counter() - t0
 
 
-def _wl_jobs(wl, n: int, texts=None):
+_CPU_IMAGES: dict = {}
+
+
+def _synth_job(job):
+    from oracle import tileprep_oracle as O
+
+    seed, k, w, h = job[:4]
+    return O.synth_image(seed, k, w, h, 3, 0)
+
+
+def _wl_jobs(wl, n: int, texts=None, start: int = 0):
     return [(wl.seed, k, int(wl.wh[k % len(wl.wh)][0]), int(wl.wh[k % len(wl.wh)][1]),
              wl.tile_edge, wl.max_tiles, tuple(wl.mean), tuple(wl.std), bool(wl.bf16),
              None if texts is None else texts[k])
-            for k in range(n)]
+            for k in range(start, start + n)]
+
+
+def _pool(cores: int):
+    import multiprocessing as mp
+
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    return mp.get_context("fork").Pool(cores)
 
 
 def cpu_latency(wl, runs: int = 15) -> dict:
-    """Batch-1 latency of the oracle path on one host core (one process,
+    """Batch-1 latency of the CPU path on one host core (one process,
     OMP/OPENBLAS_NUM_THREADS=1, p50/p99 over >= 15 runs), as a cpu_baseline object."""
     os.environ.setdefault("OMP_NUM_THREADS", "1")
     os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
@@ -287,32 +400,26 @@ def cpu_latency(wl, runs: int = 15) -> dict:
     _cpu_wl_one(job)  # warm-up
     t = np.array([_cpu_wl_one(job) for _ in range(runs)]) * 1e3
     p50 = float(np.percentile(t, 50))
-    return {"value": round(1e3 / p50, 3), "unit": UNIT, "cores": 1, "kind": "port",
+    return {"value": round(1e3 / p50, 3), "unit": UNIT, "cores": 1, "kind": cpu_kind(),
             "p50_ms": round(p50, 2), "p99_ms": round(float(np.percentile(t, 99)), 2),
-            "sample": f"{runs} runs of 1 x {job[2]}x{job[3]} through oracle/tileprep_oracle "
-                      "(numpy restatement of the vlmfp fused path), one process, one thread; "
-                      "value = 1 / p50"}
+            "sample": f"{runs} runs of 1 x {job[2]}x{job[3]} through {cpu_impl_name()}; "
+                      "one process, one thread; value = 1 / p50"}
 
 
 def cpu_throughput_wl(wl, cores: int, cpu_seconds: float, texts=None) -> dict:
-    """images/s of the oracle path on a prefix of the workload's images (and prompts),
-    one process per core (all busy at once), sized to about `cpu_seconds` of CPU work."""
-    import multiprocessing as mp
-
-    os.environ.setdefault("OMP_NUM_THREADS", "1")
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
-    ctx = mp.get_context("fork")
-    with ctx.Pool(cores) as pool:
+    """images/s of the CPU path on a prefix of the workload's images (and prompts), one
+    process per core (all busy at once, so memory-bandwidth contention is included),
+    sized to about `cpu_seconds` of CPU work: cores / mean per-image time."""
+    with _pool(cores) as pool:
         cal = np.array(pool.map(_cpu_wl_one, _wl_jobs(wl, cores, texts), chunksize=1))
         n = int(max(cores, min(len(wl.wh), cpu_seconds / max(float(cal.mean()), 1e-3))))
         per = np.array(pool.map(_cpu_wl_one, _wl_jobs(wl, n, texts), chunksize=1))
     return {"value": round(cores / float(per.mean()), 3), "unit": UNIT, "cores": cores,
-            "kind": "port",
+            "kind": cpu_kind(),
             "sample": f"first {n} of the {len(wl.wh)} {wl.name} images"
                       + (" and prompts (tokenize + expand + mask)" if texts else "")
-                      + f" through oracle/tileprep_oracle, one process per core, "
-                      f"{per.sum():.1f} CPU-s; "
-                      f"per-image p50 {np.median(per) * 1e3:.1f} ms"}
+                      + f" through {cpu_impl_name()}; one process per core, "
+                      f"{per.sum():.1f} CPU-s; per-image p50 {np.median(per) * 1e3:.1f} ms"}
 
 
 def host_cores() -> int:
@@ -322,36 +429,53 @@ def host_cores() -> int:
         return os.cpu_count() or 1
 
 
+def c2_config(wl, n: int, world: int) -> dict:
+    return {"workload": "C2: " + wl.description, "images_per_gpu": n,
+            "l2": "inputs (398 MB/GPU) larger than L2",
+            "parallelism": f"dp{world} (independent images, no collective)"}
+
+
 def run_reference(args, dist: Dist):
-    """--impl reference: the reference algorithm (oracle port of vlmfp's fused,
-    contiguous path) on all host cores, rank 0 only; each step is a bounded sample
-    of C2 images."""
+    """--impl reference: the reference's own CPU path (vlmfp from baseline/_ref) on all
+    host cores, rank 0 only; each step = the C2 batch (64 images), one process per core."""
     if dist.rank != 0:
         return
+    from oracle import tileprep_oracle as O
+    from paper_2603_16987_b200.workloads import c2
+
+    wl = c2(args.batch)
     cores = host_cores()
-    sample = max(cores, 16)
-    cpu_throughput(cores, cores)  # warm-up
-    rates, p50s, cpu_s = [], [], 0.0
-    for _ in range(args.steps):
-        ips, p50_ms, cs = cpu_throughput(sample, cores)
-        rates.append(ips)
-        p50s.append(p50_ms)
-        cpu_s += cs
-    value = float(np.median(rates))
+    jobs = _wl_jobs(wl, len(wl.wh))
+    # the synthetic batch, generated in parallel and kept in this process before the
+    # timing pool forks, so every worker inherits it (nothing generated on the clock)
+    with _pool(cores) as pool:
+        arrs = pool.map(_synth_job, jobs, chunksize=1)
+    for j, a in zip(jobs, arrs):
+        _CPU_IMAGES[j[:4]] = a
+    del arrs
+    times, per_img = [], []
+    with _pool(cores) as pool:
+        for _ in range(max(1, args.warmup)):
+            pool.map(_cpu_wl_one, jobs[:cores], chunksize=1)
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            per_img += pool.map(_cpu_wl_one, jobs, chunksize=1)
+            times.append(time.perf_counter() - t0)
+    total = float(np.sum(times))
+    value = len(jobs) * args.steps / total
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": UNIT,
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(sample / value * 1e3, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u8 in, fp32 + fp64-exact resample, bf16 out",
-        "data": "synthetic",
-        "config": {"workload": "C2: 1920x1080 RGB uint8, E=448, max 12 + thumb, "
-                               "ImageNet mean/std, bf16 out", "images_per_step": sample},
-        "p50_ms": round(float(np.median(p50s)), 3),
+        "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(total / args.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": DTYPE, "data": "synthetic",
+        "config": c2_config(wl, len(jobs), dist.world),
+        "p50_ms": round(float(np.median(per_img)) * 1e3, 3),
         "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": cores,
-                         "kind": "port",
-                         "sample": f"{sample} images x {args.steps} steps ({cpu_s:.0f} CPU-s) "
-                                   "through oracle/tileprep_oracle (numpy restatement of the "
-                                   "vlmfp fused/contiguous recipe path), one process per core"},
+                         "kind": cpu_kind(),
+                         "sample": f"the {len(jobs)}-image C2 batch x {args.steps} steps "
+                                   f"({np.sum(per_img):.0f} CPU-s) through {cpu_impl_name()}; "
+                                   "one process per core, images generated before the clock; "
+                                   "p50_ms = per-image time with all cores busy"},
         "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -360,201 +484,6 @@ def run_reference(args, dist: Dist):
 
 # ---------------------------------------------------------------------------
 # GPU side
-
-def main():
-    args = parse_args()
-    dist = Dist()
-    if args.impl == "reference":
-        run_reference(args, dist)
-        return
-
-    import torch
-
-    from paper_2603_16987_b200 import _lib
-    from paper_2603_16987_b200.engine import TilePreprocessor, empty_packed, synth_packed
-    from paper_2603_16987_b200.imgproc import PreprocessConfig
-    from paper_2603_16987_b200.workloads import c2, workload_bytes
-
-    if not torch.cuda.is_available():
-        raise SystemExit("bench.py needs a CUDA device")
-    dev_index = dist.device_index(torch.cuda.device_count())
-    torch.cuda.set_device(dev_index)
-    device = torch.device("cuda", dev_index)
-    dist.init("nccl")
-    if args.workload in ("c4", "c5"):
-        run_sweep(args, dist, device)
-        dist.close()
-        return
-    if args.workload in ("c1", "c3"):
-        run_single(args, dist, device)
-        dist.close()
-        return
-
-    wl = c2(args.batch)
-    cfg = PreprocessConfig(tile_edge=wl.tile_edge, max_tiles=wl.max_tiles, mean=wl.mean,
-                           std=wl.std, reduced_precision_normalize=wl.bf16)
-    stream = torch.cuda.Stream(device)
-    seed = wl.seed + 1_000_003 * dist.rank
-    images = synth_packed(wl.wh, 3, device, seed=seed, kind=0)
-    prep = TilePreprocessor(cfg, device)
-    n = images.n
-    out = prep(images)  # allocates outputs at the upper bound
-    torch.cuda.synchronize(device)
-    n_tiles = out.num_tiles()
-
-    wb = workload_bytes(wl)
-    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-
-    def step(i=None):
-        # K1 then K2; K2 is a programmatic dependent launch of K1 (and the next K1 of K2),
-        # so no event is recorded between them inside the timed steps
-        # steady state: the previous step's K2 is the last kernel on the stream
-        prep.plan(images, out.plans, stream, after_kernel=True)
-        prep.tile(images, out.plans, out.pixel_values, None, stream, after_plan=True)
-
-    with torch.cuda.stream(stream):
-        for _ in range(max(3, args.warmup)):
-            step()
-    torch.cuda.synchronize(device)
-    clocks = ClockSampler(dev_index)
-    clocks.start()
-    dist.barrier(device)
-    torch.cuda.synchronize(device)
-    start.record(stream)
-    for i in range(args.steps):
-        step(i)
-    stop.record(stream)
-    clocks.sample_now()
-    torch.cuda.synchronize(device)
-    dist.barrier(device)
-    clk = clocks.stop()
-    ms_local = start.elapsed_time(stop)
-    ms = dist.max(ms_local, device)
-    # K2's own launch duration (the roofline's denominator): the same launches back to back
-    # on the same stream and inputs, CUDA events around all of them
-    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize(device)
-    k0.record(stream)
-    for _ in range(args.steps):
-        prep.tile(images, out.plans, out.pixel_values, None, stream)
-    k1.record(stream)
-    torch.cuda.synchronize(device)
-    k2_ms = k0.elapsed_time(k1) / args.steps
-    ms_step = ms / args.steps
-    value = dist.world * n * args.steps / (ms / 1e3)
-
-    # ---- end to end through the public API with host buffers ----------------
-    # The batch sits in a page-locked arena, staged once (pixels + sizes + offsets, one
-    # region: transfer.stage_images). Every timed step uploads it with ONE H2D copy on a
-    # copy stream, runs K1+K2 on the compute stream and reads the plans and tile offsets
-    # back (D2H); device buffers alternate so step i+1's upload overlaps step i's kernels.
-    from paper_2603_16987_b200.transfer import HostArena, stage_images, staged_bytes, upload_images
-
-    offs, whs = images.offsets_host, images.wh_host
-    host_imgs = [images.data[int(o): int(o) + int(w) * int(h) * 3].cpu().numpy().reshape(int(h), int(w), 3)
-                 for o, (w, h) in zip(offs, whs)]
-    # only the source rows K2's stencil reads go over the link (stage_images(touched=...),
-    # tp_tile_rows: 83% of a 1080p image at E=448); full_bytes is the whole-image upload
-    full_bytes = staged_bytes(host_imgs)
-    touched = (cfg.tile_edge, cfg.max_tiles)
-    nbytes = staged_bytes(host_imgs, touched=touched)
-    staged = stage_images(host_imgs, HostArena(nbytes, 256, pin=True), touched=touched)
-    del host_imgs
-    slabs = [torch.empty(nbytes, dtype=torch.uint8, device=device) for _ in range(2)]
-    outs2 = [out, prep(images)]
-    plan_host = [torch.empty_like(out.plans.plan, device="cpu").pin_memory() for _ in range(2)]
-    off_host = [torch.empty_like(out.plans.tile_off, device="cpu").pin_memory() for _ in range(2)]
-    copy_stream = torch.cuda.Stream(device)
-    done = [None, None]
-    e2e_steps = max(5, min(args.steps, 30))
-
-    def e2e_step(i):
-        k = i % 2
-        if done[k] is not None:
-            copy_stream.wait_event(done[k])  # slab k no longer read by step i-2's K2
-        packed_k, copied = upload_images(staged, slabs[k], copy_stream)
-        stream.wait_event(copied)
-        with torch.cuda.stream(stream):
-            prep(packed_k, out=outs2[k], stream=stream)
-            plan_host[k].copy_(outs2[k].plans.plan, non_blocking=True)
-            off_host[k].copy_(outs2[k].plans.tile_off, non_blocking=True)
-            ev = torch.cuda.Event()
-            ev.record(stream)
-        done[k] = ev
-
-    for i in range(3):
-        e2e_step(i)
-    torch.cuda.synchronize(device)
-    dist.barrier(device)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(copy_stream)
-    for i in range(e2e_steps):
-        e2e_step(i)
-    e1.record(stream)
-    torch.cuda.synchronize(device)
-    e2e_ms = dist.max(e0.elapsed_time(e1), device) / e2e_steps
-    h2d = len(staged.batch.payload)  # bytes actually copied (incl. 256-byte alignment)
-    d2h = plan_host[0].numel() * 4 + off_host[0].numel() * 4
-
-    # ---- batch-1 per-image latency (1 x 1080p, device resident, CUDA graph) --
-    latency = None
-    if dist.rank == 0:
-        latency = batch1_latency(cfg, device, args.latency_iters)
-
-    # ---- CPU baseline (rank 0, N=1 only) -------------------------------------
-    cpu = None
-    if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
-        cores = host_cores()
-        # calibrate: ~`cpu-seconds` of total CPU work
-        _, p50_ms, _ = cpu_throughput(cores, cores)
-        n_cpu = int(max(cores, min(512, args.cpu_seconds * 1e3 / max(p50_ms, 1.0))))
-        ips, p50_ms, cpu_s = cpu_throughput(n_cpu, cores)
-        cpu = {"value": round(ips, 3), "unit": UNIT, "cores": cores, "kind": "port",
-               "sample": f"{n_cpu} C2 images (1920x1080) through oracle/tileprep_oracle "
-                         f"(numpy restatement of the vlmfp fused path), one process per core, "
-                         f"{cpu_s:.1f} CPU-s; per-image p50 {p50_ms:.1f} ms"}
-
-    traffic = measured_traffic("tp_tile", wb["total"])
-    if dist.rank == 0:
-        bytes_per_launch = wb["total"]
-        achieved = bytes_per_launch / (k2_ms / 1e3) / 1e9
-        peak = measured_peak()
-        line = {
-            "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": dist.world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "u8 in, fp32 + fp64-exact resample, bf16 out", "data": "synthetic",
-            "config": {"workload": "C2: " + wl.description, "images_per_gpu": n,
-                       "tiles_per_gpu": n_tiles, "l2": "inputs (398 MB/GPU) larger than L2",
-                       "parallelism": f"dp{dist.world} (independent images, no collective)"},
-            "p50_ms": latency["p50_ms"] if latency else None,
-            "latency": latency,
-            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak[0],
-                         "unit": "GB/s", "frac": round(achieved / peak[0], 4),
-                         "traffic": traffic, "peak_source": peak[1],
-                         "kernel": "tp_tile (K2)", "kernel_ms": round(k2_ms, 4),
-                         "kernel_timing": "CUDA events around K back-to-back K2 launches, "
-                                          "same stream and inputs, after the timed steps",
-                         "bytes_per_launch": bytes_per_launch,
-                         "bytes_full_image": int(wb["read_full"] + wb["write"]),
-                         "peak_nominal_gbs": 8000.0,
-                         "frac_of_nominal": round(achieved / 8000.0, 4)},
-            "cpu_baseline": cpu,
-            "e2e": {"value": round(dist.world * n / (e2e_ms / 1e3), 2), "unit": UNIT,
-                    "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                    "ms_per_step": round(e2e_ms, 4),
-                    "path": "page-locked staged batch (touched source rows and columns + maps) -> "
-                            "one H2D copy (copy stream) -> TilePreprocessor K1+K2 "
-                            "(compute stream, K2 reads rows through the maps) -> D2H "
-                            "plans/offsets; two device buffers, so step i+1's upload "
-                            "overlaps step i",
-                    "h2d_bytes_full_images": int(full_bytes)},
-            "gpu_launches": 2 * args.steps,
-            "clocks": clk,
-        }
-        print(json.dumps(dist.tag(line)), flush=True)
-    dist.close()
-
 
 def measured_traffic(kernel: str, algorithmic: int):
     """DRAM bytes per launch of the dominant kernel from the committed ncu capture
@@ -575,14 +504,176 @@ def measured_peak():
         return 6650.0, "B200_PROFILING.md fallback 6.65 TB/s"
 
 
-def batch1_latency(cfg, device, iters: int):
-    """p50/p99 of one 1920x1080 image through K1+K2 (device-resident input,
-    CUDA-graph launched), plus the same with the 6.2 MB H2D from pinned host."""
+def _timed(fn, steps: int, warmup: int, stream, device, dist):
+    """Device time of `steps` calls of fn on `stream` (CUDA events, barrier +
+    synchronize on both sides, max over ranks) and the clock record."""
+    import torch
+
+    with torch.cuda.stream(stream):
+        for _ in range(max(3, warmup)):
+            fn()
+    torch.cuda.synchronize(device)
+    clocks = ClockSampler(device.index).start()
+    dist.barrier(device)
+    torch.cuda.synchronize(device)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    with torch.cuda.stream(stream):
+        for i in range(steps):
+            fn(i)
+    b.record(stream)
+    clocks.sample_now()
+    torch.cuda.synchronize(device)
+    dist.barrier(device)
+    clk = clocks.stop()
+    return dist.max(a.elapsed_time(b), device), clk
+
+
+def run_c2(args, dist, device, dev_index):
+    """The headline: C2 device-resident steps, K2's roofline, and the e2e sub-block."""
+    import torch
+
+    from paper_2603_16987_b200.engine import TilePreprocessor, synth_packed
+    from paper_2603_16987_b200.imgproc import PreprocessConfig
+    from paper_2603_16987_b200.workloads import c2, workload_bytes
+
+    wl = c2(args.batch)
+    cfg = PreprocessConfig(tile_edge=wl.tile_edge, max_tiles=wl.max_tiles, mean=wl.mean,
+                           std=wl.std, reduced_precision_normalize=wl.bf16)
+    stream = torch.cuda.Stream(device)
+    seed = wl.seed + 1_000_003 * dist.rank
+    images = synth_packed(wl.wh, 3, device, seed=seed, kind=0)
+    prep = TilePreprocessor(cfg, device)
+    n = images.n
+    out = prep(images)  # allocates outputs at the upper bound
+    torch.cuda.synchronize(device)
+    n_tiles = out.num_tiles()
+    wb = workload_bytes(wl)
+
+    def step(i=None):
+        # K1 then K2; K2 is a programmatic dependent launch of K1 (and the next K1 of K2),
+        # so no event is recorded between them inside the timed steps.  Steady state:
+        # the previous step's K2 is the last kernel on the stream.
+        prep.plan(images, out.plans, stream, after_kernel=True)
+        prep.tile(images, out.plans, out.pixel_values, None, stream, after_plan=True)
+
+    ms, clk = _timed(step, args.steps, args.warmup, stream, device, dist)
+    # K2's own launch duration (the roofline's denominator): the same launches back to
+    # back on the same stream and inputs, CUDA events around all of them
+    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(device)
+    k0.record(stream)
+    for _ in range(args.steps):
+        prep.tile(images, out.plans, out.pixel_values, None, stream)
+    k1.record(stream)
+    torch.cuda.synchronize(device)
+    k2_ms = dist.max(k0.elapsed_time(k1) / args.steps, device)
+    res = {"ms": ms, "ms_step": ms / args.steps, "value": dist.world * n * args.steps / (ms / 1e3),
+           "clk": clk, "k2_ms": k2_ms, "n": n, "n_tiles": n_tiles, "wb": wb, "wl": wl,
+           "cfg": cfg}
+    host_imgs = [images.data[int(o): int(o) + int(w) * int(h) * 3].cpu().numpy()
+                 .reshape(int(h), int(w), 3) for o, (w, h) in zip(images.offsets_host,
+                                                                   images.wh_host)]
+    del images, out
+    res["e2e"] = run_e2e(args, dist, device, cfg, host_imgs)
+    return res
+
+
+def run_e2e(args, dist, device, cfg, host_imgs) -> dict:
+    """The C2 batch end to end through the public pipeline, from the caller's numpy HWC
+    arrays (pageable host memory): every step packs the batch into a page-locked slab
+    on the library's host threads (tp_stage_pack: only the source rows K2 reads), uploads
+    it with one H2D copy, runs K1 + K2 and reads the plans and tile offsets back.  Two
+    slabs rotate, so packing step i+1 overlaps the upload and kernels of step i.  Timed on
+    the host clock (the host work is part of it), synchronize + barrier on both sides,
+    max over ranks."""
+    import torch
+
+    from paper_2603_16987_b200.engine import TilePreprocessor
+    from paper_2603_16987_b200.transfer import PipelinedPreprocessor, staged_bytes
+
+    touched = (cfg.tile_edge, cfg.max_tiles)
+    nbytes = staged_bytes(host_imgs, touched=touched)
+    full_bytes = staged_bytes(host_imgs)
+    prep = TilePreprocessor(cfg, device)
+    pipe = PipelinedPreprocessor(prep, nbytes, depth=2, touched=True)
+    outs = [None, None]
+    plan_host = [None, None]
+    off_host = [None, None]
+    pack_s = []
+
+    def e2e_step(i):
+        k = i % 2
+        t0 = time.perf_counter()
+        outs[k] = pipe.submit(host_imgs, out=outs[k])
+        pack_s.append(time.perf_counter() - t0)
+        with torch.cuda.stream(pipe.compute_stream):
+            if plan_host[k] is None:
+                plan_host[k] = torch.empty_like(outs[k].plans.plan, device="cpu").pin_memory()
+                off_host[k] = torch.empty_like(outs[k].plans.tile_off, device="cpu").pin_memory()
+            plan_host[k].copy_(outs[k].plans.plan, non_blocking=True)
+            off_host[k].copy_(outs[k].plans.tile_off, non_blocking=True)
+
+    for i in range(3):
+        e2e_step(i)
+    torch.cuda.synchronize(device)
+    pack_s.clear()
+    steps = max(5, args.e2e_steps)
+    dist.barrier(device)
+    torch.cuda.synchronize(device)
+    t0 = time.perf_counter()
+    for i in range(steps):
+        e2e_step(i)
+    torch.cuda.synchronize(device)
+    wall = time.perf_counter() - t0
+    dist.barrier(device)
+    wall = dist.max(wall, device)
+    # the H2D link alone on the same payload (what the packing overlaps with)
+    h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    src = pipe.host[0].tensor[: pipe.last_bytes]
+    h0.record(pipe.copy_stream)
+    for _ in range(5):
+        pipe.dev[0][: pipe.last_bytes].copy_(src, non_blocking=True)
+    h1.record(pipe.copy_stream)
+    torch.cuda.synchronize(device)
+    h2d_ms = h0.elapsed_time(h1) / 5
+    n = len(host_imgs)
+    ms_step = wall / steps * 1e3
+    return {"value": round(dist.world * n / (ms_step / 1e3), 2), "unit": UNIT,
+            "h2d_bytes_per_step": int(pipe.last_bytes),
+            "d2h_bytes_per_step": int(plan_host[0].numel() * 4 + off_host[0].numel() * 4),
+            "ms_per_step": round(ms_step, 4), "steps": steps,
+            "pack_ms": round(float(np.median(pack_s)) * 1e3, 3),
+            "pack_gbs": round(pipe.last_bytes / float(np.median(pack_s)) / 1e9, 2),
+            "h2d_ms": round(h2d_ms, 3),
+            "h2d_gbs": round(pipe.last_bytes / (h2d_ms / 1e3) / 1e9, 2),
+            "host_threads": int(_host_threads()),
+            "timing": "host wall clock around all steps (synchronize + barrier both sides, "
+                      "max over ranks); pack_ms = median host time of one submit() "
+                      "(native row packing into the pinned slab + enqueue)",
+            "path": "caller's numpy HWC arrays (pageable) -> PipelinedPreprocessor.submit: "
+                    "tp_stage_pack on the host thread pool (touched source rows only) into "
+                    "a pinned slab -> one H2D copy (copy stream) -> K1 + K2 (compute "
+                    "stream, K2 reads rows through the maps) -> D2H plans/offsets; two "
+                    "slabs, so packing step i+1 overlaps the upload of step i",
+            "h2d_bytes_full_images": int(full_bytes)}
+
+
+def _host_threads() -> int:
+    from paper_2603_16987_b200 import _lib
+
+    return _lib.load().tp_host_threads()
+
+
+def batch1_latency(cfg, wh, device, iters: int, with_touched: bool = True) -> dict:
+    """p50/p99 of one image through the preprocessor (device-resident input, CUDA-graph
+    launched: the fused tp_plan_tile), the same with the pinned H2D of the whole image
+    and of its touched rows, and the graph floor; with a clock record."""
     import torch
 
     from paper_2603_16987_b200.engine import TilePreprocessor, empty_packed, synth_packed
 
-    wh = np.array([[1920, 1080]], dtype=np.int32)
+    wh = np.asarray(wh, dtype=np.int32).reshape(-1, 2)
     img = synth_packed(wh, 3, device, seed=7, kind=0)
     prep = TilePreprocessor(cfg, device)
     out = prep(img)
@@ -593,19 +684,7 @@ def batch1_latency(cfg, device, iters: int):
         prep(img, out=out, stream=torch.cuda.current_stream(device))
     host = empty_packed(wh, 3, "cpu", pin=True)
     host.data.copy_(img.data.cpu())
-
-    def timed(fn):
-        ts = []
-        for _ in range(iters):
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(s)
-            with torch.cuda.stream(s):
-                fn()
-            b.record(s)
-            b.synchronize()
-            ts.append(a.elapsed_time(b))
-        ts = np.array(ts[max(3, iters // 10):])
-        return float(np.percentile(ts, 50)), float(np.percentile(ts, 99))
+    floor = _empty_graph(device, s)
 
     def dev_only():
         g.replay()
@@ -614,17 +693,35 @@ def batch1_latency(cfg, device, iters: int):
         img.data.copy_(host.data, non_blocking=True)
         g.replay()
 
-    p50, p99 = timed(dev_only)
-    h50, h99 = timed(with_h2d)
-    f50, _ = timed(_empty_graph(device, s))
-    t50, t99, tbytes = _touched_h2d_latency(cfg, img, device, s, iters)
-    return {"p50_ms": round(p50, 4), "p99_ms": round(p99, 4), "h2d_p50_ms": round(h50, 4),
-            "h2d_p99_ms": round(h99, 4), "iters": iters,
-            "h2d_touched_p50_ms": round(t50, 4), "h2d_touched_p99_ms": round(t99, 4),
-            "h2d_touched_bytes": tbytes,
-            "graph_floor_p50_ms": round(f50, 4),
-            "workload": "1 x 1920x1080, E=448 InternVL3-2B tiling, bf16 NCHW; CUDA graph "
-                        "(K1+K2); h2d_* add the 6.2 MB pinned upload"}
+    clocks = ClockSampler(device.index).start()
+    ts = {"dev": [], "h2d": [], "floor": []}
+    for k in range(iters + 50):
+        for name, fn in (("dev", dev_only), ("h2d", with_h2d), ("floor", floor)):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(s)
+            with torch.cuda.stream(s):
+                fn()
+            b.record(s)
+            b.synchronize()
+            if k >= 50:
+                ts[name].append(a.elapsed_time(b))
+    clk = clocks.stop()
+    d, h = np.array(ts["dev"]), np.array(ts["h2d"])
+    res = {"p50_ms": round(float(np.percentile(d, 50)), 4),
+           "p99_ms": round(float(np.percentile(d, 99)), 4),
+           "h2d_p50_ms": round(float(np.percentile(h, 50)), 4),
+           "h2d_p99_ms": round(float(np.percentile(h, 99)), 4),
+           "h2d_bytes": int(host.data.numel()), "iters": iters,
+           "graph_floor_p50_ms": round(float(np.median(ts["floor"])), 4)}
+    if with_touched:
+        t50, t99, tbytes = _touched_h2d_latency(cfg, img, device, s, min(iters, 500))
+        res.update({"h2d_touched_p50_ms": round(t50, 4), "h2d_touched_p99_ms": round(t99, 4),
+                    "h2d_touched_bytes": tbytes})
+    res["clocks"] = clk
+    res["timing"] = ("CUDA events around each CUDA-graph replay (K1+K2 fused, "
+                     "tp_plan_tile); h2d_* add the pinned upload of the image (or of its "
+                     "touched rows) before the replay; 50 warm-up iterations dropped")
+    return res
 
 
 def _touched_h2d_latency(cfg, img, device, stream, iters: int):
@@ -679,43 +776,41 @@ def _empty_graph(device, stream):
     return g.replay
 
 
-def _timed(fn, steps: int, warmup: int, stream, device, dist, events_per_step=None):
-    import torch
+def run_single(args, dist, device, which: str) -> dict:
+    """C1 (1920x1080, E=512, fp32) / C3 (3840x2160, E=448, bf16): batch-1 latency on
+    rank 0's GPU, with the CPU path's batch-1 latency on one host core beside it."""
+    from paper_2603_16987_b200.imgproc import PreprocessConfig
+    from paper_2603_16987_b200.workloads import c1, c3, workload_bytes
 
-    with torch.cuda.stream(stream):
-        for _ in range(max(3, warmup)):
-            fn()
-    torch.cuda.synchronize(device)
-    clocks = ClockSampler(device.index)
-    clocks.start()
-    dist.barrier(device)
-    torch.cuda.synchronize(device)
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(stream)
-    with torch.cuda.stream(stream):
-        for i in range(steps):
-            fn(i)
-    b.record(stream)
-    clocks.sample_now()
-    torch.cuda.synchronize(device)
-    dist.barrier(device)
-    clk = clocks.stop()
-    return dist.max(a.elapsed_time(b), device), clk
+    wl = c1() if which == "c1" else c3()
+    cfg = PreprocessConfig(tile_edge=wl.tile_edge, max_tiles=wl.max_tiles, mean=wl.mean,
+                           std=wl.std, reduced_precision_normalize=wl.bf16)
+    lat = batch1_latency(cfg, wl.wh, device, max(args.latency_iters, 1000))
+    res = {"workload": wl.name + ": " + wl.description,
+           "value": round(1e3 / lat["p50_ms"], 2), "unit": UNIT, **lat,
+           "algorithmic_bytes": workload_bytes(wl)["total"]}
+    if not args.no_cpu_baseline:
+        res["cpu_baseline"] = cpu_latency(wl)
+    return res
 
 
-def run_sweep(args, dist, device):
-    """C4 (8192 mixed-aspect images, sharded over ranks by LPT; strong scaling) or C5
-    (1024 of those images + batched placeholder expansion).  Inputs are generated on
-    device before timing; a step processes the rank's whole shard in chunks of 1024."""
+def run_sweep(args, dist, device, which: str = "c4", steps: int | None = None,
+              warmup: int | None = None) -> dict:
+    """C4 (8192 mixed-aspect images, LPT-sharded over the ranks; strong scaling) or C5
+    (1024 of those images + device tokenization and placeholder expansion).  Inputs are
+    generated on device before timing; a step processes the rank's whole shard in
+    chunks of 1024 images."""
     import torch
 
     from paper_2603_16987_b200.engine import TilePreprocessor, synth_packed
     from paper_2603_16987_b200.imgproc import PreprocessConfig
-    from paper_2603_16987_b200.sharding import shard
+    from paper_2603_16987_b200.sharding import imbalance, shard
     from paper_2603_16987_b200.tokenizer import PlaceholderExpander
     from paper_2603_16987_b200.workloads import Workload, c4, workload_bytes
 
-    total = 8192 if args.workload == "c4" else 1024
+    steps = args.steps if steps is None else steps
+    warmup = args.warmup if warmup is None else warmup
+    total = 8192 if which == "c4" else 1024
     wl_all = c4(total)
     idx = shard(wl_all.wh, wl_all.tile_edge, wl_all.max_tiles, dist.rank, dist.world)
     wh = wl_all.wh[idx]
@@ -723,13 +818,12 @@ def run_sweep(args, dist, device):
                            reduced_precision_normalize=True)
     chunk = 1024
     stream = torch.cuda.Stream(device)
-    chunks = []
-    for c0 in range(0, len(idx), chunk):
-        chunks.append(synth_packed(wh[c0:c0 + chunk], 3, device, seed=wl_all.seed + c0, kind=0))
+    chunks = [synth_packed(wh[c0:c0 + chunk], 3, device, seed=wl_all.seed + c0, kind=0)
+              for c0 in range(0, len(idx), chunk)]
     prep = TilePreprocessor(cfg, device)
     outs = prep(chunks[0], capacity=chunk * 13)
     torch.cuda.synchronize(device)
-    with_expand = args.workload == "c5"
+    with_expand = which == "c5"
     if with_expand:
         # rendered prompts tokenized on the device (K6), then expanded with the tile
         # counts straight from K1 (K3): ids never leave the GPU
@@ -739,7 +833,7 @@ def run_sweep(args, dist, device):
         vocab = parse_vocab(synthetic_vocab_text(), "synthetic")
         n = len(idx)
         tok = DeviceTokenizer(vocab, device)
-        texts = tok.upload(c5_texts(n, wl_all.seed))
+        texts = tok.upload([c5_texts(total, wl_all.seed)[i] for i in idx])
         toks = tok(texts)
         count_off = torch.arange(0, n + 1, dtype=torch.int32, device=device)
         exp = PlaceholderExpander(vocab, 256, device)
@@ -757,109 +851,128 @@ def run_sweep(args, dist, device):
                 exp(toks.ids, toks.off, outs.plans.n_images, count_off, cap, out=ex,
                     stream=stream)
 
-    ms, clk = _timed(step, args.steps, args.warmup, stream, device, dist)
-    ms_step = ms / args.steps
-    wl = Workload("C4" if not with_expand else "C5", wl_all.description, wh, 448, 12,
-                  wl_all.mean, wl_all.std, True, wl_all.seed)
-    wb = workload_bytes(wl)
-    value = total * args.steps / (ms / 1e3)  # all images of the job over the max-rank time
-    if dist.rank == 0:
-        peak = measured_peak()
-        achieved = wb["total"] / (ms_step / 1e3) / 1e9
-        line = {
-            "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": dist.world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "u8 in, fp32/fp64-exact resample, bf16 out", "data": "synthetic",
-            "config": {"workload": ("C4: " if not with_expand else "C5: ") + wl_all.description
-                       + (" + device tokenization of rendered prompts (K6) and image-token"
-                          " expansion (256 tokens/tile)" if with_expand else ""),
-                       "images_total": total, "images_rank0": len(idx),
-                       "l2": "inputs larger than L2", "parallelism": f"dp{dist.world} LPT shards"},
-            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak[0],
-                         "unit": "GB/s", "frac": round(achieved / peak[0], 4), "traffic": None,
-                         "bytes_per_step_rank0": wb["total"],
-                         "note": "whole step (K1+K2" + ("+K6+K3" if with_expand else "") + ")"},
-            "gpu_launches": args.steps * len(chunks) * (8 if with_expand else 2),
-            "clocks": clk,
-        }
-        if dist.world == 1 and not args.no_cpu_baseline:
-            cpu_texts = None
-            if with_expand:
-                from paper_2603_16987_b200.workloads import c5_texts
-                cpu_texts = c5_texts(total, wl_all.seed)
-            line["cpu_baseline"] = cpu_throughput_wl(wl_all, host_cores(), args.cpu_seconds,
-                                                     cpu_texts)
-        print(json.dumps(dist.tag(line)), flush=True)
+    ms, clk = _timed(step, steps, warmup, stream, device, dist)
+    ms_step = ms / steps
+    wl = Workload(wl_all.name, wl_all.description, wh, 448, 12, wl_all.mean, wl_all.std, True,
+                  wl_all.seed)
+    wb = workload_bytes(wl)  # this rank's shard
+    peak = measured_peak()
+    achieved = wb["total"] / (ms_step / 1e3) / 1e9
+    res = {"workload": ("C4: " if not with_expand else "C5: ") + wl_all.description
+           + (" + device tokenization of rendered prompts (K6) and image-token"
+              " expansion (256 tokens/tile, K3)" if with_expand else ""),
+           "value": round(total * steps / (ms / 1e3), 2), "unit": UNIT,
+           "n_gpus": dist.world, "scaling": "strong", "steps": steps, "warmup": warmup,
+           "ms_per_step": round(ms_step, 4), "images_total": total,
+           "images_per_rank": len(idx), "parallelism": f"dp{dist.world} LPT shards",
+           "lpt_imbalance": round(imbalance(wl_all.wh, 448, 12, dist.world), 4),
+           "l2": "inputs larger than L2",
+           "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak[0],
+                        "unit": "GB/s", "frac": round(achieved / peak[0], 4),
+                        "bytes_per_step_rank0": wb["total"],
+                        "note": "per GPU: rank 0's shard bytes / the max-over-ranks step "
+                                "time, whole step (K1+K2" + ("+K6+K3" if with_expand else "")
+                                + ")"},
+           "gpu_launches": steps * len(chunks) * (8 if with_expand else 2),
+           "clocks": clk}
+    if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
+        cpu_texts = None
+        if with_expand:
+            from paper_2603_16987_b200.workloads import c5_texts
+            cpu_texts = c5_texts(total, wl_all.seed)
+        res["cpu_baseline"] = cpu_throughput_wl(wl_all, host_cores(), args.cpu_seconds,
+                                                cpu_texts)
+    del chunks, outs
+    torch.cuda.empty_cache()
+    return res
 
 
-def run_single(args, dist, device):
-    """C1 (1920x1080, E=512, fp32) / C3 (3840x2160, E=448, bf16): batch-1 latency."""
+def main(argv=None):
+    argv = list(sys.argv[1:] if argv is None else argv)
+    args = parse_args(argv)
+    rc = maybe_spawn(args, argv)
+    if rc is not None:
+        sys.exit(rc)
+    dist = Dist()
+    if args.impl == "reference":
+        run_reference(args, dist)
+        return
+
     import torch
 
-    from paper_2603_16987_b200.engine import TilePreprocessor, empty_packed, synth_packed
-    from paper_2603_16987_b200.imgproc import PreprocessConfig
-    from paper_2603_16987_b200.workloads import c1, c3, workload_bytes
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device")
+    dev_index = dist.device_index(torch.cuda.device_count())
+    torch.cuda.set_device(dev_index)
+    device = torch.device("cuda", dev_index)
+    dist.init("nccl")
 
-    wl = c1() if args.workload == "c1" else c3()
-    cfg = PreprocessConfig(tile_edge=wl.tile_edge, max_tiles=wl.max_tiles, mean=wl.mean,
-                           std=wl.std, reduced_precision_normalize=wl.bf16)
-    img = synth_packed(wl.wh, 3, device, seed=wl.seed, kind=0)
-    prep = TilePreprocessor(cfg, device)
-    out = prep(img)
-    s = torch.cuda.Stream(device)
-    torch.cuda.synchronize(device)
-    g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g, stream=s):
-        prep(img, out=out, stream=torch.cuda.current_stream(device))
-    host = empty_packed(wl.wh, 3, "cpu", pin=True)
-    host.data.copy_(img.data.cpu())
-    ts, th = [], []
-    iters = max(args.latency_iters, 1000)
-    for k in range(iters + 50):
-        for with_h2d, sink in ((False, ts), (True, th)):
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(s)
-            with torch.cuda.stream(s):
-                if with_h2d:
-                    img.data.copy_(host.data, non_blocking=True)
-                g.replay()
-            b.record(s)
-            b.synchronize()
-            if k >= 50:
-                sink.append(a.elapsed_time(b))
-    ts, th = np.array(ts), np.array(th)
-    floor_fn, tf = _empty_graph(device, s), []
-    for k in range(550):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(s)
-        with torch.cuda.stream(s):
-            floor_fn()
-        b.record(s)
-        b.synchronize()
-        if k >= 50:
-            tf.append(a.elapsed_time(b))
-    t50, t99, tbytes = _touched_h2d_latency(cfg, img, device, s, min(iters, 500))
-    wb = workload_bytes(wl)
+    if args.workload != "c2":  # one config alone as the line's workload
+        if args.workload in ("c4", "c5"):
+            r = run_sweep(args, dist, device, args.workload)
+        else:
+            r = run_single(args, dist, device, args.workload) if dist.rank == 0 else None
+        if dist.rank == 0:
+            line = {"metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": dist.world,
+                    "steps": r.get("steps", args.latency_iters), "warmup": args.warmup,
+                    "higher_is_better": True, "scaling": r.get("scaling", "weak"),
+                    "vs_baseline": None, "dtype": DTYPE, "data": "synthetic",
+                    "config": {"workload": r["workload"]}, **{k: v for k, v in r.items()
+                                                             if k not in ("value", "workload")}}
+            print(json.dumps(dist.tag(line)), flush=True)
+        dist.close()
+        return
+
+    r = run_c2(args, dist, device, dev_index)
+    wl, wb = r["wl"], r["wb"]
+    latency = batch1_latency(r["cfg"], [[1920, 1080]], device, args.latency_iters) \
+        if dist.rank == 0 else None
+    sub = {}
+    if not args.no_sub:
+        # every rank runs the sharded sweeps; only rank 0 runs the batch-1 configs
+        sub["c4"] = run_sweep(args, dist, device, "c4", steps=5, warmup=3)
+        sub["c5"] = run_sweep(args, dist, device, "c5", steps=20, warmup=3)
+        if dist.rank == 0:
+            sub["c3"] = run_single(args, dist, device, "c3")
+            sub["c1"] = run_single(args, dist, device, "c1")
+
+    cpu = None
+    if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_throughput_wl(wl, host_cores(), args.cpu_seconds)
+
+    traffic = measured_traffic("tp_tile", wb["total"])
     if dist.rank == 0:
+        bytes_per_launch = wb["total"]
+        achieved = bytes_per_launch / (r["k2_ms"] / 1e3) / 1e9
+        peak = measured_peak()
+        n_sub_launches = sum(v.get("gpu_launches", 0) for v in sub.values())
         line = {
-            "metric": METRIC, "value": round(1e3 / float(np.median(ts)), 2), "unit": UNIT,
-            "n_gpus": 1, "steps": iters, "warmup": 50,
-            "ms_per_step": round(float(np.median(ts)), 4), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u8 in, bf16/fp32 out",
-            "data": "synthetic", "config": {"workload": wl.name + ": " + wl.description},
-            "p50_ms": round(float(np.percentile(ts, 50)), 4),
-            "p99_ms": round(float(np.percentile(ts, 99)), 4),
-            "h2d_p50_ms": round(float(np.percentile(th, 50)), 4),
-            "h2d_p99_ms": round(float(np.percentile(th, 99)), 4),
-            "graph_floor_p50_ms": round(float(np.median(tf)), 4),
-            "h2d_touched_p50_ms": round(t50, 4), "h2d_touched_p99_ms": round(t99, 4),
-            "h2d_touched_bytes": tbytes, "h2d_full_bytes": int(host.data.numel()),
-            "algorithmic_bytes": wb["total"],
+            "metric": METRIC, "value": round(r["value"], 2), "unit": UNIT,
+            "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(r["ms_step"], 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": DTYPE, "data": "synthetic",
+            "config": {**c2_config(wl, r["n"], dist.world), "tiles_per_gpu": r["n_tiles"]},
+            "p50_ms": latency["p50_ms"] if latency else None,
+            "latency": latency,
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak[0],
+                         "unit": "GB/s", "frac": round(achieved / peak[0], 4),
+                         "traffic": traffic, "peak_source": peak[1],
+                         "kernel": "tp_tile (K2)", "kernel_ms": round(r["k2_ms"], 4),
+                         "kernel_timing": "CUDA events around K back-to-back K2 launches, "
+                                          "same stream and inputs, after the timed steps",
+                         "bytes_per_launch": bytes_per_launch,
+                         "bytes_full_image": int(wb["read_full"] + wb["write"]),
+                         "peak_nominal_gbs": 8000.0,
+                         "frac_of_nominal": round(achieved / 8000.0, 4)},
+            "cpu_baseline": cpu,
+            "e2e": r["e2e"],
+            "gpu_launches": 2 * args.steps,
+            "gpu_launches_sub_blocks": n_sub_launches,
+            "clocks": r["clk"],
+            **sub,
         }
-        if not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_latency(wl)
         print(json.dumps(dist.tag(line)), flush=True)
+    dist.close()
 
 
 if __name__ == "__main__":

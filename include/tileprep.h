@@ -196,6 +196,24 @@ TP_API int tp_tile_rows(const uint8_t* d_src, const int64_t* d_src_off, const in
                         int64_t out_capacity, int32_t algo, const int32_t* d_row_map,
                         const int64_t* d_row_map_off, void* stream);
 
+/* Host staging packer (replaces transfer.pack's per-buffer copies, transfer.py:211-233,
+ * for image batches).  Copies n HWC uint8 images from caller memory into one payload
+ * (normally page-locked, then uploaded with one H2D copy), on a persistent pool of
+ * host threads (`threads` <= 0: all of them; tp_host_threads() reports the count).
+ *   src[k], src_stride[k]  image k: wh[k][1] rows of wh[k][0]*channels bytes, row y at
+ *                          src[k] + y * src_stride[k]
+ *   dst + dst_off[k]       image k's block in the payload
+ *   row_map                nullable: image k copies only the rows y with
+ *                          row_map[row_map_off[k] + 1 + y] = i >= 0, to row i of its
+ *                          block (the tp_touched_rows layout read by tp_tile_rows);
+ *                          columns are copied whole.
+ * Host memory only; no CUDA calls. */
+TP_API int32_t tp_host_threads(void);
+TP_API int tp_stage_pack(int32_t n, const uint8_t* const* src, const int64_t* src_stride,
+                         const int32_t* wh, int32_t channels, const int32_t* row_map,
+                         const int64_t* row_map_off, uint8_t* dst, const int64_t* dst_off,
+                         int32_t threads);
+
 /* K2 variant for resize_bilinear / _resize_array (imgproc.py:352-367): one
  * full-frame half-pixel bilinear resize, uint8 HWC -> uint8 HWC. */
 TP_API int tp_resize(const uint8_t* d_src, int32_t width, int32_t height, int32_t channels,

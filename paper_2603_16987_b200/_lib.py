@@ -76,6 +76,9 @@ SIGNATURES = {
     "tp_tile_rows": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_void_p,
                                c_void_p, c_int32, c_void_p, c_int32, c_int32, c_void_p,
                                c_void_p, c_int64, c_int32, c_void_p, c_void_p, c_void_p]),
+    "tp_host_threads": (c_int32, []),
+    "tp_stage_pack": (c_int32, [c_int32, c_void_p, c_void_p, c_void_p, c_int32, c_void_p,
+                                c_void_p, c_void_p, c_void_p, c_int32]),
     "tp_resize": (c_int32, [c_void_p, c_int32, c_int32, c_int32, c_int32, c_int32, c_void_p,
                             c_void_p]),
     "tp_normalize": (c_int32, [c_void_p, c_int64, c_int64, c_int32, c_void_p, c_int32,

@@ -358,14 +358,31 @@ def _touched_dims(m: np.ndarray, h: int) -> tuple:
     return int(m[0]), int(m[h + 1])
 
 
-def stage_images(images: Sequence[np.ndarray], arena: HostArena,
-                 touched: Optional[tuple] = None) -> StagedImages:
-    """Pack HWC uint8 images and their sizes/offsets into one arena region.
+_map_cache: dict = {}
 
-    ``touched=(tile_edge, max_tiles)`` stages only the source rows and columns K2 will
-    read for that tiling (every tile and thumbnail output's two taps per axis; 80% of a
-    1080p image at E=448, 29% of a 4K one) plus the maps K2 reads them through
-    (tp_tile_rows): fewer bytes on the H2D link, the same tiles."""
+
+def staging_map(w: int, h: int, tile_edge: int, max_tiles: int) -> np.ndarray:
+    """The map stage_images(touched=...) stages image (w, h) through: the touched-row
+    map of touched_row_maps, then an identity column map (n_cols = w: columns are
+    staged whole, a column gather saves 3% of a 1080p image for a 3-byte-run copy).
+    Depends only on (w, h, tile_edge, max_tiles), so it is cached (read-only)."""
+    key = (int(w), int(h), int(tile_edge), int(max_tiles))
+    m = _map_cache.get(key)
+    if m is None:
+        rows = touched_row_maps(np.array([[w, h]], dtype=np.int32), tile_edge, max_tiles)[0]
+        m = np.empty(int(h) + int(w) + 2, dtype=np.int32)
+        m[: int(h) + 1] = rows[: int(h) + 1]
+        m[int(h) + 1] = int(w)
+        m[int(h) + 2:] = np.arange(int(w), dtype=np.int32)
+        m.setflags(write=False)
+        if len(_map_cache) > 4096:
+            _map_cache.clear()
+        _map_cache[key] = m
+    return m
+
+
+def _hwc(images: Sequence[np.ndarray]):
+    """(arrays as HWC views, channels, wh int32 [n, 2]) with validation."""
     if not images:
         raise DataError("no images to stage")
     arrs = [a[:, :, None] if a.ndim == 2 else a for a in images]
@@ -374,8 +391,43 @@ def stage_images(images: Sequence[np.ndarray], arena: HostArena,
         if a.dtype != np.uint8 or a.ndim != 3 or a.shape[2] != channels:
             raise DataError("images must be HWC uint8 with a common channel count")
     wh = np.array([[a.shape[1], a.shape[0]] for a in arrs], dtype=np.int32)
+    return arrs, channels, wh
+
+
+def _native_pack(arrs, wh, channels, view: np.ndarray, offs: np.ndarray, maps_all=None,
+                 map_off=None, threads: int = 0) -> None:
+    """Copy every image's pixels (all rows, or only the mapped rows) into ``view`` at
+    ``offs`` with tp_stage_pack (multithreaded host C++; the GIL is released)."""
+    n = len(arrs)
+    keep = []
+    ptrs = np.empty(n, dtype=np.uint64)
+    strides = np.empty(n, dtype=np.int64)
+    for k, a in enumerate(arrs):
+        if a.strides[2] != 1 or a.strides[1] != channels or a.strides[0] < a.shape[1] * channels:
+            a = np.ascontiguousarray(a)
+            keep.append(a)
+        ptrs[k] = a.ctypes.data
+        strides[k] = a.strides[0]
+    base = view.ctypes.data
+    _lib.call("tp_stage_pack", n, ptrs.ctypes.data, strides.ctypes.data, wh.ctypes.data,
+              channels, None if maps_all is None else maps_all.ctypes.data,
+              None if map_off is None else map_off.ctypes.data, base, offs.ctypes.data,
+              int(threads))
+    del keep
+
+
+def stage_images(images: Sequence[np.ndarray], arena: HostArena,
+                 touched: Optional[tuple] = None, threads: int = 0) -> StagedImages:
+    """Pack HWC uint8 images and their sizes/offsets into one arena region.
+
+    The pixels are copied by tp_stage_pack on the library's host thread pool
+    (``threads`` <= 0: all of it).  ``touched=(tile_edge, max_tiles)`` stages only the
+    source rows K2 will read for that tiling (every tile and thumbnail output's two row
+    taps; 83% of a 1080p image at E=448, 41% of a 4K one) plus the maps K2 reads them
+    through (tp_tile_rows): fewer bytes on the H2D link, the same tiles."""
+    arrs, channels, wh = _hwc(images)
     if touched is not None:
-        return _stage_touched(arrs, wh, channels, arena, *touched)
+        return _stage_touched(arrs, wh, channels, arena, *touched, threads=threads)
     wh_at, offsets_at, offs, total = _image_layout(wh, channels)
     if arena.alignment % IMAGE_ALIGNMENT and IMAGE_ALIGNMENT % arena.alignment:
         raise DomainError("arena alignment must divide or be a multiple of 256")
@@ -387,33 +439,40 @@ def stage_images(images: Sequence[np.ndarray], arena: HostArena,
     view[offsets_at: offsets_at + offs.nbytes] = offs.view(np.uint8)
     entries = [BatchEntry(wh_at, wh.nbytes, "int32", wh.shape),
                BatchEntry(offsets_at, offs.nbytes, "int64", offs.shape)]
+    _native_pack(arrs, wh, channels, view, offs, threads=threads)
     for a, off in zip(arrs, offs):
-        flat = np.ascontiguousarray(a).reshape(-1)
-        view[off: off + flat.size] = flat
-        entries.append(BatchEntry(int(off), int(flat.size), "uint8", a.shape))
+        entries.append(BatchEntry(int(off), int(a.size), "uint8", a.shape))
     batch = TransferBatch(payload=view[:total], entries=tuple(entries), copies=((0, total),),
                           slab=arena.tensor, base=region.offset)
     return StagedImages(batch, len(arrs), channels, wh, offs, wh_at, offsets_at)
 
 
-def _stage_touched(arrs, wh, channels, arena, tile_edge: int, max_tiles: int) -> StagedImages:
-    n = len(arrs)
-    maps = touched_row_maps(wh, tile_edge, max_tiles)
+def _touched_layout(wh, channels, tile_edge: int, max_tiles: int):
+    """(maps, map_off, maps_all, offsets_at, map_off_at, map_at, image offsets, total)."""
+    n = len(wh)
+    maps = [staging_map(int(w), int(h), tile_edge, max_tiles) for w, h in wh]
+    sizes = np.fromiter((m.size for m in maps), dtype=np.int64, count=n)
     map_off = np.zeros(n, dtype=np.int64)
     if n > 1:
-        map_off[1:] = np.cumsum([m.size for m in maps])[:-1]
-    maps_all = np.concatenate(maps)
-    wh_at = 0
+        map_off[1:] = np.cumsum(sizes)[:-1]
     offsets_at = _round_up(8 * n, 8)
     map_off_at = offsets_at + 8 * n
     map_at = map_off_at + 8 * n
-    mark = _round_up(map_at + maps_all.nbytes, IMAGE_ALIGNMENT)
+    mark = _round_up(map_at + 4 * int(sizes.sum()), IMAGE_ALIGNMENT)
     offs = np.empty(n, dtype=np.int64)
     for k in range(n):
         offs[k] = mark
-        nr, nc = _touched_dims(maps[k], int(wh[k, 1]))
-        mark = _round_up(mark + nr * nc * channels, IMAGE_ALIGNMENT)
-    total = max(mark, IMAGE_ALIGNMENT)
+        nr = int(maps[k][0])
+        mark = _round_up(mark + nr * int(wh[k, 0]) * channels, IMAGE_ALIGNMENT)
+    return maps, map_off, offsets_at, map_off_at, map_at, offs, max(mark, IMAGE_ALIGNMENT)
+
+
+def _stage_touched(arrs, wh, channels, arena, tile_edge: int, max_tiles: int,
+                   threads: int = 0) -> StagedImages:
+    n = len(arrs)
+    maps, map_off, offsets_at, map_off_at, map_at, offs, total = _touched_layout(
+        wh, channels, tile_edge, max_tiles)
+    wh_at = 0
     if arena.alignment % IMAGE_ALIGNMENT and IMAGE_ALIGNMENT % arena.alignment:
         raise DomainError("arena alignment must divide or be a multiple of 256")
     region = arena.alloc(total)
@@ -423,23 +482,22 @@ def _stage_touched(arrs, wh, channels, arena, tile_edge: int, max_tiles: int) ->
     view[wh_at: wh_at + wh.nbytes] = wh.reshape(-1).view(np.uint8)
     view[offsets_at: offsets_at + offs.nbytes] = offs.view(np.uint8)
     view[map_off_at: map_off_at + map_off.nbytes] = map_off.view(np.uint8)
-    view[map_at: map_at + maps_all.nbytes] = maps_all.view(np.uint8)
+    maps_view = view[map_at: map_at + 4 * int(map_off[-1] + maps[-1].size)].view(np.int32)
+    for m, o in zip(maps, map_off):
+        maps_view[o: o + m.size] = m
     entries = [BatchEntry(wh_at, wh.nbytes, "int32", wh.shape),
                BatchEntry(offsets_at, offs.nbytes, "int64", offs.shape),
                BatchEntry(map_off_at, map_off.nbytes, "int64", map_off.shape),
-               BatchEntry(map_at, maps_all.nbytes, "int32", maps_all.shape)]
+               BatchEntry(map_at, maps_view.nbytes, "int32", maps_view.shape)]
+    _native_pack(arrs, wh, channels, view, offs, maps_view, map_off, threads=threads)
     for a, m, off in zip(arrs, maps, offs):
-        h = a.shape[0]
-        rows = np.nonzero(m[1: h + 1] >= 0)[0]
-        cols = np.nonzero(m[h + 2:] >= 0)[0]
-        block = a[rows][:, cols].reshape(-1)  # source order = compact index order
-        view[off: off + block.size] = block
-        entries.append(BatchEntry(int(off), int(block.size), "uint8",
-                                  (len(rows), len(cols), a.shape[2])))
+        nr = int(m[0])
+        entries.append(BatchEntry(int(off), nr * a.shape[1] * channels, "uint8",
+                                  (nr, a.shape[1], channels)))
     batch = TransferBatch(payload=view[:total], entries=tuple(entries), copies=((0, total),),
                           slab=arena.tensor, base=region.offset)
     return StagedImages(batch, n, channels, wh, offs, wh_at, offsets_at, map_at,
-                        int(maps_all.size), map_off_at, (int(tile_edge), int(max_tiles)))
+                        int(maps_view.size), map_off_at, (int(tile_edge), int(max_tiles)))
 
 
 def upload_images(staged: StagedImages, dest: torch.Tensor,
@@ -467,39 +525,33 @@ _COPY_MODEL = CostModel(latency_per_copy=1e-5, bytes_per_second=5e10)
 
 def staged_bytes(images: Sequence[np.ndarray], touched: Optional[tuple] = None) -> int:
     """Payload bytes ``stage_images`` needs for these images (same ``touched``)."""
-    arrs = [a[:, :, None] if a.ndim == 2 else a for a in images]
-    wh = np.array([[a.shape[1], a.shape[0]] for a in arrs], dtype=np.int32)
-    channels = arrs[0].shape[2]
+    arrs, channels, wh = _hwc(images)
     if touched is None:
         return _image_layout(wh, channels)[3]
-    maps = touched_row_maps(wh, *touched)
-    n = len(arrs)
-    mark = _round_up(_round_up(8 * n, 8) + 16 * n + 4 * sum(m.size for m in maps),
-                     IMAGE_ALIGNMENT)
-    for (_, h), m in zip(wh, maps):
-        nr, nc = _touched_dims(m, int(h))
-        mark = _round_up(mark + nr * nc * channels, IMAGE_ALIGNMENT)
-    return max(mark, IMAGE_ALIGNMENT)
+    return _touched_layout(wh, channels, *touched)[-1]
 
 
 class PipelinedPreprocessor:
     """Host packing + one H2D copy per batch, overlapped with K1+K2 of the previous
     batch.
 
-    ``depth`` pinned slabs and device slabs rotate: while the compute stream runs
-    K1+K2 on batch i, the host packs batch i+1 into the next pinned slab and the copy
-    stream moves it to the next device slab; the compute stream waits only on that
-    batch's copy event.  A pinned slab is reused after its copy has completed, a
-    device slab after the K2 that read it has completed.  ``touched`` stages only the
-    source rows the preprocessor's tiling reads (stage_images(touched=...))."""
+    ``depth`` pinned slabs and device slabs rotate: while the copy engine uploads batch
+    i and the compute stream runs K1+K2 on it, the library's host thread pool
+    (tp_stage_pack, the GIL released) packs batch i+1 into the next pinned slab; the
+    compute stream waits only on that batch's copy event.  A pinned slab is reused
+    after its copy has completed, a device slab after the K2 that read it has
+    completed.  ``touched`` stages only the source rows the preprocessor's tiling reads
+    (stage_images(touched=...)).  ``threads``: host packing threads (<= 0: all)."""
 
-    def __init__(self, prep, slab_bytes: int, depth: int = 2, touched: bool = False):
+    def __init__(self, prep, slab_bytes: int, depth: int = 2, touched: bool = False,
+                 threads: int = 0):
         if depth < 2:
             raise DomainError("depth must be >= 2 for overlap")
         self.prep = prep
         self.touched = (prep.cfg.tile_edge, prep.cfg.max_tiles) if touched else None
         self.device = prep.device
         self.depth = depth
+        self.threads = int(threads)
         self.slab_bytes = _round_up(int(slab_bytes), IMAGE_ALIGNMENT)
         self.host = [HostArena(self.slab_bytes, IMAGE_ALIGNMENT, pin=True) for _ in range(depth)]
         self.dev = [torch.empty(self.slab_bytes, dtype=torch.uint8, device=self.device)
@@ -508,29 +560,36 @@ class PipelinedPreprocessor:
         self.compute_stream = torch.cuda.Stream(self.device)
         self._copied: list = [None] * depth  # event: copy from host slab k finished
         self._consumed: list = [None] * depth  # event: K2 reading device slab k finished
+        self._i = 0
+        self.last_bytes = 0  # payload bytes of the last submitted batch
+
+    def submit(self, images: Sequence[np.ndarray], capacity: Optional[int] = None, out=None):
+        """Pack ``images`` (HWC uint8 host arrays), upload them and enqueue K1+K2;
+        returns the TileBatch (``out`` when given: reused buffers; its previous contents
+        must no longer be needed).  Returns once the batch is packed and enqueued."""
+        k = self._i % self.depth
+        self._i += 1
+        if self._copied[k] is not None:
+            self._copied[k].synchronize()  # host slab k free again
+        self.host[k].reset()
+        staged = stage_images(images, self.host[k], touched=self.touched, threads=self.threads)
+        self.last_bytes = len(staged.batch.payload)
+        if self._consumed[k] is not None:
+            self.copy_stream.wait_event(self._consumed[k])  # device slab k free again
+        packed, copied = upload_images(staged, self.dev[k], self.copy_stream)
+        self._copied[k] = copied
+        self.compute_stream.wait_event(copied)
+        with torch.cuda.stream(self.compute_stream):  # outputs belong to this stream
+            res = self.prep(packed, capacity=capacity, out=out, stream=self.compute_stream)
+        done = torch.cuda.Event()
+        done.record(self.compute_stream)
+        self._consumed[k] = done
+        return res
 
     def run(self, batches: Iterable[Sequence[np.ndarray]], capacity: Optional[int] = None):
         """Preprocess each batch; returns one TileBatch per batch (device tensors, all
         work enqueued on the compute stream; synchronise or wait on it before use)."""
-        outs = []
-        for i, images in enumerate(batches):
-            k = i % self.depth
-            if self._copied[k] is not None:
-                self._copied[k].synchronize()  # host slab k free again
-            self.host[k].reset()
-            staged = stage_images(images, self.host[k], touched=self.touched)
-            if self._consumed[k] is not None:
-                self.copy_stream.wait_event(self._consumed[k])  # device slab k free again
-            packed, copied = upload_images(staged, self.dev[k], self.copy_stream)
-            self._copied[k] = copied
-            self.compute_stream.wait_event(copied)
-            with torch.cuda.stream(self.compute_stream):  # outputs belong to this stream
-                out = self.prep(packed, capacity=capacity, stream=self.compute_stream)
-            done = torch.cuda.Event()
-            done.record(self.compute_stream)
-            self._consumed[k] = done
-            outs.append(out)
-        return outs
+        return [self.submit(images, capacity=capacity) for images in batches]
 
     def synchronize(self) -> None:
         self.compute_stream.synchronize()

@@ -117,7 +117,38 @@ def test_bench_cpu_baselines_on_a_tiny_workload():
     wl = Workload("T", "tiny", np.array([[96, 64], [64, 96]], np.int32), 32, 6,
                   IMAGENET_MEAN, IMAGENET_STD, True, 7)
     lat = bench.cpu_latency(wl, runs=2)
-    assert lat["cores"] == 1 and lat["kind"] == "port" and lat["value"] > 0
+    assert lat["cores"] == 1 and lat["kind"] in ("port", "reference") and lat["value"] > 0
     assert lat["p99_ms"] >= lat["p50_ms"] > 0
     thr = bench.cpu_throughput_wl(wl, 2, 0.01, c5_texts(2, 7))
     assert thr["cores"] == 2 and thr["value"] > 0 and "prompts" in thr["sample"]
+
+
+def test_bench_gpus_flag_spawns_ranks_under_torchrun():
+    """`bench.py --gpus 2` outside torchrun re-launches itself under torch.distributed.run
+    with 2 ranks (the reference arm needs no GPU): rank 0 prints the one JSON line with
+    n_gpus 2, rank 1 exits 0 without work."""
+    import json
+    import subprocess
+
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    out = subprocess.run([sys.executable, str(REPO / "bench.py"), "--impl", "reference",
+                          "--gpus", "2", "--steps", "1", "--warmup", "1", "--batch", "2"],
+                         capture_output=True, text=True, env=env, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [json.loads(x) for x in out.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1
+    assert lines[0]["impl"] == "reference" and lines[0]["n_gpus"] == 2
+    assert lines[0]["config"]["images_per_gpu"] == 2 and lines[0]["value"] > 0
+
+
+def test_bench_rejects_world_size_mismatch(monkeypatch):
+    sys.path.insert(0, str(REPO))
+    import bench
+
+    monkeypatch.setenv("WORLD_SIZE", "2")
+    args = bench.parse_args(["--gpus", "4"])
+    with pytest.raises(SystemExit, match="WORLD_SIZE"):
+        bench.maybe_spawn(args, ["--gpus", "4"])
+    monkeypatch.delenv("WORLD_SIZE")
+    assert bench.maybe_spawn(bench.parse_args([]), []) is None
