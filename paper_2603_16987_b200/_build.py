@@ -20,6 +20,7 @@ CSRC = PKG_DIR / "csrc"
 INCLUDE = REPO_ROOT / "include"
 BUILD_DIR = REPO_ROOT / "build" / "tileprep"
 LIB_PATH = PKG_DIR / "libtileprep.so"
+CHECKS_LIB_PATH = REPO_ROOT / "build" / "variants" / "checks" / "libtileprep.so"
 
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = [

@@ -54,6 +54,25 @@ namespace {
 #ifndef TP_K2_DEBUG_NOLOAD
 #define TP_K2_DEBUG_NOLOAD 0
 #endif
+// Bounds-checked build (the stand-in for compute-sanitizer, which this pool does not
+// run): every bulk copy's source and destination, every consumer tap read and every
+// output store is checked against its buffer; a violation sets a bit in g_tp_checks
+// (read with tp_debug_checks) instead of touching memory.  tools/build_variants.py
+// builds it with -DTP_CHECKS=1; tests/test_gpu_checks.py runs the stress cases on it.
+#ifndef TP_CHECKS
+#define TP_CHECKS 0
+#endif
+#if TP_CHECKS
+__device__ unsigned int g_tp_checks;
+#define TP_CHECK(cond, bit)                                   \
+  do {                                                        \
+    if (!(cond)) atomicOr(&g_tp_checks, 1u << (bit));          \
+  } while (0)
+#else
+#define TP_CHECK(cond, bit) \
+  do {                      \
+  } while (0)
+#endif
 // loads of predecessor-written data: 1 = ld.global.cg (L2), 2 = ld.global.ca (L1+L2);
 // never the .nc path that plain loads through const __restrict__ pointers compile to
 #ifndef TP_K2_LDMODE
@@ -646,6 +665,9 @@ __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restri
         uint8_t* base = arena + s * ARENA;
         const uintptr_t start = gs - delta;
         uint32_t bytes = staged ? static_cast<uint32_t>((delta + rb + 15) & ~15) : 0u;
+        TP_CHECK(!staged || (incl - region >= 0 && incl <= ARENA), 0);
+        TP_CHECK(!staged || (start >= reinterpret_cast<uintptr_t>(img) - 15 &&
+                             gs + rb <= img_end), 1);
         if (staged && start + bytes > img_end) {
           const uint32_t body = static_cast<uint32_t>((img_end - start) & ~uintptr_t(15));
           uint8_t* dst = base + (incl - region);
@@ -653,12 +675,15 @@ __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restri
             dst[b] = reinterpret_cast<const uint8_t*>(start)[b];
           bytes = body;
         }
+        TP_CHECK(bytes == 0 || (start + bytes <= img_end &&
+                                (incl - region) + static_cast<int>(bytes) <= ARENA), 2);
 #if TP_K2_DEBUG_NOLOAD  // timing experiment only: consumers on whatever the stage holds
         bytes = 0;
 #endif
         int tx = static_cast<int>(bytes);
 #pragma unroll
         for (int d = 16; d > 0; d >>= 1) tx += __shfl_xor_sync(0xffffffffu, tx, d);
+        TP_CHECK(g >= 0 && g < cap_tiles && j0 + jj + nr <= E, 6);
         if (lane == 0) {
           ph.g = g;
           ph.j0 = j0 + jj;
@@ -689,6 +714,7 @@ __device__ void produce(SmemHeader& hdr, uint8_t* arena, const uint8_t* __restri
         if (bytes > 0)
           tma_row(base + (incl - region), reinterpret_cast<const void*>(start), bytes,
                   &hdr.full[s], policy);
+        TP_CHECK(nr >= 1 && nr <= 32 && jj + nr <= nrows, 3);
         jj += nr;
         if (++stage == kStages) {
           stage = 0;
@@ -789,9 +815,19 @@ struct PhaseRows {
 
 template <bool UNIFORM>
 __device__ __forceinline__ PixTaps fetch_pix(const PhaseRows& pr, int jj, uint32_t sbase, int mis,
-                                             int xo, uint32_t wo, uint32_t sh) {
+                                             int xo, uint32_t wo, uint32_t sh,
+                                             uint32_t arena_limit = 0) {
   PixTaps t;
   const uint32_t o0 = lds32(pr.base + kPhOff0 + 4 * jj), o1 = lds32(pr.base + kPhOff1 + 4 * jj);
+#if TP_CHECKS
+  {
+    const uint32_t lo0 = UNIFORM ? o0 - mis + wo : ((o0 + xo) & ~3u);
+    const uint32_t lo1 = UNIFORM ? o1 - mis + wo : ((o1 + xo) & ~3u);
+    TP_CHECK(arena_limit == 0 || (lo0 + 12 <= arena_limit && lo1 + 12 <= arena_limit), 4);
+  }
+#else
+  (void)arena_limit;
+#endif
   if (UNIFORM) {
     const uint32_t r0 = sbase + o0 - mis + wo, r1 = sbase + o1 - mis + wo;
     uint32_t w0 = lds32(r0), w1 = lds32(r0 + 4), w2 = lds32(r0 + 8);
@@ -924,6 +960,7 @@ __device__ __forceinline__ void consume_pair_rows(
   // LUT + stores of row jj (rows in order: the NCHW row pointers advance by one row)
   auto emit = [&](int jj, const uint32_t (&ka)[C], const uint32_t (&kb)[C]) {
     const int j = j0 + jj;
+    TP_CHECK(j >= 0 && j < E && ia >= 0 && (!has_a || ia < E) && (!has_b || ib < E), 5);
     const int64_t rowpix = static_cast<int64_t>(g) * EE + static_cast<int64_t>(j) * E;
     if (WRITE_U8) {
       uint8_t* ua = out_u8 + (rowpix + ia) * C;
@@ -979,17 +1016,18 @@ __device__ __forceinline__ void consume_pair_rows(
     if (fast(jj, a, b, ka, kb, xa, xb)) fix(jj, a, b, ka, kb, xa, xb);
     emit(jj, ka, kb);
   };
+  constexpr uint32_t kLim = TP_CHECKS ? static_cast<uint32_t>(arena_bytes<C, OutT>()) : 0u;
   // software pipeline, unrolled by two so the prefetched taps need no register moves
-  PixTaps a0 = fetch_pix<UNIFORM>(pr, 0, sbase, mis, xoa, wa, sha);
-  PixTaps b0 = fetch_pix<UNIFORM>(pr, 0, sbase, mis, xob, wb, shb);
+  PixTaps a0 = fetch_pix<UNIFORM>(pr, 0, sbase, mis, xoa, wa, sha, kLim);
+  PixTaps b0 = fetch_pix<UNIFORM>(pr, 0, sbase, mis, xob, wb, shb, kLim);
   int jj = 0;
   for (; jj + 1 < nrows; jj += 2) {
-    const PixTaps a1 = fetch_pix<UNIFORM>(pr, jj + 1, sbase, mis, xoa, wa, sha);
-    const PixTaps b1 = fetch_pix<UNIFORM>(pr, jj + 1, sbase, mis, xob, wb, shb);
+    const PixTaps a1 = fetch_pix<UNIFORM>(pr, jj + 1, sbase, mis, xoa, wa, sha, kLim);
+    const PixTaps b1 = fetch_pix<UNIFORM>(pr, jj + 1, sbase, mis, xob, wb, shb, kLim);
     row(jj, a0, b0);
     if (jj + 2 < nrows) {
-      a0 = fetch_pix<UNIFORM>(pr, jj + 2, sbase, mis, xoa, wa, sha);
-      b0 = fetch_pix<UNIFORM>(pr, jj + 2, sbase, mis, xob, wb, shb);
+      a0 = fetch_pix<UNIFORM>(pr, jj + 2, sbase, mis, xoa, wa, sha, kLim);
+      b0 = fetch_pix<UNIFORM>(pr, jj + 2, sbase, mis, xob, wb, shb, kLim);
     }
     row(jj + 1, a1, b1);
   }
@@ -1303,6 +1341,22 @@ TP_INSTANTIATE(3, __nv_bfloat16, TP_LAYOUT_NHWC, true)
 #undef TP_INSTANTIATE
 
 }  // namespace tp
+
+#if TP_CHECKS
+// bounds-checked builds only (not part of include/tileprep.h): the violation bits of
+// every K2 launch since the last reset (bit 0/2: bulk copy outside the stage, 1: copy
+// source outside the image, 3: phase rows, 4: consumer tap read outside the stage,
+// 5: store outside the tile, 6: tile index / row outside the output)
+extern "C" __attribute__((visibility("default"))) int tp_debug_checks(int reset) {
+  unsigned int v = 0;
+  if (cudaMemcpyFromSymbol(&v, tp::g_tp_checks, sizeof(v)) != cudaSuccess) return -1;
+  if (reset) {
+    const unsigned int z = 0;
+    if (cudaMemcpyToSymbol(tp::g_tp_checks, &z, sizeof(z)) != cudaSuccess) return -1;
+  }
+  return static_cast<int>(v);
+}
+#endif
 
 #if TP_K2_TRACE
 // diagnostic export (trace builds only; not part of include/tileprep.h)

@@ -79,8 +79,13 @@ def main(rounds: int):
         stats["images"] += n
         stats["tiles"] += int(fast.plans.tile_off[-1])
     stats["seconds"] = round(time.time() - t0, 1)
+    from paper_2603_16987_b200 import _lib
+
+    lib = _lib.load()
+    if hasattr(lib, "tp_debug_checks"):  # bounds-checked build (TP_CHECKS=1)
+        stats["check_bits"] = int(lib.tp_debug_checks(1))
     print(json.dumps(stats))
-    return 0 if not stats["failures"] else 1
+    return 0 if not stats["failures"] and not stats.get("check_bits") else 1
 
 
 if __name__ == "__main__":
