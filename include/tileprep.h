@@ -214,6 +214,50 @@ TP_API int tp_stage_pack(int32_t n, const uint8_t* const* src, const int64_t* sr
                          const int64_t* row_map_off, uint8_t* dst, const int64_t* dst_off,
                          int32_t threads);
 
+/* K7 — device JPEG decode (replaces the PIL decode of
+ * decode_image / _decode_pass, imgproc.py:213-260, for baseline JPEGs).  Bit-exact with
+ * Pillow's libjpeg-turbo (JDCT_ISLOW, fancy upsampling, jdcolor.c YCbCr->RGB).
+ * Host side:
+ *   tp_jpeg_parse     markers up to SOS of one payload (host memory); info->status says
+ *                     whether the device decoder takes it (baseline Huffman 8-bit, 1 or 3
+ *                     components, Y sampling 1x1 / 2x1 / 2x2 with 1x1 chroma, JFIF /
+ *                     YCbCr, one interleaved scan, restart markers allowed).  Anything else
+ *                     (progressive, arithmetic, 12-bit, CMYK, 4:4:0, ...) is
+ *                     TP_JPEG_UNSUPPORTED: decode it on the host, as the reference does.
+ *   tp_jpeg_describe  per-image device descriptors (tp_jpeg_desc_bytes() each) for a
+ *                     batch: image k's entropy-coded bytes sit at raw_off[k] of the payload
+ *                     (4-byte aligned), its RGB HWC output at out_off[k] of d_out; returns
+ *                     the workspace bytes tp_jpeg_decode needs (< 0: error code)
+ * Device side:
+ *   tp_jpeg_decode    unstuff -> parallel Huffman decode (self-synchronizing
+ *                     subsequences of sub_bits bits) -> DC prediction -> ISLOW IDCT ->
+ *                     fancy upsampling + colour conversion into d_out.  d_status[k] = 0,
+ *                     or nonzero when image k's entropy data is not a clean baseline
+ *                     stream (corrupt / truncated): decode that one on the host. */
+#define TP_JPEG_OK 0
+#define TP_JPEG_UNSUPPORTED 1
+#define TP_JPEG_CORRUPT 2
+typedef struct {
+  int32_t status;
+  int32_t width, height, ncomp;
+  int32_t comp_id[3], comp_h[3], comp_v[3], comp_tq[3], comp_td[3], comp_ta[3];
+  int32_t restart_interval;
+  int32_t qt_mask, dc_mask, ac_mask;
+  int64_t scan_off, scan_len; /* entropy-coded bytes: payload[scan_off, scan_off + scan_len) */
+  uint16_t qt[4][64];         /* natural order */
+  uint8_t dc_bits[2][16], dc_vals[2][256], ac_bits[2][16], ac_vals[2][256];
+  char message[96];
+} TpJpegInfo;
+TP_API int tp_jpeg_parse(const uint8_t* data, int64_t len, TpJpegInfo* info);
+TP_API int64_t tp_jpeg_desc_bytes(void);
+TP_API int64_t tp_jpeg_describe(const TpJpegInfo* infos, int32_t n, const int64_t* raw_off,
+                                const int64_t* out_off, int32_t sub_bits, void* desc,
+                                int64_t* totals /* [5]: slots, blocks, rows, zeroed range */);
+TP_API int tp_jpeg_decode(const uint8_t* d_payload, const void* d_desc, int32_t n,
+                          const int64_t* totals, int32_t sub_bits, void* d_work,
+                          int64_t work_bytes, uint8_t* d_out, int32_t* d_status,
+                          void* stream);
+
 /* K2 variant for resize_bilinear / _resize_array (imgproc.py:352-367): one
  * full-frame half-pixel bilinear resize, uint8 HWC -> uint8 HWC. */
 TP_API int tp_resize(const uint8_t* d_src, int32_t width, int32_t height, int32_t channels,

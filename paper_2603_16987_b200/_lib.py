@@ -79,6 +79,12 @@ SIGNATURES = {
     "tp_host_threads": (c_int32, []),
     "tp_stage_pack": (c_int32, [c_int32, c_void_p, c_void_p, c_void_p, c_int32, c_void_p,
                                 c_void_p, c_void_p, c_void_p, c_int32]),
+    "tp_jpeg_parse": (c_int32, [c_void_p, c_int64, c_void_p]),
+    "tp_jpeg_desc_bytes": (c_int64, []),
+    "tp_jpeg_describe": (c_int64, [c_void_p, c_int32, c_void_p, c_void_p, c_int32, c_void_p,
+                                   c_void_p]),
+    "tp_jpeg_decode": (c_int32, [c_void_p, c_void_p, c_int32, c_void_p, c_int32, c_void_p,
+                                 c_int64, c_void_p, c_void_p, c_void_p]),
     "tp_resize": (c_int32, [c_void_p, c_int32, c_int32, c_int32, c_int32, c_int32, c_void_p,
                             c_void_p]),
     "tp_normalize": (c_int32, [c_void_p, c_int64, c_int64, c_int32, c_void_p, c_int32,
