@@ -280,20 +280,25 @@ __device__ DecOut decode_run(const JDesc& d, BitReader& br, uint32_t bit0, uint3
       s = sym & 15;
     }
     const uint32_t used = static_cast<uint32_t>(len + s);
-    bool unclean = len == 0 || pos + used > seg_bits || (z != 0 && s != 0 && z + r > 63);
-    if (unclean) {
-      if (MODE == 0) {
-        ++pos;
-        u = 0;
-        z = 0;
-        c = d.slot_comp[0];
-        dct = &d.dc[d.comp_td[c]];
-        act = &d.ac[d.comp_ta[c]];
-        continue;
+    const bool ran_out = len != 0 && pos + used > seg_bits;
+    if (len == 0 || ran_out || (z != 0 && s != 0 && z + r > 63)) {
+      // An unclean symbol.  From a true entry it means a corrupt stream -- or the padding
+      // after the interval's last block (harmless: phase 3 compares the block count at
+      // the first unclean symbol with the interval's block total).  Either way the
+      // decode resynchronises like a speculative one: an entry that is still wrong
+      // (its predecessor not yet converged) must be able to fall into the true path.
+      if (MODE != 0 && o.err == kNoErr) o.err = o.blocks;
+      if (MODE == 2 || ran_out) {
+        pos = seg_bits;
+        break;
       }
-      if (o.err == kNoErr) o.err = o.blocks;
-      pos = seg_bits;  // nothing after this point is decodable: successors start at the end
-      break;
+      ++pos;
+      u = 0;
+      z = 0;
+      c = d.slot_comp[0];
+      dct = &d.dc[d.comp_td[c]];
+      act = &d.ac[d.comp_ta[c]];
+      continue;
     }
     if (z == 0) {
       if (MODE == 2) coef[static_cast<int64_t>(block) * 64] =
@@ -437,6 +442,7 @@ __global__ void __launch_bounds__(256) k_jpeg_huff(const JDesc* __restrict__ des
     if (h >= 3 && W.counters[h] == 0 && W.counters[h - 1] == 0) break;
   }
   const bool converged = h < kMaxSteps;
+  if (tid == 0) W.counters[1023] = h;  // diagnostics: half-rounds used
 
   // (3) per interval: first block of every subsequence; unclean streams go to the host
   const int lane = threadIdx.x & 31;
