@@ -13,11 +13,11 @@
 //                      (2) rounds: subsequence j re-decodes from subsequence j-1's exit
 //                          state (bit position, block slot in the MCU, zigzag index) until
 //                          no exit changes -- typically two rounds;
-//                      (3) per interval, a scan of the blocks each subsequence completes
-//                          gives its first block index;
-//                      (4) every subsequence decodes once more, writing its coefficients;
-//                      (5) DC prediction: per interval and component, a warp scan of the
-//                          DC differences (int16 like libjpeg's JCOEF)
+//                      (3) per interval, scans of the blocks and of the per-component DC
+//                          difference sums each subsequence decodes give its first block
+//                          index and its entry DC predictors;
+//                      (4) every subsequence decodes once more, writing its coefficients
+//                          with DC values predicted in place (int16, libjpeg's JCOEF)
 //   J3 k_jpeg_idct     jidctint.c jpeg_idct_islow, 8 threads per block, 64-bit JLONG
 //                      arithmetic as libjpeg's on LP64, the jdmaster.c range-limit table
 //   J4 k_jpeg_color    jdsample.c fancy upsampling (h2v1 / h2v2, edge replication of
@@ -48,15 +48,22 @@ __constant__ uint8_t c_zig[64] = {0,  1,  8,  16, 9,  2,  3,  10, 17, 24, 32, 25
 
 constexpr int kMaxSteps = 160;  // sync half-rounds before an image is handed to the host
 constexpr int kNoErr = 0x7FFFFFFF;
+constexpr int kCkpts = 7;  // checkpoints per subsequence (every sub_bits / 8 bits)
 
 struct Work {
-  unsigned* counters;  // [h]: exits changed in half-round h
+  unsigned* counters;  // [h]: exits changed in half-round h; [1023]: half-rounds used
+  unsigned long long* stamps;  // [8] phase timestamps (globaltimer), diagnostics
   long long* exitp;    // per slot: (bit << 16) | (u << 8) | z, bit relative to the interval
+  int4* dcs;           // per slot: DC difference sums per component (.y .z .w), then
+                       // (phase 3) the interval's running DC of each component at the entry
   int* blocks;         // blocks completed from the (last) entry to the exit
   int* err;            // block count at the first unclean symbol, kNoErr if none
+  int* errpos;         // its bit position
   int* bstart;         // block index (in the image) at the entry
   int* lastproc;       // half-round this slot last decoded in
   int* changed;        // half-round its exit last changed in
+  long long* ck_state; // [slot][kCkpts] checkpoint states
+  int4* ck_acc;        // [slot][kCkpts] checkpoint accumulators
 };
 
 __host__ __device__ inline int64_t al256(int64_t v) { return (v + 255) & ~int64_t(255); }
@@ -64,20 +71,33 @@ __host__ __device__ inline int64_t al256(int64_t v) { return (v + 255) & ~int64_
 __device__ inline Work work_view(uint8_t* w, int64_t slots) {
   Work v;
   v.counters = reinterpret_cast<unsigned*>(w);
+  v.stamps = reinterpret_cast<unsigned long long*>(w + 3968);
   int64_t o = 4096;
   v.exitp = reinterpret_cast<long long*>(w + o);
   o += al256(8 * slots);
-  int* arrs[5];
-  for (int i = 0; i < 5; ++i) {
+  v.dcs = reinterpret_cast<int4*>(w + o);
+  o += al256(16 * slots);
+  int* arrs[6];
+  for (int i = 0; i < 6; ++i) {
     arrs[i] = reinterpret_cast<int*>(w + o);
     o += al256(4 * slots);
   }
   v.blocks = arrs[0];
   v.err = arrs[1];
-  v.bstart = arrs[2];
-  v.lastproc = arrs[3];
-  v.changed = arrs[4];
+  v.errpos = arrs[2];
+  v.bstart = arrs[3];
+  v.lastproc = arrs[4];
+  v.changed = arrs[5];
+  v.ck_state = reinterpret_cast<long long*>(w + o);
+  o += al256(8 * kCkpts * slots);
+  v.ck_acc = reinterpret_cast<int4*>(w + o);
   return v;
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
 }
 
 __device__ inline int find_image(const JDesc* d, int n, int64_t g, int which) {
@@ -252,25 +272,112 @@ __device__ __forceinline__ int extend(uint32_t bits, int s) {
 struct DecOut {
   uint32_t pos;
   int u, z, blocks, err;
+  int dc[jpeg::kMaxComps];  // sum of the DC differences decoded, per component
 };
 
+// The per-image fields the symbol loop needs, in registers: per block slot of the MCU its
+// component, and per component its DC / AC tables.
+struct Tabs {
+  const JHuff *dc0, *dc1, *dc2, *ac0, *ac1, *ac2;  // per component (selects, no local memory)
+  uint32_t slot_comp;  // 2 bits per block slot
+  int bmcu;
+  __device__ void load(const JDesc& d) {
+    bmcu = d.bmcu;
+    slot_comp = 0;
+    for (int u = 0; u < d.bmcu; ++u) slot_comp |= static_cast<uint32_t>(d.slot_comp[u]) << (2 * u);
+    dc0 = &d.dc[d.comp_td[0]];
+    ac0 = &d.ac[d.comp_ta[0]];
+    dc1 = d.ncomp > 1 ? &d.dc[d.comp_td[1]] : dc0;
+    ac1 = d.ncomp > 1 ? &d.ac[d.comp_ta[1]] : ac0;
+    dc2 = d.ncomp > 2 ? &d.dc[d.comp_td[2]] : dc0;
+    ac2 = d.ncomp > 2 ? &d.ac[d.comp_ta[2]] : ac0;
+  }
+  __device__ __forceinline__ int comp(int u) const { return (slot_comp >> (2 * u)) & 3; }
+  __device__ __forceinline__ const JHuff* dct(int c) const { return c == 0 ? dc0 : c == 1 ? dc1 : dc2; }
+  __device__ __forceinline__ const JHuff* act(int c) const { return c == 0 ? ac0 : c == 1 ? ac1 : ac2; }
+};
+
+
+// Checkpoints of one subsequence: the decoder's state at the first symbol boundary at or
+// after each checkpoint position, with the blocks and DC sums accumulated from the entry
+// to there.  A later decode of the same subsequence from another entry that reaches a
+// checkpoint in the recorded state has rejoined the recorded path: everything after it is
+// known, so the decode stops there (a re-decode usually costs a few hundred bits, not
+// sub_bits).
+struct Ckpt {
+  long long* state;  // [kCkpts], -1 = not recorded
+  int4* acc;         // [kCkpts] (blocks, dc0, dc1, dc2) from the entry
+  uint32_t first, step;
+  bool compare;      // a previous decode of this subsequence exists (its totals below)
+  long long prev_exit;
+  int prev_blocks, prev_err;
+  uint32_t prev_errpos;
+  int4 prev_dc;
+};
+
+__device__ __forceinline__ long long pack_state(uint32_t pos, int u, int z) {
+  return (static_cast<long long>(pos) << 16) | (u << 8) | z;
+}
+
 // Decode from (pos, u, z) until the position reaches `stop` at a symbol boundary.
-// MODE 0: speculative (entry guessed: an unclean symbol skips one bit and restarts the
-// state); 1: true entry, counting; 2: true entry, writing coefficients from block
-// `block` on, stopping at `block_limit`.  pos, stop and seg_bits are bits from the
-// interval start; bit0 is the interval's first bit in the image's clean stream.
-template <int MODE>
-__device__ DecOut decode_run(const JDesc& d, BitReader& br, uint32_t bit0, uint32_t seg_bits,
+// MODE 0: speculative (entry guessed); 1: true entry, counting; 2: true entry, writing
+// coefficients from block `block` on (stopping at `block_limit`), DC values predicted
+// from `pred` (the interval's running DC of each component at this entry).  pos, stop
+// and seg_bits are bits from the interval start; bit0 is the interval's first bit in
+// the image's clean stream.  CK: record / compare checkpoints (MODE 0 and 1).
+template <int MODE, bool CK>
+__device__ DecOut decode_run(const Tabs& T, BitReader& br, uint32_t bit0, uint32_t seg_bits,
                              uint32_t stop, uint32_t pos, int u, int z, int16_t* coef, int block,
-                             int block_limit) {
+                             int block_limit, const int* pred_in, const Ckpt* ck = nullptr,
+                             uint32_t* errpos = nullptr) {
   DecOut o;
   o.blocks = 0;
   o.err = kNoErr;
-  int c = d.slot_comp[u];
-  const JHuff* dct = &d.dc[d.comp_td[c]];
-  const JHuff* act = &d.ac[d.comp_ta[c]];
+  uint32_t epos = 0xFFFFFFFFu;
+  // running DC per component: the predictors (MODE 2) or the sums of differences
+  int p0 = MODE == 2 ? pred_in[0] : 0, p1 = MODE == 2 ? pred_in[1] : 0,
+      p2 = MODE == 2 ? pred_in[2] : 0;
+  int c = T.comp(u);
+  const JHuff* dct = T.dct(c);
+  const JHuff* act = T.act(c);
+  int ci = 0;
+  uint32_t next_cp = CK ? ck->first : 0xFFFFFFFFu;
   if (MODE == 2 && block >= block_limit) stop = pos;
   while (pos < stop) {
+    if (CK && pos >= next_cp) {
+      const long long st = pack_state(pos, u, z);
+      if (ck->compare && ck->state[ci] == st) {  // rejoined the recorded path
+        const int4 a = ck->acc[ci];
+        const int4 now = make_int4(o.blocks, p0, p1, p2);
+        if (o.err == kNoErr && ck->prev_err != kNoErr && ck->prev_errpos >= pos) {
+          o.err = ck->prev_err - a.x + o.blocks;
+          epos = ck->prev_errpos;
+        }
+        o.blocks += ck->prev_blocks - a.x;
+        p0 += ck->prev_dc.y - a.y;
+        p1 += ck->prev_dc.z - a.z;
+        p2 += ck->prev_dc.w - a.w;
+        // later checkpoints hold accumulators of the recorded decode: rebase them
+        for (int i = ci; i < kCkpts; ++i) {
+          if (ck->state[i] < 0) break;
+          const int4 b = ck->acc[i];
+          ck->acc[i] = make_int4(b.x - a.x + now.x, b.y - a.y + now.y, b.z - a.z + now.z,
+                                 b.w - a.w + now.w);
+        }
+        o.pos = static_cast<uint32_t>(ck->prev_exit >> 16);
+        o.u = static_cast<int>((ck->prev_exit >> 8) & 255);
+        o.z = static_cast<int>(ck->prev_exit & 255);
+        o.dc[0] = p0;
+        o.dc[1] = p1;
+        o.dc[2] = p2;
+        if (errpos) *errpos = epos;
+        return o;
+      }
+      ck->state[ci] = st;
+      ck->acc[ci] = make_int4(o.blocks, p0, p1, p2);
+      ++ci;
+      next_cp = ci < kCkpts ? ck->first + ci * ck->step : 0xFFFFFFFFu;
+    }
     const uint32_t v = br.peek(bit0 + pos);
     int sym;
     const int len = huff_decode(z == 0 ? dct : act, v, sym);
@@ -287,7 +394,10 @@ __device__ DecOut decode_run(const JDesc& d, BitReader& br, uint32_t bit0, uint3
       // the first unclean symbol with the interval's block total).  Either way the
       // decode resynchronises like a speculative one: an entry that is still wrong
       // (its predecessor not yet converged) must be able to fall into the true path.
-      if (MODE != 0 && o.err == kNoErr) o.err = o.blocks;
+      if (MODE != 0 && o.err == kNoErr) {
+        o.err = o.blocks;
+        epos = pos;
+      }
       if (MODE == 2 || ran_out) {
         pos = seg_bits;
         break;
@@ -295,14 +405,17 @@ __device__ DecOut decode_run(const JDesc& d, BitReader& br, uint32_t bit0, uint3
       ++pos;
       u = 0;
       z = 0;
-      c = d.slot_comp[0];
-      dct = &d.dc[d.comp_td[c]];
-      act = &d.ac[d.comp_ta[c]];
+      c = T.comp(0);
+      dct = T.dct(c);
+      act = T.act(c);
       continue;
     }
     if (z == 0) {
-      if (MODE == 2) coef[static_cast<int64_t>(block) * 64] =
-          static_cast<int16_t>(s ? extend((v << len) >> (32 - s), s) : 0);
+      const int diff = s ? extend((v << len) >> (32 - s), s) : 0;
+      // libjpeg: last_dc_val[ci] += diff (int), the block keeps (JCOEF) last_dc_val
+      if (c == 0) p0 += diff; else if (c == 1) p1 += diff; else p2 += diff;
+      if (MODE == 2)
+        coef[static_cast<int64_t>(block) * 64] = static_cast<int16_t>(c == 0 ? p0 : c == 1 ? p1 : p2);
       z = 1;
     } else if (s) {
       z += r;
@@ -318,21 +431,23 @@ __device__ DecOut decode_run(const JDesc& d, BitReader& br, uint32_t bit0, uint3
     if (z >= 64) {
       z = 0;
       ++o.blocks;
-      u = u + 1 == d.bmcu ? 0 : u + 1;
-      c = d.slot_comp[u];
-      dct = &d.dc[d.comp_td[c]];
-      act = &d.ac[d.comp_ta[c]];
+      u = u + 1 == T.bmcu ? 0 : u + 1;
+      c = T.comp(u);
+      dct = T.dct(c);
+      act = T.act(c);
       if (MODE == 2 && ++block >= block_limit) break;
     }
   }
+  if (CK)
+    for (int i = ci; i < kCkpts; ++i) ck->state[i] = -1;  // not reached by this decode
   o.pos = pos;
   o.u = u;
   o.z = z;
+  o.dc[0] = p0;
+  o.dc[1] = p1;
+  o.dc[2] = p2;
+  if (errpos) *errpos = epos;
   return o;
-}
-
-__device__ __forceinline__ long long pack_state(uint32_t pos, int u, int z) {
-  return (static_cast<long long>(pos) << 16) | (u << 8) | z;
 }
 
 struct SlotRef {
@@ -376,6 +491,7 @@ __global__ void __launch_bounds__(256) k_jpeg_huff(const JDesc* __restrict__ des
   const Work W = work_view(work, total_slots);
   const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t nthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  if (tid == 0) W.stamps[0] = gtimer();
 
   // (0) subsequences per interval (sub_prefix after seg_start)
   for (int64_t k = tid; k < n; k += nthreads) {
@@ -394,23 +510,35 @@ __global__ void __launch_bounds__(256) k_jpeg_huff(const JDesc* __restrict__ des
   }
   grid.sync();
 
-  // (1) speculative decode of every subsequence
+  // (1) speculative decode of every subsequence (the first of an interval: true entry)
   for (int64_t g = tid; g < total_slots; g += nthreads) {
     SlotRef r;
     if (!slot_ref(descs, n, work, status, g, r)) continue;
-    const JDesc& d = descs[r.k];
+    Tabs T;
+    T.load(descs[r.k]);
     BitReader br;
-    br.init(work + d.clean_off);
+    br.init(work + descs[r.k].clean_off);
     const uint32_t start = static_cast<uint32_t>(r.j) * sub_bits;
     const uint32_t stop = min(start + static_cast<uint32_t>(sub_bits), r.seg_bits);
-    const DecOut o = r.j == 0 ? decode_run<1>(d, br, r.bit0, r.seg_bits, stop, 0, 0, 0, nullptr, 0, 0)
-                              : decode_run<0>(d, br, r.bit0, r.seg_bits, stop, start, 0, 0, nullptr, 0, 0);
+    Ckpt ck;
+    ck.state = W.ck_state + g * kCkpts;
+    ck.acc = W.ck_acc + g * kCkpts;
+    ck.step = static_cast<uint32_t>(sub_bits) / (kCkpts + 1);
+    ck.first = start + ck.step;
+    ck.compare = false;
+    uint32_t ep;
+    const DecOut o =
+        r.j == 0 ? decode_run<1, true>(T, br, r.bit0, r.seg_bits, stop, 0, 0, 0, nullptr, 0, 0, nullptr, &ck, &ep)
+                 : decode_run<0, true>(T, br, r.bit0, r.seg_bits, stop, start, 0, 0, nullptr, 0, 0, nullptr, &ck, &ep);
     W.exitp[g] = pack_state(o.pos, o.u, o.z);
     W.blocks[g] = o.blocks;
     W.err[g] = o.err;
+    W.errpos[g] = static_cast<int>(ep);
+    W.dcs[g] = make_int4(0, o.dc[0], o.dc[1], o.dc[2]);
     W.lastproc[g] = 0;
     W.changed[g] = 1;
   }
+  if (tid == 0) W.stamps[1] = gtimer();
 
   // (2) half-rounds: subsequences of one parity re-decode from their predecessor's exit
   int h = 2;
@@ -420,17 +548,33 @@ __global__ void __launch_bounds__(256) k_jpeg_huff(const JDesc* __restrict__ des
       SlotRef r;
       if (!slot_ref(descs, n, work, status, g, r) || r.j == 0 || (r.j & 1) != (h & 1)) continue;
       if (W.changed[g - 1] < W.lastproc[g]) continue;
-      const JDesc& d = descs[r.k];
+      atomicAdd(W.counters + 512 + h, 1u);  // diagnostics: decodes in this half-round
+      Tabs T;
+      T.load(descs[r.k]);
       BitReader br;
-      br.init(work + d.clean_off);
+      br.init(work + descs[r.k].clean_off);
       const long long e = W.exitp[g - 1];
       const uint32_t stop = min(static_cast<uint32_t>(r.j + 1) * sub_bits, r.seg_bits);
-      const DecOut o = decode_run<1>(d, br, r.bit0, r.seg_bits, stop, static_cast<uint32_t>(e >> 16),
-                                     static_cast<int>((e >> 8) & 255), static_cast<int>(e & 255),
-                                     nullptr, 0, 0);
+      Ckpt ck;
+      ck.state = W.ck_state + g * kCkpts;
+      ck.acc = W.ck_acc + g * kCkpts;
+      ck.step = static_cast<uint32_t>(sub_bits) / (kCkpts + 1);
+      ck.first = static_cast<uint32_t>(r.j) * sub_bits + ck.step;
+      ck.compare = true;
+      ck.prev_exit = W.exitp[g];
+      ck.prev_blocks = W.blocks[g];
+      ck.prev_err = W.err[g];
+      ck.prev_errpos = static_cast<uint32_t>(W.errpos[g]);
+      ck.prev_dc = W.dcs[g];
+      uint32_t ep;
+      const DecOut o = decode_run<1, true>(T, br, r.bit0, r.seg_bits, stop, static_cast<uint32_t>(e >> 16),
+                                           static_cast<int>((e >> 8) & 255), static_cast<int>(e & 255),
+                                           nullptr, 0, 0, nullptr, &ck, &ep);
       const long long x = pack_state(o.pos, o.u, o.z);
       W.blocks[g] = o.blocks;
       W.err[g] = o.err;
+      W.errpos[g] = static_cast<int>(ep);
+      W.dcs[g] = make_int4(0, o.dc[0], o.dc[1], o.dc[2]);
       W.lastproc[g] = h;
       if (x != W.exitp[g]) {
         W.exitp[g] = x;
@@ -439,12 +583,17 @@ __global__ void __launch_bounds__(256) k_jpeg_huff(const JDesc* __restrict__ des
       }
     }
     grid.sync();
+    if (tid == 0 && h < 64) reinterpret_cast<unsigned long long*>(W.counters + 640)[h] = gtimer();
     if (h >= 3 && W.counters[h] == 0 && W.counters[h - 1] == 0) break;
   }
   const bool converged = h < kMaxSteps;
-  if (tid == 0) W.counters[1023] = h;  // diagnostics: half-rounds used
+  if (tid == 0) {
+    W.counters[1023] = h;
+    W.stamps[2] = gtimer();
+  }
 
-  // (3) per interval: first block of every subsequence; unclean streams go to the host
+  // (3) per interval: first block and entry DC predictors of every subsequence (scans);
+  //     unclean streams go to the host
   const int lane = threadIdx.x & 31;
   const int64_t warp = tid >> 5, nwarps = nthreads >> 5;
   for (int64_t k = warp; k < n; k += nwarps) {
@@ -457,37 +606,54 @@ __global__ void __launch_bounds__(256) k_jpeg_huff(const JDesc* __restrict__ des
       const int T = seg_blocks(d, s);
       const int first = s * d.ri * d.bmcu;
       int carry = 0;
+      int4 dcarry = make_int4(0, 0, 0, 0);  // DC predictors reset at each restart
       for (int t0 = sub_prefix[s]; t0 < sub_prefix[s + 1]; t0 += 32) {
         const int t = t0 + lane;
         const int64_t g = d.slot_base + t;
         const bool on = t < sub_prefix[s + 1];
         const int b = on ? W.blocks[g] : 0;
-        int x = b;
+        const int4 dv = on ? W.dcs[g] : make_int4(0, 0, 0, 0);
+        int x = b, x0 = dv.y, x1 = dv.z, x2 = dv.w;
 #pragma unroll
         for (int dd = 1; dd < 32; dd <<= 1) {
           const int y = __shfl_up_sync(0xffffffffu, x, dd);
-          if (lane >= dd) x += y;
+          const int y0 = __shfl_up_sync(0xffffffffu, x0, dd);
+          const int y1 = __shfl_up_sync(0xffffffffu, x1, dd);
+          const int y2 = __shfl_up_sync(0xffffffffu, x2, dd);
+          if (lane >= dd) {
+            x += y;
+            x0 += y0;
+            x1 += y1;
+            x2 += y2;
+          }
         }
         const int before = carry + x - b;
         if (on) {
           W.bstart[g] = first + before;
+          W.dcs[g] = make_int4(0, dcarry.x + x0 - dv.y, dcarry.y + x1 - dv.z, dcarry.z + x2 - dv.w);
           const int e = W.err[g];
           if (e != kNoErr && before + e < T) bad = true;
           if (!converged && W.changed[g] >= h - 1) bad = true;
         }
         carry += __shfl_sync(0xffffffffu, x, 31);
+        dcarry.x += __shfl_sync(0xffffffffu, x0, 31);
+        dcarry.y += __shfl_sync(0xffffffffu, x1, 31);
+        dcarry.z += __shfl_sync(0xffffffffu, x2, 31);
       }
       if (carry < T) bad = true;  // the data ends before the interval's last block
     }
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(status + k, TP_JPEG_CORRUPT);
   }
   grid.sync();
+  if (tid == 0) W.stamps[3] = gtimer();
 
-  // (4) write pass
+  // (4) write pass: coefficients, with the DC values predicted in place
   for (int64_t g = tid; g < total_slots; g += nthreads) {
     SlotRef r;
     if (!slot_ref(descs, n, work, status, g, r)) continue;
     const JDesc& d = descs[r.k];
+    Tabs T;
+    T.load(d);
     BitReader br;
     br.init(work + d.clean_off);
     uint32_t pos = 0;
@@ -500,71 +666,39 @@ __global__ void __launch_bounds__(256) k_jpeg_huff(const JDesc* __restrict__ des
     }
     const uint32_t stop = min(static_cast<uint32_t>(r.j + 1) * sub_bits, r.seg_bits);
     const int limit = r.s * d.ri * d.bmcu + seg_blocks(d, r.s);
-    decode_run<2>(d, br, r.bit0, r.seg_bits, stop, pos, u, z,
-                  reinterpret_cast<int16_t*>(work + d.coef_off), W.bstart[g], limit);
+    const int4 pv = W.dcs[g];
+    const int pred[3] = {pv.y, pv.z, pv.w};
+    decode_run<2, false>(T, br, r.bit0, r.seg_bits, stop, pos, u, z,
+                  reinterpret_cast<int16_t*>(work + d.coef_off), W.bstart[g], limit, pred);
   }
-  grid.sync();
-
-  // (5) DC prediction per interval and component (diffs -> values, int16 stores)
-  for (int64_t k = warp; k < n; k += nwarps) {
-    const JDesc& d = descs[k];
-    if (d.n_slots == 0 || status[k]) continue;
-    int16_t* coef = reinterpret_cast<int16_t*>(work + d.coef_off);
-    const int n_mcu = d.mcux * d.mcuy;
-    for (int c = 0; c < d.ncomp; ++c) {
-      int u0 = 0;
-      while (d.slot_comp[u0] != c) ++u0;
-      int nb = 0;
-      while (u0 + nb < d.bmcu && d.slot_comp[u0 + nb] == c) ++nb;
-      for (int s = 0; s < d.n_seg; ++s) {
-        const int m0 = s * d.ri, m1 = min(n_mcu, m0 + d.ri);
-        int carry = 0;  // libjpeg's last_dc_val (int), reset at each restart
-        for (int mb = m0; mb < m1; mb += 32) {
-          const int m = mb + lane;
-          int sum = 0;
-          if (m < m1)
-            for (int b = 0; b < nb; ++b) sum += coef[(static_cast<int64_t>(m) * d.bmcu + u0 + b) * 64];
-          int x = sum;
-#pragma unroll
-          for (int dd = 1; dd < 32; dd <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, x, dd);
-            if (lane >= dd) x += y;
-          }
-          int run = carry + x - sum;
-          if (m < m1)
-            for (int b = 0; b < nb; ++b) {
-              int16_t* p = coef + (static_cast<int64_t>(m) * d.bmcu + u0 + b) * 64;
-              run += *p;
-              *p = static_cast<int16_t>(run);
-            }
-          carry += __shfl_sync(0xffffffffu, x, 31);
-        }
-      }
-    }
-  }
+  if (tid == 0) W.stamps[4] = gtimer();
 }
 
 // ---------------------------------------------------------------------------
 // J3: ISLOW IDCT (jidctint.c), 8 threads per block
 
-constexpr long long F0298 = 2446, F0390 = 3196, F0541 = 4433, F0765 = 6270, F0899 = 7373,
-                    F1175 = 9633, F1501 = 12299, F1847 = 15137, F1961 = 16069, F2053 = 16819,
-                    F2562 = 20995, F3072 = 25172;
+constexpr int F0298 = 2446, F0390 = 3196, F0541 = 4433, F0765 = 6270, F0899 = 7373, F1175 = 9633,
+              F1501 = 12299, F1847 = 15137, F1961 = 16069, F2053 = 16819, F2562 = 20995,
+              F3072 = 25172;
 
-__device__ __forceinline__ void idct_1d(const long long (&in)[8], long long (&out)[8]) {
-  long long z2 = in[2], z3 = in[6];
-  long long z1 = (z2 + z3) * F0541;
-  const long long tmp2 = z1 + z3 * -F1847;
-  const long long tmp3 = z1 + z2 * F0765;
-  const long long tmp0 = (in[0] + in[4]) * 8192;  // << CONST_BITS
-  const long long tmp1 = (in[0] - in[4]) * 8192;
-  const long long tmp10 = tmp0 + tmp3, tmp13 = tmp0 - tmp3, tmp11 = tmp1 + tmp2, tmp12 = tmp1 - tmp2;
-  long long t0 = in[7], t1 = in[5], t2 = in[3], t3 = in[1];
+// One jidctint.c butterfly.  libjpeg computes in JLONG (64-bit on LP64); T = int is
+// exact whenever the inputs are bounded as the callers check (|in| <= 2^13 keeps every
+// intermediate below 2^30.3), T = long long otherwise (corrupt-looking coefficients).
+template <typename T>
+__device__ __forceinline__ void idct_1d(const T (&in)[8], T (&out)[8]) {
+  T z2 = in[2], z3 = in[6];
+  T z1 = (z2 + z3) * F0541;
+  const T tmp2 = z1 + z3 * -F1847;
+  const T tmp3 = z1 + z2 * F0765;
+  const T tmp0 = (in[0] + in[4]) * 8192;  // << CONST_BITS
+  const T tmp1 = (in[0] - in[4]) * 8192;
+  const T tmp10 = tmp0 + tmp3, tmp13 = tmp0 - tmp3, tmp11 = tmp1 + tmp2, tmp12 = tmp1 - tmp2;
+  T t0 = in[7], t1 = in[5], t2 = in[3], t3 = in[1];
   z1 = t0 + t3;
   z2 = t1 + t2;
   z3 = t0 + t2;
-  long long z4 = t1 + t3;
-  const long long z5 = (z3 + z4) * F1175;
+  T z4 = t1 + t3;
+  const T z5 = (z3 + z4) * F1175;
   t0 *= F0298;
   t1 *= F2053;
   t2 *= F3072;
@@ -587,62 +721,100 @@ __device__ __forceinline__ void idct_1d(const long long (&in)[8], long long (&ou
   out[4] = tmp13 - t0;
 }
 
-__device__ __forceinline__ uint32_t range_limit(long long x) {
+__device__ __forceinline__ uint32_t range_limit(int x) {
   const uint32_t v = static_cast<uint32_t>(x) & 1023u;  // RANGE_MASK
   return v < 128 ? v + 128 : v < 512 ? 255u : v < 896 ? 0u : v - 896;
+}
+
+// pass 1 of one column: DEQUANTIZE (short coef x short quant, ISLOW_MULT_TYPE) then the
+// butterfly, DESCALE(x, CONST_BITS - PASS1_BITS) into the int workspace
+__device__ __forceinline__ void idct_col(const int (&dq)[8], int (&ws)[8]) {
+  int m = 0;
+#pragma unroll
+  for (int r = 0; r < 8; ++r) m = max(m, abs(dq[r]));
+  if (m <= (1 << 13)) {
+    int out[8];
+    idct_1d<int>(dq, out);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) ws[r] = (out[r] + (1 << 10)) >> 11;
+  } else {
+    long long in[8], out[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) in[r] = dq[r];
+    idct_1d<long long>(in, out);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) ws[r] = static_cast<int>((out[r] + (1LL << 10)) >> 11);
+  }
+}
+
+// pass 2 of one row: butterfly, DESCALE(x, CONST_BITS + PASS1_BITS + 3), range limit
+__device__ __forceinline__ void idct_row(const int (&w)[8], uint32_t& lo, uint32_t& hi) {
+  int m = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) m = max(m, abs(w[i]));
+  int px[8];
+  if (m <= (1 << 13)) {
+    int out[8];
+    idct_1d<int>(w, out);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) px[i] = (out[i] + (1 << 17)) >> 18;
+  } else {
+    long long in[8], out[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) in[i] = w[i];
+    idct_1d<long long>(in, out);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) px[i] = static_cast<int>((out[i] + (1LL << 17)) >> 18);
+  }
+  lo = hi = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    lo |= range_limit(px[i]) << (8 * i);
+    hi |= range_limit(px[i + 4]) << (8 * i);
+  }
 }
 
 __global__ void __launch_bounds__(256) k_jpeg_idct(const JDesc* __restrict__ descs, int n,
                                                    int64_t total_blocks, uint8_t* __restrict__ work,
                                                    const int32_t* __restrict__ status) {
-  __shared__ int ws[32][64];
+  __shared__ int ws[32][65];
   const int sub = threadIdx.x & 7, lb = threadIdx.x >> 3;
   for (int64_t gb0 = static_cast<int64_t>(blockIdx.x) * 32; gb0 < total_blocks;
        gb0 += static_cast<int64_t>(gridDim.x) * 32) {
     const int64_t gb = gb0 + lb;
     const bool on = gb < total_blocks;
-    int k = 0;
     const JDesc* d = nullptr;
     bool live = false;
     if (on) {
-      k = find_image(descs, n, gb, 1);
+      const int k = find_image(descs, n, gb, 1);
       d = descs + k;
       live = d->n_slots > 0 && status[k] == 0;
     }
     const int b = on ? static_cast<int>(gb - d->block_base) : 0;
-    int c = 0;
-    const int16_t* blk = nullptr;
+    const int u = live ? b % d->bmcu : 0;
+    const int c = live ? d->slot_comp[u] : 0;
     if (live) {
-      c = d->slot_comp[b % d->bmcu];
-      blk = reinterpret_cast<const int16_t*>(work + d->coef_off) + static_cast<int64_t>(b) * 64;
-      // pass 1: column `sub` (DEQUANTIZE: short coef x short quant, as ISLOW_MULT_TYPE)
-      long long in[8], out[8];
+      const int16_t* blk = reinterpret_cast<const int16_t*>(work + d->coef_off) + static_cast<int64_t>(b) * 64;
+      int dq[8], w[8];
 #pragma unroll
       for (int r = 0; r < 8; ++r)
-        in[r] = static_cast<long long>(blk[8 * r + sub]) *
-                static_cast<long long>(static_cast<int16_t>(d->quant[c][8 * r + sub]));
-      idct_1d(in, out);
+        dq[r] = static_cast<int>(blk[8 * r + sub]) * static_cast<int>(static_cast<int16_t>(d->quant[c][8 * r + sub]));
+      idct_col(dq, w);
 #pragma unroll
-      for (int r = 0; r < 8; ++r)  // DESCALE(x, CONST_BITS - PASS1_BITS), stored as int
-        ws[lb][8 * r + sub] = static_cast<int>((out[r] + (1LL << 10)) >> 11);
+      for (int r = 0; r < 8; ++r) ws[lb][8 * r + sub] = w[r];
     }
     __syncthreads();
     if (live) {
-      long long in[8], out[8];
+      int w[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) in[i] = ws[lb][8 * sub + i];
-      idct_1d(in, out);
-      const int mcu = b / d->bmcu, u = b % d->bmcu;
+      for (int i = 0; i < 8; ++i) w[i] = ws[lb][8 * sub + i];
+      uint32_t lo, hi;
+      idct_row(w, lo, hi);
+      const int mcu = b / d->bmcu;
       const int my = mcu / d->mcux, mx = mcu % d->mcux;
       const int by = d->ncomp == 1 ? my : my * d->comp_v[c] + d->slot_bv[u];
       const int bx = d->ncomp == 1 ? mx : mx * d->comp_h[c] + d->slot_bh[u];
       uint8_t* dst = work + d->plane_off[c] + static_cast<int64_t>(by * 8 + sub) * d->plane_w[c] + bx * 8;
-      uint32_t lo = 0, hi = 0;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {  // DESCALE(x, CONST_BITS + PASS1_BITS + 3), range limit
-        lo |= range_limit((out[i] + (1LL << 17)) >> 18) << (8 * i);
-        hi |= range_limit((out[i + 4] + (1LL << 17)) >> 18) << (8 * i);
-      }
       *reinterpret_cast<uint2*>(dst) = make_uint2(lo, hi);
     }
     __syncthreads();
@@ -678,6 +850,16 @@ __device__ __forceinline__ int chroma(const uint8_t* __restrict__ p, int pw, int
 
 __device__ __forceinline__ uint32_t clamp255(int v) { return static_cast<uint32_t>(min(max(v, 0), 255)); }
 
+__device__ __forceinline__ uint32_t ycc_px(int Y, int cb, int cr) {
+  // jdcolor.c build_ycc_rgb_table: FIX(x) = x * 65536 + 0.5, ONE_HALF = 32768
+  const int r = Y + ((91881 * cr + 32768) >> 16);
+  const int g = Y + ((-22554 * cb + 32768 - 46802 * cr) >> 16);
+  const int b = Y + ((116130 * cb + 32768) >> 16);
+  return clamp255(r) | (clamp255(g) << 8) | (clamp255(b) << 16);
+}
+
+// One CTA per output row; each thread 4 consecutive pixels (12 bytes, three 32-bit stores
+// when the row is 4-byte aligned, which it is whenever the width is a multiple of 4).
 __global__ void __launch_bounds__(256) k_jpeg_color(const JDesc* __restrict__ descs, int n,
                                                     int64_t total_rows, const uint8_t* __restrict__ work,
                                                     uint8_t* __restrict__ out,
@@ -687,31 +869,40 @@ __global__ void __launch_bounds__(256) k_jpeg_color(const JDesc* __restrict__ de
     const JDesc& d = descs[k];
     if (d.n_slots == 0 || status[k]) continue;
     const int y = static_cast<int>(gr - d.row_base);
-    uint8_t* o = out + d.out_off + static_cast<int64_t>(y) * d.width * 3;
-    const uint8_t* py = work + d.plane_off[0];
-    if (d.ncomp == 1) {
-      for (int x = threadIdx.x; x < d.width; x += blockDim.x) {
-        const uint8_t g = py[static_cast<int64_t>(y) * d.plane_w[0] + x];
-        o[3 * x] = g;
-        o[3 * x + 1] = g;
-        o[3 * x + 2] = g;
+    const int W = d.width;
+    uint8_t* o = out + d.out_off + static_cast<int64_t>(y) * W * 3;
+    const bool aligned = (reinterpret_cast<uintptr_t>(o) & 3) == 0;
+    const uint8_t* py = work + d.plane_off[0] + static_cast<int64_t>(y) * d.plane_w[0];
+    const int hx = d.ncomp == 1 ? 1 : d.hmax / d.comp_h[1], vx = d.ncomp == 1 ? 1 : d.vmax / d.comp_v[1];
+    const uint8_t* pcb = work + d.plane_off[d.ncomp == 1 ? 0 : 1];
+    const uint8_t* pcr = work + d.plane_off[d.ncomp == 1 ? 0 : 2];
+    for (int x0 = 4 * threadIdx.x; x0 < W; x0 += 4 * blockDim.x) {
+      const uint32_t yw = *reinterpret_cast<const uint32_t*>(py + x0);  // planes are 8-padded
+      uint32_t px[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int Y = (yw >> (8 * i)) & 255;
+        if (d.ncomp == 1) {
+          px[i] = static_cast<uint32_t>(Y) * 0x010101u;
+        } else {
+          const int x = x0 + i;
+          const int cb = chroma(pcb, d.plane_w[1], d.ds_w[1], d.ds_h[1], hx, vx, x, y) - 128;
+          const int cr = chroma(pcr, d.plane_w[2], d.ds_w[2], d.ds_h[2], hx, vx, x, y) - 128;
+          px[i] = ycc_px(Y, cb, cr);
+        }
       }
-      continue;
-    }
-    const uint8_t* pcb = work + d.plane_off[1];
-    const uint8_t* pcr = work + d.plane_off[2];
-    const int hx = d.hmax / d.comp_h[1], vx = d.vmax / d.comp_v[1];
-    for (int x = threadIdx.x; x < d.width; x += blockDim.x) {
-      const int Y = py[static_cast<int64_t>(y) * d.plane_w[0] + x];
-      const int cb = chroma(pcb, d.plane_w[1], d.ds_w[1], d.ds_h[1], hx, vx, x, y) - 128;
-      const int cr = chroma(pcr, d.plane_w[2], d.ds_w[2], d.ds_h[2], hx, vx, x, y) - 128;
-      // jdcolor.c build_ycc_rgb_table: FIX(x) = x * 65536 + 0.5, ONE_HALF = 32768
-      const int r = Y + ((91881 * cr + 32768) >> 16);
-      const int g = Y + ((-22554 * cb + 32768 - 46802 * cr) >> 16);
-      const int b = Y + ((116130 * cb + 32768) >> 16);
-      o[3 * x] = static_cast<uint8_t>(clamp255(r));
-      o[3 * x + 1] = static_cast<uint8_t>(clamp255(g));
-      o[3 * x + 2] = static_cast<uint8_t>(clamp255(b));
+      if (aligned && x0 + 4 <= W) {
+        uint32_t* o32 = reinterpret_cast<uint32_t*>(o + 3 * x0);
+        o32[0] = px[0] | (px[1] << 24);
+        o32[1] = (px[1] >> 8) | (px[2] << 16);
+        o32[2] = (px[2] >> 16) | (px[3] << 8);
+      } else {
+        for (int i = 0; i < 4 && x0 + i < W; ++i) {
+          o[3 * (x0 + i)] = static_cast<uint8_t>(px[i]);
+          o[3 * (x0 + i) + 1] = static_cast<uint8_t>(px[i] >> 8);
+          o[3 * (x0 + i) + 2] = static_cast<uint8_t>(px[i] >> 16);
+        }
+      }
     }
   }
 }

@@ -309,7 +309,10 @@ TP_API int64_t tp_jpeg_describe(const TpJpegInfo* infos, int32_t n, const int64_
   // workspace layout (zeroed by tp_jpeg_decode: the counters and the coefficients)
   int64_t w = 4096;                         // step counters
   w += align_up(8 * slots, 256);            // exit
-  w += 5 * align_up(4 * slots, 256);        // blocks, err, bstart, lastproc, changed
+  w += align_up(16 * slots, 256);           // DC sums / predictors
+  w += 6 * align_up(4 * slots, 256);        // blocks, err, errpos, bstart, lastproc, changed
+  w += align_up(8 * 7 * slots, 256);        // checkpoint states (jpeg.cu kCkpts = 7)
+  w += align_up(16 * 7 * slots, 256);       // checkpoint accumulators
   totals[3] = w;
   for (int k = 0; k < n; ++k) {
     JDesc& j = descs[k];

@@ -20,6 +20,7 @@ reported (skip_pixel_mask, the mask is an all-ones no-op, imgproc.py:516-532).
 
 from __future__ import annotations
 
+import threading
 import time
 from dataclasses import dataclass
 from typing import Optional
@@ -309,56 +310,115 @@ def normalize_tiles(tiles: list[ImageBuffer], cfg: PreprocessConfig) -> list[Ima
 # ---------------------------------------------------------------------------
 # full preprocessing pass
 
+class _Session:
+    """Per-thread, per-device state of the drop-in ``preprocess``: the device JPEG decoder,
+    one batch preprocessor per tiling / output configuration, and grow-only pinned and
+    device buffers, so a request costs no allocation beyond its result arrays."""
+
+    def __init__(self, device: torch.device):
+        self.device = device
+        self.jpeg = None
+        self.preps: dict = {}
+        self.host = None  # pinned staging for host-decoded pixels
+        self.dev = None
+
+    def prep(self, cfg: PreprocessConfig, defer: bool):
+        from .engine import TilePreprocessor
+
+        key = (cfg.tile_edge, cfg.max_tiles, tuple(cfg.mean), tuple(cfg.std),
+               cfg.effective_precision, defer)
+        p = self.preps.get(key)
+        if p is None:
+            p = TilePreprocessor(cfg, self.device, layout="NHWC", emit_uint8=defer,
+                                 normalize=not defer)
+            self.preps[key] = p
+        return p
+
+    def upload(self, arr: np.ndarray, stream):
+        """Host pixels -> a 1-image device batch through the pinned slab."""
+        from .engine import PackedImages
+
+        nbytes = arr.size
+        if self.host is None or self.host.numel() < nbytes:
+            cap = (nbytes * 5 // 4 + (1 << 20)) & ~((1 << 20) - 1)
+            self.host = torch.empty(cap, dtype=torch.uint8, pin_memory=True)
+            self.dev = torch.empty(cap, dtype=torch.uint8, device=self.device)
+        stream.synchronize()  # the previous request's upload no longer reads the slab
+        self.host[:nbytes].numpy()[:] = arr.reshape(-1)
+        with torch.cuda.stream(stream):
+            self.dev[:nbytes].copy_(self.host[:nbytes], non_blocking=True)
+        wh = np.array([[arr.shape[1], arr.shape[0]]], dtype=np.int32)
+        off = np.zeros(1, dtype=np.int64)
+        return PackedImages(self.dev, torch.zeros(1, dtype=torch.int64, device=self.device),
+                            torch.from_numpy(wh).to(self.device), 3, wh, off)
+
+
+_tls = threading.local()
+
+
+def _session(device: torch.device) -> _Session:
+    s = getattr(_tls, "session", None)
+    if s is None or s.device != device:
+        s = _Session(device)
+        _tls.session = s
+    return s
+
+
 def preprocess(payload: bytes, cfg: PreprocessConfig, *,
                defer_normalize: bool = False) -> PreprocessResult:
     """decode -> plan -> resize -> tile -> normalize (or defer) -> mask
-    (imgproc.py:538-598).  Stage keys are the reference's; on the device path
-    "plan" spans the image upload + K1, "resize" is empty (fused into K2),
-    "tile" is K2 (resample + crop + thumbnail, with normalize fused unless
-    deferred), and "normalize"/"defer" is the readback into ImageBuffers."""
+    (imgproc.py:538-598).  Stage keys are the reference's.  On the device path:
+    "decode" is the baseline-JPEG decode on the GPU (K7: host marker parse, upload of
+    the compressed bytes, device decode) -- or, for PNG and the JPEG variants K7 does
+    not take, the reference's Pillow decode on the host plus the pixel upload; "plan"
+    is K1's exact rule on the host (the TilePlan the result carries); "resize" is empty
+    (fused into K2); "tile" is K1 + K2 in one launch (resample + crop + thumbnail, with
+    normalize fused unless deferred); "normalize"/"defer" is the readback into
+    ImageBuffers."""
+    from .jpeg import TP_JPEG_OK, JpegDecoder, parse
+
     timings: dict[str, int] = {}
+    device = require_device()
+    stream = torch.cuda.current_stream(device)
+    sess = _session(device)
     t0 = time.perf_counter_ns()
-    img = decode_image(payload, cfg)
+    if payload[:2] == b"\xff\xd8" and parse(payload).status == TP_JPEG_OK:
+        if sess.jpeg is None:
+            sess.jpeg = JpegDecoder(device)
+        images = sess.jpeg.decode([payload], stream=stream)  # host fallback inside
+        width, height = (int(v) for v in images.wh_host[0])
+    else:
+        arr = decode_rgb(payload)
+        height, width = arr.shape[:2]
+        _check_plan_args(width, height, cfg)
+        images = sess.upload(arr, stream)
     timings["decode"] = time.perf_counter_ns() - t0
 
-    _check_plan_args(img.width, img.height, cfg)
-    device = require_device()
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-    ev[0].record(torch.cuda.current_stream(device))
-    run = _Run(img)
-    rec = torch.empty((1, _lib.TP_PLAN_FIELDS), dtype=torch.int32, device=run.device)
-    n_img = torch.empty((1,), dtype=torch.int32, device=run.device)
-    tile_off = torch.empty((2,), dtype=torch.int32, device=run.device)
-    _lib.call("tp_plan", _lib.ptr(run.wh), 1, cfg.tile_edge, cfg.max_tiles, _lib.ptr(rec),
-              _lib.ptr(n_img), _lib.ptr(tile_off), run.handle)
-    ev[1].record(run.stream)
+    t0 = time.perf_counter_ns()
+    _check_plan_args(width, height, cfg)
+    plan_rec = np.zeros(_lib.TP_PLAN_FIELDS, dtype=np.int32)
+    _lib.check(_lib.load().tp_plan_host(width, height, cfg.tile_edge, cfg.max_tiles,
+                                        plan_rec.ctypes.data), "tp_plan_host")
+    plan = TilePlan.from_record(plan_rec)
+    timings["plan"] = time.perf_counter_ns() - t0
 
-    cap = cfg.max_tiles + 1  # upper bound; no host round trip before K2
-    if defer_normalize:
-        out, u8 = run.tile(rec, tile_off, cfg.tile_edge, cap, None, _lib.TP_DTYPE_NONE,
-                           _lib.TP_LAYOUT_NHWC, True)
-        elem = UINT8
-    else:
-        dtype = dtype_code(cfg.effective_precision)
-        lut, affine = normalize_tables(cfg.mean, cfg.std, img.channels, dtype, run.device)
-        out, u8 = run.tile(rec, tile_off, cfg.tile_edge, cap, lut, dtype, _lib.TP_LAYOUT_NHWC,
-                           False, affine)
-        elem = cfg.effective_precision
-    ev[2].record(run.stream)
-    plan = TilePlan.from_record(rec.cpu().numpy()[0])
-    dev_tiles = (u8 if defer_normalize else out)[: plan.n_images]
-    backing = _to_numpy(dev_tiles, elem)
-    ev[3].record(run.stream)
-    ev[3].synchronize()
-
-    ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(3)]
-    timings["plan"] = int(ms[0] * 1e6)
-    timings["resize"] = 0
-    timings["tile"] = int(ms[1] * 1e6)
-    timings["defer" if defer_normalize else "normalize"] = int(ms[2] * 1e6)
+    timings["resize"] = 0  # fused into K2
+    prep = sess.prep(cfg, defer_normalize)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    ev[0].record(stream)
+    with torch.cuda.stream(stream):
+        out = prep(images, capacity=plan.n_images, stream=stream)
+    ev[1].record(stream)
+    dev_tiles = out.pixel_u8 if defer_normalize else out.pixel_values
+    elem = UINT8 if defer_normalize else cfg.effective_precision
+    backing = _to_numpy(dev_tiles[: plan.n_images], elem)
+    ev[2].record(stream)
+    ev[2].synchronize()
+    timings["tile"] = int(ev[0].elapsed_time(ev[1]) * 1e6)
+    timings["defer" if defer_normalize else "normalize"] = int(ev[1].elapsed_time(ev[2]) * 1e6)
     if not cfg.skip_pixel_mask:
         timings["mask"] = 0  # all-ones validity mask: values unchanged, no work
-    tiles = _split(backing, cfg.tile_edge, img.channels, elem, cfg.avoid_per_item_split)
+    tiles = _split(backing, cfg.tile_edge, 3, elem, cfg.avoid_per_item_split)
     return PreprocessResult(tiles, plan, timings, deferred=defer_normalize)
 
 

@@ -163,11 +163,8 @@ class JpegDecoder:
             self._dev[:payload_bytes].copy_(self._host[:payload_bytes], non_blocking=True)
             self._copied = torch.cuda.Event()
             self._copied.record(stream)
-            with torch.cuda.device(self.device):
-                _lib.call("tp_jpeg_decode", self._dev.data_ptr(), self._dev.data_ptr() + desc_at, n,
-                          totals.ctypes.data, self.sub_bits, self._work.data_ptr(),
-                          self._work.numel(), out.data.data_ptr(), status.data_ptr(),
-                          stream_handle(self.device, stream))
+        self._launch_args = (desc_at, n, totals, out, status)
+        self.launch(stream)
         self._status = status
         if not sync:
             return out
@@ -182,6 +179,18 @@ class JpegDecoder:
             o = int(out_off[k])
             out.data[o: o + a.size].copy_(torch.from_numpy(np.ascontiguousarray(a).reshape(-1)))
         return out
+
+
+    def launch(self, stream: Optional[torch.cuda.Stream] = None) -> None:
+        """(Re)launch the device decode of the last uploaded batch (K7 only: no host work,
+        no copies) -- what bench.py times as the decode kernels."""
+        desc_at, n, totals, out, status = self._launch_args
+        stream = stream or torch.cuda.current_stream(self.device)
+        with torch.cuda.device(self.device):
+            _lib.call("tp_jpeg_decode", self._dev.data_ptr(), self._dev.data_ptr() + desc_at, n,
+                      totals.ctypes.data, self.sub_bits, self._work.data_ptr(),
+                      self._work.numel(), out.data.data_ptr(), status.data_ptr(),
+                      stream_handle(self.device, stream))
 
 
 def decode_images(payloads: Sequence[bytes], device=None) -> list[np.ndarray]:
