@@ -576,6 +576,7 @@ def run_c2(args, dist, device, dev_index):
                                                                    images.wh_host)]
     del images, out
     res["e2e"] = run_e2e(args, dist, device, cfg, host_imgs)
+    res["e2e_jpeg"] = run_e2e_jpeg(args, dist, device, cfg)
     return res
 
 
@@ -657,6 +658,125 @@ def run_e2e(args, dist, device, cfg, host_imgs) -> dict:
                     "stream, K2 reads rows through the maps) -> D2H plans/offsets; two "
                     "slabs, so packing step i+1 overlaps the upload of step i",
             "h2d_bytes_full_images": int(full_bytes)}
+
+
+def _cpu_jpeg_one(args):
+    """One JPEG payload through the reference's own preprocess (vlmfp: decode with Pillow
+    + plan + fused tiles + normalize, fastest toggles), or the port (Pillow + oracle)."""
+    idx, e, mt, mean, std, bf16 = args
+    payload = _CPU_PAYLOADS[idx]
+    V = reference_module()
+    t0 = time.perf_counter()
+    if V is not None:
+        cfg = V.PreprocessConfig(tile_edge=e, max_tiles=mt, mean=tuple(mean), std=tuple(std),
+                                 reduced_precision_normalize=bf16, fused_transform=True,
+                                 contiguous_tensor_path=True, avoid_per_item_split=True,
+                                 skip_pixel_mask=True, decode_once=True, simd_decode=True)
+        V.preprocess(payload, cfg)
+    else:
+        import io
+
+        from PIL import Image
+
+        arr = np.asarray(Image.open(io.BytesIO(payload)).convert("RGB"))
+        cpu_preprocess(arr, e, mt, mean, std, bf16)
+    return time.perf_counter() - t0
+
+
+_CPU_PAYLOADS: list = []
+
+
+def run_e2e_jpeg(args, dist, device, cfg) -> dict:
+    """The C2 batch as JPEG payloads (64 corpus-like 1080p scenes, q85 baseline 4:2:0),
+    end to end from the caller's bytes: device JPEG decode (K7: host marker parse + one
+    H2D of the compressed scans + parallel Huffman / IDCT / colour on the GPU) -> K1 + K2
+    -> D2H of the plans; two buffer sets, so the host work of step i+1 overlaps step i.
+    Host wall clock; the reference's own preprocess (decode included) on all host cores
+    beside it."""
+    import torch
+
+    from paper_2603_16987_b200.engine import TilePreprocessor
+    from paper_2603_16987_b200.jpeg import JpegDecoder
+    from paper_2603_16987_b200.workloads import jpeg_payloads
+
+    payloads = jpeg_payloads(args.batch, seed=20260817 + 97 * dist.rank)
+    dec = JpegDecoder(device, depth=2)
+    prep = TilePreprocessor(cfg, device)
+    stream = torch.cuda.Stream(device)
+    outs, pend = [None, None], [None, None]
+    plan_host = [None, None]
+    refits = [0]
+
+    def step(i):
+        k = i % 2
+        if pend[k] is not None:  # the batch that used these buffers two steps ago
+            b, o = pend[k]
+            if b.finish():  # host-decoded images patched in: tile that batch again
+                refits[0] += 1
+                with torch.cuda.stream(stream):
+                    prep(b.images, out=o, stream=stream)
+        b = dec.decode(payloads, stream=stream, sync=False)
+        with torch.cuda.stream(stream):
+            outs[k] = prep(b.images, out=outs[k], stream=stream)
+            if plan_host[k] is None:
+                plan_host[k] = torch.empty_like(outs[k].plans.plan, device="cpu").pin_memory()
+            plan_host[k].copy_(outs[k].plans.plan, non_blocking=True)
+        pend[k] = (b, outs[k])
+
+    for i in range(4):
+        step(i)
+    torch.cuda.synchronize(device)
+    steps = max(5, args.e2e_steps)
+    dist.barrier(device)
+    t0 = time.perf_counter()
+    for i in range(steps):
+        step(i)
+    for k in range(2):
+        if pend[k] is not None:
+            pend[k][0].finish()
+    torch.cuda.synchronize(device)
+    wall = dist.max(time.perf_counter() - t0, device)
+    # the decode kernels alone on the last batch (CUDA events around relaunches)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(5):
+        dec.launch(stream)
+    b.record(stream)
+    torch.cuda.synchronize(device)
+    n = len(payloads)
+    res = {"value": round(dist.world * n * steps / wall, 2), "unit": UNIT,
+           "ms_per_step": round(wall / steps * 1e3, 4), "steps": steps,
+           "h2d_bytes_per_step": int(dec.last_h2d_bytes),
+           "d2h_bytes_per_step": int(plan_host[0].numel() * 4 + 4 * n),
+           "payload_kb_avg": round(sum(map(len, payloads)) / n / 1e3, 1),
+           "decode_kernels_ms": round(a.elapsed_time(b) / 5, 4),
+           "host_fallbacks": dec.last_fallback, "refits": refits[0],
+           "path": "caller's JPEG bytes -> JpegDecoder.decode(sync=False): tp_jpeg_parse + "
+                   "tp_jpeg_describe + tp_stage_pack into a pinned slab -> one H2D of the "
+                   "compressed scans -> K7 (unstuff, self-synchronizing parallel Huffman, "
+                   "ISLOW IDCT, fancy upsampling + YCbCr->RGB) -> K1 + K2 -> D2H plans",
+           "timing": "host wall clock around all steps (synchronize + barrier both sides, "
+                     "max over ranks)"}
+    if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
+        _CPU_PAYLOADS[:] = payloads
+        cores = host_cores()
+        from paper_2603_16987_b200.dtypes import FLOAT16_WIDE
+
+        jobs = [(i, cfg.tile_edge, cfg.max_tiles, tuple(cfg.mean), tuple(cfg.std),
+                 cfg.effective_precision == FLOAT16_WIDE) for i in range(n)]
+        with _pool(cores) as pool:
+            pool.map(_cpu_jpeg_one, jobs[:cores], chunksize=1)
+            t1 = time.perf_counter()
+            per = pool.map(_cpu_jpeg_one, jobs, chunksize=1)
+            dt = time.perf_counter() - t1
+        res["cpu_baseline"] = {
+            "value": round(n / dt, 3), "unit": UNIT, "cores": cores, "kind": cpu_kind(),
+            "sample": f"the same {n} JPEG payloads through "
+                      + ("vlmfp.preprocess (the reference: Pillow decode + plan + fused tiles "
+                         "+ normalize, fastest toggles)" if reference_module() is not None
+                         else "Pillow decode + the oracle port")
+                      + f", one process per core; per-image p50 {np.median(per) * 1e3:.1f} ms"}
+    return res
 
 
 def _host_threads() -> int:
@@ -966,6 +1086,7 @@ def main(argv=None):
                          "frac_of_nominal": round(achieved / 8000.0, 4)},
             "cpu_baseline": cpu,
             "e2e": r["e2e"],
+            "e2e_jpeg": r["e2e_jpeg"],
             "gpu_launches": 2 * args.steps,
             "gpu_launches_sub_blocks": n_sub_launches,
             "clocks": r["clk"],

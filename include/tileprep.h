@@ -252,7 +252,7 @@ TP_API int tp_jpeg_parse(const uint8_t* data, int64_t len, TpJpegInfo* info);
 TP_API int64_t tp_jpeg_desc_bytes(void);
 TP_API int64_t tp_jpeg_describe(const TpJpegInfo* infos, int32_t n, const int64_t* raw_off,
                                 const int64_t* out_off, int32_t sub_bits, void* desc,
-                                int64_t* totals /* [5]: slots, blocks, rows, zeroed range */);
+                                int64_t* totals /* [8]: slots, blocks, rows, zeroed range, chunks, counts */);
 TP_API int tp_jpeg_decode(const uint8_t* d_payload, const void* d_desc, int32_t n,
                           const int64_t* totals, int32_t sub_bits, void* d_work,
                           int64_t work_bytes, uint8_t* d_out, int32_t* d_status,

@@ -51,17 +51,17 @@ constexpr int kNoErr = 0x7FFFFFFF;
 constexpr int kCkpts = 7;  // checkpoints per subsequence (every sub_bits / 8 bits)
 
 struct Work {
-  unsigned* counters;  // [h]: exits changed in half-round h; [1023]: half-rounds used
+  unsigned* counters;  // [h]: exits changed in half-round h; [512 + h]: decodes in it;
+                       // [1023]: half-rounds used
   unsigned long long* stamps;  // [8] phase timestamps (globaltimer), diagnostics
   long long* exitp;    // per slot: (bit << 16) | (u << 8) | z, bit relative to the interval
+  long long* entry;    // per slot: the entry state its counts below were decoded from
   int4* dcs;           // per slot: DC difference sums per component (.y .z .w), then
                        // (phase 3) the interval's running DC of each component at the entry
-  int* blocks;         // blocks completed from the (last) entry to the exit
+  int* blocks;         // blocks completed from the entry to the exit
   int* err;            // block count at the first unclean symbol, kNoErr if none
   int* errpos;         // its bit position
   int* bstart;         // block index (in the image) at the entry
-  int* lastproc;       // half-round this slot last decoded in
-  int* changed;        // half-round its exit last changed in
   long long* ck_state; // [slot][kCkpts] checkpoint states
   int4* ck_acc;        // [slot][kCkpts] checkpoint accumulators
 };
@@ -75,10 +75,12 @@ __device__ inline Work work_view(uint8_t* w, int64_t slots) {
   int64_t o = 4096;
   v.exitp = reinterpret_cast<long long*>(w + o);
   o += al256(8 * slots);
+  v.entry = reinterpret_cast<long long*>(w + o);
+  o += al256(8 * slots);
   v.dcs = reinterpret_cast<int4*>(w + o);
   o += al256(16 * slots);
-  int* arrs[6];
-  for (int i = 0; i < 6; ++i) {
+  int* arrs[4];
+  for (int i = 0; i < 4; ++i) {
     arrs[i] = reinterpret_cast<int*>(w + o);
     o += al256(4 * slots);
   }
@@ -86,8 +88,6 @@ __device__ inline Work work_view(uint8_t* w, int64_t slots) {
   v.err = arrs[1];
   v.errpos = arrs[2];
   v.bstart = arrs[3];
-  v.lastproc = arrs[4];
-  v.changed = arrs[5];
   v.ck_state = reinterpret_cast<long long*>(w + o);
   o += al256(8 * kCkpts * slots);
   v.ck_acc = reinterpret_cast<int4*>(w + o);
@@ -140,83 +140,169 @@ __device__ inline unsigned block_excl_scan(unsigned v, unsigned* sh, unsigned& t
   return before;
 }
 
-__global__ void __launch_bounds__(512) k_jpeg_unstuff(const uint8_t* __restrict__ payload,
-                                                      const JDesc* __restrict__ descs, int n,
-                                                      uint8_t* __restrict__ work,
-                                                      int32_t* __restrict__ status) {
+// The scan is cut into chunks of kChunk raw bytes (one CTA each, many per image): a
+// counting pass, then a writing pass that places each chunk's kept bytes after the kept
+// bytes of the image's earlier chunks.  A thread owns 16 raw bytes per step (one 16-byte
+// load; a step without a 0xFF byte keeps all 16), the CTA compacts them in shared memory
+// and stores the step's output with consecutive threads writing consecutive bytes.
+constexpr int kUnstuffThreads = 512;
+constexpr int kChunk = 32768;  // raw bytes per CTA (4 steps of 512 x 16)
+
+struct ByteFlags {
+  uint32_t keep, rst;  // bit i: byte i kept / byte i is the second byte of an RST marker
+  bool bad;            // a marker other than RST inside the scan
+};
+
+__device__ __forceinline__ ByteFlags flag_bytes(const uint8_t* raw, int64_t p0, int64_t len) {
+  ByteFlags f{0u, 0u, false};
+  if (p0 >= len) return f;
+  const int nb = len - p0 < 16 ? static_cast<int>(len - p0) : 16;
+  uint32_t w[4] = {0, 0, 0, 0};
+  if (nb == 16) {
+    const uint4 q = *reinterpret_cast<const uint4*>(raw + p0);
+    w[0] = q.x;
+    w[1] = q.y;
+    w[2] = q.z;
+    w[3] = q.w;
+  } else {
+    for (int i = 0; i < nb; ++i) w[i >> 2] |= static_cast<uint32_t>(raw[p0 + i]) << (8 * (i & 3));
+  }
+  const int prev0 = p0 > 0 ? raw[p0 - 1] : 0;
+  bool any_ff = prev0 == 0xFF;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) any_ff |= __vcmpeq4(w[i], 0xFFFFFFFFu) != 0;
+  if (!any_ff) {  // the common case: no 0xFF anywhere near
+    f.keep = nb == 16 ? 0xFFFFu : (1u << nb) - 1u;
+    return f;
+  }
+  int prev = prev0;
+  for (int i = 0; i < nb; ++i) {
+    const int cur = (w[i >> 2] >> (8 * (i & 3))) & 255;
+    int nxt;
+    if (i + 1 < nb) nxt = (w[(i + 1) >> 2] >> (8 * ((i + 1) & 3))) & 255;
+    else nxt = p0 + i + 1 < len ? raw[p0 + i + 1] : -1;  // -1: end (EOI follows)
+    if (cur == 0xFF) {
+      if (nxt == 0x00) f.keep |= 1u << i;  // a data 0xFF (its stuffed 0x00 follows)
+      else if (!(nxt == 0xFF || nxt == -1 || (nxt >= 0xD0 && nxt <= 0xD7))) f.bad = true;
+    } else if (prev == 0xFF) {
+      if (cur >= 0xD0 && cur <= 0xD7) f.rst |= 1u << i;
+      else if (cur != 0x00) f.bad = true;
+    } else {
+      f.keep |= 1u << i;
+    }
+    prev = cur;
+  }
+  return f;
+}
+
+__device__ inline int find_chunk_image(const JDesc* d, int n, int64_t c) {
+  int lo = 0, hi = n;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (d[mid].chunk_base <= c) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(kUnstuffThreads) k_jpeg_unstuff_count(
+    const uint8_t* __restrict__ payload, const JDesc* __restrict__ descs, int n,
+    int2* __restrict__ chunk_counts, int32_t* __restrict__ status) {
+  __shared__ int sk[kUnstuffThreads / 32], sr[kUnstuffThreads / 32];
+  __shared__ int sbad;
+  const int64_t c = blockIdx.x;
+  const int k = find_chunk_image(descs, n, c);
+  const JDesc& d = descs[k];
+  const int64_t c0 = (c - d.chunk_base) * kChunk;
+  if (threadIdx.x == 0) sbad = 0;
+  __syncthreads();
+  int kept = 0, rst = 0;
+  bool bad = false;
+  for (int step = 0; step < kChunk / (16 * kUnstuffThreads); ++step) {
+    const int64_t p0 = c0 + (static_cast<int64_t>(step) * kUnstuffThreads + threadIdx.x) * 16;
+    const ByteFlags f = flag_bytes(payload + d.raw_off, p0, d.raw_len);
+    kept += __popc(f.keep);
+    rst += __popc(f.rst);
+    bad |= f.bad;
+  }
+  kept = __reduce_add_sync(0xffffffffu, kept);
+  rst = __reduce_add_sync(0xffffffffu, rst);
+  if (bad) sbad = 1;
+  if ((threadIdx.x & 31) == 0) {
+    sk[threadIdx.x >> 5] = kept;
+    sr[threadIdx.x >> 5] = rst;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int tk = 0, tr = 0;
+    for (int w = 0; w < kUnstuffThreads / 32; ++w) {
+      tk += sk[w];
+      tr += sr[w];
+    }
+    chunk_counts[c] = make_int2(tk, tr);
+    if (sbad) atomicOr(status + k, TP_JPEG_CORRUPT);
+  }
+}
+
+__global__ void __launch_bounds__(kUnstuffThreads) k_jpeg_unstuff_write(
+    const uint8_t* __restrict__ payload, const JDesc* __restrict__ descs, int n,
+    const int2* __restrict__ chunk_counts, uint8_t* __restrict__ work,
+    int32_t* __restrict__ status) {
   __shared__ unsigned sh[32];
-  __shared__ unsigned carry_kept, carry_rst, bad;
-  for (int k = blockIdx.x; k < n; k += gridDim.x) {
-    const JDesc& d = descs[k];
-    if (d.n_slots == 0) continue;
-    const uint8_t* raw = payload + d.raw_off;
-    const int64_t len = d.raw_len;
-    uint8_t* clean = work + d.clean_off;
-    int32_t* seg_start = reinterpret_cast<int32_t*>(work + d.seg_off);
-    if (threadIdx.x == 0) {
-      carry_kept = 0;
-      carry_rst = 0;
-      bad = 0;
+  __shared__ uint8_t sout[16 * kUnstuffThreads];
+  __shared__ int carry_k, carry_r;
+  const int64_t c = blockIdx.x;
+  const int k = find_chunk_image(descs, n, c);
+  const JDesc& d = descs[k];
+  const int64_t ci = c - d.chunk_base;
+  const int64_t c0 = ci * kChunk;
+  uint8_t* clean = work + d.clean_off;
+  int32_t* seg_start = reinterpret_cast<int32_t*>(work + d.seg_off);
+  if (threadIdx.x == 0) {
+    int tk = 0, tr = 0;
+    for (int64_t j = d.chunk_base; j < c; ++j) {
+      const int2 v = chunk_counts[j];
+      tk += v.x;
+      tr += v.y;
+    }
+    carry_k = tk;
+    carry_r = tr;
+  }
+  __syncthreads();
+  const uint8_t* raw = payload + d.raw_off;
+  for (int step = 0; step < kChunk / (16 * kUnstuffThreads); ++step) {
+    const int64_t sbase = c0 + static_cast<int64_t>(step) * kUnstuffThreads * 16;
+    if (sbase >= d.raw_len) break;  // uniform across the CTA
+    const int64_t p0 = sbase + static_cast<int64_t>(threadIdx.x) * 16;
+    const ByteFlags f = flag_bytes(raw, p0, d.raw_len);
+    unsigned total;
+    const unsigned before = block_excl_scan((static_cast<unsigned>(__popc(f.rst)) << 16) |
+                                                static_cast<unsigned>(__popc(f.keep)), sh, total);
+    unsigned o = before & 0xFFFF;
+    unsigned r = carry_r + (before >> 16);
+    for (int i = 0; i < 16; ++i) {
+      if (f.keep >> i & 1) sout[o++] = raw[p0 + i];
+      if (f.rst >> i & 1) {
+        ++r;
+        if (r < static_cast<unsigned>(d.n_seg)) seg_start[r] = static_cast<int32_t>(carry_k + o);
+      }
     }
     __syncthreads();
-    constexpr int kPer = 16;
-    for (int64_t base = 0; base < len; base += static_cast<int64_t>(blockDim.x) * kPer) {
-      const int64_t p0 = base + static_cast<int64_t>(threadIdx.x) * kPer;
-      uint32_t keep = 0, rst = 0;  // bit i: byte p0 + i kept / is the 2nd byte of an RST
-      int n_keep = 0, n_rst = 0;
-      bool my_bad = false;
-      if (p0 < len) {
-        int prev = p0 > 0 ? raw[p0 - 1] : 0;
-        for (int i = 0; i < kPer && p0 + i < len; ++i) {
-          const int cur = raw[p0 + i];
-          const int nxt = p0 + i + 1 < len ? raw[p0 + i + 1] : -1;  // -1: end (EOI follows)
-          bool kp = false;
-          if (cur == 0xFF) {
-            if (nxt == 0x00) kp = true;  // a data 0xFF (its stuffed 0x00 follows)
-            else if (!(nxt == 0xFF || nxt == -1 || (nxt >= 0xD0 && nxt <= 0xD7))) my_bad = true;
-          } else if (prev == 0xFF) {
-            if (cur >= 0xD0 && cur <= 0xD7) {
-              rst |= 1u << i;
-              ++n_rst;
-            } else if (cur != 0x00) {
-              my_bad = true;  // a marker other than RST inside the scan
-            }
-          } else {
-            kp = true;
-          }
-          if (kp) {
-            keep |= 1u << i;
-            ++n_keep;
-          }
-          prev = cur;
-        }
-      }
-      if (my_bad) atomicOr(&bad, 1u);
-      unsigned total;
-      const unsigned before = block_excl_scan((static_cast<unsigned>(n_rst) << 16) | n_keep, sh, total);
-      unsigned ck = carry_kept + (before & 0xFFFF);
-      unsigned cr = carry_rst + (before >> 16);
-      for (int i = 0; i < kPer; ++i) {
-        if (keep >> i & 1) clean[ck++] = raw[p0 + i];
-        if (rst >> i & 1) {
-          ++cr;
-          if (cr < static_cast<unsigned>(d.n_seg)) seg_start[cr] = static_cast<int32_t>(ck);
-        }
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        carry_kept += total & 0xFFFF;
-        carry_rst += total >> 16;
-      }
-      __syncthreads();
+    const int nk = static_cast<int>(total & 0xFFFF);
+    for (int i = threadIdx.x; i < nk; i += kUnstuffThreads) clean[carry_k + i] = sout[i];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      carry_k += nk;
+      carry_r += static_cast<int>(total >> 16);
     }
+    __syncthreads();
+  }
+  if (ci == d.n_chunks - 1) {  // the image's last chunk closes the interval table
     if (threadIdx.x == 0) {
       seg_start[0] = 0;
-      seg_start[d.n_seg] = static_cast<int32_t>(carry_kept);
-      if (bad || carry_rst != static_cast<unsigned>(d.n_seg - 1)) atomicOr(status + k, TP_JPEG_CORRUPT);
+      seg_start[d.n_seg] = carry_k;
+      if (carry_r != d.n_seg - 1) atomicOr(status + k, TP_JPEG_CORRUPT);
     }
-    for (int i = threadIdx.x; i < 64; i += blockDim.x) clean[carry_kept + i] = 0;  // peek slack
-    __syncthreads();
+    for (int i = threadIdx.x; i < 64; i += kUnstuffThreads) clean[carry_k + i] = 0;  // peek slack
   }
 }
 
@@ -278,25 +364,25 @@ struct DecOut {
 // The per-image fields the symbol loop needs, in registers: per block slot of the MCU its
 // component, and per component its DC / AC tables.
 struct Tabs {
-  const JHuff *dc0, *dc1, *dc2, *ac0, *ac1, *ac2;  // per component (selects, no local memory)
-  uint32_t slot_comp;  // 2 bits per block slot
+  const JHuff* base;   // [4]: dc0 dc1 ac0 ac1 (a shared-memory copy or the descriptor's own)
+  uint32_t slot_comp;  // 2 bits per block slot of the MCU: its component
+  uint32_t dcid, acid; // bit c: table id of component c
   int bmcu;
-  __device__ void load(const JDesc& d) {
+  __device__ void load(const JDesc& d, const JHuff* tables) {
+    base = tables;
     bmcu = d.bmcu;
     slot_comp = 0;
     for (int u = 0; u < d.bmcu; ++u) slot_comp |= static_cast<uint32_t>(d.slot_comp[u]) << (2 * u);
-    dc0 = &d.dc[d.comp_td[0]];
-    ac0 = &d.ac[d.comp_ta[0]];
-    dc1 = d.ncomp > 1 ? &d.dc[d.comp_td[1]] : dc0;
-    ac1 = d.ncomp > 1 ? &d.ac[d.comp_ta[1]] : ac0;
-    dc2 = d.ncomp > 2 ? &d.dc[d.comp_td[2]] : dc0;
-    ac2 = d.ncomp > 2 ? &d.ac[d.comp_ta[2]] : ac0;
+    dcid = acid = 0;
+    for (int c = 0; c < d.ncomp; ++c) {
+      dcid |= static_cast<uint32_t>(d.comp_td[c] & 1) << c;
+      acid |= static_cast<uint32_t>(d.comp_ta[c] & 1) << c;
+    }
   }
   __device__ __forceinline__ int comp(int u) const { return (slot_comp >> (2 * u)) & 3; }
-  __device__ __forceinline__ const JHuff* dct(int c) const { return c == 0 ? dc0 : c == 1 ? dc1 : dc2; }
-  __device__ __forceinline__ const JHuff* act(int c) const { return c == 0 ? ac0 : c == 1 ? ac1 : ac2; }
+  __device__ __forceinline__ const JHuff* dct(int c) const { return base + ((dcid >> c) & 1); }
+  __device__ __forceinline__ const JHuff* act(int c) const { return base + 2 + ((acid >> c) & 1); }
 };
-
 
 // Checkpoints of one subsequence: the decoder's state at the first symbol boundary at or
 // after each checkpoint position, with the blocks and DC sums accumulated from the entry
@@ -483,15 +569,103 @@ __device__ inline int seg_blocks(const JDesc& d, int s) {
   return m * d.bmcu;
 }
 
+// Huffman tables of the (at most two) images a CTA's chunk of 256 slots belongs to, in
+// shared memory; slots of a third image in the same chunk (tiny images) read the
+// descriptor's tables from global memory.
+struct ChunkTables {
+  JHuff tab[2][4];
+  int img[2];
+};
+
+__device__ inline const JHuff* chunk_tables(ChunkTables& ct, const JDesc* descs, int n,
+                                            int64_t base, int64_t total, int my_k) {
+  const int k0 = find_image(descs, n, base, 0);
+  const int k1 = find_image(descs, n, min(base + static_cast<int64_t>(blockDim.x) - 1, total - 1), 0);
+  __syncthreads();  // the previous chunk's readers are done
+  for (int side = 0; side < 2; ++side) {
+    const int k = side == 0 ? k0 : k1;
+    if (side == 1 && k1 == k0) break;
+    if (ct.img[side] == k) continue;  // still loaded (same value in every thread)
+    const int4* src = reinterpret_cast<const int4*>(descs[k].dc);
+    int4* dst = reinterpret_cast<int4*>(ct.tab[side]);
+    constexpr int kWords = static_cast<int>(4 * sizeof(JHuff) / 16);
+    for (int i = threadIdx.x; i < kWords; i += blockDim.x) dst[i] = src[i];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ct.img[0] = k0;
+    ct.img[1] = k1;
+  }
+  // (every thread read ct.img before the first barrier above; the writes land after it)
+  return my_k == k0 ? ct.tab[0] : my_k == k1 ? ct.tab[1] : descs[my_k].dc;
+}
+
+__device__ inline void init_ckpt(Ckpt& ck, const Work& W, int64_t g, int j, int sub_bits) {
+  ck.state = W.ck_state + g * kCkpts;
+  ck.acc = W.ck_acc + g * kCkpts;
+  ck.step = static_cast<uint32_t>(sub_bits) / (kCkpts + 1);
+  ck.first = static_cast<uint32_t>(j) * sub_bits + ck.step;
+  ck.compare = false;
+}
+
+__device__ __forceinline__ void unpack_state(long long e, uint32_t& pos, int& u, int& z) {
+  pos = static_cast<uint32_t>(e >> 16);
+  u = static_cast<int>((e >> 8) & 255);
+  z = static_cast<int>(e & 255);
+}
+
+// block-wide exclusive scan of 4 ints (x: block counts, y..w: DC sums)
+__device__ inline int4 block_scan4(int4 v, int4* sh, int4& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int4 x = v;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    int4 y;
+    y.x = __shfl_up_sync(0xffffffffu, x.x, d);
+    y.y = __shfl_up_sync(0xffffffffu, x.y, d);
+    y.z = __shfl_up_sync(0xffffffffu, x.z, d);
+    y.w = __shfl_up_sync(0xffffffffu, x.w, d);
+    if (lane >= d) {
+      x.x += y.x;
+      x.y += y.y;
+      x.z += y.z;
+      x.w += y.w;
+    }
+  }
+  if (lane == 31) sh[warp] = x;
+  __syncthreads();
+  int4 pre = make_int4(0, 0, 0, 0);
+  for (int w = 0; w < warp; ++w) {
+    pre.x += sh[w].x;
+    pre.y += sh[w].y;
+    pre.z += sh[w].z;
+    pre.w += sh[w].w;
+  }
+  total = make_int4(0, 0, 0, 0);
+  for (int w = 0; w < nw; ++w) {
+    total.x += sh[w].x;
+    total.y += sh[w].y;
+    total.z += sh[w].z;
+    total.w += sh[w].w;
+  }
+  __syncthreads();
+  return make_int4(pre.x + x.x - v.x, pre.y + x.y - v.y, pre.z + x.z - v.z, pre.w + x.w - v.w);
+}
+
 __global__ void __launch_bounds__(256) k_jpeg_huff(const JDesc* __restrict__ descs, int n,
                                                    int64_t total_slots, int sub_bits,
                                                    uint8_t* __restrict__ work,
                                                    int32_t* __restrict__ status) {
   cg::grid_group grid = cg::this_grid();
+  __shared__ ChunkTables ct;
+  __shared__ int4 scan_sh[8];
+  __shared__ int bad_sh;
   const Work W = work_view(work, total_slots);
   const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t nthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  if (threadIdx.x == 0) ct.img[0] = ct.img[1] = -1;
   if (tid == 0) W.stamps[0] = gtimer();
+  const uint32_t overlap = static_cast<uint32_t>(sub_bits);  // speculative lead-in
 
   // (0) subsequences per interval (sub_prefix after seg_start)
   for (int64_t k = tid; k < n; k += nthreads) {
@@ -510,56 +684,73 @@ __global__ void __launch_bounds__(256) k_jpeg_huff(const JDesc* __restrict__ des
   }
   grid.sync();
 
-  // (1) speculative decode of every subsequence (the first of an interval: true entry)
-  for (int64_t g = tid; g < total_slots; g += nthreads) {
+  // (1) every subsequence: a speculative lead-in of `overlap` bits before its start (from a
+  // guessed state; from the interval start, exactly, when that is closer), which almost
+  // always falls into the true path, then the counting decode of its own bits
+  for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x; base < total_slots; base += nthreads) {
+    const int64_t g = base + threadIdx.x;
     SlotRef r;
-    if (!slot_ref(descs, n, work, status, g, r)) continue;
+    const bool on = g < total_slots && slot_ref(descs, n, work, status, g, r);
+    const JHuff* tabs = chunk_tables(ct, descs, n, base, total_slots, on ? r.k : -1);
+    if (!on) continue;
+    const JDesc& d = descs[r.k];
     Tabs T;
-    T.load(descs[r.k]);
+    T.load(d, tabs);
     BitReader br;
-    br.init(work + descs[r.k].clean_off);
+    br.init(work + d.clean_off);
     const uint32_t start = static_cast<uint32_t>(r.j) * sub_bits;
     const uint32_t stop = min(start + static_cast<uint32_t>(sub_bits), r.seg_bits);
+    uint32_t pos = 0;
+    int u = 0, z = 0;
+    if (r.j > 0) {
+      const uint32_t lead = start > overlap ? start - overlap : 0u;
+      const DecOut s0 = decode_run<0, false>(T, br, r.bit0, r.seg_bits, start, lead, 0, 0, nullptr,
+                                             0, 0, nullptr);
+      pos = s0.pos;
+      u = s0.u;
+      z = s0.z;
+    }
     Ckpt ck;
-    ck.state = W.ck_state + g * kCkpts;
-    ck.acc = W.ck_acc + g * kCkpts;
-    ck.step = static_cast<uint32_t>(sub_bits) / (kCkpts + 1);
-    ck.first = start + ck.step;
-    ck.compare = false;
+    init_ckpt(ck, W, g, r.j, sub_bits);
     uint32_t ep;
-    const DecOut o =
-        r.j == 0 ? decode_run<1, true>(T, br, r.bit0, r.seg_bits, stop, 0, 0, 0, nullptr, 0, 0, nullptr, &ck, &ep)
-                 : decode_run<0, true>(T, br, r.bit0, r.seg_bits, stop, start, 0, 0, nullptr, 0, 0, nullptr, &ck, &ep);
+    const DecOut o = decode_run<1, true>(T, br, r.bit0, r.seg_bits, stop, pos, u, z, nullptr, 0, 0,
+                                         nullptr, &ck, &ep);
+    W.entry[g] = pack_state(pos, u, z);
     W.exitp[g] = pack_state(o.pos, o.u, o.z);
     W.blocks[g] = o.blocks;
     W.err[g] = o.err;
     W.errpos[g] = static_cast<int>(ep);
     W.dcs[g] = make_int4(0, o.dc[0], o.dc[1], o.dc[2]);
-    W.lastproc[g] = 0;
-    W.changed[g] = 1;
   }
   if (tid == 0) W.stamps[1] = gtimer();
 
-  // (2) half-rounds: subsequences of one parity re-decode from their predecessor's exit
+  // (2) half-rounds: a subsequence whose recorded entry is not its predecessor's exit
+  // re-decodes from that exit (stopping as soon as it rejoins its recorded path); one
+  // parity per half-round, so no exit is read while it is rewritten
   int h = 2;
   for (; h < kMaxSteps; ++h) {
     grid.sync();
-    for (int64_t g = tid; g < total_slots; g += nthreads) {
+    for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x; base < total_slots; base += nthreads) {
+      const int64_t g = base + threadIdx.x;
       SlotRef r;
-      if (!slot_ref(descs, n, work, status, g, r) || r.j == 0 || (r.j & 1) != (h & 1)) continue;
-      if (W.changed[g - 1] < W.lastproc[g]) continue;
-      atomicAdd(W.counters + 512 + h, 1u);  // diagnostics: decodes in this half-round
+      bool need = g < total_slots && slot_ref(descs, n, work, status, g, r) && r.j > 0 &&
+                  (r.j & 1) == (h & 1) && W.exitp[g - 1] != W.entry[g];
+      if (!__syncthreads_or(need)) continue;
+      const JHuff* tabs = chunk_tables(ct, descs, n, base, total_slots, need ? r.k : -1);
+      if (!need) continue;
+      atomicAdd(W.counters + 512 + h, 1u);
+      const JDesc& d = descs[r.k];
       Tabs T;
-      T.load(descs[r.k]);
+      T.load(d, tabs);
       BitReader br;
-      br.init(work + descs[r.k].clean_off);
+      br.init(work + d.clean_off);
       const long long e = W.exitp[g - 1];
+      uint32_t pos;
+      int u, z;
+      unpack_state(e, pos, u, z);
       const uint32_t stop = min(static_cast<uint32_t>(r.j + 1) * sub_bits, r.seg_bits);
       Ckpt ck;
-      ck.state = W.ck_state + g * kCkpts;
-      ck.acc = W.ck_acc + g * kCkpts;
-      ck.step = static_cast<uint32_t>(sub_bits) / (kCkpts + 1);
-      ck.first = static_cast<uint32_t>(r.j) * sub_bits + ck.step;
+      init_ckpt(ck, W, g, r.j, sub_bits);
       ck.compare = true;
       ck.prev_exit = W.exitp[g];
       ck.prev_blocks = W.blocks[g];
@@ -567,18 +758,16 @@ __global__ void __launch_bounds__(256) k_jpeg_huff(const JDesc* __restrict__ des
       ck.prev_errpos = static_cast<uint32_t>(W.errpos[g]);
       ck.prev_dc = W.dcs[g];
       uint32_t ep;
-      const DecOut o = decode_run<1, true>(T, br, r.bit0, r.seg_bits, stop, static_cast<uint32_t>(e >> 16),
-                                           static_cast<int>((e >> 8) & 255), static_cast<int>(e & 255),
-                                           nullptr, 0, 0, nullptr, &ck, &ep);
+      const DecOut o = decode_run<1, true>(T, br, r.bit0, r.seg_bits, stop, pos, u, z, nullptr, 0, 0,
+                                           nullptr, &ck, &ep);
       const long long x = pack_state(o.pos, o.u, o.z);
+      W.entry[g] = e;
       W.blocks[g] = o.blocks;
       W.err[g] = o.err;
       W.errpos[g] = static_cast<int>(ep);
       W.dcs[g] = make_int4(0, o.dc[0], o.dc[1], o.dc[2]);
-      W.lastproc[g] = h;
       if (x != W.exitp[g]) {
         W.exitp[g] = x;
-        W.changed[g] = h;
         atomicAdd(W.counters + h, 1u);
       }
     }
@@ -592,11 +781,9 @@ __global__ void __launch_bounds__(256) k_jpeg_huff(const JDesc* __restrict__ des
     W.stamps[2] = gtimer();
   }
 
-  // (3) per interval: first block and entry DC predictors of every subsequence (scans);
-  //     unclean streams go to the host
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = tid >> 5, nwarps = nthreads >> 5;
-  for (int64_t k = warp; k < n; k += nwarps) {
+  // (3) per interval (one CTA per image): first block and entry DC predictors of every
+  //     subsequence (block scans); unclean streams go to the host
+  for (int k = blockIdx.x; k < n; k += gridDim.x) {
     const JDesc& d = descs[k];
     if (d.n_slots == 0 || status[k]) continue;
     const int32_t* seg_start = reinterpret_cast<const int32_t*>(work + d.seg_off);
@@ -605,73 +792,62 @@ __global__ void __launch_bounds__(256) k_jpeg_huff(const JDesc* __restrict__ des
     for (int s = 0; s < d.n_seg; ++s) {
       const int T = seg_blocks(d, s);
       const int first = s * d.ri * d.bmcu;
-      int carry = 0;
-      int4 dcarry = make_int4(0, 0, 0, 0);  // DC predictors reset at each restart
-      for (int t0 = sub_prefix[s]; t0 < sub_prefix[s + 1]; t0 += 32) {
-        const int t = t0 + lane;
+      int4 carry = make_int4(0, 0, 0, 0);  // DC predictors reset at each restart
+      for (int t0 = sub_prefix[s]; t0 < sub_prefix[s + 1]; t0 += blockDim.x) {
+        const int t = t0 + threadIdx.x;
         const int64_t g = d.slot_base + t;
         const bool on = t < sub_prefix[s + 1];
-        const int b = on ? W.blocks[g] : 0;
-        const int4 dv = on ? W.dcs[g] : make_int4(0, 0, 0, 0);
-        int x = b, x0 = dv.y, x1 = dv.z, x2 = dv.w;
-#pragma unroll
-        for (int dd = 1; dd < 32; dd <<= 1) {
-          const int y = __shfl_up_sync(0xffffffffu, x, dd);
-          const int y0 = __shfl_up_sync(0xffffffffu, x0, dd);
-          const int y1 = __shfl_up_sync(0xffffffffu, x1, dd);
-          const int y2 = __shfl_up_sync(0xffffffffu, x2, dd);
-          if (lane >= dd) {
-            x += y;
-            x0 += y0;
-            x1 += y1;
-            x2 += y2;
-          }
-        }
-        const int before = carry + x - b;
+        int4 v = make_int4(0, 0, 0, 0);
         if (on) {
+          const int4 dv = W.dcs[g];
+          v = make_int4(W.blocks[g], dv.y, dv.z, dv.w);
+        }
+        int4 tot;
+        const int4 ex = block_scan4(v, scan_sh, tot);
+        if (on) {
+          const int before = carry.x + ex.x;
           W.bstart[g] = first + before;
-          W.dcs[g] = make_int4(0, dcarry.x + x0 - dv.y, dcarry.y + x1 - dv.z, dcarry.z + x2 - dv.w);
+          W.dcs[g] = make_int4(0, carry.y + ex.y, carry.z + ex.z, carry.w + ex.w);
           const int e = W.err[g];
           if (e != kNoErr && before + e < T) bad = true;
-          if (!converged && W.changed[g] >= h - 1) bad = true;
+          if (!converged && t > sub_prefix[s] && W.exitp[g - 1] != W.entry[g]) bad = true;
         }
-        carry += __shfl_sync(0xffffffffu, x, 31);
-        dcarry.x += __shfl_sync(0xffffffffu, x0, 31);
-        dcarry.y += __shfl_sync(0xffffffffu, x1, 31);
-        dcarry.z += __shfl_sync(0xffffffffu, x2, 31);
+        carry.x += tot.x;
+        carry.y += tot.y;
+        carry.z += tot.z;
+        carry.w += tot.w;
       }
-      if (carry < T) bad = true;  // the data ends before the interval's last block
+      if (carry.x < T) bad = true;  // the data ends before the interval's last block
     }
-    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(status + k, TP_JPEG_CORRUPT);
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(status + k, TP_JPEG_CORRUPT);
   }
   grid.sync();
   if (tid == 0) W.stamps[3] = gtimer();
 
   // (4) write pass: coefficients, with the DC values predicted in place
-  for (int64_t g = tid; g < total_slots; g += nthreads) {
+  for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x; base < total_slots; base += nthreads) {
+    const int64_t g = base + threadIdx.x;
     SlotRef r;
-    if (!slot_ref(descs, n, work, status, g, r)) continue;
+    const bool on = g < total_slots && slot_ref(descs, n, work, status, g, r);
+    const JHuff* tabs = chunk_tables(ct, descs, n, base, total_slots, on ? r.k : -1);
+    if (!on) continue;
     const JDesc& d = descs[r.k];
     Tabs T;
-    T.load(d);
+    T.load(d, tabs);
     BitReader br;
     br.init(work + d.clean_off);
-    uint32_t pos = 0;
-    int u = 0, z = 0;
-    if (r.j > 0) {
-      const long long e = W.exitp[g - 1];
-      pos = static_cast<uint32_t>(e >> 16);
-      u = static_cast<int>((e >> 8) & 255);
-      z = static_cast<int>(e & 255);
-    }
+    uint32_t pos;
+    int u, z;
+    unpack_state(W.entry[g], pos, u, z);
     const uint32_t stop = min(static_cast<uint32_t>(r.j + 1) * sub_bits, r.seg_bits);
     const int limit = r.s * d.ri * d.bmcu + seg_blocks(d, r.s);
     const int4 pv = W.dcs[g];
     const int pred[3] = {pv.y, pv.z, pv.w};
     decode_run<2, false>(T, br, r.bit0, r.seg_bits, stop, pos, u, z,
-                  reinterpret_cast<int16_t*>(work + d.coef_off), W.bstart[g], limit, pred);
+                         reinterpret_cast<int16_t*>(work + d.coef_off), W.bstart[g], limit, pred);
   }
   if (tid == 0) W.stamps[4] = gtimer();
+  (void)bad_sh;
 }
 
 // ---------------------------------------------------------------------------
@@ -876,19 +1052,51 @@ __global__ void __launch_bounds__(256) k_jpeg_color(const JDesc* __restrict__ de
     const int hx = d.ncomp == 1 ? 1 : d.hmax / d.comp_h[1], vx = d.ncomp == 1 ? 1 : d.vmax / d.comp_v[1];
     const uint8_t* pcb = work + d.plane_off[d.ncomp == 1 ? 0 : 1];
     const uint8_t* pcr = work + d.plane_off[d.ncomp == 1 ? 0 : 2];
+    // the chroma rows this output row reads: nearer row and (h2v2) the further one, the
+    // jdmainct.c context rows replicating the edges
+    const int dsw = d.ds_w[1], dsh = d.ds_h[1];
+    const int crow = vx == 2 ? y >> 1 : y;
+    const int orow = vx == 2 ? ((y & 1) ? min(crow + 1, dsh - 1) : max(crow - 1, 0)) : crow;
+    const int64_t pw1 = d.plane_w[1];
+    const uint8_t* cb0 = pcb + crow * pw1;
+    const uint8_t* cb1 = pcb + orow * pw1;
+    const uint8_t* cr0 = pcr + crow * pw1;
+    const uint8_t* cr1 = pcr + orow * pw1;
+    const bool fancy = hx == 2 && dsw > 2;
     for (int x0 = 4 * threadIdx.x; x0 < W; x0 += 4 * blockDim.x) {
       const uint32_t yw = *reinterpret_cast<const uint32_t*>(py + x0);  // planes are 8-padded
       uint32_t px[4];
+      if (d.ncomp == 1) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int Y = (yw >> (8 * i)) & 255;
-        if (d.ncomp == 1) {
-          px[i] = static_cast<uint32_t>(Y) * 0x010101u;
-        } else {
-          const int x = x0 + i;
-          const int cb = chroma(pcb, d.plane_w[1], d.ds_w[1], d.ds_h[1], hx, vx, x, y) - 128;
-          const int cr = chroma(pcr, d.plane_w[2], d.ds_w[2], d.ds_h[2], hx, vx, x, y) - 128;
-          px[i] = ycc_px(Y, cb, cr);
+        for (int i = 0; i < 4; ++i) px[i] = ((yw >> (8 * i)) & 255) * 0x010101u;
+      } else if (fancy) {
+        // 4 pixels = chroma columns i0, i0 + 1: column sums at i0 - 1 .. i0 + 2, clamped
+        // (clamping the neighbour reproduces jdsample.c's first / last column cases)
+        const int i0 = x0 >> 1;
+        int cb[4], cr[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int ii = min(max(i0 - 1 + q, 0), dsw - 1);
+          cb[q] = vx == 2 ? cb0[ii] * 3 + cb1[ii] : cb0[ii];
+          cr[q] = vx == 2 ? cr0[ii] * 3 + cr1[ii] : cr0[ii];
+        }
+        const int sh = vx == 2 ? 4 : 2;
+        const int be = vx == 2 ? 8 : 1, bo = vx == 2 ? 7 : 2;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int q = 1 + (i >> 1);              // this column's sum
+          const int nb = (i & 1) ? q + 1 : q - 1;  // the neighbour it blends with
+          const int b = (i & 1) ? bo : be;
+          const int ccb = ((cb[q] * 3 + cb[nb] + b) >> sh) - 128;
+          const int ccr = ((cr[q] * 3 + cr[nb] + b) >> sh) - 128;
+          px[i] = ycc_px((yw >> (8 * i)) & 255, ccb, ccr);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int x = min(x0 + i, W - 1);
+          const int ci = hx == 2 ? x >> 1 : x;  // 4:4:4, or plain replication (dsw <= 2)
+          px[i] = ycc_px((yw >> (8 * i)) & 255, cb0[ci] - 128, cr0[ci] - 128);
         }
       }
       if (aligned && x0 + 4 <= W) {
@@ -936,7 +1144,12 @@ TP_API int tp_jpeg_decode(const uint8_t* d_payload, const void* d_desc, int32_t 
       cudaMemsetAsync(work + coef_begin, 0, coef_end - coef_begin, s) != cudaSuccess)
     return set_error(TP_ERR_CUDA, "tp_jpeg_decode: memset failed");
   const int sms = device_sm_count();
-  k_jpeg_unstuff<<<min(n, 4 * sms), 512, 0, s>>>(d_payload, descs, n, work, d_status);
+  const int64_t chunks = totals[5];
+  if (chunks > 0) {
+    int2* counts = reinterpret_cast<int2*>(work + totals[6]);
+    k_jpeg_unstuff_count<<<static_cast<unsigned>(chunks), kUnstuffThreads, 0, s>>>(d_payload, descs, n, counts, d_status);
+    k_jpeg_unstuff_write<<<static_cast<unsigned>(chunks), kUnstuffThreads, 0, s>>>(d_payload, descs, n, counts, work, d_status);
+  }
   if (slots > 0) {
     static int per_sm_of[64];
     int dev = 0;

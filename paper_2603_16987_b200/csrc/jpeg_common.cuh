@@ -11,7 +11,7 @@ constexpr int kMaxBlocksPerMcu = 6;  // 4:2:0: Y0 Y1 Y2 Y3 Cb Cr
 constexpr int kFastBits = 9;
 
 // One Huffman table, decode-ready (T.81 C.2 canonical codes).
-struct JHuff {
+struct __align__(16) JHuff {
   uint16_t fast[1 << kFastBits];  // next 9 bits -> (len << 8) | symbol; 0: longer code
   int32_t maxcode[18];            // largest code of length l, -1 when none
   int32_t valoff[18];             // symbol index of code c of length l: valoff[l] + c
@@ -30,12 +30,14 @@ struct __align__(16) JDesc {
   int64_t row_base;    // global index of this image's first output row (colour grid)
   int64_t out_off;     // RGB HWC uint8 in the output buffer
   int64_t plane_off[kMaxComps];  // workspace: uint8 component planes
+  int64_t chunk_base;  // first unstuff chunk (32 KB of entropy-coded bytes) of this image
   int32_t raw_len;
   int32_t n_slots;     // slots reserved (an upper bound)
   int32_t n_seg;       // restart intervals
   int32_t ri;          // MCUs per restart interval
   int32_t width, height, ncomp, mcux, mcuy, bmcu, hmax, vmax;
   int32_t n_blocks;
+  int32_t n_chunks;
   int32_t plane_w[kMaxComps], plane_h[kMaxComps];  // block-padded
   int32_t ds_w[kMaxComps], ds_h[kMaxComps];        // real (downsampled) samples
   int32_t comp_h[kMaxComps], comp_v[kMaxComps];

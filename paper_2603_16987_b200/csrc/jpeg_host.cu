@@ -234,7 +234,8 @@ TP_API int64_t tp_jpeg_describe(const TpJpegInfo* infos, int32_t n, const int64_
       sub_bits < 64 || (sub_bits & 31))
     return -tp::set_error(TP_ERR_INVALID_ARGUMENT, "tp_jpeg_describe: bad arguments");
   JDesc* descs = static_cast<JDesc*>(desc_out);
-  int64_t slots = 0, blocks = 0, rows = 0;
+  int64_t slots = 0, blocks = 0, rows = 0, chunks = 0;
+  constexpr int64_t kChunk = 32768;  // jpeg.cu
   for (int k = 0; k < n; ++k) {
     const TpJpegInfo& in = infos[k];
     JDesc& j = descs[k];
@@ -242,6 +243,7 @@ TP_API int64_t tp_jpeg_describe(const TpJpegInfo* infos, int32_t n, const int64_
     j.slot_base = slots;  // bases stay monotone across skipped images (kernel binary searches)
     j.block_base = blocks;
     j.row_base = rows;
+    j.chunk_base = chunks;
     if (in.status != TP_JPEG_OK) continue;  // decoded on the host
     if (raw_off[k] & 3)
       return -tp::set_error(TP_ERR_INVALID_ARGUMENT, "raw_off[%d] not 4-byte aligned", k);
@@ -302,17 +304,21 @@ TP_API int64_t tp_jpeg_describe(const TpJpegInfo* infos, int32_t n, const int64_
         return -tp::set_error(TP_ERR_INVALID_ARGUMENT, "image %d: bad AC Huffman table", k);
     }
     j.out_off = out_off[k];
+    j.n_chunks = static_cast<int32_t>((in.scan_len + kChunk - 1) / kChunk);
+    chunks += j.n_chunks;
     slots += j.n_slots;
     blocks += j.n_blocks;
     rows += j.height;
   }
   // workspace layout (zeroed by tp_jpeg_decode: the counters and the coefficients)
   int64_t w = 4096;                         // step counters
-  w += align_up(8 * slots, 256);            // exit
+  w += 2 * align_up(8 * slots, 256);        // exit, entry
   w += align_up(16 * slots, 256);           // DC sums / predictors
-  w += 6 * align_up(4 * slots, 256);        // blocks, err, errpos, bstart, lastproc, changed
+  w += 4 * align_up(4 * slots, 256);        // blocks, err, errpos, bstart
   w += align_up(8 * 7 * slots, 256);        // checkpoint states (jpeg.cu kCkpts = 7)
   w += align_up(16 * 7 * slots, 256);       // checkpoint accumulators
+  totals[6] = w;                            // unstuff chunk counts
+  w = align_up(w + 8 * chunks, 256);
   totals[3] = w;
   for (int k = 0; k < n; ++k) {
     JDesc& j = descs[k];
@@ -336,6 +342,7 @@ TP_API int64_t tp_jpeg_describe(const TpJpegInfo* infos, int32_t n, const int64_
   totals[0] = slots;
   totals[1] = blocks;
   totals[2] = rows;
+  totals[5] = chunks;
   return w;
 }
 

@@ -31,7 +31,7 @@ from .runtime import require_device, stream_handle
 TP_JPEG_OK = 0
 TP_JPEG_UNSUPPORTED = 1
 TP_JPEG_CORRUPT = 2
-DEFAULT_SUB_BITS = 2048
+DEFAULT_SUB_BITS = 4096
 
 
 class TpJpegInfo(ctypes.Structure):
@@ -72,38 +72,93 @@ def _round_up(v: int, a: int) -> int:
     return (v + a - 1) // a * a
 
 
+class _Slot:
+    """One in-flight batch's buffers: pinned staging, device payload, workspace, status."""
+
+    def __init__(self):
+        self.host = None
+        self.dev = None
+        self.work = None
+        self.status = None
+        self.status_host = None
+        self.copied = None  # event: the upload out of `host` finished
+        self.done = None    # event: the decode (and the status copy) finished
+
+
+class JpegBatch:
+    """A submitted batch: ``images`` (device, filled by the decode enqueued on the
+    stream) and ``finish()``, which waits for the decode and patches in the images the
+    host decoder must take (returns their indices; the caller re-runs anything it
+    enqueued on ``images`` when the list is not empty)."""
+
+    def __init__(self, dec, slot, payloads, images, host_arrays, wh, out_off, n):
+        self._dec, self._slot, self._payloads = dec, slot, payloads
+        self.images = images
+        self._host_arrays, self._wh, self._out_off, self._n = host_arrays, wh, out_off, n
+        self.fallback: Optional[list] = None
+
+    def finish(self) -> list:
+        if self.fallback is not None:
+            return self.fallback
+        sl = self._slot
+        sl.done.synchronize()
+        st = sl.status_host[: self._n].numpy()
+        fb = sorted(set(self._host_arrays) | {k for k in range(self._n) if st[k] != 0})
+        for k in fb:
+            a = self._host_arrays.get(k)
+            if a is None:
+                a = _host_decode(self._payloads[k])
+                if (a.shape[1], a.shape[0]) != tuple(self._wh[k]):
+                    raise RuntimeError("host decode size differs from the JPEG frame header")
+            o = int(self._out_off[k])
+            self.images.data[o: o + a.size].copy_(
+                torch.from_numpy(np.ascontiguousarray(a).reshape(-1).copy()))
+        self.fallback = fb
+        self._dec.last_fallback = fb
+        return fb
+
+
 class JpegDecoder:
     """Batched device JPEG decode into a packed RGB batch.
 
     ``sub_bits``: subsequence length of the parallel Huffman decode (bits per thread).
-    Pinned staging, device payload and workspace buffers grow on demand and are reused
-    across calls (one decoder per stream)."""
+    ``depth`` buffer sets rotate, so with ``sync=False`` the host work of batch i+1
+    (marker parse, descriptors, packing the scans into the pinned slab) overlaps the
+    upload and decode of batch i.  Buffers grow on demand and are reused."""
 
-    def __init__(self, device=None, sub_bits: int = DEFAULT_SUB_BITS):
+    def __init__(self, device=None, sub_bits: int = DEFAULT_SUB_BITS, depth: int = 2):
         self.device = require_device(device)
         self.sub_bits = int(sub_bits)
         self.lib = _lib.load()
         self.desc_bytes = int(self.lib.tp_jpeg_desc_bytes())
-        self._host = None
-        self._dev = None
-        self._work = None
+        self.slots = [_Slot() for _ in range(max(1, depth))]
+        self._i = 0
         self.last_fallback: list[int] = []  # images decoded on the host in the last call
         self.last_h2d_bytes = 0
-        self._copied = None  # event: the last upload out of the pinned slab finished
+        self._last = None
 
-    def _buffers(self, payload_bytes: int, work_bytes: int):
-        if self._host is None or self._host.numel() < payload_bytes:
+    @property
+    def _work(self):  # diagnostics (tools/jpeg_bench.py): the last batch's workspace
+        return self._last[0].work
+
+    def _buffers(self, sl: _Slot, payload_bytes: int, work_bytes: int, n: int):
+        if sl.host is None or sl.host.numel() < payload_bytes:
             cap = _round_up(int(payload_bytes * 1.25) + 4096, 1 << 20)
-            self._host = torch.empty(cap, dtype=torch.uint8, pin_memory=True)
-            self._dev = torch.empty(cap, dtype=torch.uint8, device=self.device)
-        if self._work is None or self._work.numel() < work_bytes:
-            self._work = torch.empty(_round_up(int(work_bytes * 1.25) + 4096, 1 << 20),
-                                     dtype=torch.uint8, device=self.device)
+            sl.host = torch.empty(cap, dtype=torch.uint8, pin_memory=True)
+            sl.dev = torch.empty(cap, dtype=torch.uint8, device=self.device)
+        if sl.work is None or sl.work.numel() < work_bytes:
+            sl.work = torch.empty(_round_up(int(work_bytes * 1.25) + 4096, 1 << 20),
+                                  dtype=torch.uint8, device=self.device)
+        if sl.status is None or sl.status.numel() < n:
+            cap = _round_up(n, 256)
+            sl.status = torch.empty(cap, dtype=torch.int32, device=self.device)
+            sl.status_host = torch.empty(cap, dtype=torch.int32, pin_memory=True)
 
     def decode(self, payloads: Sequence[bytes], out: Optional[PackedImages] = None,
-               stream: Optional[torch.cuda.Stream] = None, sync: bool = True) -> PackedImages:
+               stream: Optional[torch.cuda.Stream] = None, sync: bool = True):
         """Decode every payload to RGB uint8 HWC in one packed device batch (the
-        engine.layout_offsets layout).  Host fallbacks are patched in before returning."""
+        engine.layout_offsets layout).  sync=True: returns the PackedImages with host
+        fallbacks patched in; sync=False: returns a JpegBatch (call finish())."""
         n = len(payloads)
         if n == 0:
             raise ValueError("no payloads")
@@ -125,71 +180,69 @@ class JpegDecoder:
         desc_at = 0
         mark = _round_up(n * self.desc_bytes, 256)
         raw_off = np.zeros(n, dtype=np.int64)
-        for k in range(n):
-            if infos[k].status == TP_JPEG_OK:
-                raw_off[k] = mark
-                mark = _round_up(mark + int(infos[k].scan_len) + 64, 16)
-        payload_bytes = _round_up(mark, 256)
-        totals = np.zeros(5, dtype=np.int64)
+        scan_len = np.array([infos[k].scan_len for k in range(n)], dtype=np.int64)
+        ok = np.array([infos[k].status == TP_JPEG_OK for k in range(n)])
+        sizes = np.where(ok, (scan_len + 64 + 15) // 16 * 16, 0)
+        raw_off[:] = mark + np.concatenate([[0], np.cumsum(sizes)[:-1]]) if n else 0
+        raw_off[~ok] = 0
+        payload_bytes = _round_up(int(mark + sizes.sum()), 256)
+        totals = np.zeros(8, dtype=np.int64)
+        sl = self.slots[self._i % len(self.slots)]
+        self._i += 1
+        if sl.copied is not None:
+            sl.copied.synchronize()  # the slot's previous upload no longer reads the slab
+        if sl.done is not None:
+            sl.done.synchronize()  # nor its decode the workspace / status
         desc_host = (ctypes.c_uint8 * (n * self.desc_bytes))()
         work_bytes = int(self.lib.tp_jpeg_describe(
             ctypes.byref(infos), n, raw_off.ctypes.data, out_off.ctypes.data, self.sub_bits,
             ctypes.cast(desc_host, ctypes.c_void_p), totals.ctypes.data))
         if work_bytes < 0:
             _lib.check(-work_bytes, "tp_jpeg_describe")
-        if self._copied is not None:
-            self._copied.synchronize()  # the previous upload no longer reads the slab
-        self._buffers(payload_bytes, max(work_bytes, 4096))
-        hv = self._host.numpy()
-        hv[desc_at: desc_at + n * self.desc_bytes] = np.frombuffer(desc_host, dtype=np.uint8)
-        dev_idx = [k for k in range(n) if infos[k].status == TP_JPEG_OK]
-        if dev_idx:  # scan bytes into the pinned slab on the host thread pool
+        self._buffers(sl, payload_bytes, max(work_bytes, 4096), n)
+        ctypes.memmove(sl.host.data_ptr() + desc_at, desc_host, n * self.desc_bytes)
+        dev_idx = np.nonzero(ok)[0]
+        if len(dev_idx):  # scan bytes into the pinned slab on the host thread pool
             keep = [np.frombuffer(payloads[k], dtype=np.uint8) for k in dev_idx]
             src = np.array([a.ctypes.data + int(infos[k].scan_off) for a, k in zip(keep, dev_idx)],
                            dtype=np.uint64)
-            lens = np.array([[int(infos[k].scan_len), 1] for k in dev_idx], dtype=np.int32)
-            stride = lens[:, 0].astype(np.int64).copy()
+            lens = np.stack([scan_len[dev_idx], np.ones(len(dev_idx), np.int64)], 1).astype(np.int32)
+            stride = scan_len[dev_idx].copy()
             dst_off = raw_off[dev_idx].copy()
             _lib.call("tp_stage_pack", len(dev_idx), src.ctypes.data, stride.ctypes.data,
-                      lens.ctypes.data, 1, None, None, self._host.data_ptr(), dst_off.ctypes.data, 0)
+                      lens.ctypes.data, 1, None, None, sl.host.data_ptr(), dst_off.ctypes.data, 0)
         self.last_h2d_bytes = payload_bytes
+        stream = stream or torch.cuda.current_stream(self.device)
         if out is None:
             data = torch.empty(out_total, dtype=torch.uint8, device=self.device)
-            out = PackedImages(data, torch.from_numpy(out_off).to(self.device),
-                               torch.from_numpy(wh.copy()).to(self.device), 3, wh, out_off)
-        stream = stream or torch.cuda.current_stream(self.device)
-        status = torch.empty(n, dtype=torch.int32, device=self.device)
+            meta = torch.from_numpy(np.concatenate([out_off, wh.reshape(-1).astype(np.int64)]))
+            meta = meta.pin_memory().to(self.device, non_blocking=True)
+            out = PackedImages(data, meta[:n], meta[n:].to(torch.int32).view(n, 2), 3, wh, out_off)
         with torch.cuda.stream(stream):
-            self._dev[:payload_bytes].copy_(self._host[:payload_bytes], non_blocking=True)
-            self._copied = torch.cuda.Event()
-            self._copied.record(stream)
-        self._launch_args = (desc_at, n, totals, out, status)
+            sl.dev[:payload_bytes].copy_(sl.host[:payload_bytes], non_blocking=True)
+            sl.copied = torch.cuda.Event()
+            sl.copied.record(stream)
+        self._last = (sl, desc_at, n, totals, out)
         self.launch(stream)
-        self._status = status
+        with torch.cuda.stream(stream):
+            sl.status_host[:n].copy_(sl.status[:n], non_blocking=True)
+            sl.done = torch.cuda.Event()
+            sl.done.record(stream)
+        batch = JpegBatch(self, sl, payloads, out, host_arrays, wh, out_off, n)
         if not sync:
-            return out
-        st = status.cpu().numpy()  # synchronises the stream (the host slab is reusable)
-        self.last_fallback = sorted(set(host_arrays) | {k for k in range(n) if st[k] != 0})
-        for k in self.last_fallback:
-            a = host_arrays.get(k)
-            if a is None:
-                a = _host_decode(payloads[k])
-                if (a.shape[1], a.shape[0]) != tuple(wh[k]):
-                    raise RuntimeError("host decode size differs from the JPEG frame header")
-            o = int(out_off[k])
-            out.data[o: o + a.size].copy_(torch.from_numpy(np.ascontiguousarray(a).reshape(-1)))
+            return batch
+        batch.finish()
         return out
-
 
     def launch(self, stream: Optional[torch.cuda.Stream] = None) -> None:
         """(Re)launch the device decode of the last uploaded batch (K7 only: no host work,
-        no copies) -- what bench.py times as the decode kernels."""
-        desc_at, n, totals, out, status = self._launch_args
+        no copies) -- what tools/jpeg_bench.py times as the decode kernels."""
+        sl, desc_at, n, totals, out = self._last
         stream = stream or torch.cuda.current_stream(self.device)
         with torch.cuda.device(self.device):
-            _lib.call("tp_jpeg_decode", self._dev.data_ptr(), self._dev.data_ptr() + desc_at, n,
-                      totals.ctypes.data, self.sub_bits, self._work.data_ptr(),
-                      self._work.numel(), out.data.data_ptr(), status.data_ptr(),
+            _lib.call("tp_jpeg_decode", sl.dev.data_ptr(), sl.dev.data_ptr() + desc_at, n,
+                      totals.ctypes.data, self.sub_bits, sl.work.data_ptr(),
+                      sl.work.numel(), out.data.data_ptr(), sl.status.data_ptr(),
                       stream_handle(self.device, stream))
 
 
@@ -202,5 +255,5 @@ def decode_images(payloads: Sequence[bytes], device=None) -> list[np.ndarray]:
             for o, (w, h) in zip(pk.offsets_host, pk.wh_host)]
 
 
-__all__ = ["JpegDecoder", "TpJpegInfo", "decode_images", "parse",
+__all__ = ["JpegBatch", "JpegDecoder", "TpJpegInfo", "decode_images", "parse",
            "TP_JPEG_OK", "TP_JPEG_UNSUPPORTED", "TP_JPEG_CORRUPT"]

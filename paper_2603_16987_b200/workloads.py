@@ -132,6 +132,42 @@ def workload_bytes(wl: Workload, with_u8: bool = False) -> dict:
 
 
 # ---------------------------------------------------------------------------
+# compressed inputs: corpus-like content encoded as JPEG (decode-inclusive end to end)
+
+def scene_image(width: int, height: int, seed: int, noise: float = 10.0) -> np.ndarray:
+    """Smooth gradients + a few flat blocks + Gaussian noise, the character of the
+    reference corpus (make_corpus.py:111-136 draws sinusoid fields, blocks and N(0, 10)
+    noise); synthetic, generated here."""
+    rng = np.random.default_rng(seed)
+    yy, xx = np.mgrid[0:height, 0:width].astype(np.float32)
+    a = np.stack([(xx * 0.9 + yy * 0.4) % 256, 128 + 100 * np.sin(xx / 37.0 + yy / 53.0),
+                  (yy * 0.7 + 40) % 256], axis=-1)
+    for _ in range(3):
+        x0 = int(rng.integers(0, max(width // 2, 1)))
+        y0 = int(rng.integers(0, max(height // 2, 1)))
+        a[y0: y0 + height // 4, x0: x0 + width // 4] = rng.uniform(0, 255, 3)
+    a += rng.normal(0.0, noise, a.shape).astype(np.float32)
+    return np.clip(a, 0, 255).astype(np.uint8)
+
+
+def jpeg_payloads(n: int, width: int = 1920, height: int = 1080, quality: int = 85,
+                  seed: int = 20260817, distinct: int = 8) -> list:
+    """n JPEG payloads (Pillow, baseline 4:2:0, the reference corpus encoder settings,
+    make_corpus.py:139-142) of `distinct` different scenes, repeated."""
+    import io
+
+    from PIL import Image
+
+    base = []
+    for k in range(min(n, distinct)):
+        buf = io.BytesIO()
+        Image.fromarray(scene_image(width, height, seed + k)).save(buf, format="JPEG",
+                                                                   quality=quality)
+        base.append(buf.getvalue())
+    return [base[k % len(base)] for k in range(n)]
+
+
+# ---------------------------------------------------------------------------
 # C5 prompts: rendered chat prompts tokenized on the device (K6)
 
 C5_PROMPTS = [

@@ -60,7 +60,7 @@ def test_describe_layout_host_only():
     out_off = np.array([0, 64 * 48 * 3, 64 * 48 * 3 + 40 * 30 * 3], dtype=np.int64)
     lib = PJ._lib.load()
     desc = (ctypes.c_uint8 * (n * int(lib.tp_jpeg_desc_bytes())))()
-    totals = np.zeros(5, dtype=np.int64)
+    totals = np.zeros(8, dtype=np.int64)
     w = lib.tp_jpeg_describe(ctypes.byref(infos), n, raw_off.ctypes.data, out_off.ctypes.data,
                              2048, ctypes.cast(desc, ctypes.c_void_p), totals.ctypes.data)
     assert w > totals[4] >= totals[3] >= 4096
