@@ -779,6 +779,73 @@ def run_e2e_jpeg(args, dist, device, cfg) -> dict:
     return res
 
 
+def run_dropin(args, device, runs: int = 60) -> dict:
+    """The drop-in per-request path: preprocess(payload, cfg) for one 1080p image as a
+    JPEG (device decode) and as a PNG (Pillow decode on the host, as the reference),
+    C2 tiling, sequential requests; p50/p99 and the median of every stage_timings_ns
+    key, beside the reference's own vlmfp.preprocess (fastest toggles, one host core)
+    on the same payloads."""
+    import io
+
+    import torch
+    from PIL import Image
+
+    from paper_2603_16987_b200 import imgproc
+    from paper_2603_16987_b200.workloads import IMAGENET_MEAN, IMAGENET_STD, scene_image
+
+    px = scene_image(1920, 1080, 4242)
+    payloads = {}
+    for fmt, kw in (("jpeg", {"quality": 85}), ("png", {})):
+        buf = io.BytesIO()
+        Image.fromarray(px).save(buf, format=fmt.upper(), **kw)
+        payloads[fmt] = buf.getvalue()
+    cfg = imgproc.PreprocessConfig(tile_edge=448, max_tiles=12, mean=IMAGENET_MEAN,
+                                   std=IMAGENET_STD, reduced_precision_normalize=True,
+                                   fused_transform=True, contiguous_tensor_path=True,
+                                   avoid_per_item_split=True, skip_pixel_mask=True,
+                                   decode_once=True, simd_decode=True)
+    out = {}
+    for fmt, p in payloads.items():
+        for _ in range(5):
+            imgproc.preprocess(p, cfg)
+        torch.cuda.synchronize(device)
+        ts, stages = [], {}
+        for _ in range(runs):
+            t0 = time.perf_counter_ns()
+            r = imgproc.preprocess(p, cfg)
+            ts.append((time.perf_counter_ns() - t0) / 1e6)
+            for k, v in r.stage_timings_ns.items():
+                stages.setdefault(k, []).append(v / 1e6)
+        res = {"payload_kb": round(len(p) / 1e3, 1), "p50_ms": round(float(np.median(ts)), 3),
+               "p99_ms": round(float(np.percentile(ts, 99)), 3),
+               "stages_ms_p50": {k: round(float(np.median(v)), 3) for k, v in stages.items()},
+               "tiles": len(r.tiles), "dtype": r.tiles[0].elem}
+        V = reference_module()
+        if V is not None and not args.no_cpu_baseline:
+            vcfg = V.PreprocessConfig(**{f: getattr(cfg, f) for f in (
+                "tile_edge", "max_tiles", "mean", "std", "normalize_precision", "fused_transform",
+                "contiguous_tensor_path", "decode_once", "reduced_precision_normalize",
+                "simd_decode", "skip_pixel_mask", "avoid_per_item_split")})
+            V.preprocess(p, vcfg)
+            rt, rst = [], {}
+            for _ in range(15):
+                t0 = time.perf_counter_ns()
+                rr = V.preprocess(p, vcfg)
+                rt.append((time.perf_counter_ns() - t0) / 1e6)
+                for k, v in rr.stage_timings_ns.items():
+                    rst.setdefault(k, []).append(v / 1e6)
+            res["reference"] = {"p50_ms": round(float(np.median(rt)), 3),
+                                "p99_ms": round(float(np.percentile(rt, 99)), 3),
+                                "stages_ms_p50": {k: round(float(np.median(v)), 3)
+                                                  for k, v in rst.items()},
+                                "cores": 1, "kind": "reference",
+                                "sample": "15 sequential vlmfp.preprocess calls, fastest toggles"}
+        out[fmt] = res
+    out["timing"] = ("host wall clock per call (the drop-in returns host ImageBuffers, so "
+                     "each call ends after the tiles' readback); sequential, one stream")
+    return out
+
+
 def _host_threads() -> int:
     from paper_2603_16987_b200 import _lib
 
@@ -1055,6 +1122,7 @@ def main(argv=None):
         if dist.rank == 0:
             sub["c3"] = run_single(args, dist, device, "c3")
             sub["c1"] = run_single(args, dist, device, "c1")
+            sub["dropin"] = run_dropin(args, device)
 
     cpu = None
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:

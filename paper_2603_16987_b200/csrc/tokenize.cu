@@ -101,28 +101,172 @@ __global__ void k_tok_match(const uint8_t* __restrict__ vocab, const uint8_t* __
   }
 }
 
-// K6b: the greedy walk of each text through the match table; ids land at the text's
-// byte offset (a text of B bytes yields at most B ids), counts per text
-__global__ void k_tok_walk(const int64_t* __restrict__ text_off, int n_texts,
-                           const int32_t* __restrict__ m_id, const uint8_t* __restrict__ m_len,
-                           int32_t* __restrict__ stage_ids, int32_t* __restrict__ counts,
-                           int32_t* __restrict__ err) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n_texts) return;
-  const int64_t beg = text_off[t], end = text_off[t + 1];
-  int64_t pos = beg;
-  int k = 0, e = 0;
-  while (pos < end) {
-    const int id = m_id[pos];
-    if (id < 0) {
-      e = -id;  // 0x100 | offending byte
-      break;
+// K6b: the greedy walk through the match table, one warp per text, in segments of
+// kSeg bytes (one lane each) so a long text is walked in parallel:
+//  (1) every segment walks speculatively from its first byte to its end, recording the
+//      rank (tokens before it) of each position it visits;
+//  (2) the true walk enters a segment at one of its first kMaxTokenBytes positions (the
+//      first boundary at or after its start); for each such candidate entry the lane
+//      walks until it lands on a position its speculative walk visited -- greedy walks
+//      are deterministic, so from there the speculative tail is the true one (usually
+//      one or two tokens) -- giving (exit, token count) per candidate;
+//  (3) lane 0 chains the segments: entry of segment j+1 = exit of segment j for its
+//      entry (a table lookup per segment), then a warp scan of the counts places every
+//      segment's first id, and each lane re-walks its segment writing the ids.
+// A byte with neither a token nor a fallback on the true path makes the text an error.
+constexpr int kSeg = 256;
+constexpr int kCand = kMaxTokenBytes;
+
+struct SegCand {
+  int32_t exit[kCand];
+  int32_t cnt[kCand];   // tokens from the candidate entry to the exit; -1: error on the path
+  int32_t spec_exit, spec_cnt, spec_err;  // the speculative walk from the segment start
+};
+
+__device__ __forceinline__ int64_t seg_index(int64_t beg, int t, int j) {
+  return beg / kSeg + t + j;  // unique across texts (texts are disjoint byte ranges)
+}
+
+__global__ void __launch_bounds__(128) k_tok_walk(const int64_t* __restrict__ text_off, int n_texts,
+                                                  const int32_t* __restrict__ m_id,
+                                                  const uint8_t* __restrict__ m_len,
+                                                  int32_t* __restrict__ rank,
+                                                  SegCand* __restrict__ cand,
+                                                  int32_t* __restrict__ seg_entry,
+                                                  int32_t* __restrict__ stage_ids,
+                                                  int32_t* __restrict__ counts,
+                                                  int32_t* __restrict__ err) {
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < n_texts; t += warps) {
+    const int64_t beg = text_off[t], end = text_off[t + 1];
+    const int nseg = static_cast<int>((end - beg + kSeg - 1) / kSeg);
+    // (1) speculative walks; positions are text-relative (< 2^31)
+    for (int j = lane; j < nseg; j += 32) {
+      const int64_t q = beg + static_cast<int64_t>(j) * kSeg;
+      const int64_t qe = q + kSeg < end ? q + kSeg : end;
+      int64_t pos = q;
+      int k = 0, bad = 0;
+      while (pos < qe) {
+        const int id = m_id[pos];
+        rank[pos] = id < 0 ? -2 : k;  // -2: the walk stops here (no token, no fallback)
+        if (id < 0) {
+          bad = 1;
+          break;
+        }
+        ++k;
+        pos += m_len[pos];
+      }
+      SegCand& sc = cand[seg_index(beg, t, j)];
+      sc.spec_exit = static_cast<int32_t>(pos - beg);
+      sc.spec_cnt = k;
+      sc.spec_err = bad;
     }
-    stage_ids[beg + k++] = id;
-    pos += m_len[pos];
+    __syncwarp();
+    // (2) every candidate entry of every segment
+    for (int j = lane; j < nseg; j += 32) {
+      const int64_t q = beg + static_cast<int64_t>(j) * kSeg;
+      const int64_t qe = q + kSeg < end ? q + kSeg : end;
+      SegCand& sc = cand[seg_index(beg, t, j)];
+      const int64_t sx = beg + sc.spec_exit;  // the speculative walk's own totals
+      const int sk = sc.spec_cnt;
+      const bool serr = sc.spec_err != 0;
+      for (int c = 0; c < kCand; ++c) {
+        int64_t pos = q + c;
+        int k = 0;
+        int out_cnt = -1;
+        int64_t out_exit = pos;
+        if (pos >= qe) {  // the entry is already past this segment
+          out_cnt = 0;
+        } else {
+          while (true) {
+            if (pos >= qe) {
+              out_cnt = k;
+              out_exit = pos;
+              break;
+            }
+            const int r = rank[pos];
+            if (r >= 0) {  // joined the speculative walk
+              out_cnt = serr ? -1 : k + sk - r;
+              out_exit = sx;
+              break;
+            }
+            const int id = m_id[pos];
+            if (id < 0) break;  // error on this path
+            ++k;
+            pos += m_len[pos];
+          }
+        }
+        sc.exit[c] = static_cast<int32_t>(out_exit - beg);
+        sc.cnt[c] = out_cnt;
+      }
+    }
+    __syncwarp();
+    // (3) chain the segments (lane 0), scan, write
+    int e_code = 0;
+    if (lane == 0) {
+      int64_t e = beg;
+      for (int j = 0; j < nseg; ++j) {
+        const int64_t q = beg + static_cast<int64_t>(j) * kSeg;
+        if (e >= end) {
+          seg_entry[seg_index(beg, t, j)] = -1;  // nothing left to walk
+          continue;
+        }
+        const SegCand& sc = cand[seg_index(beg, t, j)];
+        const int c = static_cast<int>(e - q);
+        seg_entry[seg_index(beg, t, j)] = static_cast<int32_t>(e - beg);
+        if (sc.cnt[c] < 0) {
+          // find the offending byte on the true path (the reference raises there)
+          int64_t pos = e;
+          while (pos < end && m_id[pos] >= 0) pos += m_len[pos];
+          e_code = pos < end ? -m_id[pos] : 0x100;
+          break;
+        }
+        e = beg + sc.exit[c];
+      }
+    }
+    e_code = __shfl_sync(0xffffffffu, e_code, 0);
+    if (e_code) {
+      if (lane == 0) {
+        counts[t] = 0;
+        err[t] = e_code;
+      }
+      continue;
+    }
+    int carry = 0;
+    for (int j0 = 0; j0 < nseg; j0 += 32) {
+      const int j = j0 + lane;
+      int cnt = 0, e_rel = -1;
+      if (j < nseg) {
+        e_rel = seg_entry[seg_index(beg, t, j)];
+        if (e_rel >= 0) {
+          const int64_t q = beg + static_cast<int64_t>(j) * kSeg;
+          cnt = cand[seg_index(beg, t, j)].cnt[static_cast<int>(beg + e_rel - q)];
+        }
+      }
+      int x = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (e_rel >= 0) {
+        const int64_t q = beg + static_cast<int64_t>(j) * kSeg;
+        const int64_t qe = q + kSeg < end ? q + kSeg : end;
+        int64_t pos = beg + e_rel;
+        int k = carry + x - cnt;
+        while (pos < qe) {
+          stage_ids[beg + k++] = m_id[pos];
+          pos += m_len[pos];
+        }
+      }
+      carry += __shfl_sync(0xffffffffu, x, 31);
+    }
+    if (lane == 0) {
+      counts[t] = carry;
+      err[t] = 0;
+    }
   }
-  counts[t] = e ? 0 : k;
-  err[t] = e;
 }
 
 // K6c: exclusive scan of the counts -> out_off (one CTA); out_off[n] = total
@@ -201,13 +345,20 @@ extern "C" int tp_vocab_build(const uint8_t* tok_bytes, const int32_t* tok_off,
   return TP_OK;
 }
 
+namespace {
+// workspace: match ids | staged ids | walk ranks (int32 per byte) | match lengths (u8 per
+// byte) | counts (int32 per text) | per segment: candidates, true entry
+int64_t n_segs(int64_t total_bytes, int32_t n_texts) { return total_bytes / tp::kSeg + n_texts + 1; }
+int64_t al256(int64_t v) { return (v + 255) & ~int64_t(255); }
+}  // namespace
+
 extern "C" int64_t tp_tokenize_workspace_bytes(int64_t total_bytes, int32_t n_texts) {
   if (total_bytes < 0 || n_texts < 0) return -1;
-  // match ids (int32), match lengths (u8), staged ids (int32), counts (int32)
-  const int64_t a = (total_bytes * 4 + 255) & ~int64_t(255);
-  const int64_t b = (total_bytes + 255) & ~int64_t(255);
-  const int64_t c = (static_cast<int64_t>(n_texts) * 4 + 255) & ~int64_t(255);
-  return 2 * a + b + c;
+  const int64_t a = al256(total_bytes * 4);
+  const int64_t b = al256(total_bytes);
+  const int64_t c = al256(static_cast<int64_t>(n_texts) * 4);
+  const int64_t segs = n_segs(total_bytes, n_texts);
+  return 3 * a + b + c + al256(segs * static_cast<int64_t>(sizeof(tp::SegCand))) + al256(segs * 4);
 }
 
 extern "C" int tp_tokenize(const void* d_vocab, const uint8_t* d_text, const int64_t* d_text_off,
@@ -224,12 +375,18 @@ extern "C" int tp_tokenize(const void* d_vocab, const uint8_t* d_text, const int
     return tp::set_error(TP_ERR_UNSUPPORTED, "tp_tokenize: more than 2^31 bytes per batch");
   cudaStream_t s = tp::as_stream(stream);
   uint8_t* ws = static_cast<uint8_t*>(d_workspace);
-  const int64_t a = (total_bytes * 4 + 255) & ~int64_t(255);
-  const int64_t b = (total_bytes + 255) & ~int64_t(255);
+  const int64_t a = al256(total_bytes * 4);
+  const int64_t b = al256(total_bytes);
+  const int64_t c = al256(static_cast<int64_t>(n_texts) * 4);
+  const int64_t segs = n_segs(total_bytes, n_texts);
   int32_t* m_id = reinterpret_cast<int32_t*>(ws);
   int32_t* stage = reinterpret_cast<int32_t*>(ws + a);
-  uint8_t* m_len = ws + 2 * a;
-  int32_t* counts = reinterpret_cast<int32_t*>(ws + 2 * a + b);
+  int32_t* rank = reinterpret_cast<int32_t*>(ws + 2 * a);
+  uint8_t* m_len = ws + 3 * a;
+  int32_t* counts = reinterpret_cast<int32_t*>(ws + 3 * a + b);
+  auto* cand = reinterpret_cast<tp::SegCand*>(ws + 3 * a + b + c);
+  int32_t* seg_entry = reinterpret_cast<int32_t*>(ws + 3 * a + b + c +
+                                                  al256(segs * static_cast<int64_t>(sizeof(tp::SegCand))));
   if (n_texts > 0) {
     const int sms = std::max(1, tp::device_sm_count());
     if (total_bytes > 0) {
@@ -238,8 +395,10 @@ extern "C" int tp_tokenize(const void* d_vocab, const uint8_t* d_text, const int
       tp::k_tok_match<<<std::min(n_texts, 16 * sms), 128, 0, s>>>(
           static_cast<const uint8_t*>(d_vocab), d_text, d_text_off, n_texts, m_id, m_len);
     }
-    tp::k_tok_walk<<<(n_texts + 127) / 128, 128, 0, s>>>(d_text_off, n_texts, m_id, m_len,
-                                                         stage, counts, d_err);
+    if (total_bytes > 0 && cudaMemsetAsync(rank, 0xFF, 4 * total_bytes, s) != cudaSuccess)
+      return tp::set_error(TP_ERR_CUDA, "tp_tokenize: memset failed");
+    tp::k_tok_walk<<<std::min<int>((n_texts + 3) / 4, 16 * sms), 128, 0, s>>>(
+        d_text_off, n_texts, m_id, m_len, rank, cand, seg_entry, stage, counts, d_err);
   }
   tp::k_tok_scan<<<1, 1024, 0, s>>>(counts, n_texts, d_out_off);
   if (n_texts > 0 && total_bytes > 0) {

@@ -331,6 +331,14 @@ class PlaceholderExpander:
         self.tpt = int(tokens_per_tile)
         self.with_mask = with_mask
         self.device = require_device(device)
+        self._work = None
+
+    def workspace(self, n_seq: int) -> torch.Tensor:
+        """tp_expand's workspace (per-sequence output lengths), grown on demand."""
+        nbytes = max(8, int(_lib.load().tp_expand_workspace_bytes(n_seq)))
+        if self._work is None or self._work.numel() < nbytes:
+            self._work = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        return self._work
 
     def __call__(self, ids: torch.Tensor, seq_off: torch.Tensor, counts: torch.Tensor,
                  count_off: torch.Tensor, capacity: int, out: Optional[ExpandedBatch] = None,
@@ -352,7 +360,8 @@ class PlaceholderExpander:
                       _lib.ptr(count_off), self.tpt, self.marker, self.ctx, self.asst,
                       1 if self.with_mask else 0, _lib.ptr(out.ids), capacity,
                       _lib.ptr(out.out_off), _lib.ptr(out.spans), _lib.ptr(out.first_assistant),
-                      _lib.ptr(out.mask), _lib.ptr(out.err), None, stream_handle(d, stream))
+                      _lib.ptr(out.mask), _lib.ptr(out.err), _lib.ptr(self.workspace(n_seq)),
+                      stream_handle(d, stream))
         return out
 
 
