@@ -93,10 +93,6 @@ __device__ unsigned int g_tp_checks;
 #ifndef TP_K2_DWIN  // affine path: window test on d = T - round(T) instead of N = round(8192 t)
 #define TP_K2_DWIN 1
 #endif
-#ifndef TP_K2_DEFER  // affine bf16 NCHW path: flagged values queued (2 per thread, in registers)
-                     // and recomputed in fp64 after the phase's rows, warp-uniformly
-#define TP_K2_DEFER 0
-#endif
 #ifndef TP_K2_BAND_ADAPT  // with TP_K2_BAND 32: use 16 when tiles per image <= 4
 #define TP_K2_BAND_ADAPT 1
 #endif
@@ -1015,55 +1011,9 @@ __device__ __forceinline__ void consume_pair_rows(
       if (EK > 0 && LAYOUT == TP_LAYOUT_NCHW) oc[0] += E;
     }
   };
-  // Deferred fallback (TP_K2_DEFER, the affine bf16 NCHW instance): a flagged value is
-  // stored with its fast result now and queued -- its four taps packed in one word, its
-  // row / channel / pixel in another -- and recomputed exactly after the phase's rows,
-  // every lane of the warp at once, so the fp64 work no longer diverges row by row.  A
-  // thread holds two queued values; beyond that the value is fixed inline as before.
-  constexpr bool DEFER = TP_K2_DEFER && DW && LAYOUT == TP_LAYOUT_NCHW && sizeof(OutT) == 2;
-  uint32_t q0t = 0, q0m = 0, q1t = 0, q1m = 0;
-  int qn = 0;
-  auto taps4 = [&](const PixTaps& p, int c) -> uint32_t {  // bytes s00 s01 s10 s11
-    const uint32_t sel = static_cast<uint32_t>(c) | (static_cast<uint32_t>(C + c) << 4);
-    return __byte_perm(__byte_perm(p.r0w0, p.r0w1, sel), __byte_perm(p.r1w0, p.r1w1, sel), 0x5410);
-  };
   auto row = [&](int jj, const PixTaps& a, const PixTaps& b) {
     uint32_t ka[C], kb[C], xa[C], xb[C];
-    if (fast(jj, a, b, ka, kb, xa, xb)) {
-      if (DEFER) {
-        uint32_t fa[C], fb[C];  // flagged values beyond the queue: fixed inline
-        bool inline_fix = false;
-#pragma unroll
-        for (int c = 0; c < C; ++c) {
-#pragma unroll
-          for (int side = 0; side < 2; ++side) {
-            const uint32_t x = side ? xb[c] : xa[c];
-            uint32_t& keep = side ? fb[c] : fa[c];
-            keep = 0u;  // not flagged: fix() skips it
-            if (!flagged(x)) continue;
-            if (qn < 2) {
-              const uint32_t t = taps4(side ? b : a, c);
-              const uint32_t m = static_cast<uint32_t>(jj) | (static_cast<uint32_t>(c) << 5) |
-                                 (static_cast<uint32_t>(side) << 7);
-              if (qn == 0) {
-                q0t = t;
-                q0m = m;
-              } else {
-                q1t = t;
-                q1m = m;
-              }
-              ++qn;
-            } else {
-              keep = x;
-              inline_fix = true;
-            }
-          }
-        }
-        if (inline_fix) fix(jj, a, b, ka, kb, fa, fb);
-      } else {
-        fix(jj, a, b, ka, kb, xa, xb);
-      }
-    }
+    if (fast(jj, a, b, ka, kb, xa, xb)) fix(jj, a, b, ka, kb, xa, xb);
     emit(jj, ka, kb);
   };
   constexpr uint32_t kLim = TP_CHECKS ? static_cast<uint32_t>(arena_bytes<C, OutT>()) : 0u;
@@ -1082,29 +1032,6 @@ __device__ __forceinline__ void consume_pair_rows(
     row(jj + 1, a1, b1);
   }
   if (jj < nrows) row(jj, a0, b0);
-  if (DEFER) {
-    // the queued values, warp-uniformly: exact fp64 in the reference order, normalize,
-    // and the store over the fast result
-    const int nq = __reduce_max_sync(0xffffffffu, qn);
-    for (int i = 0; i < nq; ++i) {
-      if (i < qn) {
-        const uint32_t t = i == 0 ? q0t : q1t, m = i == 0 ? q0m : q1m;
-        const int qj = static_cast<int>(m & 31), c = static_cast<int>((m >> 5) & 3);
-        const bool sb = (m >> 7) & 1;
-        const double fy64 = ldsd(pr.base + kPhFy64 + 8 * qj), omfy64 = __dsub_rn(1.0, fy64);
-        const double nw1 = __dmul_rn(fy64, -4503599627370496.0),
-                     nw0 = __dmul_rn(omfy64, -4503599627370496.0);
-        const uint32_t k = blend_exact_fma(t & 255, (t >> 8) & 255, (t >> 16) & 255, t >> 24, fy64,
-                                           omfy64, nw1, nw0, sb ? fxb64 : fxa64,
-                                           sb ? omfxb64 : omfxa64);
-        const float ac = c == 0 ? aff_a[0] : c == 1 ? aff_a[C > 1 ? 1 : 0] : aff_a[C > 2 ? 2 : 0];
-        const float bc = c == 0 ? aff_b[0] : c == 1 ? aff_b[C > 1 ? 1 : 0] : aff_b[C > 2 ? 2 : 0];
-        const __nv_bfloat16 y = __float2bfloat16_rn(fmaf(static_cast<float>(k), ac, bc));
-        OutT* dst = tile_a + static_cast<int64_t>(j0 + qj) * E + c * EE + (sb ? ob_off : 0);
-        *reinterpret_cast<__nv_bfloat16*>(dst) = y;
-      }
-    }
-  }
 }
 
 template <int C, typename OutT, int LAYOUT, bool WRITE_OUT, bool WRITE_U8, bool AFFINE, int EK>

@@ -69,6 +69,9 @@ def main():
     # ABW=c2,c4k,c3x32,up,tall,c2s selects the workloads (default: c2,c4k,c3x32);
     # c2s is C2 on smooth synthetic content (kind 1), which flags more exact ties
     variants = sorted(p for p in (ROOT / "build" / "variants").glob("*/libtileprep.so"))
+    if os.environ.get("ABV"):  # ABV=name,name selects the variants
+        keep = os.environ["ABV"].split(",")
+        variants = [p for p in variants if p.parent.name in keep]
     results = {p.parent.name: [] for p in variants}
     for r in range(rounds):
         for lib in variants:
