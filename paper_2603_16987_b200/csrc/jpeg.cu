@@ -48,6 +48,7 @@ __constant__ uint8_t c_zig[64] = {0,  1,  8,  16, 9,  2,  3,  10, 17, 24, 32, 25
 
 constexpr int kMaxSteps = 160;  // sync half-rounds before an image is handed to the host
 constexpr int kNoErr = 0x7FFFFFFF;
+constexpr int kMaxHops = 16;  // subsequences one thread re-decodes in a chain per half-round
 constexpr int kCkpts = 7;  // checkpoints per subsequence (every sub_bits / 8 bits)
 
 struct Work {
@@ -62,6 +63,7 @@ struct Work {
   int* err;            // block count at the first unclean symbol, kNoErr if none
   int* errpos;         // its bit position
   int* bstart;         // block index (in the image) at the entry
+  int* claim;          // half-round in which a thread last took this slot (one decode each)
   long long* ck_state; // [slot][kCkpts] checkpoint states
   int4* ck_acc;        // [slot][kCkpts] checkpoint accumulators
 };
@@ -79,8 +81,8 @@ __device__ inline Work work_view(uint8_t* w, int64_t slots) {
   o += al256(8 * slots);
   v.dcs = reinterpret_cast<int4*>(w + o);
   o += al256(16 * slots);
-  int* arrs[4];
-  for (int i = 0; i < 4; ++i) {
+  int* arrs[5];
+  for (int i = 0; i < 5; ++i) {
     arrs[i] = reinterpret_cast<int*>(w + o);
     o += al256(4 * slots);
   }
@@ -88,6 +90,7 @@ __device__ inline Work work_view(uint8_t* w, int64_t slots) {
   v.err = arrs[1];
   v.errpos = arrs[2];
   v.bstart = arrs[3];
+  v.claim = arrs[4];
   v.ck_state = reinterpret_cast<long long*>(w + o);
   o += al256(8 * kCkpts * slots);
   v.ck_acc = reinterpret_cast<int4*>(w + o);
@@ -654,7 +657,7 @@ __device__ inline int4 block_scan4(int4 v, int4* sh, int4& total) {
 
 __global__ void __launch_bounds__(256) k_jpeg_huff(const JDesc* __restrict__ descs, int n,
                                                    int64_t total_slots, int sub_bits,
-                                                   uint8_t* __restrict__ work,
+                                                   int lead_bits, uint8_t* __restrict__ work,
                                                    int32_t* __restrict__ status) {
   cg::grid_group grid = cg::this_grid();
   __shared__ ChunkTables ct;
@@ -665,7 +668,8 @@ __global__ void __launch_bounds__(256) k_jpeg_huff(const JDesc* __restrict__ des
   const int64_t nthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;
   if (threadIdx.x == 0) ct.img[0] = ct.img[1] = -1;
   if (tid == 0) W.stamps[0] = gtimer();
-  const uint32_t overlap = static_cast<uint32_t>(sub_bits);  // speculative lead-in
+  const uint32_t overlap = lead_bits > 0 ? static_cast<uint32_t>(lead_bits)
+                                         : static_cast<uint32_t>(sub_bits);  // speculative lead-in
 
   // (0) subsequences per interval (sub_prefix after seg_start)
   for (int64_t k = tid; k < n; k += nthreads) {
@@ -721,6 +725,7 @@ __global__ void __launch_bounds__(256) k_jpeg_huff(const JDesc* __restrict__ des
     W.err[g] = o.err;
     W.errpos[g] = static_cast<int>(ep);
     W.dcs[g] = make_int4(0, o.dc[0], o.dc[1], o.dc[2]);
+    W.claim[g] = 0;
   }
   if (tid == 0) W.stamps[1] = gtimer();
 
@@ -738,37 +743,51 @@ __global__ void __launch_bounds__(256) k_jpeg_huff(const JDesc* __restrict__ des
       if (!__syncthreads_or(need)) continue;
       const JHuff* tabs = chunk_tables(ct, descs, n, base, total_slots, need ? r.k : -1);
       if (!need) continue;
-      atomicAdd(W.counters + 512 + h, 1u);
       const JDesc& d = descs[r.k];
       Tabs T;
       T.load(d, tabs);
       BitReader br;
       br.init(work + d.clean_off);
-      const long long e = W.exitp[g - 1];
-      uint32_t pos;
-      int u, z;
-      unpack_state(e, pos, u, z);
-      const uint32_t stop = min(static_cast<uint32_t>(r.j + 1) * sub_bits, r.seg_bits);
-      Ckpt ck;
-      init_ckpt(ck, W, g, r.j, sub_bits);
-      ck.compare = true;
-      ck.prev_exit = W.exitp[g];
-      ck.prev_blocks = W.blocks[g];
-      ck.prev_err = W.err[g];
-      ck.prev_errpos = static_cast<uint32_t>(W.errpos[g]);
-      ck.prev_dc = W.dcs[g];
-      uint32_t ep;
-      const DecOut o = decode_run<1, true>(T, br, r.bit0, r.seg_bits, stop, pos, u, z, nullptr, 0, 0,
-                                           nullptr, &ck, &ep);
-      const long long x = pack_state(o.pos, o.u, o.z);
-      W.entry[g] = e;
-      W.blocks[g] = o.blocks;
-      W.err[g] = o.err;
-      W.errpos[g] = static_cast<int>(ep);
-      W.dcs[g] = make_int4(0, o.dc[0], o.dc[1], o.dc[2]);
-      if (x != W.exitp[g]) {
-        W.exitp[g] = x;
+      const int32_t* sub_prefix =
+          reinterpret_cast<const int32_t*>(work + d.seg_off) + d.n_seg + 1;
+      const int n_sub = sub_prefix[r.s + 1] - sub_prefix[r.s];
+      long long e = W.exitp[g - 1];
+      // a changed exit is carried into the next subsequence(s) right away: that one has
+      // the other parity, so no other thread decodes it in this half-round, and a chain
+      // of subsequences that missed their lead-in is resolved in one half-round, not one
+      // half-round per link (the successor of the chain is re-checked next half-round)
+      for (int hop = 0, j = r.j; hop < kMaxHops && j < n_sub; ++hop, ++j) {
+        const int64_t gg = g + hop;
+        if (hop > 0 && W.entry[gg] == e) break;
+        // one decode per slot and half-round: a chain running into a slot another thread
+        // took (or the other way round) stops; the next half-round re-checks it
+        if (atomicMax(W.claim + gg, h) == h) break;
+        atomicAdd(W.counters + 512 + h, 1u);
+        uint32_t pos;
+        int u, z;
+        unpack_state(e, pos, u, z);
+        const uint32_t stop = min(static_cast<uint32_t>(j + 1) * sub_bits, r.seg_bits);
+        Ckpt ck;
+        init_ckpt(ck, W, gg, j, sub_bits);
+        ck.compare = true;
+        ck.prev_exit = W.exitp[gg];
+        ck.prev_blocks = W.blocks[gg];
+        ck.prev_err = W.err[gg];
+        ck.prev_errpos = static_cast<uint32_t>(W.errpos[gg]);
+        ck.prev_dc = W.dcs[gg];
+        uint32_t ep;
+        const DecOut o = decode_run<1, true>(T, br, r.bit0, r.seg_bits, stop, pos, u, z, nullptr,
+                                             0, 0, nullptr, &ck, &ep);
+        const long long x = pack_state(o.pos, o.u, o.z);
+        W.entry[gg] = e;
+        W.blocks[gg] = o.blocks;
+        W.err[gg] = o.err;
+        W.errpos[gg] = static_cast<int>(ep);
+        W.dcs[gg] = make_int4(0, o.dc[0], o.dc[1], o.dc[2]);
+        if (x == W.exitp[gg]) break;
+        W.exitp[gg] = x;
         atomicAdd(W.counters + h, 1u);
+        e = x;
       }
     }
     grid.sync();
@@ -1166,8 +1185,9 @@ TP_API int tp_jpeg_decode(const uint8_t* d_payload, const void* d_desc, int32_t 
     int nn = n;
     int64_t ts = slots;
     int sb = sub_bits;
+    int lb = static_cast<int>(totals[7]);  // speculative lead-in bits (0: sub_bits)
     int32_t* st = d_status;
-    void* args[] = {&descs, &nn, &ts, &sb, &work, &st};
+    void* args[] = {&descs, &nn, &ts, &sb, &lb, &work, &st};
     cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_jpeg_huff), grid, 256,
                                                 args, 0, s);
     if (e != cudaSuccess) return set_error(TP_ERR_CUDA, "tp_jpeg_decode: %s", cudaGetErrorString(e));

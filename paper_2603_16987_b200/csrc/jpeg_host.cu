@@ -314,7 +314,7 @@ TP_API int64_t tp_jpeg_describe(const TpJpegInfo* infos, int32_t n, const int64_
   int64_t w = 4096;                         // step counters
   w += 2 * align_up(8 * slots, 256);        // exit, entry
   w += align_up(16 * slots, 256);           // DC sums / predictors
-  w += 4 * align_up(4 * slots, 256);        // blocks, err, errpos, bstart
+  w += 5 * align_up(4 * slots, 256);        // blocks, err, errpos, bstart, claim
   w += align_up(8 * 7 * slots, 256);        // checkpoint states (jpeg.cu kCkpts = 7)
   w += align_up(16 * 7 * slots, 256);       // checkpoint accumulators
   totals[6] = w;                            // unstuff chunk counts

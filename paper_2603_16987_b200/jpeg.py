@@ -126,9 +126,11 @@ class JpegDecoder:
     (marker parse, descriptors, packing the scans into the pinned slab) overlaps the
     upload and decode of batch i.  Buffers grow on demand and are reused."""
 
-    def __init__(self, device=None, sub_bits: int = DEFAULT_SUB_BITS, depth: int = 2):
+    def __init__(self, device=None, sub_bits: int = DEFAULT_SUB_BITS, depth: int = 2,
+                 lead_bits: int = 0):
         self.device = require_device(device)
         self.sub_bits = int(sub_bits)
+        self.lead_bits = int(lead_bits)  # speculative lead-in per subsequence (0: sub_bits)
         self.lib = _lib.load()
         self.desc_bytes = int(self.lib.tp_jpeg_desc_bytes())
         self.slots = [_Slot() for _ in range(max(1, depth))]
@@ -199,6 +201,7 @@ class JpegDecoder:
             ctypes.cast(desc_host, ctypes.c_void_p), totals.ctypes.data))
         if work_bytes < 0:
             _lib.check(-work_bytes, "tp_jpeg_describe")
+        totals[7] = self.lead_bits
         self._buffers(sl, payload_bytes, max(work_bytes, 4096), n)
         ctypes.memmove(sl.host.data_ptr() + desc_at, desc_host, n * self.desc_bytes)
         dev_idx = np.nonzero(ok)[0]

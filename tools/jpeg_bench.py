@@ -41,8 +41,10 @@ def pil_rate(payloads):
     return 2 * len(payloads) / dt, cores
 
 
-def run(name, payloads, sub_bits):
-    dec = JpegDecoder(DEV, sub_bits=sub_bits)
+def run(name, payloads, spec):
+    sub_bits, _, lead = str(spec).partition(":")
+    sub_bits, lead = int(sub_bits), int(lead or 0)
+    dec = JpegDecoder(DEV, sub_bits=sub_bits, lead_bits=lead)
     for _ in range(3):
         dec.decode(payloads)
     torch.cuda.synchronize()
@@ -68,7 +70,7 @@ def run(name, payloads, sub_bits):
               for h in range(2, steps + 1) if h < 64]
     phases = {"spec_us": (st[1] - st[0]) / 1e3, "rounds_us": (st[2] - st[1]) / 1e3,
               "scan_us": (st[3] - st[2]) / 1e3, "write_us": (st[4] - st[3]) / 1e3}
-    return {"set": name, "sub_bits": sub_bits, "images": len(payloads),
+    return {"set": name, "sub_bits": sub_bits, "lead_bits": lead, "images": len(payloads),
             "avg_kb": round(sum(map(len, payloads)) / len(payloads) / 1e3, 1),
             "e2e_ms": round(e2e * 1e3, 3), "e2e_images_s": round(len(payloads) / e2e, 1),
             "kernel_ms": round(k, 3), "kernel_images_s": round(len(payloads) / (k / 1e3), 1),
@@ -77,7 +79,7 @@ def run(name, payloads, sub_bits):
 
 
 def main():
-    subs = [int(x) for x in sys.argv[1:]] or [2048]
+    subs = sys.argv[1:] or ["4096"]  # sub_bits[:lead_bits]
     sets = {"scene1080_q85": [encode(scene(1920, 1080, s)) for s in range(64)],
             "noise1080_q85": [encode(np.random.default_rng(s).integers(0, 256, (1080, 1920, 3),
                                                                         dtype=np.uint8)) for s in range(16)]}
