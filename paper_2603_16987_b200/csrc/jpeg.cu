@@ -48,7 +48,8 @@ __constant__ uint8_t c_zig[64] = {0,  1,  8,  16, 9,  2,  3,  10, 17, 24, 32, 25
 
 constexpr int kMaxSteps = 160;  // sync half-rounds before an image is handed to the host
 constexpr int kNoErr = 0x7FFFFFFF;
-constexpr int kMaxHops = 16;  // subsequences one thread re-decodes in a chain per half-round
+constexpr int kMaxHops = 1;  // subsequences one thread re-decodes per half-round (longer
+                              // chains measured slower: one thread's serial decodes)
 constexpr int kCkpts = 7;  // checkpoints per subsequence (every sub_bits / 8 bits)
 
 struct Work {
@@ -320,6 +321,13 @@ struct BitReader {
     wi = 0xFFFFFFF0u;  // no word index: neither it nor its successor is ever requested
   }
   __device__ __forceinline__ uint32_t ld(uint32_t i) const { return __byte_perm(w[i], 0, 0x0123); }
+  // pull the bits [b0, b1) into L1 ahead of the serial decode: its loads then hit L1
+  // instead of paying the L2 latency every 32 bits
+  __device__ __forceinline__ void prefetch(uint32_t b0, uint32_t b1) const {
+    const char* p = reinterpret_cast<const char*>(w);
+    for (uint32_t byte = (b0 >> 3) & ~127u; byte < ((b1 + 7) >> 3) + 8; byte += 128)
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(p + byte));
+  }
   // the 32 bits starting at bit p (big-endian bit order)
   __device__ __forceinline__ uint32_t peek(uint32_t p) {
     const uint32_t i = p >> 5;
@@ -432,6 +440,7 @@ __device__ DecOut decode_run(const Tabs& T, BitReader& br, uint32_t bit0, uint32
   int ci = 0;
   uint32_t next_cp = CK ? ck->first : 0xFFFFFFFFu;
   if (MODE == 2 && block >= block_limit) stop = pos;
+  if (pos < stop) br.prefetch(bit0 + pos, bit0 + stop);
   while (pos < stop) {
     if (CK && pos >= next_cp) {
       const long long st = pack_state(pos, u, z);
@@ -969,42 +978,61 @@ __device__ __forceinline__ void idct_row(const int (&w)[8], uint32_t& lo, uint32
   }
 }
 
+// 8 threads per block, four blocks per warp: thread `sub` loads row `sub` of its block
+// (one 16-byte load of 8 coefficients, one of 8 quantizers), the dequantized rows go
+// through shared memory to become columns for pass 1 and back to rows for pass 2 (the
+// eight threads of a block are in one warp: __syncwarp), and each thread stores its
+// output row as one 8-byte store.
 __global__ void __launch_bounds__(256) k_jpeg_idct(const JDesc* __restrict__ descs, int n,
                                                    int64_t total_blocks, uint8_t* __restrict__ work,
                                                    const int32_t* __restrict__ status) {
-  __shared__ int ws[32][65];
+  __shared__ int ws[32][8][9];  // [block][row][col], padded
   const int sub = threadIdx.x & 7, lb = threadIdx.x >> 3;
-  for (int64_t gb0 = static_cast<int64_t>(blockIdx.x) * 32; gb0 < total_blocks;
-       gb0 += static_cast<int64_t>(gridDim.x) * 32) {
-    const int64_t gb = gb0 + lb;
-    const bool on = gb < total_blocks;
+  for (int64_t gb = static_cast<int64_t>(blockIdx.x) * 32 + lb; gb < total_blocks + lb;
+       gb += static_cast<int64_t>(gridDim.x) * 32) {
+    bool live = gb < total_blocks;
     const JDesc* d = nullptr;
-    bool live = false;
-    if (on) {
+    if (live) {
       const int k = find_image(descs, n, gb, 1);
       d = descs + k;
       live = d->n_slots > 0 && status[k] == 0;
     }
-    const int b = on ? static_cast<int>(gb - d->block_base) : 0;
+    const int b = live ? static_cast<int>(gb - d->block_base) : 0;
     const int u = live ? b % d->bmcu : 0;
     const int c = live ? d->slot_comp[u] : 0;
+    int (&blk)[8][9] = ws[lb];
     if (live) {
-      const int16_t* blk = reinterpret_cast<const int16_t*>(work + d->coef_off) + static_cast<int64_t>(b) * 64;
-      int dq[8], w[8];
+      const uint4 cv = *reinterpret_cast<const uint4*>(
+          reinterpret_cast<const int16_t*>(work + d->coef_off) + static_cast<int64_t>(b) * 64 + 8 * sub);
+      const uint4 qv = *reinterpret_cast<const uint4*>(&d->quant[c][8 * sub]);
+      const uint32_t cw[4] = {cv.x, cv.y, cv.z, cv.w}, qw[4] = {qv.x, qv.y, qv.z, qv.w};
 #pragma unroll
-      for (int r = 0; r < 8; ++r)
-        dq[r] = static_cast<int>(blk[8 * r + sub]) * static_cast<int>(static_cast<int16_t>(d->quant[c][8 * r + sub]));
-      idct_col(dq, w);
-#pragma unroll
-      for (int r = 0; r < 8; ++r) ws[lb][8 * r + sub] = w[r];
+      for (int i = 0; i < 8; ++i) {  // DEQUANTIZE: short coef x short quant (ISLOW_MULT_TYPE)
+        const int coef = static_cast<int16_t>(cw[i >> 1] >> (16 * (i & 1)));
+        const int q = static_cast<int16_t>(qw[i >> 1] >> (16 * (i & 1)));
+        blk[sub][i] = coef * q;
+      }
     }
-    __syncthreads();
-    if (live) {
-      int w[8];
+    __syncwarp();
+    int w[8];
+    if (live) {  // pass 1: column `sub`
+      int dq[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) w[i] = ws[lb][8 * sub + i];
+      for (int r = 0; r < 8; ++r) dq[r] = blk[r][sub];
+      idct_col(dq, w);
+    }
+    __syncwarp();
+    if (live) {
+#pragma unroll
+      for (int r = 0; r < 8; ++r) blk[r][sub] = w[r];
+    }
+    __syncwarp();
+    if (live) {  // pass 2: row `sub`
+      int rw[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) rw[i] = blk[sub][i];
       uint32_t lo, hi;
-      idct_row(w, lo, hi);
+      idct_row(rw, lo, hi);
       const int mcu = b / d->bmcu;
       const int my = mcu / d->mcux, mx = mcu % d->mcux;
       const int by = d->ncomp == 1 ? my : my * d->comp_v[c] + d->slot_bv[u];
@@ -1012,7 +1040,7 @@ __global__ void __launch_bounds__(256) k_jpeg_idct(const JDesc* __restrict__ des
       uint8_t* dst = work + d->plane_off[c] + static_cast<int64_t>(by * 8 + sub) * d->plane_w[c] + bx * 8;
       *reinterpret_cast<uint2*>(dst) = make_uint2(lo, hi);
     }
-    __syncthreads();
+    __syncwarp();
   }
 }
 
@@ -1082,49 +1110,72 @@ __global__ void __launch_bounds__(256) k_jpeg_color(const JDesc* __restrict__ de
     const uint8_t* cr0 = pcr + crow * pw1;
     const uint8_t* cr1 = pcr + orow * pw1;
     const bool fancy = hx == 2 && dsw > 2;
-    for (int x0 = 4 * threadIdx.x; x0 < W; x0 += 4 * blockDim.x) {
-      const uint32_t yw = *reinterpret_cast<const uint32_t*>(py + x0);  // planes are 8-padded
-      uint32_t px[4];
+    // 8 pixels per thread: one 8-byte Y load; for the fancy paths the chroma column sums
+    // at 4t - 1 .. 4t + 4 come from one aligned word per row and plane plus its two
+    // neighbours (clamped at the plane's real edges, which reproduces jdsample.c's first
+    // and last column cases)
+    for (int x0 = 8 * threadIdx.x; x0 < W; x0 += 8 * blockDim.x) {
+      const uint2 yv = *reinterpret_cast<const uint2*>(py + x0);  // planes are 8-padded
+      uint32_t px[8];
       if (d.ncomp == 1) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) px[i] = ((yw >> (8 * i)) & 255) * 0x010101u;
+        for (int i = 0; i < 8; ++i) px[i] = (((i < 4 ? yv.x : yv.y) >> (8 * (i & 3))) & 255) * 0x010101u;
       } else if (fancy) {
-        // 4 pixels = chroma columns i0, i0 + 1: column sums at i0 - 1 .. i0 + 2, clamped
-        // (clamping the neighbour reproduces jdsample.c's first / last column cases)
-        const int i0 = x0 >> 1;
-        int cb[4], cr[4];
+        const int i0 = x0 >> 1;  // chroma columns i0 .. i0 + 3
+        int cb[6], cr[6];        // column sums at i0 - 1 .. i0 + 4
+        if (i0 >= 1 && i0 + 4 <= dsw - 1) {
+          const uint32_t b0 = *reinterpret_cast<const uint32_t*>(cb0 + i0);
+          const uint32_t r0 = *reinterpret_cast<const uint32_t*>(cr0 + i0);
+          const uint32_t b1 = vx == 2 ? *reinterpret_cast<const uint32_t*>(cb1 + i0) : 0u;
+          const uint32_t r1 = vx == 2 ? *reinterpret_cast<const uint32_t*>(cr1 + i0) : 0u;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int ii = min(max(i0 - 1 + q, 0), dsw - 1);
-          cb[q] = vx == 2 ? cb0[ii] * 3 + cb1[ii] : cb0[ii];
-          cr[q] = vx == 2 ? cr0[ii] * 3 + cr1[ii] : cr0[ii];
+          for (int q = 0; q < 4; ++q) {
+            const int bb0 = (b0 >> (8 * q)) & 255, rr0 = (r0 >> (8 * q)) & 255;
+            cb[q + 1] = vx == 2 ? bb0 * 3 + static_cast<int>((b1 >> (8 * q)) & 255) : bb0;
+            cr[q + 1] = vx == 2 ? rr0 * 3 + static_cast<int>((r1 >> (8 * q)) & 255) : rr0;
+          }
+          cb[0] = vx == 2 ? cb0[i0 - 1] * 3 + cb1[i0 - 1] : cb0[i0 - 1];
+          cr[0] = vx == 2 ? cr0[i0 - 1] * 3 + cr1[i0 - 1] : cr0[i0 - 1];
+          cb[5] = vx == 2 ? cb0[i0 + 4] * 3 + cb1[i0 + 4] : cb0[i0 + 4];
+          cr[5] = vx == 2 ? cr0[i0 + 4] * 3 + cr1[i0 + 4] : cr0[i0 + 4];
+        } else {
+#pragma unroll
+          for (int q = 0; q < 6; ++q) {
+            const int ii = min(max(i0 - 1 + q, 0), dsw - 1);
+            cb[q] = vx == 2 ? cb0[ii] * 3 + cb1[ii] : cb0[ii];
+            cr[q] = vx == 2 ? cr0[ii] * 3 + cr1[ii] : cr0[ii];
+          }
         }
         const int sh = vx == 2 ? 4 : 2;
         const int be = vx == 2 ? 8 : 1, bo = vx == 2 ? 7 : 2;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < 8; ++i) {
           const int q = 1 + (i >> 1);              // this column's sum
           const int nb = (i & 1) ? q + 1 : q - 1;  // the neighbour it blends with
-          const int b = (i & 1) ? bo : be;
-          const int ccb = ((cb[q] * 3 + cb[nb] + b) >> sh) - 128;
-          const int ccr = ((cr[q] * 3 + cr[nb] + b) >> sh) - 128;
-          px[i] = ycc_px((yw >> (8 * i)) & 255, ccb, ccr);
+          const int bias = (i & 1) ? bo : be;
+          const int ccb = ((cb[q] * 3 + cb[nb] + bias) >> sh) - 128;
+          const int ccr = ((cr[q] * 3 + cr[nb] + bias) >> sh) - 128;
+          px[i] = ycc_px(((i < 4 ? yv.x : yv.y) >> (8 * (i & 3))) & 255, ccb, ccr);
         }
       } else {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < 8; ++i) {
           const int x = min(x0 + i, W - 1);
           const int ci = hx == 2 ? x >> 1 : x;  // 4:4:4, or plain replication (dsw <= 2)
-          px[i] = ycc_px((yw >> (8 * i)) & 255, cb0[ci] - 128, cr0[ci] - 128);
+          px[i] = ycc_px(((i < 4 ? yv.x : yv.y) >> (8 * (i & 3))) & 255, cb0[ci] - 128, cr0[ci] - 128);
         }
       }
-      if (aligned && x0 + 4 <= W) {
+      if (aligned && x0 + 8 <= W) {
         uint32_t* o32 = reinterpret_cast<uint32_t*>(o + 3 * x0);
-        o32[0] = px[0] | (px[1] << 24);
-        o32[1] = (px[1] >> 8) | (px[2] << 16);
-        o32[2] = (px[2] >> 16) | (px[3] << 8);
+#pragma unroll
+        for (int h4 = 0; h4 < 2; ++h4) {
+          const uint32_t* p4 = px + 4 * h4;
+          o32[3 * h4] = p4[0] | (p4[1] << 24);
+          o32[3 * h4 + 1] = (p4[1] >> 8) | (p4[2] << 16);
+          o32[3 * h4 + 2] = (p4[2] >> 16) | (p4[3] << 8);
+        }
       } else {
-        for (int i = 0; i < 4 && x0 + i < W; ++i) {
+        for (int i = 0; i < 8 && x0 + i < W; ++i) {
           o[3 * (x0 + i)] = static_cast<uint8_t>(px[i]);
           o[3 * (x0 + i) + 1] = static_cast<uint8_t>(px[i] >> 8);
           o[3 * (x0 + i) + 2] = static_cast<uint8_t>(px[i] >> 16);
