@@ -978,6 +978,20 @@ __device__ __forceinline__ void idct_row(const int (&w)[8], uint32_t& lo, uint32
   }
 }
 
+// q = a / b, r = a % b for 0 <= a < 2^24, b >= 1, through a float reciprocal and one
+// correction step (an integer division is ~20 instructions on the GPU)
+__device__ __forceinline__ void div_small(int a, int b, int& q, int& r) {
+  q = __float2int_rz(__int2float_rn(a) * __frcp_rn(__int2float_rn(b)));
+  r = a - q * b;
+  if (r < 0) {
+    --q;
+    r += b;
+  } else if (r >= b) {
+    ++q;
+    r -= b;
+  }
+}
+
 // 8 threads per block, four blocks per warp: thread `sub` loads row `sub` of its block
 // (one 16-byte load of 8 coefficients, one of 8 quantizers), the dequantized rows go
 // through shared memory to become columns for pass 1 and back to rows for pass 2 (the
@@ -988,17 +1002,26 @@ __global__ void __launch_bounds__(256) k_jpeg_idct(const JDesc* __restrict__ des
                                                    const int32_t* __restrict__ status) {
   __shared__ int ws[32][8][9];  // [block][row][col], padded
   const int sub = threadIdx.x & 7, lb = threadIdx.x >> 3;
+  int ck_img = -1;
+  int64_t ck_lo = 0, ck_hi = 0;
   for (int64_t gb = static_cast<int64_t>(blockIdx.x) * 32 + lb; gb < total_blocks + lb;
        gb += static_cast<int64_t>(gridDim.x) * 32) {
     bool live = gb < total_blocks;
     const JDesc* d = nullptr;
     if (live) {
-      const int k = find_image(descs, n, gb, 1);
-      d = descs + k;
-      live = d->n_slots > 0 && status[k] == 0;
+      // the image of this block: the one of the thread's previous block when it still
+      // covers it (consecutive iterations walk forward), else a binary search
+      if (!(ck_img >= 0 && gb >= ck_lo && gb < ck_hi)) {
+        ck_img = find_image(descs, n, gb, 1);
+        ck_lo = descs[ck_img].block_base;
+        ck_hi = ck_lo + descs[ck_img].n_blocks;
+      }
+      d = descs + ck_img;
+      live = d->n_slots > 0 && status[ck_img] == 0;
     }
     const int b = live ? static_cast<int>(gb - d->block_base) : 0;
-    const int u = live ? b % d->bmcu : 0;
+    int mcu = 0, u = 0;
+    if (live) div_small(b, d->bmcu, mcu, u);
     const int c = live ? d->slot_comp[u] : 0;
     int (&blk)[8][9] = ws[lb];
     if (live) {
@@ -1033,8 +1056,8 @@ __global__ void __launch_bounds__(256) k_jpeg_idct(const JDesc* __restrict__ des
       for (int i = 0; i < 8; ++i) rw[i] = blk[sub][i];
       uint32_t lo, hi;
       idct_row(rw, lo, hi);
-      const int mcu = b / d->bmcu;
-      const int my = mcu / d->mcux, mx = mcu % d->mcux;
+      int my, mx;
+      div_small(mcu, d->mcux, my, mx);
       const int by = d->ncomp == 1 ? my : my * d->comp_v[c] + d->slot_bv[u];
       const int bx = d->ncomp == 1 ? mx : mx * d->comp_h[c] + d->slot_bh[u];
       uint8_t* dst = work + d->plane_off[c] + static_cast<int64_t>(by * 8 + sub) * d->plane_w[c] + bx * 8;
@@ -1087,8 +1110,14 @@ __global__ void __launch_bounds__(256) k_jpeg_color(const JDesc* __restrict__ de
                                                     int64_t total_rows, const uint8_t* __restrict__ work,
                                                     uint8_t* __restrict__ out,
                                                     const int32_t* __restrict__ status) {
+  int k = -1;
+  int64_t lo = 0, hi = 0;
   for (int64_t gr = blockIdx.x; gr < total_rows; gr += gridDim.x) {
-    const int k = find_image(descs, n, gr, 2);
+    if (!(k >= 0 && gr >= lo && gr < hi)) {  // rows of one image are consecutive
+      k = find_image(descs, n, gr, 2);
+      lo = descs[k].row_base;
+      hi = lo + descs[k].height;
+    }
     const JDesc& d = descs[k];
     if (d.n_slots == 0 || status[k]) continue;
     const int y = static_cast<int>(gr - d.row_base);

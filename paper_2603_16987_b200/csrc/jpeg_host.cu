@@ -125,6 +125,9 @@ TP_API int tp_jpeg_parse(const uint8_t* d, int64_t n, TpJpegInfo* info) {
       if (sl < 6 + 3 * info->ncomp) return status(info, TP_JPEG_CORRUPT, "short SOF");
       if (info->width < 1 || info->height < 1)
         return status(info, TP_JPEG_UNSUPPORTED, "zero-size frame (DNL)");
+      // block / MCU indices stay below 2^22 (the kernels' float-reciprocal divisions)
+      if (static_cast<int64_t>(info->width) * info->height > (int64_t(1) << 27))
+        return status(info, TP_JPEG_UNSUPPORTED, "more than 2^27 pixels");
       for (int c = 0; c < info->ncomp; ++c) {
         info->comp_id[c] = s[6 + 3 * c];
         info->comp_h[c] = s[7 + 3 * c] >> 4;
