@@ -15,12 +15,14 @@
 #include <atomic>
 #include <condition_variable>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <mutex>
 #include <thread>
 #include <vector>
 
+#include <immintrin.h>
 #include <sched.h>
 #include <unistd.h>
 
@@ -118,6 +120,41 @@ class Pool {
   std::atomic<int64_t> next_{0};
 };
 
+// Copy with non-temporal (streaming) stores: the staging slab is read next by the copy
+// engine's DMA, not by this CPU, so writing around the caches saves the read-for-
+// ownership of every destination line (a third of the memory traffic of a cached copy)
+// and leaves the caller's data in cache.  AVX2 when the CPU has it, memcpy otherwise.
+__attribute__((target("avx2"))) void copy_nt_avx2(uint8_t* dst, const uint8_t* src, size_t n) {
+  size_t head = (32 - (reinterpret_cast<uintptr_t>(dst) & 31)) & 31;
+  if (head > n) head = n;
+  std::memcpy(dst, src, head);
+  dst += head;
+  src += head;
+  n -= head;
+  const size_t m = n & ~size_t(127);
+  for (size_t i = 0; i < m; i += 128) {
+    const __m256i a = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(src + i));
+    const __m256i b = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(src + i + 32));
+    const __m256i c = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(src + i + 64));
+    const __m256i d = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(src + i + 96));
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(dst + i), a);
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(dst + i + 32), b);
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(dst + i + 64), c);
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(dst + i + 96), d);
+  }
+  std::memcpy(dst + m, src + m, n - m);
+}
+
+bool have_avx2() {
+  static const bool v = __builtin_cpu_supports("avx2");
+  return v;
+}
+
+inline void copy_block(uint8_t* dst, const uint8_t* src, size_t n, bool nt) {
+  if (nt) copy_nt_avx2(dst, src, n);
+  else std::memcpy(dst, src, n);
+}
+
 struct Chunk {
   int32_t image;
   int32_t y0, y1;  // source rows [y0, y1)
@@ -149,6 +186,7 @@ TP_API int tp_stage_pack(int32_t n, const uint8_t* const* src, const int64_t* sr
       chunks.push_back({k, static_cast<int32_t>(y), static_cast<int32_t>(std::min<int64_t>(h, y + rows_per))});
   }
   const int nthreads = threads > 0 ? threads : Pool::get().size();
+  const bool nt = have_avx2() && getenv("TP_PACK_NO_NT") == nullptr;
   std::function<void(int64_t)> fn = [&](int64_t t) {
     const Chunk& c = chunks[static_cast<size_t>(t)];
     const int64_t w = wh[2 * c.image];
@@ -158,13 +196,28 @@ TP_API int tp_stage_pack(int32_t n, const uint8_t* const* src, const int64_t* sr
     const int64_t st = src_stride[c.image];
     if (row_map) {
       const int32_t* m = row_map + row_map_off[c.image] + 1;  // m[y]: compact row or -1
-      for (int32_t y = c.y0; y < c.y1; ++y)
-        if (m[y] >= 0) std::memcpy(d + static_cast<int64_t>(m[y]) * row, s + y * st, row);
+      // runs of consecutive staged rows are one copy
+      int32_t y = c.y0;
+      while (y < c.y1) {
+        if (m[y] < 0) {
+          ++y;
+          continue;
+        }
+        int32_t e = y + 1;
+        while (e < c.y1 && m[e] == m[e - 1] + 1) ++e;
+        if (st == row)
+          copy_block(d + static_cast<int64_t>(m[y]) * row, s + y * st, static_cast<size_t>(e - y) * row, nt);
+        else
+          for (int32_t yy = y; yy < e; ++yy)
+            copy_block(d + static_cast<int64_t>(m[yy]) * row, s + yy * st, row, nt);
+        y = e;
+      }
     } else if (st == row) {
-      std::memcpy(d + c.y0 * row, s + c.y0 * st, (c.y1 - c.y0) * row);
+      copy_block(d + c.y0 * row, s + c.y0 * st, (c.y1 - c.y0) * row, nt);
     } else {
-      for (int32_t y = c.y0; y < c.y1; ++y) std::memcpy(d + y * row, s + y * st, row);
+      for (int32_t y = c.y0; y < c.y1; ++y) copy_block(d + y * row, s + y * st, row, nt);
     }
+    if (nt) _mm_sfence();  // streaming stores visible before the caller uploads the slab
   };
   if (nthreads <= 1 || chunks.size() <= 1) {
     for (size_t t = 0; t < chunks.size(); ++t) fn(static_cast<int64_t>(t));

@@ -232,3 +232,25 @@ def test_touched_row_maps_match_oracle_taps(seed):
             assert part[0] == len(want) and set(got.tolist()) == want
             assert np.array_equal(part[1:][got], np.arange(len(got)))
 
+
+
+@pytest.mark.parametrize("threads", [1, 0])
+def test_native_pack_strided_views_whole_and_touched(threads):
+    """tp_stage_pack on non-contiguous caller views (row stride > row bytes): whole
+    images round-trip; touched staging holds exactly the mapped rows, in order."""
+    from paper_2603_16987_b200.transfer import staging_map
+
+    rng = np.random.default_rng(4)
+    big = [rng.integers(0, 256, (300, 420, 3), dtype=np.uint8) for _ in range(3)]
+    imgs = [b[7:290, 11:400] for b in big]
+    st_ = stage_images(imgs, HostArena(staged_bytes(imgs), 256), threads=threads)
+    for got, want in zip(unpack(st_.batch)[2:], imgs):
+        assert np.array_equal(got, want)
+    tt = (64, 6)
+    st2 = stage_images(imgs, HostArena(staged_bytes(imgs, touched=tt), 256), touched=tt,
+                       threads=threads)
+    blocks = unpack(st2.batch)[4:]
+    for a, blk in zip(imgs, blocks):
+        m = staging_map(a.shape[1], a.shape[0], *tt)
+        rows = np.nonzero(m[1: a.shape[0] + 1] >= 0)[0]
+        assert np.array_equal(blk, a[rows])
