@@ -664,7 +664,10 @@ __device__ inline int4 block_scan4(int4 v, int4* sh, int4& total) {
   return make_int4(pre.x + x.x - v.x, pre.y + x.y - v.y, pre.z + x.z - v.z, pre.w + x.w - v.w);
 }
 
-__global__ void __launch_bounds__(256) k_jpeg_huff(const JDesc* __restrict__ descs, int n,
+#ifndef TP_JPEG_HUFF_MINB  // resident CTAs per SM the register allocation must allow
+#define TP_JPEG_HUFF_MINB 1
+#endif
+__global__ void __launch_bounds__(256, TP_JPEG_HUFF_MINB) k_jpeg_huff(const JDesc* __restrict__ descs, int n,
                                                    int64_t total_slots, int sub_bits,
                                                    int lead_bits, uint8_t* __restrict__ work,
                                                    int32_t* __restrict__ status) {
