@@ -43,7 +43,7 @@ def pil_rate(payloads):
 
 def run(name, payloads, spec):
     sub_bits, _, lead = str(spec).partition(":")
-    sub_bits, lead = int(sub_bits), int(lead or 0)
+    sub_bits, lead = int(sub_bits), int(lead or 0)  # 0: the decoder's choice
     dec = JpegDecoder(DEV, sub_bits=sub_bits, lead_bits=lead)
     for _ in range(3):
         dec.decode(payloads)
