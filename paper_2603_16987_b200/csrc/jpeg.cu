@@ -362,8 +362,8 @@ __device__ __forceinline__ int huff_decode(const JHuff* __restrict__ t, uint32_t
   return 0;
 }
 
-__device__ __forceinline__ int extend(uint32_t bits, int s) {
-  return bits < (1u << (s - 1)) ? static_cast<int>(bits) - (1 << s) + 1 : static_cast<int>(bits);
+__device__ __forceinline__ int extend(uint32_t bits, int s) {  // T.81 F.12 EXTEND, s >= 1
+  return bits < (1u << ((s - 1) & 31)) ? static_cast<int>(bits) - (1 << s) + 1 : static_cast<int>(bits);
 }
 
 struct DecOut {
@@ -508,33 +508,32 @@ __device__ DecOut decode_run(const Tabs& T, BitReader& br, uint32_t bit0, uint32
       act = T.act(c);
       continue;
     }
-    if (z == 0) {
-      const int diff = s ? extend((v << len) >> (32 - s), s) : 0;
-      // libjpeg: last_dc_val[ci] += diff (int), the block keeps (JCOEF) last_dc_val
-      if (c == 0) p0 += diff; else if (c == 1) p1 += diff; else p2 += diff;
-      if (MODE == 2)
+    // the symbol's effect without branching on its kind (lanes of a warp decode different
+    // streams): DC (z == 0, r = 0: the value is the difference), AC with a value (z += r,
+    // the coefficient, z += 1), ZRL (r = 15, s = 0: z += 16 = r + 1) or EOB (the block ends)
+    const bool dc = z == 0;
+    const int val = s ? extend((v << len) >> ((32 - s) & 31), s) : 0;
+    const int dcv = dc ? val : 0;
+    // libjpeg: last_dc_val[ci] += diff (int), the block keeps (JCOEF) last_dc_val
+    p0 += c == 0 ? dcv : 0;
+    p1 += c == 1 ? dcv : 0;
+    p2 += c == 2 ? dcv : 0;
+    if (MODE == 2) {
+      if (dc)
         coef[static_cast<int64_t>(block) * 64] = static_cast<int16_t>(c == 0 ? p0 : c == 1 ? p1 : p2);
-      z = 1;
-    } else if (s) {
-      z += r;
-      if (MODE == 2) coef[static_cast<int64_t>(block) * 64 + c_zig[z]] =
-          static_cast<int16_t>(extend((v << len) >> (32 - s), s));
-      ++z;
-    } else if (r == 15) {
-      z += 16;
-    } else {
-      z = 64;
+      else if (s)
+        coef[static_cast<int64_t>(block) * 64 + c_zig[z + r]] = static_cast<int16_t>(val);
     }
+    const int zn = (dc || s != 0 || r == 15) ? z + r + 1 : 64;
     pos += used;
-    if (z >= 64) {
-      z = 0;
-      ++o.blocks;
-      u = u + 1 == T.bmcu ? 0 : u + 1;
-      c = T.comp(u);
-      dct = T.dct(c);
-      act = T.act(c);
-      if (MODE == 2 && ++block >= block_limit) break;
-    }
+    const bool bend = zn >= 64;
+    z = bend ? 0 : zn;
+    o.blocks += bend ? 1 : 0;
+    u = bend ? (u + 1 == T.bmcu ? 0 : u + 1) : u;
+    c = T.comp(u);
+    dct = T.dct(c);
+    act = T.act(c);
+    if (MODE == 2 && bend && ++block >= block_limit) break;
   }
   if (CK)
     for (int i = ci; i < kCkpts; ++i) ck->state[i] = -1;  // not reached by this decode
