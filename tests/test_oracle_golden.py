@@ -197,3 +197,44 @@ def test_tokenize_vs_live_reference(reference, text):
     vocab = T.load_vocab(Path("/root/reference/pkg/src/vlmfp/data/base_vocab.txt"))
     want = T.tokenize(text, vocab)
     assert O.tokenize(text, vocab.byte_ids, vocab.match_table, vocab.max_token_bytes) == want
+
+
+@pytest.mark.reference
+@pytest.mark.parametrize("w,h,e", [(1920, 1080, 512), (3840, 2160, 448), (640, 480, 448)])
+def test_port_costs_what_vlmfp_costs(reference, w, h, e):
+    """The oracle port (bench.py's CPU leg when baseline/_ref is absent) restates vlmfp's
+    fused path with the same band sharing and in-place ops, so it also costs what vlmfp
+    costs: C1 (1080p, E=512), C3 (4K) and a 13-tile image, best of 3 on one core, within
+    30% (the restatement was measured within 10%; the margin absorbs timer noise on a
+    shared build box)."""
+    import time
+
+    from oracle import tileprep_oracle as O
+
+    V = reference
+    arr = O.synth_image(5, 0, w, h, 3, 0)
+    mean, std = (0.485, 0.456, 0.406), (0.229, 0.224, 0.225)
+    cfg = V.PreprocessConfig(tile_edge=e, max_tiles=12, mean=mean, std=std,
+                             reduced_precision_normalize=True, fused_transform=True,
+                             contiguous_tensor_path=True, avoid_per_item_split=True,
+                             skip_pixel_mask=True)
+
+    def ref():
+        img = V.ImageBuffer.from_array(arr)
+        plan = V.select_tile_plan(img.width, img.height, cfg)
+        V.normalize_tiles(V.tile_image(img, plan, cfg), cfg)
+
+    def port():
+        O.preprocess_image(arr, e, 12, mean, std, True)
+
+    def best(fn):
+        fn()
+        ts = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            fn()
+            ts.append(time.perf_counter() - t0)
+        return min(ts)
+
+    r, p = best(ref), best(port)
+    assert 1 / 1.3 <= p / r <= 1.3, (r, p)
