@@ -369,6 +369,7 @@ __device__ __forceinline__ int extend(uint32_t bits, int s) {  // T.81 F.12 EXTE
 struct DecOut {
   uint32_t pos;
   int u, z, blocks, err;
+  int symbols;  // decoded in this call (diagnostics)
   int dc[jpeg::kMaxComps];  // sum of the DC differences decoded, per component
 };
 
@@ -430,6 +431,7 @@ __device__ DecOut decode_run(const Tabs& T, BitReader& br, uint32_t bit0, uint32
   DecOut o;
   o.blocks = 0;
   o.err = kNoErr;
+  o.symbols = 0;
   uint32_t epos = 0xFFFFFFFFu;
   // running DC per component: the predictors (MODE 2) or the sums of differences
   int p0 = MODE == 2 ? pred_in[0] : 0, p1 = MODE == 2 ? pred_in[1] : 0,
@@ -476,6 +478,7 @@ __device__ DecOut decode_run(const Tabs& T, BitReader& br, uint32_t bit0, uint32
       ++ci;
       next_cp = ci < kCkpts ? ck->first + ci * ck->step : 0xFFFFFFFFu;
     }
+    ++o.symbols;
     const uint32_t v = br.peek(bit0 + pos);
     int sym;
     const int len = huff_decode(z == 0 ? dct : act, v, sym);
@@ -787,8 +790,13 @@ __global__ void __launch_bounds__(256, TP_JPEG_HUFF_MINB) k_jpeg_huff(const JDes
         ck.prev_errpos = static_cast<uint32_t>(W.errpos[gg]);
         ck.prev_dc = W.dcs[gg];
         uint32_t ep;
+        const long long c0 = clock64();
         const DecOut o = decode_run<1, true>(T, br, r.bit0, r.seg_bits, stop, pos, u, z, nullptr,
                                              0, 0, nullptr, &ck, &ep);
+        if (h < 128) {  // diagnostics: the longest re-decode of this half-round
+          atomicMax(W.counters + 256 + h, static_cast<unsigned>(o.symbols));
+          atomicMax(W.counters + 384 + h, static_cast<unsigned>(min(clock64() - c0, 0x7FFFFFFFLL)));
+        }
         const long long x = pack_state(o.pos, o.u, o.z);
         W.entry[gg] = e;
         W.blocks[gg] = o.blocks;

@@ -66,7 +66,8 @@ def run(name, payloads, spec):
     st = dec._work[3968:3968 + 40].view(torch.int64).cpu().numpy()
     cnt = dec._work[:4096].view(torch.int32).cpu().numpy()
     ts = dec._work[640 * 4: 640 * 4 + 64 * 8].view(torch.int64).cpu().numpy()
-    rounds = [(h, int(cnt[512 + h]), int(cnt[h]), round((ts[h] - (ts[h - 1] if h > 2 else st[1])) / 1e3, 1))
+    rounds = [(h, int(cnt[512 + h]), int(cnt[h]), round((ts[h] - (ts[h - 1] if h > 2 else st[1])) / 1e3, 1),
+               int(cnt[256 + h]), int(cnt[384 + h]))
               for h in range(2, steps + 1) if h < 64]
     phases = {"spec_us": (st[1] - st[0]) / 1e3, "rounds_us": (st[2] - st[1]) / 1e3,
               "scan_us": (st[3] - st[2]) / 1e3, "write_us": (st[4] - st[3]) / 1e3}
@@ -74,7 +75,7 @@ def run(name, payloads, spec):
             "avg_kb": round(sum(map(len, payloads)) / len(payloads) / 1e3, 1),
             "e2e_ms": round(e2e * 1e3, 3), "e2e_images_s": round(len(payloads) / e2e, 1),
             "kernel_ms": round(k, 3), "kernel_images_s": round(len(payloads) / (k / 1e3), 1),
-            "half_rounds": steps, "rounds(h,decoded,changed,us)": rounds, "huff_phases": {k: round(float(v), 1) for k, v in phases.items()}, "fallback": dec.last_fallback,
+            "half_rounds": steps, "rounds(h,decoded,changed,us,max_symbols,max_cycles)": rounds, "huff_phases": {k: round(float(v), 1) for k, v in phases.items()}, "fallback": dec.last_fallback,
             "h2d_bytes": dec.last_h2d_bytes}
 
 
