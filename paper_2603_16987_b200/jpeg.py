@@ -83,6 +83,8 @@ class _Slot:
         self.status_host = None
         self.copied = None  # event: the upload out of `host` finished
         self.done = None    # event: the decode (and the status copy) finished
+        self.meta_host = None  # pinned image offsets / sizes of the output batch
+        self.meta_copied = None
 
 
 class JpegBatch:
@@ -219,9 +221,21 @@ class JpegDecoder:
         stream = stream or torch.cuda.current_stream(self.device)
         if out is None:
             data = torch.empty(out_total, dtype=torch.uint8, device=self.device)
-            meta = torch.from_numpy(np.concatenate([out_off, wh.reshape(-1).astype(np.int64)]))
-            meta = meta.pin_memory().to(self.device, non_blocking=True)
-            out = PackedImages(data, meta[:n], meta[n:].to(torch.int32).view(n, 2), 3, wh, out_off)
+            # offsets and sizes ride in the slot's pinned slab (no per-call pinning)
+            if sl.meta_host is None or sl.meta_host.numel() < 3 * n:
+                sl.meta_host = torch.empty(3 * _round_up(n, 64), dtype=torch.int64, pin_memory=True)
+            if sl.meta_copied is not None:
+                sl.meta_copied.synchronize()
+            mh = sl.meta_host.numpy()
+            mh[:n] = out_off
+            mh[n: 3 * n] = wh.reshape(-1)
+            meta = torch.empty(3 * n, dtype=torch.int64, device=self.device)
+            with torch.cuda.stream(stream):
+                meta.copy_(sl.meta_host[: 3 * n], non_blocking=True)
+                sl.meta_copied = torch.cuda.Event()
+                sl.meta_copied.record(stream)
+                wh_dev = meta[n:].to(torch.int32).view(n, 2)
+            out = PackedImages(data, meta[:n], wh_dev, 3, wh, out_off)
         with torch.cuda.stream(stream):
             sl.dev[:payload_bytes].copy_(sl.host[:payload_bytes], non_blocking=True)
             sl.copied = torch.cuda.Event()
@@ -241,12 +255,13 @@ class JpegDecoder:
     def _pick(self, scan_bits: int) -> tuple:
         """(sub_bits, lead_bits) for a batch of `scan_bits` entropy-coded bits.  Measured on
         corpus-like 1080p JPEGs (profiles/r02/jpeg/): one image decodes fastest with short
-        subsequences (1024: 1.14 ms, 4096: 1.71 ms per call), 64 images with 4096-bit
-        subsequences and a 2048-bit lead-in (3.2 ms vs 3.8 ms at 2048)."""
+        subsequences and a long lead-in (1024 + 2048: K7 0.69 ms, decode() 1.0 ms; 4096:
+        1.71 ms per call), 64 images with 4096-bit subsequences and a 2048-bit lead-in
+        (2.8 ms; 3.8 ms at 2048)."""
         if self.sub_bits:
             return self.sub_bits, self.lead_bits
         if scan_bits < 32 * 2**20:  # fewer than ~8 corpus-like 1080p images
-            return 1024, 1024
+            return 1024, 2048
         return 4096, 2048
 
     def launch(self, stream: Optional[torch.cuda.Stream] = None) -> None:
