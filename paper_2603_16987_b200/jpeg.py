@@ -140,6 +140,8 @@ class JpegDecoder:
         self.last_fallback: list[int] = []  # images decoded on the host in the last call
         self.last_h2d_bytes = 0
         self._last = None
+        # uploads run on their own stream, so batch i+1's H2D overlaps batch i's decode
+        self._copy_stream = torch.cuda.Stream(self.device)
 
     @property
     def _work(self):  # diagnostics (tools/jpeg_bench.py): the last batch's workspace
@@ -236,10 +238,14 @@ class JpegDecoder:
                 sl.meta_copied.record(stream)
                 wh_dev = meta[n:].to(torch.int32).view(n, 2)
             out = PackedImages(data, meta[:n], wh_dev, 3, wh, out_off)
-        with torch.cuda.stream(stream):
+        # the slot's previous decode finished (sl.done above), so the upload may start at
+        # once on the copy stream; the decode waits for it on `stream`
+        cs = self._copy_stream
+        with torch.cuda.stream(cs):
             sl.dev[:payload_bytes].copy_(sl.host[:payload_bytes], non_blocking=True)
             sl.copied = torch.cuda.Event()
-            sl.copied.record(stream)
+            sl.copied.record(cs)
+        stream.wait_event(sl.copied)
         self._last = (sl, desc_at, n, totals, out, sub_bits)
         self.launch(stream)
         with torch.cuda.stream(stream):
