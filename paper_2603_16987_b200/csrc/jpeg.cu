@@ -41,11 +41,6 @@ namespace {
 using jpeg::JDesc;
 using jpeg::JHuff;
 
-__constant__ uint8_t c_zig[64] = {0,  1,  8,  16, 9,  2,  3,  10, 17, 24, 32, 25, 18, 11, 4,  5,
-                                  12, 19, 26, 33, 40, 48, 41, 34, 27, 20, 13, 6,  7,  14, 21, 28,
-                                  35, 42, 49, 56, 57, 50, 43, 36, 29, 22, 15, 23, 30, 37, 44, 51,
-                                  58, 59, 52, 45, 38, 31, 39, 46, 53, 60, 61, 54, 47, 55, 62, 63};
-
 constexpr int kMaxSteps = 160;  // sync half-rounds before an image is handed to the host
 constexpr int kNoErr = 0x7FFFFFFF;
 constexpr int kMaxHops = 1;  // subsequences one thread re-decodes per half-round (longer
@@ -525,7 +520,7 @@ __device__ DecOut decode_run(const Tabs& T, BitReader& br, uint32_t bit0, uint32
       if (dc)
         coef[static_cast<int64_t>(block) * 64] = static_cast<int16_t>(c == 0 ? p0 : c == 1 ? p1 : p2);
       else if (s)
-        coef[static_cast<int64_t>(block) * 64 + c_zig[z + r]] = static_cast<int16_t>(val);
+        coef[static_cast<int64_t>(block) * 64 + z + r] = static_cast<int16_t>(val);  // zigzag order
     }
     const int zn = (dc || s != 0 || r == 15) ? z + r + 1 : 64;
     pos += used;
@@ -676,7 +671,6 @@ __global__ void __launch_bounds__(256, TP_JPEG_HUFF_MINB) k_jpeg_huff(const JDes
   cg::grid_group grid = cg::this_grid();
   __shared__ ChunkTables ct;
   __shared__ int4 scan_sh[8];
-  __shared__ int bad_sh;
   const Work W = work_view(work, total_slots);
   const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t nthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;
@@ -885,15 +879,21 @@ __global__ void __launch_bounds__(256, TP_JPEG_HUFF_MINB) k_jpeg_huff(const JDes
                          reinterpret_cast<int16_t*>(work + d.coef_off), W.bstart[g], limit, pred);
   }
   if (tid == 0) W.stamps[4] = gtimer();
-  (void)bad_sh;
 }
 
 // ---------------------------------------------------------------------------
-// J3: ISLOW IDCT (jidctint.c), 8 threads per block
+// J3: ISLOW IDCT (jidctint.c), one thread per block
 
 constexpr int F0298 = 2446, F0390 = 3196, F0541 = 4433, F0765 = 6270, F0899 = 7373, F1175 = 9633,
               F1501 = 12299, F1847 = 15137, F1961 = 16069, F2053 = 16819, F2562 = 20995,
               F3072 = 25172;
+
+// zigzag index of each natural-order coefficient (the inverse of c_zig): the write pass
+// stores coefficients in zigzag order, the IDCT picks them into natural order at compile time
+__device__ constexpr int kNat2Zig[64] = {0,  1,  5,  6,  14, 15, 27, 28, 2,  4,  7,  13, 16, 26, 29, 42,
+                              3,  8,  12, 17, 25, 30, 41, 43, 9,  11, 18, 24, 31, 40, 44, 53,
+                              10, 19, 23, 32, 39, 45, 52, 54, 20, 22, 33, 38, 46, 51, 55, 60,
+                              21, 34, 37, 47, 50, 56, 59, 61, 35, 36, 48, 49, 57, 58, 62, 63};
 
 // One jidctint.c butterfly.  libjpeg computes in JLONG (64-bit on LP64); T = int is
 // exact whenever the inputs are bounded as the callers check (|in| <= 2^13 keeps every
@@ -935,56 +935,55 @@ __device__ __forceinline__ void idct_1d(const T (&in)[8], T (&out)[8]) {
   out[4] = tmp13 - t0;
 }
 
-__device__ __forceinline__ uint32_t range_limit(int x) {
-  const uint32_t v = static_cast<uint32_t>(x) & 1023u;  // RANGE_MASK
-  return v < 128 ? v + 128 : v < 512 ? 255u : v < 896 ? 0u : v - 896;
+// jdmaster.c prepare_range_limit_table + the IDCT's `range_limit[x & RANGE_MASK]` with
+// CENTERJSAMPLE folded into the descale: t = (x + 128) & 1023 maps [0, 256) to itself,
+// [256, 640) to 255 and [640, 1024) to 0 -- the table's wrap-around for corrupt data
+__device__ __forceinline__ uint32_t range_limit128(int x128) {
+  const uint32_t t = static_cast<uint32_t>(x128) & 1023u;
+  return t < 640u ? min(t, 255u) : 0u;
 }
 
-// pass 1 of one column: DEQUANTIZE (short coef x short quant, ISLOW_MULT_TYPE) then the
-// butterfly, DESCALE(x, CONST_BITS - PASS1_BITS) into the int workspace
-__device__ __forceinline__ void idct_col(const int (&dq)[8], int (&ws)[8]) {
-  int m = 0;
+// |v| <= 2^13 for all 64 values: min / max trees (three-input VIMNMX3)
+__device__ __forceinline__ bool all_small(const int (&v)[8][8]) {
+  int mx = v[0][0], mn = v[0][0];
 #pragma unroll
-  for (int r = 0; r < 8; ++r) m = max(m, abs(dq[r]));
-  if (m <= (1 << 13)) {
-    int out[8];
-    idct_1d<int>(dq, out);
+  for (int i = 1; i < 64; i += 2) {
+    const int a = v[i >> 3][i & 7], b = i + 1 < 64 ? v[(i + 1) >> 3][(i + 1) & 7] : a;
+    mx = max(mx, max(a, b));
+    mn = min(mn, min(a, b));
+  }
+  return mx <= (1 << 13) && mn >= -(1 << 13);
+}
+
+// pass 1 (columns): DESCALE(x, CONST_BITS - PASS1_BITS) into the int workspace, in place
+template <typename T>
+__device__ __forceinline__ void idct_pass1(int (&blk)[8][8]) {
 #pragma unroll
-    for (int r = 0; r < 8; ++r) ws[r] = (out[r] + (1 << 10)) >> 11;
-  } else {
-    long long in[8], out[8];
+  for (int col = 0; col < 8; ++col) {
+    T in[8], out[8];
 #pragma unroll
-    for (int r = 0; r < 8; ++r) in[r] = dq[r];
-    idct_1d<long long>(in, out);
+    for (int r = 0; r < 8; ++r) in[r] = blk[r][col];
+    idct_1d<T>(in, out);
 #pragma unroll
-    for (int r = 0; r < 8; ++r) ws[r] = static_cast<int>((out[r] + (1LL << 10)) >> 11);
+    for (int r = 0; r < 8; ++r) blk[r][col] = static_cast<int>((out[r] + T(1 << 10)) >> 11);
   }
 }
 
-// pass 2 of one row: butterfly, DESCALE(x, CONST_BITS + PASS1_BITS + 3), range limit
-__device__ __forceinline__ void idct_row(const int (&w)[8], uint32_t& lo, uint32_t& hi) {
-  int m = 0;
+// pass 2 (rows): DESCALE(x, CONST_BITS + PASS1_BITS + 3) + 128, range limit, 8 bytes a row
+template <typename T>
+__device__ __forceinline__ void idct_pass2(const int (&blk)[8][8], uint32_t (&lo)[8], uint32_t (&hi)[8]) {
 #pragma unroll
-  for (int i = 0; i < 8; ++i) m = max(m, abs(w[i]));
-  int px[8];
-  if (m <= (1 << 13)) {
-    int out[8];
-    idct_1d<int>(w, out);
+  for (int r = 0; r < 8; ++r) {
+    T in[8], out[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) px[i] = (out[i] + (1 << 17)) >> 18;
-  } else {
-    long long in[8], out[8];
+    for (int i = 0; i < 8; ++i) in[i] = blk[r][i];
+    idct_1d<T>(in, out);
+    uint32_t px[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) in[i] = w[i];
-    idct_1d<long long>(in, out);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) px[i] = static_cast<int>((out[i] + (1LL << 17)) >> 18);
-  }
-  lo = hi = 0;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    lo |= range_limit(px[i]) << (8 * i);
-    hi |= range_limit(px[i + 4]) << (8 * i);
+    for (int i = 0; i < 8; ++i)
+      px[i] = range_limit128(static_cast<int>((out[i] + T((1 << 17) + (128 << 18))) >> 18));
+    lo[r] = __byte_perm(__byte_perm(px[0], px[1], 0x0040), __byte_perm(px[2], px[3], 0x0040), 0x5410);
+    hi[r] = __byte_perm(__byte_perm(px[4], px[5], 0x0040), __byte_perm(px[6], px[7], 0x0040), 0x5410);
   }
 }
 
@@ -1002,201 +1001,260 @@ __device__ __forceinline__ void div_small(int a, int b, int& q, int& r) {
   }
 }
 
-// One thread per block: the 64 coefficients in registers (eight 16-byte loads), eight
-// column transforms then eight row transforms, eight 8-byte row stores.  (Eight threads per
-// block spent ~4x more instructions on per-thread set-up than on the transforms.)
-__global__ void __launch_bounds__(128) k_jpeg_idct(const JDesc* __restrict__ descs, int n,
-                                                   int64_t total_blocks, uint8_t* __restrict__ work,
-                                                   const int32_t* __restrict__ status) {
-  int ck_img = -1;
-  int64_t ck_lo = 0, ck_hi = 0;
-  for (int64_t gb = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; gb < total_blocks;
-       gb += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    if (!(ck_img >= 0 && gb >= ck_lo && gb < ck_hi)) {  // consecutive blocks: same image
-      ck_img = find_image(descs, n, gb, 1);
-      ck_lo = descs[ck_img].block_base;
-      ck_hi = ck_lo + descs[ck_img].n_blocks;
+// One thread per block: the 64 zigzag-ordered coefficients in registers (eight 16-byte
+// loads), DEQUANTIZE (short coef x short quant, ISLOW_MULT_TYPE) into natural order,
+// eight column transforms then eight row transforms, eight 8-byte row stores.  Each CTA
+// takes a contiguous range of blocks (one image lookup per CTA, not per block); each pass
+// checks its 64 inputs once for the int32 bound.
+constexpr int kIdctThreads = 128;
+
+__global__ void __launch_bounds__(kIdctThreads) k_jpeg_idct(const JDesc* __restrict__ descs, int n,
+                                                            int64_t total_blocks, int64_t per_cta,
+                                                            uint8_t* __restrict__ work,
+                                                            const int32_t* __restrict__ status) {
+  const int64_t b_lo = static_cast<int64_t>(blockIdx.x) * per_cta;
+  const int64_t b_hi = min(total_blocks, b_lo + per_cta);
+  if (b_lo >= b_hi) return;
+  int k = find_image(descs, n, b_lo, 1);
+  int64_t img_hi = descs[k].block_base + descs[k].n_blocks;
+  for (int64_t gb = b_lo + threadIdx.x; gb < b_hi; gb += kIdctThreads) {
+    while (gb >= img_hi && k + 1 < n) {  // images' blocks are consecutive
+      ++k;
+      img_hi = descs[k].block_base + descs[k].n_blocks;
     }
-    const JDesc* d = descs + ck_img;
-    if (d->n_slots == 0 || status[ck_img] != 0) continue;
+    const JDesc* d = descs + k;
+    if (d->n_slots == 0 || status[k] != 0) continue;
     const int b = static_cast<int>(gb - d->block_base);
     int mcu, u;
     div_small(b, d->bmcu, mcu, u);
     const int c = d->slot_comp[u];
     const uint4* src = reinterpret_cast<const uint4*>(
         reinterpret_cast<const int16_t*>(work + d->coef_off) + static_cast<int64_t>(b) * 64);
-    const uint4* qsrc = reinterpret_cast<const uint4*>(d->quant[c]);
-    int blk[8][8];  // [row][col], dequantized, then the workspace, then the output
+    uint32_t cw[32];
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      const uint4 cv = src[r], qv = qsrc[r];
-      const uint32_t cw[4] = {cv.x, cv.y, cv.z, cv.w}, qw[4] = {qv.x, qv.y, qv.z, qv.w};
-#pragma unroll
-      for (int i = 0; i < 8; ++i)  // DEQUANTIZE: short coef x short quant (ISLOW_MULT_TYPE)
-        blk[r][i] = static_cast<int>(static_cast<int16_t>(cw[i >> 1] >> (16 * (i & 1)))) *
-                    static_cast<int>(static_cast<int16_t>(qw[i >> 1] >> (16 * (i & 1))));
+    for (int i = 0; i < 8; ++i) {
+      const uint4 v = src[i];
+      cw[4 * i] = v.x;
+      cw[4 * i + 1] = v.y;
+      cw[4 * i + 2] = v.z;
+      cw[4 * i + 3] = v.w;
     }
+    const int4* q4 = reinterpret_cast<const int4*>(d->quant[c]);
+    int blk[8][8];  // [row][col]: dequantized, then the workspace
 #pragma unroll
-    for (int col = 0; col < 8; ++col) {  // pass 1: columns
-      int in[8], w[8];
+    for (int i = 0; i < 16; ++i) {
+      const int4 qv = q4[i];
+      const int qs[4] = {qv.x, qv.y, qv.z, qv.w};
 #pragma unroll
-      for (int r = 0; r < 8; ++r) in[r] = blk[r][col];
-      idct_col(in, w);
-#pragma unroll
-      for (int r = 0; r < 8; ++r) blk[r][col] = w[r];
+      for (int e = 0; e < 4; ++e) {
+        const int nat = 4 * i + e, zz = kNat2Zig[nat];
+        const uint32_t w = cw[zz >> 1];
+        const int coef = (zz & 1) ? static_cast<int>(w) >> 16 : static_cast<int>(static_cast<int16_t>(w));
+        blk[nat >> 3][nat & 7] = coef * qs[e];
+      }
     }
+    if (all_small(blk)) idct_pass1<int>(blk); else idct_pass1<long long>(blk);
+    uint32_t lo[8], hi[8];
+    if (all_small(blk)) idct_pass2<int>(blk, lo, hi); else idct_pass2<long long>(blk, lo, hi);
     int my, mx;
     div_small(mcu, d->mcux, my, mx);
     const int by = d->ncomp == 1 ? my : my * d->comp_v[c] + d->slot_bv[u];
     const int bx = d->ncomp == 1 ? mx : mx * d->comp_h[c] + d->slot_bh[u];
-    uint8_t* dst = work + d->plane_off[c] + static_cast<int64_t>(by * 8) * d->plane_w[c] + bx * 8;
+    const int64_t pw = d->plane_w[c];
+    uint8_t* dst = work + d->plane_off[c] + static_cast<int64_t>(by * 8) * pw + bx * 8;
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {  // pass 2: rows
-      uint32_t lo, hi;
-      idct_row(blk[r], lo, hi);
-      *reinterpret_cast<uint2*>(dst + static_cast<int64_t>(r) * d->plane_w[c]) = make_uint2(lo, hi);
-    }
+    for (int r = 0; r < 8; ++r) *reinterpret_cast<uint2*>(dst + r * pw) = make_uint2(lo[r], hi[r]);
   }
 }
 
 // ---------------------------------------------------------------------------
 // J4: upsampling + colour conversion -> RGB HWC
 
-__device__ __forceinline__ int chroma(const uint8_t* __restrict__ p, int pw, int dsw, int dsh, int hx,
-                                      int vx, int x, int y) {
-  if (hx == 1 && vx == 1) return p[static_cast<int64_t>(y) * pw + x];
-  if (dsw <= 2) return p[static_cast<int64_t>(y / vx) * pw + (x >> 1)];  // plain replication
-  const int i = x >> 1;
-  if (vx == 1) {  // h2v1 fancy
-    const uint8_t* row = p + static_cast<int64_t>(y) * pw;
-    if (x & 1) return i == dsw - 1 ? row[i] : (row[i] * 3 + row[i + 1] + 2) >> 2;
-    return i == 0 ? row[0] : (row[i] * 3 + row[i - 1] + 1) >> 2;
-  }
-  // h2v2 fancy: nearer row inrow, further row above (even y) / below (odd y), replicated
-  const int inrow = y >> 1;
-  const int other = (y & 1) ? min(inrow + 1, dsh - 1) : max(inrow - 1, 0);
-  const uint8_t* r0 = p + static_cast<int64_t>(inrow) * pw;
-  const uint8_t* r1 = p + static_cast<int64_t>(other) * pw;
-  const int cs = r0[i] * 3 + r1[i];
-  if (x & 1) {
-    if (i == dsw - 1) return (cs * 4 + 7) >> 4;
-    return (cs * 3 + r0[i + 1] * 3 + r1[i + 1] + 7) >> 4;
-  }
-  if (i == 0) return (cs * 4 + 8) >> 4;
-  return (cs * 3 + r0[i - 1] * 3 + r1[i - 1] + 8) >> 4;
+// jdcolor.c ycc_rgb_convert of one pixel (build_ycc_rgb_table: FIX(x) = x * 65536 + 0.5,
+// ONE_HALF = 32768, the tables' CENTERJSAMPLE folded into the constants) -> bytes
+// [R, G, B, 0].  R and B are clamped as two 16-bit lanes (add.s16x2 + max.s16x2.relu,
+// min.s16x2), G as one 32-bit lane.  ypair = Y | Y << 16.
+__device__ __forceinline__ uint32_t ycc_px(uint32_t ypair, int y, int cb, int cr) {
+  const int roff = (91881 * cr + (32768 - 91881 * 128)) >> 16;
+  const int boff = (116130 * cb + (32768 - 116130 * 128)) >> 16;
+  const int goff = (-22554 * cb - 46802 * cr + (32768 + (22554 + 46802) * 128)) >> 16;
+  uint32_t rb = __viaddmax_s16x2_relu(__byte_perm(static_cast<uint32_t>(roff), static_cast<uint32_t>(boff), 0x5410),
+                                      ypair, 0u);
+  asm("min.s16x2 %0, %0, %1;" : "+r"(rb) : "r"(0x00FF00FFu));
+  const int g = min(__viaddmax_s32_relu(goff, y, 0), 255);
+  return __byte_perm(rb, static_cast<uint32_t>(g), 0x1240);
 }
 
-__device__ __forceinline__ uint32_t clamp255(int v) { return static_cast<uint32_t>(min(max(v, 0), 255)); }
-
-__device__ __forceinline__ uint32_t ycc_px(int Y, int cb, int cr) {
-  // jdcolor.c build_ycc_rgb_table: FIX(x) = x * 65536 + 0.5, ONE_HALF = 32768
-  const int r = Y + ((91881 * cr + 32768) >> 16);
-  const int g = Y + ((-22554 * cb + 32768 - 46802 * cr) >> 16);
-  const int b = Y + ((116130 * cb + 32768) >> 16);
-  return clamp255(r) | (clamp255(g) << 8) | (clamp255(b) << 16);
+// 4 RGB pixels -> 3 words
+__device__ __forceinline__ void pack3(const uint32_t* p4, uint32_t* w3) {
+  w3[0] = __byte_perm(p4[0], p4[1], 0x4210);
+  w3[1] = __byte_perm(p4[1], p4[2], 0x5421);
+  w3[2] = __byte_perm(p4[2], p4[3], 0x6542);
 }
 
-// One CTA per output row; each thread 4 consecutive pixels (12 bytes, three 32-bit stores
-// when the row is 4-byte aligned, which it is whenever the width is a multiple of 4).
-__global__ void __launch_bounds__(256) k_jpeg_color(const JDesc* __restrict__ descs, int n,
-                                                    int64_t total_rows, const uint8_t* __restrict__ work,
-                                                    uint8_t* __restrict__ out,
-                                                    const int32_t* __restrict__ status) {
-  int k = -1;
-  int64_t lo = 0, hi = 0;
-  for (int64_t gr = blockIdx.x; gr < total_rows; gr += gridDim.x) {
-    if (!(k >= 0 && gr >= lo && gr < hi)) {  // rows of one image are consecutive
-      k = find_image(descs, n, gr, 2);
-      lo = descs[k].row_base;
-      hi = lo + descs[k].height;
+__device__ __forceinline__ uint32_t ld32(const uint8_t* p) { return *reinterpret_cast<const uint32_t*>(p); }
+
+constexpr int kColorThreads = 256;
+
+enum ColorMode { kGray = 0, kH2V2 = 1, kH2V1 = 2, kH1V1 = 3, kRepl = 4 };
+
+struct ColorRow {
+  const uint8_t *py, *cb0, *cb1, *cr0, *cr1;  // Y row; chroma nearer / further rows
+  int W, dsw;
+};
+
+// The raw samples 8 output pixels x0 .. x0 + 7 read (chroma columns i0 .. i0 + 3 and
+// their neighbours), loaded one step ahead of their use (the row loop is software
+// pipelined: the loads of step s + 1 are in flight while step s converts).
+struct Raw8 {
+  uint2 y;
+  uint32_t nb, fb, nr, fr;  // chroma words: nearer / further row, Cb / Cr
+  uint32_t eb[4], er[4];    // neighbour columns (fancy): near L, near R, far L, far R
+  uint32_t sel;             // the byte selector repeating the last real column
+};
+
+// fancy upsampling (h2v1 / h2v2) loads of one plane; the neighbour bytes are combined
+// only when converted, so nothing here waits for the loads
+template <bool V2>
+__device__ __forceinline__ void load_fancy(const uint8_t* near, const uint8_t* far, uint32_t& n, uint32_t& f,
+                                           uint32_t (&e)[4]) {
+  // the columns before and after the word, at immediate offsets from one address (the
+  // edge cases are selected when converting; the plane has slack before and after it)
+  n = ld32(near);
+  e[0] = near[-1];
+  e[1] = near[4];
+  if (V2) {
+    f = ld32(far);
+    e[2] = far[-1];
+    e[3] = far[4];
+  } else {
+    f = e[2] = e[3] = 0;
+  }
+}
+
+template <int MODE>
+__device__ __forceinline__ void load8(const ColorRow& c, int x0, Raw8& r) {
+  r.y = *reinterpret_cast<const uint2*>(c.py + x0);  // planes are 8-padded
+  if (MODE == kH2V2 || MODE == kH2V1) {
+    const int i0 = x0 >> 1;
+    const int lim = c.dsw - 1 - i0;  // >= 0; < 3 only at the plane's right edge
+    r.sel = lim >= 3 ? 0x3210u : static_cast<uint32_t>((0x0000221011100000ull >> (16 * min(lim, 2))) & 0xFFFFu);
+    load_fancy<MODE == kH2V2>(c.cb0 + i0, c.cb1 + i0, r.nb, r.fb, r.eb);
+    load_fancy<MODE == kH2V2>(c.cr0 + i0, c.cr1 + i0, r.nr, r.fr, r.er);
+  }
+}
+
+// jdsample.c fancy upsampling of one chroma plane for the 8 output pixels, as 16-bit lanes:
+// out[0] = (px0, px4), [1] = (px1, px5), [2] = (px2, px6), [3] = (px3, px7).  h2v2 (V2):
+// column sums 3 * nearer + further, then (3 * this + neighbour + 8 or 7) >> 4; h2v1:
+// (3 * this + neighbour + 1 or 2) >> 2.  Columns past the plane's last real column repeat
+// it (its own neighbour, through `sel`), the column before the first is the first
+// (clamped neighbour loads): jdsample.c's edge cases.
+template <bool V2>
+__device__ __forceinline__ void fancy4(uint32_t nw, uint32_t fw, uint32_t sel, const uint32_t (&e)[4],
+                                       bool first, bool last, uint32_t (&out)[4]) {
+  uint32_t L = e[0], R = e[1];
+  if (V2) {
+    L = L * 3 + e[2];
+    R = R * 3 + e[3];
+  }
+  const uint32_t n = __byte_perm(nw, 0, sel);
+  uint32_t csE = __byte_perm(n, 0, 0x4240), csO = __byte_perm(n, 0, 0x4341);  // cols (0, 2), (1, 3)
+  if (V2) {
+    const uint32_t f = __byte_perm(fw, 0, sel);
+    csE = csE * 3 + __byte_perm(f, 0, 0x4240);
+    csO = csO * 3 + __byte_perm(f, 0, 0x4341);
+  }
+  if (first) L = csE & 0xFFFFu;  // column -1 is column 0
+  if (last) R = csO >> 16;       // past the last real column: the last one (sel repeats it)
+  const uint32_t LE = csO * 65536u + L;          // cols (-1, 1)
+  const uint32_t RO = R * 65536u + (csE >> 16);  // cols (2, 4)
+  constexpr uint32_t Be = V2 ? 0x00080008u : 0x00010001u, Bo = V2 ? 0x00070007u : 0x00020002u;
+  constexpr int S = V2 ? 4 : 2;
+  const uint32_t t3E = csE * 3, t3O = csO * 3;
+  out[0] = ((t3E + LE + Be) >> S) & 0x00FF00FFu;
+  out[1] = ((t3E + csO + Bo) >> S) & 0x00FF00FFu;
+  out[2] = ((t3O + csE + Be) >> S) & 0x00FF00FFu;
+  out[3] = ((t3O + RO + Bo) >> S) & 0x00FF00FFu;
+}
+
+// RGB of the 8 pixels x0 .. x0 + 7 of one row (x0 < W; pixels past W are don't-cares)
+template <int MODE>
+__device__ __forceinline__ void color8(const ColorRow& c, int x0, const Raw8& r, uint32_t (&px)[8]) {
+  const uint32_t yw[2] = {r.y.x, r.y.y};
+  if (MODE == kGray) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) px[i] = ((yw[i >> 2] >> (8 * (i & 3))) & 255) * 0x010101u;
+    return;
+  }
+  int cbv[8], crv[8];
+  if (MODE == kH2V2 || MODE == kH2V1) {
+    uint32_t ub[4], ur[4];
+    const int i0 = x0 >> 1;
+    const bool first = i0 == 0, last = i0 + 4 > c.dsw - 1;
+    fancy4<MODE == kH2V2>(r.nb, r.fb, r.sel, r.eb, first, last, ub);
+    fancy4<MODE == kH2V2>(r.nr, r.fr, r.sel, r.er, first, last, ur);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      cbv[i] = static_cast<int>((ub[i & 3] >> (16 * (i >> 2))) & 0xFFu);
+      crv[i] = static_cast<int>((ur[i & 3] >> (16 * (i >> 2))) & 0xFFu);
     }
-    const JDesc& d = descs[k];
-    if (d.n_slots == 0 || status[k]) continue;
-    const int y = static_cast<int>(gr - d.row_base);
-    const int W = d.width;
-    uint8_t* o = out + d.out_off + static_cast<int64_t>(y) * W * 3;
-    const bool aligned = (reinterpret_cast<uintptr_t>(o) & 3) == 0;
-    const uint8_t* py = work + d.plane_off[0] + static_cast<int64_t>(y) * d.plane_w[0];
-    const int hx = d.ncomp == 1 ? 1 : d.hmax / d.comp_h[1], vx = d.ncomp == 1 ? 1 : d.vmax / d.comp_v[1];
-    const uint8_t* pcb = work + d.plane_off[d.ncomp == 1 ? 0 : 1];
-    const uint8_t* pcr = work + d.plane_off[d.ncomp == 1 ? 0 : 2];
-    // the chroma rows this output row reads: nearer row and (h2v2) the further one, the
-    // jdmainct.c context rows replicating the edges
-    const int dsw = d.ds_w[1], dsh = d.ds_h[1];
-    const int crow = vx == 2 ? y >> 1 : y;
-    const int orow = vx == 2 ? ((y & 1) ? min(crow + 1, dsh - 1) : max(crow - 1, 0)) : crow;
-    const int64_t pw1 = d.plane_w[1];
-    const uint8_t* cb0 = pcb + crow * pw1;
-    const uint8_t* cb1 = pcb + orow * pw1;
-    const uint8_t* cr0 = pcr + crow * pw1;
-    const uint8_t* cr1 = pcr + orow * pw1;
-    const bool fancy = hx == 2 && dsw > 2;
-    // 8 pixels per thread: one 8-byte Y load; for the fancy paths the chroma column sums
-    // at 4t - 1 .. 4t + 4 come from one aligned word per row and plane plus its two
-    // neighbours (clamped at the plane's real edges, which reproduces jdsample.c's first
-    // and last column cases)
-    for (int x0 = 8 * threadIdx.x; x0 < W; x0 += 8 * blockDim.x) {
-      const uint2 yv = *reinterpret_cast<const uint2*>(py + x0);  // planes are 8-padded
-      uint32_t px[8];
-      if (d.ncomp == 1) {
+  } else {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) px[i] = (((i < 4 ? yv.x : yv.y) >> (8 * (i & 3))) & 255) * 0x010101u;
-      } else if (fancy) {
-        const int i0 = x0 >> 1;  // chroma columns i0 .. i0 + 3
-        int cb[6], cr[6];        // column sums at i0 - 1 .. i0 + 4
-        if (i0 >= 1 && i0 + 4 <= dsw - 1) {
-          const uint32_t b0 = *reinterpret_cast<const uint32_t*>(cb0 + i0);
-          const uint32_t r0 = *reinterpret_cast<const uint32_t*>(cr0 + i0);
-          const uint32_t b1 = vx == 2 ? *reinterpret_cast<const uint32_t*>(cb1 + i0) : 0u;
-          const uint32_t r1 = vx == 2 ? *reinterpret_cast<const uint32_t*>(cr1 + i0) : 0u;
+    for (int i = 0; i < 8; ++i) {
+      const int x = min(x0 + i, c.W - 1);
+      const int ci = MODE == kRepl ? x >> 1 : x;  // plain replication (dsw <= 2), or 4:4:4
+      cbv[i] = c.cb0[ci];
+      crv[i] = c.cr0[ci];
+    }
+  }
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int bb0 = (b0 >> (8 * q)) & 255, rr0 = (r0 >> (8 * q)) & 255;
-            cb[q + 1] = vx == 2 ? bb0 * 3 + static_cast<int>((b1 >> (8 * q)) & 255) : bb0;
-            cr[q + 1] = vx == 2 ? rr0 * 3 + static_cast<int>((r1 >> (8 * q)) & 255) : rr0;
-          }
-          cb[0] = vx == 2 ? cb0[i0 - 1] * 3 + cb1[i0 - 1] : cb0[i0 - 1];
-          cr[0] = vx == 2 ? cr0[i0 - 1] * 3 + cr1[i0 - 1] : cr0[i0 - 1];
-          cb[5] = vx == 2 ? cb0[i0 + 4] * 3 + cb1[i0 + 4] : cb0[i0 + 4];
-          cr[5] = vx == 2 ? cr0[i0 + 4] * 3 + cr1[i0 + 4] : cr0[i0 + 4];
-        } else {
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t ypair = __byte_perm(yw[i >> 2], 0, 0x4040 + 0x0101 * (i & 3));
+    px[i] = ycc_px(ypair, static_cast<int>(ypair & 255u), cbv[i], crv[i]);
+  }
+}
+
+// one step of a row: 8 pixels per lane, 256 per warp; rows starting 16-byte aligned (width
+// a multiple of 16) are staged in the warp's shared memory and written with 16-byte
+// stores, others with 32-bit (4-byte aligned rows) or byte stores
+template <int MODE>
+__device__ __forceinline__ void color_step(const ColorRow& c, uint8_t* o, uint8_t* stage, int xw, bool row16,
+                                           bool row4, const Raw8& raw) {
+  const int lane = threadIdx.x & 31;
+  const int x0 = xw + 8 * lane;
+  uint32_t px[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (x0 < c.W) color8<MODE>(c, x0, raw, px);
+  uint32_t w[6];
+  pack3(px, w);
+  pack3(px + 4, w + 3);
+  if (row16) {
+    uint2* st = reinterpret_cast<uint2*>(stage + 24 * lane);
+    st[0] = make_uint2(w[0], w[1]);
+    st[1] = make_uint2(w[2], w[3]);
+    st[2] = make_uint2(w[4], w[5]);
+    __syncwarp();
+    uint8_t* ow = o + 3 * static_cast<int64_t>(xw);
+    const int nbytes = 3 * min(256, c.W - xw);
+    if (nbytes == 768) {  // a full step: 48 chunks of 16 bytes
+      reinterpret_cast<uint4*>(ow)[lane] = reinterpret_cast<const uint4*>(stage)[lane];
+      if (lane < 16)
+        reinterpret_cast<uint4*>(ow)[32 + lane] = reinterpret_cast<const uint4*>(stage)[32 + lane];
+    } else {
+      for (int i = lane; i < (nbytes >> 4); i += 32)
+        reinterpret_cast<uint4*>(ow)[i] = reinterpret_cast<const uint4*>(stage)[i];
+      for (int i = (nbytes & ~15) + lane; i < nbytes; i += 32) ow[i] = stage[i];
+    }
+    __syncwarp();
+  } else if (x0 < c.W) {
+    if (row4 && x0 + 8 <= c.W) {
+      uint32_t* o32 = reinterpret_cast<uint32_t*>(o + 3 * x0);
 #pragma unroll
-          for (int q = 0; q < 6; ++q) {
-            const int ii = min(max(i0 - 1 + q, 0), dsw - 1);
-            cb[q] = vx == 2 ? cb0[ii] * 3 + cb1[ii] : cb0[ii];
-            cr[q] = vx == 2 ? cr0[ii] * 3 + cr1[ii] : cr0[ii];
-          }
-        }
-        const int sh = vx == 2 ? 4 : 2;
-        const int be = vx == 2 ? 8 : 1, bo = vx == 2 ? 7 : 2;
+      for (int i = 0; i < 6; ++i) o32[i] = w[i];
+    } else {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int q = 1 + (i >> 1);              // this column's sum
-          const int nb = (i & 1) ? q + 1 : q - 1;  // the neighbour it blends with
-          const int bias = (i & 1) ? bo : be;
-          const int ccb = ((cb[q] * 3 + cb[nb] + bias) >> sh) - 128;
-          const int ccr = ((cr[q] * 3 + cr[nb] + bias) >> sh) - 128;
-          px[i] = ycc_px(((i < 4 ? yv.x : yv.y) >> (8 * (i & 3))) & 255, ccb, ccr);
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int x = min(x0 + i, W - 1);
-          const int ci = hx == 2 ? x >> 1 : x;  // 4:4:4, or plain replication (dsw <= 2)
-          px[i] = ycc_px(((i < 4 ? yv.x : yv.y) >> (8 * (i & 3))) & 255, cb0[ci] - 128, cr0[ci] - 128);
-        }
-      }
-      if (aligned && x0 + 8 <= W) {
-        uint32_t* o32 = reinterpret_cast<uint32_t*>(o + 3 * x0);
-#pragma unroll
-        for (int h4 = 0; h4 < 2; ++h4) {
-          const uint32_t* p4 = px + 4 * h4;
-          o32[3 * h4] = p4[0] | (p4[1] << 24);
-          o32[3 * h4 + 1] = (p4[1] >> 8) | (p4[2] << 16);
-          o32[3 * h4 + 2] = (p4[2] >> 16) | (p4[3] << 8);
-        }
-      } else {
-        for (int i = 0; i < 8 && x0 + i < W; ++i) {
+      for (int i = 0; i < 8; ++i) {
+        if (x0 + i < c.W) {
           o[3 * (x0 + i)] = static_cast<uint8_t>(px[i]);
           o[3 * (x0 + i) + 1] = static_cast<uint8_t>(px[i] >> 8);
           o[3 * (x0 + i) + 2] = static_cast<uint8_t>(px[i] >> 16);
@@ -1204,6 +1262,103 @@ __global__ void __launch_bounds__(256) k_jpeg_color(const JDesc* __restrict__ de
       }
     }
   }
+}
+
+// one output row by one warp, step by step; the loads of the next step are in flight while
+// a step converts
+template <int MODE>
+__device__ __forceinline__ void color_row(const ColorRow& c, uint8_t* o, uint8_t* stage) {
+  const int lane = threadIdx.x & 31;
+  const uintptr_t oa = reinterpret_cast<uintptr_t>(o);
+  const bool row16 = (oa & 15) == 0, row4 = (oa & 3) == 0;
+  Raw8 raw;
+  if (8 * lane < c.W) load8<MODE>(c, 8 * lane, raw);
+  for (int xw = 0; xw < c.W; xw += 256) {
+    Raw8 next;
+    if (xw + 256 + 8 * lane < c.W) load8<MODE>(c, xw + 256 + 8 * lane, next);
+    color_step<MODE>(c, o, stage, xw, row16, row4, raw);
+    raw = next;
+  }
+}
+
+// Each CTA takes a contiguous range of output rows, its warps one row each at a time; an
+// image's geometry and colour mode are set up once per image and warp (warp-uniform), each
+// mode runs its own specialised row code.
+__global__ void __launch_bounds__(kColorThreads, 2) k_jpeg_color(const JDesc* __restrict__ descs, int n,
+                                                              int64_t total_rows, int64_t per_cta,
+                                                              const uint8_t* __restrict__ work,
+                                                              uint8_t* __restrict__ out,
+                                                              const int32_t* __restrict__ status) {
+  __shared__ __align__(16) uint8_t stage[kColorThreads / 32][32 * 24];
+  constexpr int kWarps = kColorThreads / 32;
+  const int warp = threadIdx.x >> 5;
+  const int64_t r_lo = static_cast<int64_t>(blockIdx.x) * per_cta;
+  const int64_t r_hi = min(total_rows, r_lo + per_cta);
+  if (r_lo + warp >= r_hi) return;
+  int k = find_image(descs, n, r_lo + warp, 2) - 1;
+  int64_t img_lo = 0, img_hi = -1;
+  bool skip = true;
+  int mode = kGray, vx = 1, dsh = 1;
+  int64_t pw0 = 0, pw1 = 0;
+  const uint8_t *pY = nullptr, *pcb = nullptr, *pcr = nullptr;
+  uint8_t* o_img = nullptr;
+  ColorRow c;
+  c.W = 0;
+  c.dsw = 1;
+  uint8_t* st = stage[warp];
+  for (int64_t gr = r_lo + warp; gr < r_hi; gr += kWarps) {
+    while (gr >= img_hi && k + 1 < n) {  // the next image: geometry once (warp-uniform)
+      ++k;
+      const JDesc& d = descs[k];
+      img_lo = d.row_base;
+      img_hi = img_lo + d.height;
+      skip = d.n_slots == 0 || status[k] != 0;
+      c.W = d.width;
+      const int ncomp = d.ncomp;
+      const int hx = ncomp == 1 ? 1 : d.hmax / d.comp_h[1];
+      vx = ncomp == 1 ? 1 : d.vmax / d.comp_v[1];
+      c.dsw = d.ds_w[1];
+      dsh = d.ds_h[1];
+      mode = ncomp == 1 ? kGray : hx == 1 ? kH1V1 : c.dsw <= 2 ? kRepl : vx == 2 ? kH2V2 : kH2V1;
+      pw0 = d.plane_w[0];
+      pw1 = d.plane_w[1];
+      pY = work + d.plane_off[0];
+      pcb = work + d.plane_off[ncomp == 1 ? 0 : 1];
+      pcr = work + d.plane_off[ncomp == 1 ? 0 : 2];
+      o_img = out + d.out_off;
+    }
+    if (skip) continue;
+    const int y = static_cast<int>(gr - img_lo);
+    uint8_t* o = o_img + static_cast<int64_t>(y) * c.W * 3;
+    c.py = pY + static_cast<int64_t>(y) * pw0;
+    // the chroma rows this output row reads: nearer row and (h2v2) the further one, the
+    // jdmainct.c context rows replicating the edges
+    const int crow = vx == 2 ? y >> 1 : y;
+    const int orow = vx == 2 ? ((y & 1) ? min(crow + 1, dsh - 1) : max(crow - 1, 0)) : crow;
+    c.cb0 = pcb + crow * pw1;
+    c.cb1 = pcb + orow * pw1;
+    c.cr0 = pcr + crow * pw1;
+    c.cr1 = pcr + orow * pw1;
+    switch (mode) {
+      case kH2V2: color_row<kH2V2>(c, o, st); break;
+      case kH2V1: color_row<kH2V1>(c, o, st); break;
+      case kH1V1: color_row<kH1V1>(c, o, st); break;
+      case kRepl: color_row<kRepl>(c, o, st); break;
+      default: color_row<kGray>(c, o, st); break;
+    }
+  }
+}
+
+// resident CTAs per SM of a kernel at `threads` threads (cached per device in `cache`)
+template <typename K>
+int resident_per_sm(K* kernel, int threads, int dev, int (&cache)[64]) {
+  int& v = cache[dev];
+  if (v == 0) {
+    int r = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, kernel, threads, 0);
+    v = r > 0 ? r : 1;
+  }
+  return v;
 }
 
 __global__ void k_jpeg_status_init(const JDesc* __restrict__ descs, int n, int32_t* status) {
@@ -1241,11 +1396,12 @@ TP_API int tp_jpeg_decode(const uint8_t* d_payload, const void* d_desc, int32_t 
     k_jpeg_unstuff_count<<<static_cast<unsigned>(chunks), kUnstuffThreads, 0, s>>>(d_payload, descs, n, counts, d_status);
     k_jpeg_unstuff_write<<<static_cast<unsigned>(chunks), kUnstuffThreads, 0, s>>>(d_payload, descs, n, counts, work, d_status);
   }
+  static int idct_occ[64], color_occ[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64)
+    return set_error(TP_ERR_CUDA, "tp_jpeg_decode: no usable device");
   if (slots > 0) {
     static int per_sm_of[64];
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64)
-      return set_error(TP_ERR_CUDA, "tp_jpeg_decode: no usable device");
     int& per_sm = per_sm_of[dev];
     if (per_sm == 0) {
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_jpeg_huff, 256, 0);
@@ -1265,11 +1421,19 @@ TP_API int tp_jpeg_decode(const uint8_t* d_payload, const void* d_desc, int32_t 
     if (e != cudaSuccess) return set_error(TP_ERR_CUDA, "tp_jpeg_decode: %s", cudaGetErrorString(e));
   }
   if (blocks > 0) {
-    const int64_t g = (blocks + 127) / 128;
-    k_jpeg_idct<<<static_cast<unsigned>(g < 32 * sms ? g : 32 * sms), 128, 0, s>>>(descs, n, blocks, work, d_status);
+    // contiguous ranges of whole thread-rows, one wave of resident CTAs
+    const int64_t target = static_cast<int64_t>(resident_per_sm(k_jpeg_idct, kIdctThreads, dev, idct_occ)) * sms;
+    int64_t per = (blocks + target - 1) / target;
+    per = (per + kIdctThreads - 1) / kIdctThreads * kIdctThreads;
+    const int64_t g = (blocks + per - 1) / per;
+    k_jpeg_idct<<<static_cast<unsigned>(g), kIdctThreads, 0, s>>>(descs, n, blocks, per, work, d_status);
   }
   if (rows > 0) {
-    k_jpeg_color<<<static_cast<unsigned>(rows < 64 * sms ? rows : 64 * sms), 256, 0, s>>>(descs, n, rows, work, d_out, d_status);
+    // contiguous row ranges, one wave of resident CTAs
+    const int64_t target = static_cast<int64_t>(resident_per_sm(k_jpeg_color, kColorThreads, dev, color_occ)) * sms;
+    const int64_t per = (rows + target - 1) / target;
+    const int64_t g = (rows + per - 1) / per;
+    k_jpeg_color<<<static_cast<unsigned>(g), kColorThreads, 0, s>>>(descs, n, rows, per, work, d_out, d_status);
   }
   return check_launch("tp_jpeg_decode");
 }

@@ -44,7 +44,9 @@ struct __align__(16) JDesc {
   int32_t comp_td[kMaxComps], comp_ta[kMaxComps], comp_tq[kMaxComps];
   int8_t slot_comp[kMaxBlocksPerMcu], slot_bh[kMaxBlocksPerMcu], slot_bv[kMaxBlocksPerMcu];
   int8_t pad_[2];
-  alignas(16) uint16_t quant[kMaxComps][64];  // natural order, per component (16-byte rows)
+  // natural order, per component, as libjpeg's ISLOW_MULT_TYPE (short) holds them:
+  // (int16) quantval, sign-extended
+  alignas(16) int32_t quant[kMaxComps][64];
   JHuff dc[2], ac[2];
 };
 

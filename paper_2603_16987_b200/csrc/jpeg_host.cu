@@ -298,7 +298,7 @@ TP_API int64_t tp_jpeg_describe(const TpJpegInfo* infos, int32_t n, const int64_
       j.plane_h[c] = j.mcuy * vc * 8;
       j.ds_w[c] = static_cast<int32_t>((static_cast<int64_t>(in.width) * in.comp_h[c] + hmax - 1) / hmax);
       j.ds_h[c] = static_cast<int32_t>((static_cast<int64_t>(in.height) * in.comp_v[c] + vmax - 1) / vmax);
-      for (int i = 0; i < 64; ++i) j.quant[c][i] = in.qt[in.comp_tq[c]][i];
+      for (int i = 0; i < 64; ++i) j.quant[c][i] = static_cast<int16_t>(in.qt[in.comp_tq[c]][i]);
     }
     for (int t = 0; t < 2; ++t) {
       if ((in.dc_mask >> t & 1) && !build_huff(in.dc_bits[t], in.dc_vals[t], true, &j.dc[t]))
@@ -339,7 +339,8 @@ TP_API int64_t tp_jpeg_describe(const TpJpegInfo* infos, int32_t n, const int64_
     w = align_up(w + 8 * (static_cast<int64_t>(j.n_seg) + 1), 256);
     for (int c = 0; c < j.ncomp; ++c) {
       j.plane_off[c] = w;
-      w = align_up(w + static_cast<int64_t>(j.plane_w[c]) * j.plane_h[c], 256);
+      // + 64: the colour kernel reads a row's neighbour byte one past the plane's last row
+      w = align_up(w + static_cast<int64_t>(j.plane_w[c]) * j.plane_h[c] + 64, 256);
     }
   }
   totals[0] = slots;

@@ -58,6 +58,16 @@ def test_1080p_variants(kw):
     _check([encode(px, **kw)], expect_device=[0])
 
 
+@pytest.mark.parametrize("ss", [0, 1, 2])
+def test_wide_rows(ss):
+    # rows wider than one CTA pass (2048 pixels): 16-byte aligned (staged stores), 4-byte
+    # aligned and unaligned rows, each with a partial last warp; plus one gray
+    payloads = [encode(scene(w, h, w + ss), 85, subsampling=ss)
+                for (w, h) in [(2304, 24), (2600, 18), (4097, 9), (2050, 33)]]
+    payloads.append(encode(scene(2333, 12, 1), 90, gray=True))
+    _check(payloads, expect_device=[0, 1, 2, 3, 4])
+
+
 @pytest.mark.parametrize("sub_bits", [256, 1024, 2048, 8192])
 def test_noise_and_sub_bits(sub_bits):
     rng = np.random.default_rng(sub_bits)
