@@ -258,6 +258,51 @@ TP_API int tp_jpeg_decode(const uint8_t* d_payload, const void* d_desc, int32_t 
                           int64_t work_bytes, uint8_t* d_out, int32_t* d_status,
                           void* stream);
 
+/* K8 — device PNG decode (replaces the PIL decode of
+ * decode_image / _decode_pass, imgproc.py:213-260, for 8-bit L / RGB / P PNGs).  PNG is
+ * lossless, so the pixels are Pillow's by construction; what must match is which
+ * payloads the device takes.
+ * Host side:
+ *   tp_png_parse      chunk walk of one payload (host memory) with Pillow's rules
+ *                     (PngImagePlugin: CRCs before the first IDAT, handlers that can
+ *                     raise); info->status TP_PNG_OK: 8-bit non-interlaced colour type 0,
+ *                     2 or 3, one IDAT run, zlib without preset dictionary.  The first
+ *                     idat_cap IDAT chunks' data extents go to idat_off / idat_len
+ *                     (info->n_idat counts all of them).  Anything else is
+ *                     TP_PNG_UNSUPPORTED: decode it on the host, as the reference does.
+ *   tp_png_describe   per-image descriptors (tp_png_desc_bytes() each): image k's zlib
+ *                     stream (its IDAT data back to back) at in_off[k] of the payload
+ *                     (4-byte aligned, 16 readable bytes after it), RGB HWC output at
+ *                     out_off[k]; returns the workspace bytes tp_png_decode needs.
+ * Device side:
+ *   tp_png_decode     block finder (deflate block headers at unit boundaries) ->
+ *                     parallel inflate of the units to tokens -> chain check + unit
+ *                     offsets -> token expansion with window markers -> window
+ *                     propagation -> marker resolution -> unfilter (Sub/Up/Average/Paeth
+ *                     wavefront) + L/P -> RGB.  d_status[k] = 0, or nonzero when image k
+ *                     must be decoded on the host (corrupt, truncated, or a stream the
+ *                     finder could not chain). */
+#define TP_PNG_OK 0
+#define TP_PNG_UNSUPPORTED 1
+typedef struct {
+  int32_t status;
+  int32_t width, height, bit_depth, color_type, interlace;
+  int32_t pal_n;   /* PLTE entries (colour type 3) */
+  int32_t n_idat; /* IDAT chunks in the (first) IDAT run */
+  int64_t zlib_len; /* bytes of IDAT data */
+  uint8_t pal[768];
+  char message[96];
+} TpPngInfo;
+TP_API int tp_png_parse(const uint8_t* data, int64_t len, TpPngInfo* info, int64_t* idat_off,
+                        int64_t* idat_len, int32_t idat_cap);
+TP_API int64_t tp_png_desc_bytes(void);
+TP_API int64_t tp_png_describe(const TpPngInfo* infos, int32_t n, const int64_t* in_off,
+                               const int64_t* out_off, void* desc,
+                               int64_t* totals /* [8]: units, tokens, raw bytes, 4 offsets, bytes */);
+TP_API int tp_png_decode(const uint8_t* d_payload, const void* d_desc, int32_t n,
+                         const int64_t* totals, void* d_work, int64_t work_bytes, uint8_t* d_out,
+                         int32_t* d_status, void* stream);
+
 /* K2 variant for resize_bilinear / _resize_array (imgproc.py:352-367): one
  * full-frame half-pixel bilinear resize, uint8 HWC -> uint8 HWC. */
 TP_API int tp_resize(const uint8_t* d_src, int32_t width, int32_t height, int32_t channels,

@@ -85,6 +85,11 @@ SIGNATURES = {
                                    c_void_p]),
     "tp_jpeg_decode": (c_int32, [c_void_p, c_void_p, c_int32, c_void_p, c_int32, c_void_p,
                                  c_int64, c_void_p, c_void_p, c_void_p]),
+    "tp_png_parse": (c_int32, [c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_int32]),
+    "tp_png_desc_bytes": (c_int64, []),
+    "tp_png_describe": (c_int64, [c_void_p, c_int32, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "tp_png_decode": (c_int32, [c_void_p, c_void_p, c_int32, c_void_p, c_void_p, c_int64,
+                                c_void_p, c_void_p, c_void_p]),
     "tp_resize": (c_int32, [c_void_p, c_int32, c_int32, c_int32, c_int32, c_int32, c_void_p,
                             c_void_p]),
     "tp_normalize": (c_int32, [c_void_p, c_int64, c_int64, c_int32, c_void_p, c_int32,

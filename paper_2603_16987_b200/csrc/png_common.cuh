@@ -1,0 +1,90 @@
+// Device PNG decoder (K8): shared layouts (host describe <-> device kernels).
+#pragma once
+
+#include <stdint.h>
+
+namespace tp {
+namespace png {
+
+// Block-finder chunk: unit u of an image starts at the first deflate block header found
+// in bits [u * kUnitBits, (u + 1) * kUnitBits) of its zlib stream (unit 0 at bit 16,
+// right after the two-byte zlib header).  One thread inflates one unit.
+constexpr int64_t kUnitBits = 8 * 12288;
+constexpr int kWindow = 32768;  // deflate's back-reference window
+
+// Unit states (PUnit::status): 0 ok; the rest send the image to the host decoder.
+enum : int32_t {
+  kUnitOk = 0,
+  kUnitBadCode = 1,      // invalid / over-subscribed / incomplete code, bad symbol
+  kUnitOverrun = 2,      // read past the stream, or tokens past the unit's capacity
+  kUnitBadStored = 3,    // stored block LEN / NLEN mismatch
+  kUnitBadDistance = 4,  // back reference before the image start
+  kUnitTokens = 5,       // tokens past the unit's capacity (its decode passed the next
+                         // start, or the stream spends < 2 bits per token)
+};
+
+// Image states (d_status): 0 ok; nonzero: decode this one on the host (Pillow).  The
+// chain kernel sets one of the first four; the later kernels OR in the flags.
+enum : int32_t {
+  kImgOk = 0,
+  kImgInflate = 1,     // a unit failed (see kUnit*)
+  kImgChain = 2,       // units do not chain after kRounds rounds
+  kImgLength = 3,      // inflated length differs from height * (1 + rowbytes)
+  kImgNotFinal = 4,    // the stream ends without a final block
+  kImgDistance = 16,   // a back reference before the image start
+  kImgFilter = 32,     // filter type > 4
+  kImgPalette = 64,    // palette index beyond the PLTE entries
+  kImgAdler = 128,     // Adler-32 trailer present and wrong (Pillow's zlib raises)
+};
+
+// Inflate rounds: a header the finder accepted that is not a real block start is caught
+// when the preceding unit's decode passes it; that unit is then re-decoded up to the next
+// start in the following round.
+constexpr int kRounds = 3;
+
+// Per image, written by tp_png_describe and uploaded with the compressed bytes.
+struct __align__(16) PDesc {
+  int64_t in_off;     // zlib stream (header included) in the payload, 4-byte aligned
+  int64_t in_bits;    // bits of the zlib stream (deflate data starts at bit 16)
+  int64_t raw_off;    // inflated scanlines: offset in the T (u16) / R (u8) workspaces
+  int64_t raw_len;    // height * (1 + width * bpp)
+  int64_t out_off;    // RGB HWC uint8 in the output buffer
+  int64_t tok_off;    // token workspace (u32) of this image: in_bits / 2 + slack
+  int32_t width, height;
+  int32_t bpp;        // bytes per pixel of the scanlines: 1 (L, P) or 3 (RGB)
+  int32_t ctype;      // PNG colour type: 0 (L), 2 (RGB), 3 (P)
+  int32_t unit_base;  // first unit of this image
+  int32_t n_units;
+  int32_t pal_n;      // PLTE entries (P)
+  int32_t pad_;
+  uint8_t pal[768];   // PLTE (P)
+};
+
+// Per unit (workspace), filled by the finder and the inflate kernel.
+// Unit starts and ends are canonical block positions: the header bit of a dynamic or
+// fixed block, but for a stored block the byte boundary of its LEN field (the header bits
+// and zero padding before it can begin at several bit positions that all look alike).
+struct __align__(16) PUnit {
+  int64_t start;    // first bit (relative to the zlib stream); -1: no header found
+  int64_t end;      // bit after the unit's last block
+  int64_t out_len;  // inflated bytes
+  int64_t out_off;  // first inflated byte (relative to raw_off), by the chain scan
+  int32_t ntok;     // tokens written
+  int32_t status;   // kUnit*
+  int32_t final_;   // the unit ended with the BFINAL block
+  int32_t dirty;    // (re)decode in the next inflate round
+  int32_t stored;   // start is the LEN field of a stored block (its header not read)
+  int32_t pad_[3];
+  int64_t final_end;  // (an image's first unit) bit after the final block, by the chain
+  int64_t pad2_;
+};
+
+// Token (u32), what the inflate kernel writes and the expand kernel turns into bytes:
+//   type 0 (bits 31..30 = 00): 1-3 literals, count in bits 25..24, bytes in 7..0, 15..8, 23..16
+//   type 1 (01): match, length - 3 in bits 23..16, distance - 1 in bits 15..0
+//   type 2 (10): stored block, byte offset of its data in the zlib stream in bits 29..0;
+//                LEN is the 16-bit word 4 bytes before the data
+constexpr uint32_t kTokMatch = 1u << 30, kTokStored = 2u << 30;
+
+}  // namespace png
+}  // namespace tp
