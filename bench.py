@@ -590,7 +590,8 @@ def run_c2(args, dist, device, dev_index):
                                                                    images.wh_host)]
     del images, out
     res["e2e"] = run_e2e(args, dist, device, cfg, host_imgs)
-    res["e2e_jpeg"] = run_e2e_jpeg(args, dist, device, cfg)
+    res["e2e_jpeg"] = run_e2e_coded(args, dist, device, cfg, "jpeg")
+    res["e2e_png"] = run_e2e_coded(args, dist, device, cfg, "png")
     return res
 
 
@@ -700,21 +701,28 @@ def _cpu_jpeg_one(args):
 _CPU_PAYLOADS: list = []
 
 
-def run_e2e_jpeg(args, dist, device, cfg) -> dict:
-    """The C2 batch as JPEG payloads (64 corpus-like 1080p scenes, q85 baseline 4:2:0),
-    end to end from the caller's bytes: device JPEG decode (K7: host marker parse + one
-    H2D of the compressed scans + parallel Huffman / IDCT / colour on the GPU) -> K1 + K2
-    -> D2H of the plans; two buffer sets, so the host work of step i+1 overlaps step i.
-    Host wall clock; the reference's own preprocess (decode included) on all host cores
-    beside it."""
+def run_e2e_coded(args, dist, device, cfg, fmt: str = "jpeg") -> dict:
+    """The C2 batch as coded payloads, end to end from the caller's bytes -- fmt "jpeg":
+    64 corpus-like 1080p scenes, q85 baseline 4:2:0, device JPEG decode (K7: host marker
+    parse + one H2D of the compressed scans + parallel Huffman / IDCT / colour on the GPU);
+    fmt "png": the same scenes as Pillow PNGs, device PNG decode (K8: host chunk walk +
+    one H2D of the IDAT data + block finder / parallel inflate / unfilter on the GPU) --
+    then K1 + K2 -> D2H of the plans; two buffer sets, so the host work of step i+1
+    overlaps step i.  Host wall clock; the reference's own preprocess (decode included)
+    on all host cores beside it."""
     import torch
 
     from paper_2603_16987_b200.engine import TilePreprocessor
     from paper_2603_16987_b200.jpeg import JpegDecoder
-    from paper_2603_16987_b200.workloads import jpeg_payloads
+    from paper_2603_16987_b200.png import PngDecoder
+    from paper_2603_16987_b200.workloads import jpeg_payloads, png_payloads
 
-    payloads = jpeg_payloads(args.batch, seed=20260817 + 97 * dist.rank)
-    dec = JpegDecoder(device, depth=2)
+    if fmt == "png":
+        payloads = png_payloads(args.batch, seed=20260817 + 97 * dist.rank)
+        dec = PngDecoder(device, depth=2)
+    else:
+        payloads = jpeg_payloads(args.batch, seed=20260817 + 97 * dist.rank)
+        dec = JpegDecoder(device, depth=2)
     prep = TilePreprocessor(cfg, device)
     stream = torch.cuda.Stream(device)
     outs, pend = [None, None], [None, None]
@@ -765,10 +773,16 @@ def run_e2e_jpeg(args, dist, device, cfg) -> dict:
            "payload_kb_avg": round(sum(map(len, payloads)) / n / 1e3, 1),
            "decode_kernels_ms": round(a.elapsed_time(b) / 5, 4),
            "host_fallbacks": dec.last_fallback, "refits": refits[0],
-           "path": "caller's JPEG bytes -> JpegDecoder.decode(sync=False): tp_jpeg_parse + "
-                   "tp_jpeg_describe + tp_stage_pack into a pinned slab -> one H2D of the "
-                   "compressed scans -> K7 (unstuff, self-synchronizing parallel Huffman, "
-                   "ISLOW IDCT, fancy upsampling + YCbCr->RGB) -> K1 + K2 -> D2H plans",
+           "path": ("caller's JPEG bytes -> JpegDecoder.decode(sync=False): tp_jpeg_parse + "
+                    "tp_jpeg_describe + tp_stage_pack into a pinned slab -> one H2D of the "
+                    "compressed scans -> K7 (unstuff, self-synchronizing parallel Huffman, "
+                    "ISLOW IDCT, fancy upsampling + YCbCr->RGB) -> K1 + K2 -> D2H plans")
+           if fmt == "jpeg" else
+           ("caller's PNG bytes (Pillow, default settings) -> PngDecoder.decode(sync=False): "
+            "tp_png_parse + tp_png_describe + tp_stage_pack of the IDAT data into a pinned "
+            "slab -> one H2D -> K8 (block finder, warp-parallel speculative inflate, chain "
+            "check, token expansion, window markers, Adler-32, unfilter wavefront) -> "
+            "K1 + K2 -> D2H plans"),
            "timing": "host wall clock around all steps (synchronize + barrier both sides, "
                      "max over ranks)"}
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
@@ -785,7 +799,7 @@ def run_e2e_jpeg(args, dist, device, cfg) -> dict:
             dt = time.perf_counter() - t1
         res["cpu_baseline"] = {
             "value": round(n / dt, 3), "unit": UNIT, "cores": cores, "kind": cpu_kind(),
-            "sample": f"the same {n} JPEG payloads through "
+            "sample": f"the same {n} {fmt.upper()} payloads through "
                       + ("vlmfp.preprocess (the reference: Pillow decode + plan + fused tiles "
                          "+ normalize, fastest toggles)" if reference_module() is not None
                          else "Pillow decode + the oracle port")
@@ -795,7 +809,7 @@ def run_e2e_jpeg(args, dist, device, cfg) -> dict:
 
 def run_dropin(args, device, runs: int = 60) -> dict:
     """The drop-in per-request path: preprocess(payload, cfg) for one 1080p image as a
-    JPEG (device decode) and as a PNG (Pillow decode on the host, as the reference),
+    JPEG (device decode, K7) and as a PNG (device decode, K8),
     C2 tiling, sequential requests; p50/p99 and the median of every stage_timings_ns
     key, beside the reference's own vlmfp.preprocess (fastest toggles, one host core)
     on the same payloads."""
@@ -1175,6 +1189,7 @@ def main(argv=None):
             "cpu_baseline": cpu,
             "e2e": r["e2e"],
             "e2e_jpeg": r["e2e_jpeg"],
+            "e2e_png": r["e2e_png"],
             "gpu_launches": 2 * args.steps,
             "gpu_launches_sub_blocks": n_sub_launches,
             "clocks": r["clk"],

@@ -272,7 +272,7 @@ TP_API int tp_jpeg_decode(const uint8_t* d_payload, const void* d_desc, int32_t 
  *                     TP_PNG_UNSUPPORTED: decode it on the host, as the reference does.
  *   tp_png_describe   per-image descriptors (tp_png_desc_bytes() each): image k's zlib
  *                     stream (its IDAT data back to back) at in_off[k] of the payload
- *                     (4-byte aligned, 16 readable bytes after it), RGB HWC output at
+ *                     (16-byte aligned, 64 readable bytes after it), RGB HWC output at
  *                     out_off[k]; returns the workspace bytes tp_png_decode needs.
  * Device side:
  *   tp_png_decode     block finder (deflate block headers at unit boundaries) ->
@@ -298,7 +298,7 @@ TP_API int tp_png_parse(const uint8_t* data, int64_t len, TpPngInfo* info, int64
 TP_API int64_t tp_png_desc_bytes(void);
 TP_API int64_t tp_png_describe(const TpPngInfo* infos, int32_t n, const int64_t* in_off,
                                const int64_t* out_off, void* desc,
-                               int64_t* totals /* [8]: units, tokens, raw bytes, 4 offsets, bytes */);
+                               int64_t* totals /* [16]: workspace layout (csrc/png_common.cuh) */);
 TP_API int tp_png_decode(const uint8_t* d_payload, const void* d_desc, int32_t n,
                          const int64_t* totals, void* d_work, int64_t work_bytes, uint8_t* d_out,
                          int32_t* d_status, void* stream);

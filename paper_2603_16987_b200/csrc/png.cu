@@ -37,36 +37,51 @@ using namespace tp::png;
 constexpr int kLitRoot = 9;
 constexpr int kLitCap = 852;  // zlib's ENOUGH_LENS for a 9-bit root: worst-case entries
 constexpr int kDistRoot = 6;
-constexpr int kInflateThreads = 96;
-// per-thread shared memory: literal/length table (u16), distance root table (u8),
-// distance code counts (u8[16]) and symbols in canonical order (u8[32])
+// distance table: root of 2^kDistRoot bytes, code counts (u8[16]) and the symbols in
+// canonical order (u8[32])
 constexpr int kDistBytes = (1 << kDistRoot) + 16 + 32;
-constexpr int kThreadSmem = kLitCap * 2 + kDistBytes;
-static_assert(kThreadSmem % 4 == 0, "table alignment");
 
 // ---------------------------------------------------------------------------
-// bit reader: deflate packs bits LSB first; the stream is 4-byte aligned in the payload
-// with 16 readable bytes after it
+// bit reader: deflate packs bits LSB first; the stream is 16-byte aligned in the payload
+// with 64 readable bytes after it
 
 struct Bits {
-  const uint32_t* w;
-  int64_t wi;
+  // 16-byte loads queued two ahead (`cur` being consumed, `nxt` in flight): a thread
+  // decodes ~16 symbols per 16 bytes, which covers the load latency
+  const uint4* w4;
+  int64_t qi;  // next 16-byte group to load
+  uint4 cur, nxt;
+  int ci;      // next word of `cur`
   uint64_t buf;
   int n;
+  __device__ __forceinline__ static uint32_t word(const uint4& v, int i) {
+    return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
+  }
+  __device__ __forceinline__ uint32_t next_word() {
+    if (ci == 4) {
+      cur = nxt;
+      nxt = __ldg(w4 + qi++);
+      ci = 0;
+    }
+    return word(cur, ci++);
+  }
   __device__ __forceinline__ void init(const uint32_t* words, int64_t bit) {
-    w = words;
-    wi = bit >> 5;
+    w4 = reinterpret_cast<const uint4*>(words);
+    const int64_t wd = bit >> 5;
+    qi = wd >> 2;
+    cur = __ldg(w4 + qi);
+    nxt = __ldg(w4 + qi + 1);
+    qi += 2;
+    ci = static_cast<int>(wd & 3);
     const int s = static_cast<int>(bit & 31);
-    buf = static_cast<uint64_t>(__ldg(w + wi)) >> s;
+    buf = static_cast<uint64_t>(word(cur, ci++)) >> s;
     n = 32 - s;
-    ++wi;
     refill();
   }
   __device__ __forceinline__ void refill() {
     if (n <= 32) {
-      buf |= static_cast<uint64_t>(__ldg(w + wi)) << n;
+      buf |= static_cast<uint64_t>(next_word()) << n;
       n += 32;
-      ++wi;
     }
   }
   __device__ __forceinline__ uint32_t peek(int k) const {
@@ -76,7 +91,7 @@ struct Bits {
     buf >>= k;
     n -= k;
   }
-  __device__ __forceinline__ int64_t pos() const { return wi * 32 - n; }
+  __device__ __forceinline__ int64_t pos() const { return (((qi - 2) << 2) + ci) * 32 - n; }
 };
 
 // 64 bits starting at bit p (for the finder's header probes)
@@ -368,16 +383,74 @@ __device__ __forceinline__ bool dynamic_probe(const uint32_t* w, int64_t p) {
   return sum == 128;
 }
 
-__device__ bool dynamic_full(const uint32_t* w, int64_t p, int64_t in_bits) {
+// Full check of a dynamic header at p (after the quick probe): decode the code lengths
+// with the code-length code and require complete literal/length and distance codes
+// (zlib always writes complete codes) with an end-of-block code.  Kraft sums run while
+// decoding, so random bits fail within a few lengths; no length array is kept.
+// tab: 128 bytes of scratch (shared memory) for the code-length code.
+__device__ bool dynamic_full(const uint32_t* w, int64_t p, int64_t in_bits, uint8_t* tab) {
   Bits br;
   br.init(w, p + 3);
-  uint8_t lens[320];
-  uint8_t tab[128];
-  int hlit, hdist;
-  if (!read_dynamic_lengths(br, lens, tab, hlit, hdist, in_bits)) return false;
-  if (br.pos() > in_bits) return false;
-  int count[16];
-  return kraft_ok(lens, hlit, 15, count) && kraft_ok(lens + hlit, hdist, 15, count);
+  const int hlit = static_cast<int>(br.peek(5)) + 257;
+  br.drop(5);
+  const int hdist = static_cast<int>(br.peek(5)) + 1;
+  br.drop(5);
+  const int hclen = static_cast<int>(br.peek(4)) + 4;
+  br.drop(4);
+  if (hlit > 286 || hdist > 30) return false;
+  uint8_t cl[19];
+  for (int i = 0; i < 19; ++i) cl[i] = 0;
+  const uint8_t kOrder[19] = {16, 17, 18, 0, 8, 7, 9, 6, 10, 5, 11, 4, 12, 3, 13, 2, 14, 1, 15};
+  for (int i = 0; i < hclen; ++i) {
+    br.refill();
+    cl[kOrder[i]] = static_cast<uint8_t>(br.peek(3));
+    br.drop(3);
+  }
+  if (!build_precode(cl, tab)) return false;
+  const int total = hlit + hdist;
+  int lit_left = 1 << 15, dist_left = 1 << 15;
+  int prev = 0, i = 0;
+  bool eob = false;
+  auto put = [&](int l, int rep) -> bool {
+    for (int r = 0; r < rep; ++r, ++i) {
+      if (!l) continue;
+      if (i < hlit) {
+        lit_left -= (1 << 15) >> l;
+        if (lit_left < 0) return false;
+        if (i == 256) eob = true;
+      } else {
+        dist_left -= (1 << 15) >> l;
+        if (dist_left < 0) return false;
+      }
+    }
+    return true;
+  };
+  while (i < total) {
+    if (br.pos() > in_bits) return false;
+    br.refill();
+    const uint8_t e = tab[br.peek(7)];
+    br.drop(e >> 5);
+    const int sym = e & 31;
+    int l = 0, rep = 1;
+    if (sym < 16) {
+      l = sym;
+    } else if (sym == 16) {
+      if (i == 0) return false;
+      l = prev;
+      rep = 3 + static_cast<int>(br.peek(2));
+      br.drop(2);
+    } else if (sym == 17) {
+      rep = 3 + static_cast<int>(br.peek(3));
+      br.drop(3);
+    } else {
+      rep = 11 + static_cast<int>(br.peek(7));
+      br.drop(7);
+    }
+    if (i + rep > total) return false;
+    if (!put(l, rep)) return false;
+    prev = l;
+  }
+  return eob && lit_left == 0 && dist_left == 0;
 }
 
 // stored header at p (BTYPE 00): zero padding to the byte boundary, LEN == ~NLEN;
@@ -397,15 +470,15 @@ __device__ __forceinline__ bool stored_probe(const uint32_t* w, int64_t p, int64
 }
 
 // 0: no header at p; 1: dynamic header; 2: stored header (canonical start: its LEN byte)
-__device__ int header_candidate(const uint32_t* w, int64_t p, int64_t in_bits) {
+__device__ int header_candidate(const uint32_t* w, int64_t p, int64_t in_bits, uint8_t* tab) {
   if (p + 3 > in_bits) return 0;
-  if (dynamic_probe(w, p)) return dynamic_full(w, p, in_bits) ? 1 : 0;
+  if (dynamic_probe(w, p)) return dynamic_full(w, p, in_bits, tab) ? 1 : 0;
   int64_t nxt;
   if (!stored_probe(w, p, in_bits, &nxt)) return 0;
   if (nxt == in_bits - 32) return 2;  // the last block: the Adler-32 trailer follows
   // a stored block must be followed by another plausible header
   if (nxt + 3 > in_bits) return 0;
-  if (dynamic_probe(w, nxt)) return dynamic_full(w, nxt, in_bits) ? 2 : 0;
+  if (dynamic_probe(w, nxt)) return dynamic_full(w, nxt, in_bits, tab) ? 2 : 0;
   int64_t nxt2;
   return stored_probe(w, nxt, in_bits, &nxt2) ? 2 : 0;
 }
@@ -422,34 +495,131 @@ __device__ __forceinline__ int unit_image(const PDesc* __restrict__ desc, int n,
 // ---------------------------------------------------------------------------
 // find: one warp per unit
 
-__global__ void k_png_find(const uint8_t* __restrict__ payload, const PDesc* __restrict__ desc,
-                           int n, PUnit* __restrict__ units, int U) {
+constexpr int kFindThreads = 256;
+
+// bits [k, k + 32) of the 128-bit little-endian window (w3 w2 w1 w0), k in [0, 96]
+__device__ __forceinline__ uint32_t win32(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3,
+                                          uint32_t k) {
+  const uint32_t s = k & 31;
+  const uint32_t lo = k < 32 ? w0 : k < 64 ? w1 : w2, hi = k < 32 ? w1 : k < 64 ? w2 : w3;
+  return __funnelshift_r(lo, hi, s);
+}
+
+// One warp per unit; each lane tests the 32 positions of one word per step (a warp
+// step covers 1024 positions).  Stage 1 is bit-parallel over the word: BTYPE = 2 and
+// HLIT, HDIST <= 29 (~22% of random positions pass).  Stage 2 sums the code-length
+// code's Kraft terms with a 9-bit table (three 3-bit lengths per lookup); ~0.09% of
+// random positions have a complete code.  Those go to the full check (decoding the code
+// lengths: hundreds of dependent steps when the random lengths are mostly zeros), which
+// the warp runs 32 candidates at a time, one per lane, from a per-warp queue -- run
+// inline they would serialise the warp once per step.  Stored blocks are tested per byte
+// boundary (LEN == ~NLEN).  Any true block start will do; the warp takes the first
+// success of its first successful batch.
+constexpr int kFindQueue = 32;
+
+__global__ void __launch_bounds__(kFindThreads)
+    k_png_find(const uint8_t* __restrict__ payload, const PDesc* __restrict__ desc, int n,
+               PUnit* __restrict__ units, int U) {
+  __shared__ uint8_t tabs[kFindThreads][128];  // code-length code of a lane's full check
+  __shared__ uint8_t kraft9[512];              // Kraft terms of three 3-bit lengths
+  __shared__ int64_t queue[kFindThreads / 32][kFindQueue];
+  for (int i = threadIdx.x; i < 512; i += blockDim.x) {
+    int sum = 0;
+    for (int f = 0; f < 3; ++f) {
+      const int l = (i >> (3 * f)) & 7;
+      if (l) sum += 128 >> l;
+    }
+    kraft9[i] = static_cast<uint8_t>(sum);
+  }
+  __syncthreads();
   const int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (u >= U) return;
+  int64_t* q = queue[threadIdx.x >> 5];
   const int k = unit_image(desc, n, u);
   const PDesc& d = desc[k];
   const int local = u - d.unit_base;
   const uint32_t* w = reinterpret_cast<const uint32_t*>(payload + d.in_off);
+  uint8_t* tab = tabs[threadIdx.x];
   int64_t start = -1;
   int stored = 0;
   if (local == 0) {
     start = 16;  // after the zlib header
   } else {
-    const int64_t lo = static_cast<int64_t>(local) * kUnitBits;
-    const int64_t hi = min(lo + kUnitBits, d.in_bits);
-    for (int64_t p0 = lo; p0 < hi; p0 += 32) {
-      const int64_t p = p0 + lane;
-      const int kind = p < hi ? header_candidate(w, p, d.in_bits) : 0;
-      const unsigned m = __ballot_sync(0xffffffffu, kind != 0);
-      if (m) {
-        const int l = __ffs(m) - 1;
-        start = p0 + l;
-        stored = (__ballot_sync(0xffffffffu, kind == 2) >> l) & 1;
-        if (stored) start = (start + 3 + 7) & ~int64_t(7);
+    const int64_t lo = static_cast<int64_t>(local) * kUnitBits;  // multiple of 1024
+    const int64_t hi = min(lo + kUnitBits, d.in_bits - 3);
+    int qn = 0;  // queued candidates (warp-uniform)
+    // run the queued full checks, one per lane; the first success is the start
+    auto flush = [&]() -> bool {
+      __syncwarp();
+      const bool ok = lane < qn && dynamic_full(w, q[lane], d.in_bits, tab);
+      const unsigned m = __ballot_sync(0xffffffffu, ok);
+      qn = 0;
+      __syncwarp();
+      if (!m) return false;
+      start = q[__ffs(m) - 1];
+      return true;
+    };
+    for (int64_t p0 = lo; p0 < hi; p0 += 1024) {
+      const int64_t wi = (p0 >> 5) + lane;
+      const int64_t pw = wi << 5;  // this lane's first position
+      int64_t found = -1;
+      int64_t mine[2];
+      int nmine = 0;
+      if (pw < hi) {
+        const uint32_t w0 = __ldg(w + wi), w1 = __ldg(w + wi + 1), w2 = __ldg(w + wi + 2),
+                       w3 = __ldg(w + wi + 3);
+        auto bits = [&](uint32_t kk) { return win32(w0, w1, w2, w3, kk); };
+        const uint32_t lim = hi - pw >= 32 ? 0xFFFFFFFFu : ((1u << (hi - pw)) - 1u);
+        uint32_t cand = ~bits(1) & bits(2) & ~(bits(4) & bits(5) & bits(6) & bits(7)) &
+                        ~(bits(9) & bits(10) & bits(11) & bits(12)) & lim;
+        while (cand) {
+          const uint32_t b = __ffs(cand) - 1;
+          cand &= cand - 1;
+          const int hclen = static_cast<int>((bits(b + 13) & 15)) + 4;
+          const uint64_t y = (static_cast<uint64_t>(bits(b + 49)) << 32) | bits(b + 17);
+          const uint64_t ym = y & ((1ull << (3 * hclen)) - 1);
+          int sum = 0;
+#pragma unroll
+          for (int g = 0; g < 7; ++g) sum += kraft9[(ym >> (9 * g)) & 511];
+          if (sum == 128 && nmine < 2) mine[nmine++] = pw + b;
+        }
+        // stored: LEN / NLEN at the byte boundaries q in (pw + 3, pw + 42]
+        const uint32_t none = ~bits(1) & ~bits(2) & lim;  // BTYPE = 00 positions
+        for (uint32_t qb = 8; qb <= 40 && found < 0; qb += 8) {
+          const uint32_t v = bits(qb);
+          if (((v & 0xFFFF) ^ (v >> 16)) != 0xFFFF) continue;
+          // a header position p in [q - 10, q - 3] of this word, zero-padded to q
+          for (int pb = static_cast<int>(qb) - 10; pb <= static_cast<int>(qb) - 3; ++pb) {
+            if (pb < 0 || pb > 31 || !((none >> pb) & 1)) continue;
+            const int pad = static_cast<int>(qb) - (pb + 3);
+            if (pad && (bits(pb + 3) & ((1u << pad) - 1)) != 0) continue;
+            if (header_candidate(w, pw + pb, d.in_bits, tab) == 2) {
+              found = pw + qb;  // canonical start: the LEN byte
+              break;
+            }
+          }
+        }
+      }
+      const unsigned ms = __ballot_sync(0xffffffffu, found >= 0);
+      if (ms) {
+        start = __shfl_sync(0xffffffffu, found, __ffs(ms) - 1);
+        stored = 1;
         break;
       }
+      // queue this step's candidates (at most two per lane; more only cost parallelism)
+      for (int c = 0; c < 2; ++c) {
+        const bool has = c < nmine;
+        const unsigned mh = __ballot_sync(0xffffffffu, has);
+        if (!mh) break;
+        const int slot = qn + __popc(mh & ((1u << lane) - 1u));
+        if (has && slot < kFindQueue) q[slot] = mine[c];
+        qn = min(kFindQueue, qn + __popc(mh));
+        if (qn == kFindQueue && flush()) break;
+      }
+      if (start >= 0) break;
     }
+    if (start < 0 && qn > 0) flush();
   }
   if (lane == 0) {
     PUnit& o = units[u];
@@ -466,22 +636,118 @@ __global__ void k_png_find(const uint8_t* __restrict__ payload, const PDesc* __r
 }
 
 // ---------------------------------------------------------------------------
-// inflate: one thread per unit
+// inflate: one warp per unit.  Block headers (and stored blocks) are read by lane 0,
+// which builds the block's Huffman tables in the warp's shared memory.  A block's data
+// is decoded in rounds of 32 subsequences of kSubBits bits, one per lane: lane 0 starts
+// at the round's true position, lane j at a speculative position kLeadBits before its
+// nominal start, and takes the first symbol boundary at or past the nominal start as its
+// entry (Huffman codes self-synchronise, so after the lead-in it is almost always on the
+// true symbol grid).  Lanes whose entry differs from their predecessor's exit are decoded
+// again from that exit, lowest first, until the subsequences tile the round; then every
+// lane decodes its subsequence once more, writing its tokens at its prefix-sum offset.
 
-__global__ void __launch_bounds__(kInflateThreads)
+constexpr int kSubBits = 512;
+constexpr int kLeadBits = 384;
+constexpr int kInflateWarps = 4;
+
+struct SegResult {
+  int64_t exit;  // first symbol boundary >= end, or the bit after the end-of-block code
+  int ntok;
+  int nout;
+  int stop;      // 0: reached `end`; 1: end of block; 2: invalid code / overrun
+};
+
+// Decode from `from` (taken as a symbol boundary) until the position reaches `end`, an
+// end-of-block code or an invalid code.  out != nullptr: write the tokens (literal packs
+// are flushed at the segment's end, so counts depend only on the segment).
+__device__ SegResult decode_seg(const uint32_t* w, int64_t from, int64_t end, int64_t in_bits,
+                                const uint16_t* lt, const uint8_t* dt, uint32_t* out) {
+  SegResult r;
+  r.ntok = 0;
+  r.nout = 0;
+  r.stop = 0;
+  Bits br;
+  br.init(w, from);
+  uint32_t pack = 0;
+  int pc = 0;
+  const int64_t qlim = (in_bits >> 7) + 3;
+  while (true) {
+    if (br.pos() >= end) break;
+    if (br.qi > qlim) { r.stop = 2; break; }
+    br.refill();
+    uint32_t e = lt[br.peek(kLitRoot)];
+    if (e & 0x8000u) {
+      const int sub = (e >> 12) & 7;
+      if (sub == 7) { r.stop = 2; break; }
+      e = lt[(e & 0xFFFu) + (br.peek(kLitRoot + sub) >> kLitRoot)];
+      if (e & 0x8000u) { r.stop = 2; break; }
+    }
+    br.drop((e >> 11) & 15);
+    const int sym = static_cast<int>(e & 511u);
+    if (sym < 256) {
+      pack |= static_cast<uint32_t>(sym) << (8 * pc);
+      ++r.nout;
+      if (++pc == 3) {
+        if (out) out[r.ntok] = (3u << 24) | pack;
+        ++r.ntok;
+        pc = 0;
+        pack = 0;
+      }
+      continue;
+    }
+    if (sym == 256) { r.stop = 1; break; }
+    if (sym > 285) { r.stop = 2; break; }
+    int base, extra;
+    length_base(sym - 257, base, extra);
+    const int len = base + static_cast<int>(br.peek(extra));
+    br.drop(extra);
+    br.refill();
+    const int ds = decode_dist(br, dt);
+    if (ds < 0 || ds > 29) { r.stop = 2; break; }
+    int dbase, dextra;
+    dist_base(ds, dbase, dextra);
+    const int dist = dbase + static_cast<int>(br.peek(dextra));
+    br.drop(dextra);
+    if (pc) {
+      if (out) out[r.ntok] = (static_cast<uint32_t>(pc) << 24) | pack;
+      ++r.ntok;
+      pc = 0;
+      pack = 0;
+    }
+    if (out) out[r.ntok] = kTokMatch | (static_cast<uint32_t>(len - 3) << 16) | static_cast<uint32_t>(dist - 1);
+    ++r.ntok;
+    r.nout += len;
+  }
+  if (pc && r.stop != 2) {
+    if (out) out[r.ntok] = (static_cast<uint32_t>(pc) << 24) | pack;
+    ++r.ntok;
+  }
+  r.exit = br.pos();
+  return r;
+}
+
+struct __align__(16) WarpTables {
+  uint16_t lit[kLitCap];
+  uint8_t dist[kDistBytes];
+  uint8_t lens[320];   // code lengths of the block being set up
+  uint8_t pre[128];    // code-length code
+};
+
+__global__ void __launch_bounds__(32 * kInflateWarps)
     k_png_inflate(const uint8_t* __restrict__ payload, const PDesc* __restrict__ desc, int n,
                   PUnit* __restrict__ units, int U, uint32_t* __restrict__ toks,
                   const int32_t* __restrict__ img_status) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  __shared__ WarpTables wt_all[kInflateWarps];
+  const int lane = threadIdx.x & 31;
+  const int u = blockIdx.x * kInflateWarps + (threadIdx.x >> 5);
   if (u >= U) return;
+  WarpTables& wt = wt_all[threadIdx.x >> 5];
   PUnit& me = units[u];
   if (!me.dirty) return;
   const int k = unit_image(desc, n, u);
   const PDesc& d = desc[k];
   if (img_status[k] != kImgOk) return;
   const int64_t start = me.start;
-  // stop: the next unit's start (the first block boundary at or past it ends this unit)
   int64_t stop = -1;
   const int ulast = d.unit_base + d.n_units;
   for (int j = u + 1; j < ulast; ++j) {
@@ -493,170 +759,185 @@ __global__ void __launch_bounds__(kInflateThreads)
   }
   const bool last = stop < 0;
   const int64_t in_bits = d.in_bits;
-  uint16_t* lt = reinterpret_cast<uint16_t*>(smem + threadIdx.x * kThreadSmem);
-  uint8_t* dt = smem + threadIdx.x * kThreadSmem + kLitCap * 2;
   const uint32_t* w = reinterpret_cast<const uint32_t*>(payload + d.in_off);
   uint32_t* tk = toks + d.tok_off + (start >> 1);
   const int64_t cap = last ? d.in_bits / 2 + 256 - (start >> 1) : (stop >> 1) - (start >> 1);
-  int64_t ntok = 0, out = 0;
+  int64_t ntok = 0, out = 0, cur = start, end = start;
   int status = kUnitOk, fin = 0;
-  uint32_t pack = 0;
-  int pc = 0;
-  auto emit = [&](uint32_t t) -> bool {
-    if (ntok >= cap) return false;
-    tk[ntok++] = t;
-    return true;
-  };
-  Bits br;
-  br.init(w, start);
-  bool stored_start = me.stored != 0;  // the first block's LEN field is at `start`
-  int64_t end = start;
+  bool stored_start = me.stored != 0;
+  const unsigned below = (1u << lane) - 1u;
   while (true) {
-    const int64_t pos = br.pos();
-    uint32_t hdr = 0;
-    int btype = 0;
-    if (stored_start) {
-      end = pos;
-    } else {
-      if (pos + 3 > in_bits) {
+    // ---- block boundary at `cur` (lane 0 reads the header; the state is broadcast)
+    int btype = 0, bfinal = 0, action = 0;  // action: 0 data, 1 stored done, 2 stop, 3 error
+    int64_t h = cur;
+    if (lane == 0) {
+      Bits br;
+      br.init(w, cur);
+      if (stored_start) {
+        btype = 0;
+        end = cur;
+      } else if (cur + 3 > in_bits) {
+        action = 3;
         status = kUnitOverrun;
-        break;
-      }
-      br.refill();
-      hdr = br.peek(3);
-      btype = static_cast<int>(hdr >> 1);
-      // canonical block position: a stored block's is its LEN byte
-      end = btype == 0 ? (pos + 3 + 7) & ~int64_t(7) : pos;
-      if (!last && end >= stop) break;
-      br.drop(3);
-    }
-    if (btype == 0) {  // stored
-      if (!stored_start) br.drop(br.n & 7);  // to the byte boundary (pos % 8 = -n % 8)
-      stored_start = false;
-      const int64_t q = br.pos();
-      br.refill();
-      const uint32_t v32 = static_cast<uint32_t>(br.buf);  // n >= 33 after the refill
-      const uint32_t len = v32 & 0xFFFF, nlen = v32 >> 16;
-      if ((len ^ nlen) != 0xFFFF) {
-        status = kUnitBadStored;
-        break;
-      }
-      const int64_t data_bit = q + 32;
-      const int64_t next = data_bit + 8 * static_cast<int64_t>(len);
-      if (next > in_bits) {
-        status = kUnitOverrun;
-        break;
-      }
-      if (pc) {
-        if (!emit((static_cast<uint32_t>(pc) << 24) | pack)) { status = kUnitTokens; break; }
-        pc = 0;
-        pack = 0;
-      }
-      if (len) {
-        if (!emit(kTokStored | static_cast<uint32_t>(data_bit >> 3))) { status = kUnitTokens; break; }
-        out += len;
-      }
-      br.init(w, next);
-      // only the final block is followed directly by the Adler-32 trailer (the BFINAL bit
-      // of a stored start is not read: a canonical start skips its header)
-      if (next == in_bits - 32) hdr |= 1;
-    } else if (btype == 1 || btype == 2) {
-      if (btype == 1) {  // fixed codes (RFC 1951 §3.2.6)
-        uint8_t lens[320];
-        for (int i = 0; i < 144; ++i) lens[i] = 8;
-        for (int i = 144; i < 256; ++i) lens[i] = 9;
-        for (int i = 256; i < 280; ++i) lens[i] = 7;
-        for (int i = 280; i < 288; ++i) lens[i] = 8;
-        for (int i = 0; i < 32; ++i) lens[288 + i] = 5;
-        if (!build_lit(lens, 288, lt) || !build_dist(lens + 288, 32, dt)) {
-          status = kUnitBadCode;
-          break;
-        }
       } else {
-        uint8_t lens[320];
-        int hlit, hdist;
-        // the precode table lives in the (not yet built) literal table's space
-        if (!read_dynamic_lengths(br, lens, reinterpret_cast<uint8_t*>(lt), hlit, hdist, in_bits) ||
-            !build_lit(lens, hlit, lt) || !build_dist(lens + hlit, hdist, dt)) {
-          status = kUnitBadCode;
-          break;
-        }
+        const uint32_t hdr = br.peek(3);
+        btype = static_cast<int>(hdr >> 1);
+        bfinal = static_cast<int>(hdr & 1);
+        end = btype == 0 ? (cur + 3 + 7) & ~int64_t(7) : cur;
+        if (!last && end >= stop) action = 2;
+        else br.drop(3);
       }
-      bool ok = true;
-      while (true) {
-        if (br.pos() > in_bits) { ok = false; status = kUnitOverrun; break; }
+      if (action == 0 && btype == 0) {  // stored
+        if (!stored_start) br.drop(br.n & 7);
+        const int64_t q = br.pos();
         br.refill();
-        uint32_t e = lt[br.peek(kLitRoot)];
-        if (e & 0x8000u) {
-          const int sub = (e >> 12) & 7;
-          if (sub == 7) { ok = false; break; }
-          e = lt[(e & 0xFFFu) + (br.peek(kLitRoot + sub) >> kLitRoot)];
-          if (e & 0x8000u) { ok = false; break; }
-        }
-        br.drop((e >> 11) & 15);
-        const int s = static_cast<int>(e & 511u);
-        if (s < 256) {
-          pack |= static_cast<uint32_t>(s) << (8 * pc);
-          if (++pc == 3) {
-            if (ntok >= cap) { ok = false; status = kUnitTokens; break; }
-            tk[ntok++] = (3u << 24) | pack;
-            pc = 0;
-            pack = 0;
+        const uint32_t v32 = static_cast<uint32_t>(br.buf);
+        const uint32_t len = v32 & 0xFFFF, nlen = v32 >> 16;
+        const int64_t next = q + 32 + 8 * static_cast<int64_t>(len);
+        if ((len ^ nlen) != 0xFFFF) {
+          action = 3;
+          status = kUnitBadStored;
+        } else if (next > in_bits) {
+          action = 3;
+          status = kUnitOverrun;
+        } else {
+          if (len) {
+            if (ntok >= cap) {
+              action = 3;
+              status = kUnitTokens;
+            } else {
+              tk[ntok++] = kTokStored | static_cast<uint32_t>((q + 32) >> 3);
+              out += len;
+            }
           }
-          ++out;
-          continue;
+          if (action == 0) {
+            action = 1;
+            h = next;
+            if (next == in_bits - 32) bfinal = 1;  // only the final block meets the trailer
+          }
         }
-        if (s == 256) break;
-        if (s > 285) { ok = false; break; }
-        int base, extra;
-        length_base(s - 257, base, extra);
-        const int len = base + static_cast<int>(br.peek(extra));
-        br.drop(extra);
-        br.refill();
-        const int ds = decode_dist(br, dt);
-        if (ds < 0 || ds > 29) { ok = false; break; }
-        int dbase, dextra;
-        dist_base(ds, dbase, dextra);
-        const int dist = dbase + static_cast<int>(br.peek(dextra));
-        br.drop(dextra);
-        if (pc) {
-          if (ntok >= cap) { ok = false; status = kUnitTokens; break; }
-          tk[ntok++] = (static_cast<uint32_t>(pc) << 24) | pack;
-          pc = 0;
-          pack = 0;
+      } else if (action == 0 && (btype == 1 || btype == 2)) {
+        bool ok;
+        if (btype == 1) {
+          for (int i = 0; i < 144; ++i) wt.lens[i] = 8;
+          for (int i = 144; i < 256; ++i) wt.lens[i] = 9;
+          for (int i = 256; i < 280; ++i) wt.lens[i] = 7;
+          for (int i = 280; i < 288; ++i) wt.lens[i] = 8;
+          for (int i = 0; i < 32; ++i) wt.lens[288 + i] = 5;
+          ok = build_lit(wt.lens, 288, wt.lit) && build_dist(wt.lens + 288, 32, wt.dist);
+        } else {
+          int hlit, hdist;
+          ok = read_dynamic_lengths(br, wt.lens, wt.pre, hlit, hdist, in_bits) &&
+               build_lit(wt.lens, hlit, wt.lit) && build_dist(wt.lens + hlit, hdist, wt.dist);
         }
-        if (ntok >= cap) { ok = false; status = kUnitTokens; break; }
-        tk[ntok++] = kTokMatch | (static_cast<uint32_t>(len - 3) << 16) | static_cast<uint32_t>(dist - 1);
-        out += len;
+        if (!ok) {
+          action = 3;
+          status = kUnitBadCode;
+        }
+        h = br.pos();
+      } else if (action == 0) {
+        action = 3;
+        status = kUnitBadCode;
       }
-      if (!ok) {
-        if (status == kUnitOk) status = kUnitBadCode;
-        break;
-      }
-      if (br.pos() > in_bits) {
-        status = kUnitOverrun;
-        break;
-      }
-    } else {
-      status = kUnitBadCode;
-      break;
     }
-    if (hdr & 1) {
+    stored_start = false;
+    action = __shfl_sync(0xffffffffu, action, 0);
+    status = __shfl_sync(0xffffffffu, status, 0);
+    bfinal = __shfl_sync(0xffffffffu, bfinal, 0);
+    h = __shfl_sync(0xffffffffu, h, 0);
+    end = __shfl_sync(0xffffffffu, end, 0);
+    ntok = __shfl_sync(0xffffffffu, ntok, 0);
+    out = __shfl_sync(0xffffffffu, out, 0);
+    if (action >= 2) break;
+    if (action == 1) {  // stored block done
+      cur = h;
+      if (bfinal) {
+        fin = 1;
+        break;
+      }
+      continue;
+    }
+    __syncwarp();  // tables visible to every lane
+    // ---- the block's data, in rounds of 32 subsequences
+    bool eob = false;
+    while (true) {
+      const int64_t nom = h + static_cast<int64_t>(lane) * kSubBits, nom_end = nom + kSubBits;
+      int64_t entry;
+      SegResult r;
+      if (lane == 0) {
+        entry = h;
+        r = decode_seg(w, h, nom_end, in_bits, wt.lit, wt.dist, nullptr);
+      } else {
+        const SegResult lead = decode_seg(w, max(h, nom - kLeadBits), nom, in_bits, wt.lit,
+                                          wt.dist, nullptr);
+        if (lead.stop == 0) {
+          entry = lead.exit;
+          r = decode_seg(w, entry, nom_end, in_bits, wt.lit, wt.dist, nullptr);
+        } else {  // the speculative path stopped in the lead-in
+          entry = -1;
+          r = lead;
+          r.stop = 2;
+        }
+      }
+      // fix-up: the lowest lane whose entry is not its predecessor's exit decodes again
+      while (true) {
+        const int64_t pexit = __shfl_up_sync(0xffffffffu, r.exit, 1);
+        const unsigned stops = __ballot_sync(0xffffffffu, r.stop != 0);
+        const bool bad = lane > 0 && !(stops & below) && entry != pexit;
+        const unsigned mb = __ballot_sync(0xffffffffu, bad);
+        if (!mb) break;
+        if (lane == __ffs(mb) - 1) {
+          entry = pexit;
+          r = decode_seg(w, entry, nom_end, in_bits, wt.lit, wt.dist, nullptr);
+        }
+      }
+      const unsigned stops = __ballot_sync(0xffffffffu, r.stop != 0);
+      const int J = stops ? __ffs(stops) - 1 : 31;  // last lane of the round
+      const bool in_round = lane <= J;
+      const int jstop = __shfl_sync(0xffffffffu, r.stop, J);
+      if (jstop == 2) {
+        status = kUnitBadCode;
+        break;
+      }
+      // token offsets of the round's lanes
+      int incl = in_round ? r.ntok : 0;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      const int rtok = __shfl_sync(0xffffffffu, incl, 31);
+      int rout = in_round ? r.nout : 0;
+      for (int o = 16; o > 0; o >>= 1) rout += __shfl_xor_sync(0xffffffffu, rout, o);
+      if (ntok + rtok > cap) {
+        status = kUnitTokens;
+        end = h;
+        break;
+      }
+      if (in_round) decode_seg(w, entry, nom_end, in_bits, wt.lit, wt.dist, tk + ntok + incl - r.ntok);
+      ntok += rtok;
+      out += rout;
+      h = __shfl_sync(0xffffffffu, r.exit, J);
+      if (jstop == 1) {
+        eob = true;
+        break;
+      }
+    }
+    if (status != kUnitOk) break;
+    cur = h;
+    if (eob && bfinal) {
       fin = 1;
       break;
     }
+    __syncwarp();  // the next header rebuilds the tables
   }
-  if (status == kUnitOk && pc) {
-    if (ntok < cap) tk[ntok++] = (static_cast<uint32_t>(pc) << 24) | pack;
-    else status = kUnitTokens;
+  if (lane == 0) {
+    me.end = (last || status == kUnitTokens || fin) ? (status == kUnitTokens ? end : cur) : end;
+    me.ntok = static_cast<int32_t>(ntok);
+    me.out_len = out;
+    me.status = status;
+    me.final_ = fin;
+    me.dirty = 0;
   }
-  // a token overflow is judged by how far the decode got (past the next start or not)
-  me.end = (last || status == kUnitTokens) ? br.pos() : end;
-  me.ntok = static_cast<int32_t>(ntok);
-  me.out_len = out;
-  me.status = status;
-  me.final_ = fin;
-  me.dirty = 0;
 }
 
 // ---------------------------------------------------------------------------
@@ -723,12 +1004,14 @@ __global__ void k_png_chain(const PDesc* __restrict__ desc, int n, PUnit* __rest
 }
 
 // ---------------------------------------------------------------------------
-// expand: one warp per unit, tokens -> u16 bytes (>= 256: window markers)
+// expand: one warp per unit, tokens -> u16 bytes (>= 256: window markers).  The
+// positions of marker bytes go to the unit's list (a warp-aggregated append: the warp
+// walks its unit's tokens in order, so a register counter is the list's length).
 
 __global__ void k_png_expand(const uint8_t* __restrict__ payload, const PDesc* __restrict__ desc,
-                             int n, const PUnit* __restrict__ units, int U,
+                             int n, PUnit* __restrict__ units, int U,
                              const uint32_t* __restrict__ toks, uint16_t* __restrict__ T,
-                             int32_t* __restrict__ img_status) {
+                             uint32_t* __restrict__ M, int32_t* __restrict__ img_status) {
   const int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (u >= U) return;
@@ -742,6 +1025,9 @@ __global__ void k_png_expand(const uint8_t* __restrict__ payload, const PDesc* _
   uint16_t* img = T + d.raw_off;
   const int64_t ws = cu.out_off;          // unit start (image-relative)
   const int64_t wbase = ws - kWindow;     // marker 256 + i refers to image byte wbase + i
+  uint32_t* list = M + d.raw_off + ws;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  int nmark = 0;
   int64_t cur = ws;
   bool bad = false;
   for (int b = 0; b < cu.ntok; b += 32) {
@@ -782,69 +1068,100 @@ __global__ void k_png_expand(const uint8_t* __restrict__ payload, const PDesc* _
         for (int j = lane; j < ln; j += 32) img[dst + j] = src[j];
       } else {
         const int dist = static_cast<int>(tt & 0xFFFFu) + 1;
-        for (int j = lane; j < ln; j += 32) {
-          const int64_t s = dst - dist + (dist >= ln ? j : j % dist);
-          uint16_t v;
-          if (s >= ws) {
-            v = img[s];
-          } else if (s >= 0 && s >= wbase) {
-            v = static_cast<uint16_t>(256 + (s - wbase));
-          } else {
-            v = 0;
-            bad = true;
+        for (int j0 = 0; j0 < ln; j0 += 32) {
+          const int j = j0 + lane;
+          bool mk = false;
+          if (j < ln) {
+            const int64_t s = dst - dist + (dist >= ln ? j : j % dist);
+            uint16_t v;
+            if (s >= ws) {
+              v = img[s];
+            } else if (s >= 0 && s >= wbase) {
+              v = static_cast<uint16_t>(256 + (s - wbase));
+            } else {
+              v = 0;
+              bad = true;
+            }
+            img[dst + j] = v;
+            mk = v >= 256;
           }
-          img[dst + j] = v;
+          const unsigned mm = __ballot_sync(0xffffffffu, mk);
+          if (mk) list[nmark + __popc(mm & lt_mask)] = static_cast<uint32_t>(dst + j);
+          nmark += __popc(mm);
         }
       }
       __syncwarp();
     }
     cur += total;
   }
+  if (lane == 0) units[u].nmark = nmark;
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(img_status + k, kImgDistance);
 }
 
 // ---------------------------------------------------------------------------
-// window: one CTA per image, units in order; each unit's last 32 KB resolved
+// final: every byte of T into the row layout of R (markers too, as garbage: `window`
+// rewrites them); one CTA per row of the batch, eight bytes per thread
 
+__device__ __forceinline__ int row_image(const PDesc* __restrict__ desc, int n, int g) {
+  int lo = 0, hi = n;  // largest k with row_base <= g
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (desc[mid].row_base <= g) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// R byte of inflated byte p (image-relative) of image d
+__device__ __forceinline__ uint8_t* r_byte(const PDesc& d, uint8_t* r, uint32_t p) {
+  const uint32_t stride = static_cast<uint32_t>(d.width) * d.bpp + 1;
+  const uint32_t y = p / stride, x = p - y * stride;
+  return x == 0 ? r + y : r + r_filter_bytes(d.height) + static_cast<int64_t>(y) * d.r_stride + (x - 1);
+}
+
+__global__ void k_png_final(const PDesc* __restrict__ desc, int n, const uint16_t* __restrict__ T,
+                            uint8_t* __restrict__ R, const int32_t* __restrict__ img_status) {
+  const int g = blockIdx.x;
+  const int k = row_image(desc, n, g);
+  const PDesc& d = desc[k];
+  if (d.n_units == 0 || img_status[k] != kImgOk) return;
+  const int y = g - d.row_base;
+  const int64_t rowbytes = static_cast<int64_t>(d.width) * d.bpp;
+  const uint16_t* t = T + d.raw_off + static_cast<int64_t>(y) * (rowbytes + 1);
+  uint8_t* r = R + d.r_off;
+  if (threadIdx.x == 0) r[y] = static_cast<uint8_t>(t[0]);
+  uint8_t* row = r + r_filter_bytes(d.height) + static_cast<int64_t>(y) * d.r_stride;
+  for (int64_t x = 8 * static_cast<int64_t>(threadIdx.x); x < rowbytes; x += 8 * blockDim.x) {
+    uint32_t b[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) b[j] = x + j < rowbytes ? (t[1 + x + j] & 255u) : 0u;
+    uint2 v;
+    v.x = b[0] | (b[1] << 8) | (b[2] << 16) | (b[3] << 24);
+    v.y = b[4] | (b[5] << 8) | (b[6] << 16) | (b[7] << 24);
+    *reinterpret_cast<uint2*>(row + x) = v;  // r_stride is a multiple of 16
+  }
+}
+
+// window: one CTA per image, units in order: each unit's marker bytes read the window
+// before the unit, whose bytes are final by then (earlier units' markers resolved)
 __global__ void k_png_window(const PDesc* __restrict__ desc, int n, const PUnit* __restrict__ units,
-                             const uint16_t* __restrict__ T, uint8_t* __restrict__ R,
-                             const int32_t* __restrict__ img_status) {
+                             const uint16_t* __restrict__ T, const uint32_t* __restrict__ M,
+                             uint8_t* __restrict__ R, const int32_t* __restrict__ img_status) {
   const int k = blockIdx.x;
   const PDesc& d = desc[k];
   if (d.n_units == 0 || img_status[k] != kImgOk) return;
   const uint16_t* t = T + d.raw_off;
-  uint8_t* r = R + d.raw_off;
+  uint8_t* r = R + d.r_off;
   for (int u = d.unit_base; u < d.unit_base + d.n_units; ++u) {
-    const PUnit cu = units[u];
-    if (cu.start < 0 || cu.out_len == 0) continue;
-    const int64_t os = cu.out_off, oe = os + cu.out_len;
-    const int64_t lo = max(os, oe - kWindow);
-    const int64_t wb = os - kWindow;
-    for (int64_t p = lo + threadIdx.x; p < oe; p += blockDim.x) {
-      const uint32_t v = t[p];
-      r[p] = v < 256 ? static_cast<uint8_t>(v) : r[wb + (v - 256)];
+    const int cnt = units[u].start < 0 ? 0 : units[u].nmark;
+    if (!cnt) continue;  // uniform across the CTA
+    const int64_t os = units[u].out_off, wb = os - kWindow;
+    const uint32_t* list = M + d.raw_off + os;
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+      const uint32_t p = list[i];
+      const uint32_t src = static_cast<uint32_t>(wb + (t[p] - 256));
+      *r_byte(d, r, p) = *r_byte(d, r, src);
     }
     __syncthreads();
-  }
-}
-
-// final: one CTA per unit, the bytes before the unit's last 32 KB
-__global__ void k_png_final(const PDesc* __restrict__ desc, int n, const PUnit* __restrict__ units,
-                            int U, const uint16_t* __restrict__ T, uint8_t* __restrict__ R,
-                            const int32_t* __restrict__ img_status) {
-  const int u = blockIdx.x;
-  if (u >= U) return;
-  const int k = unit_image(desc, n, u);
-  const PDesc& d = desc[k];
-  if (img_status[k] != kImgOk) return;
-  const PUnit cu = units[u];
-  if (cu.start < 0 || cu.out_len <= kWindow) return;
-  const uint16_t* t = T + d.raw_off;
-  uint8_t* r = R + d.raw_off;
-  const int64_t os = cu.out_off, hi = os + cu.out_len - kWindow, wb = os - kWindow;
-  for (int64_t p = os + threadIdx.x; p < hi; p += blockDim.x) {
-    const uint32_t v = t[p];
-    r[p] = v < 256 ? static_cast<uint8_t>(v) : r[wb + (v - 256)];
   }
 }
 
@@ -870,25 +1187,34 @@ __global__ void __launch_bounds__(kAdlerThreads)
   const int64_t at = (fin + 7) >> 3;  // trailer bytes, big-endian
   if (at + 4 > (d.in_bits >> 3)) return;
   const int64_t len = d.raw_len;
-  const int64_t seg = (len + blockDim.x - 1) / blockDim.x;
-  const int64_t s0 = min(len, seg * static_cast<int64_t>(threadIdx.x)), s1e = min(len, s0 + seg);
-  const uint8_t* r = R + d.raw_off;
-  uint64_t a = 0, b = 0;  // a: sum d_i; b: sum (s1e - i) d_i, reduced every 4096 bytes
-  int64_t i = s0;
-  while (i < s1e) {
-    const int64_t e = min(s1e, i + 4096);
-    uint64_t la = 0, lb = 0;
-    for (int64_t j = i; j < e; ++j) {
-      const uint32_t v = r[j];
-      la += v;
-      lb += static_cast<uint64_t>(s1e - j) * v;
+  const int64_t rowbytes = static_cast<int64_t>(d.width) * d.bpp, stride = rowbytes + 1;
+  const int H = d.height;
+  // thread t: rows [y0, y1), the raw range [y0 * stride, y1 * stride)
+  const int per = (H + blockDim.x - 1) / blockDim.x;
+  const int y0 = min(H, per * static_cast<int>(threadIdx.x)), y1 = min(H, y0 + per);
+  const int64_t E = static_cast<int64_t>(y1) * stride;
+  const uint8_t* fb = R + d.r_off;
+  const uint8_t* rows = fb + r_filter_bytes(H);
+  uint64_t a = 0, b = 0;  // a: sum d_i; b: sum (E - i) d_i (mod, per row)
+  for (int y = y0; y < y1; ++y) {
+    const int64_t i0 = static_cast<int64_t>(y) * stride;
+    uint64_t la = fb[y], lb = static_cast<uint64_t>(E - i0) * fb[y];
+    const uint8_t* row = rows + static_cast<int64_t>(y) * d.r_stride;
+    for (int64_t x = 0; x < rowbytes; x += 16) {
+      const uint4 v = *reinterpret_cast<const uint4*>(row + x);
+      const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+      const uint64_t wt0 = static_cast<uint64_t>(E - (i0 + 1 + x));  // weight of byte x
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const uint32_t dj = x + j < rowbytes ? (wv[j >> 2] >> (8 * (j & 3))) & 255u : 0u;
+        la += dj;
+        lb += (wt0 - j) * dj;
+      }
     }
     a = (a + la) % kAdlerMod;
-    b = (b + lb) % kAdlerMod;
-    i = e;
+    b = (b + lb % kAdlerMod) % kAdlerMod;
   }
-  // this segment's weight in the whole: (n - i) = (s1e - i) + (n - s1e)
-  b = (b + (static_cast<uint64_t>(len - s1e) % kAdlerMod) * a) % kAdlerMod;
+  b = (b + (static_cast<uint64_t>(len - E) % kAdlerMod) * a) % kAdlerMod;
   for (int o = 16; o > 0; o >>= 1) {
     a += __shfl_down_sync(0xffffffffu, a, o);
     b += __shfl_down_sync(0xffffffffu, b, o);
@@ -916,107 +1242,145 @@ __global__ void __launch_bounds__(kAdlerThreads)
 // ---------------------------------------------------------------------------
 // unfilter (PNG §9.2) + L/P -> RGB: one CTA per image, thread = scanline
 
-__device__ __forceinline__ uint32_t paeth(uint32_t a, uint32_t b, uint32_t c) {
-  const int p = static_cast<int>(a) + static_cast<int>(b) - static_cast<int>(c);
-  const int pa = abs(p - static_cast<int>(a)), pb = abs(p - static_cast<int>(b)),
-            pc = abs(p - static_cast<int>(c));
-  return (pa <= pb && pa <= pc) ? a : (pb <= pc ? b : c);
-}
 
 constexpr int kUnfilterThreads = 1024;
 
-__global__ void __launch_bounds__(kUnfilterThreads)
-    k_png_unfilter(const PDesc* __restrict__ desc, int n, uint8_t* __restrict__ R,
-                   uint8_t* __restrict__ out, int32_t* __restrict__ img_status) {
-  __shared__ uint32_t xch[2][kUnfilterThreads];
-  __shared__ uint8_t pal[768];
-  const int k = blockIdx.x;
-  const PDesc& d = desc[k];
-  if (d.n_units == 0 || img_status[k] != kImgOk) return;
+__device__ __forceinline__ uint32_t byte_at(const uint4& v, int j) {  // j: compile-time
+  const uint32_t w = j < 4 ? v.x : j < 8 ? v.y : j < 12 ? v.z : v.w;
+  return (w >> (8 * (j & 3))) & 255u;
+}
+
+__device__ __forceinline__ uint32_t pack4(const uint32_t* b) {
+  return b[0] | (b[1] << 8) | (b[2] << 16) | (b[3] << 24);
+}
+
+// One image per CTA, thread = scanline: at step t thread y reconstructs 16-byte chunk
+// t - y of its row, whose prior-row bytes thread y - 1 reconstructed at step t - 1
+// (shared-memory exchange, double-buffered).  Groups of blockDim rows run in turn; a
+// group's last row is written back in place for the next group's first row.  Rows sit
+// at a 16-byte aligned stride in R, so every chunk is one vector load.
+template <int BPP>
+__device__ void unfilter_image(const PDesc& d, uint8_t* __restrict__ r, uint8_t* __restrict__ o,
+                               const uint8_t* pal, uint4 (*xch)[kUnfilterThreads], bool& bad_filter,
+                               bool& bad_pal) {
   const int tid = threadIdx.x;
-  const int W = d.width, H = d.height, bpp = d.bpp;
+  const int W = d.width, H = d.height;
   const bool is_p = d.ctype == 3;
-  for (int i = tid; i < 768; i += blockDim.x) pal[i] = d.pal[i];
-  const int64_t rowbytes = static_cast<int64_t>(W) * bpp, stride = rowbytes + 1;
-  const int nch = static_cast<int>((rowbytes + 3) >> 2);
-  uint8_t* raw = R + d.raw_off;
-  uint8_t* o = out + d.out_off;
+  const int64_t rowbytes = static_cast<int64_t>(W) * BPP, S = d.r_stride;
+  const int nch = static_cast<int>((rowbytes + 15) >> 4);
+  const uint8_t* fbytes = r;
+  uint8_t* rows_base = r + r_filter_bytes(H);
   const int G = blockDim.x;
-  bool bad_filter = false, bad_pal = false;
-  __syncthreads();
   for (int g0 = 0; g0 < H; g0 += G) {
     const int rows = min(G, H - g0);
     const int y = g0 + tid;
     const bool has_row = tid < rows;
-    uint8_t* row = raw + static_cast<int64_t>(y) * stride;
-    const uint32_t ft = has_row ? row[0] : 0u;
+    uint8_t* row = rows_base + static_cast<int64_t>(y) * S;
+    const uint32_t ft = has_row ? fbytes[y] : 0u;
     if (ft > 4) bad_filter = true;
-    const uint8_t* prior = y > 0 ? row - stride : nullptr;  // recon (written in place below)
-    uint32_t up_prev = 0, cur_prev = 0;
+    const uint8_t* prior = y > 0 ? row - S : nullptr;  // recon of the previous group
+    uint4 up_prev = make_uint4(0, 0, 0, 0), rec_prev = make_uint4(0, 0, 0, 0);
+    uint4 fnext = make_uint4(0, 0, 0, 0);
+    if (has_row) fnext = __ldcg(reinterpret_cast<const uint4*>(row));
+    // output rows: 16-byte stores when this row's output start is 16-byte aligned
+    uint8_t* orow = o + static_cast<int64_t>(y) * W * 3;
+    const bool oal = (reinterpret_cast<uintptr_t>(orow) & 15) == 0;
     const int steps = nch + rows - 1;
     for (int t = 0; t < steps; ++t) {
       const int i = t - tid;
       if (has_row && i >= 0 && i < nch) {
-        uint32_t up = 0;
+        const uint4 f = fnext;
+        if (i + 1 < nch) fnext = __ldcg(reinterpret_cast<const uint4*>(row) + i + 1);
+        uint4 up = make_uint4(0, 0, 0, 0);
         if (tid == 0) {
-          if (prior)
-            for (int j = 0; j < 4; ++j) {
-              const int64_t x = 4 * static_cast<int64_t>(i) + j;
-              if (x < rowbytes) up |= static_cast<uint32_t>(prior[1 + x]) << (8 * j);
-            }
+          if (prior) up = __ldcg(reinterpret_cast<const uint4*>(prior) + i);
         } else {
           up = xch[(t - 1) & 1][tid - 1];
         }
-        uint32_t rec = 0;
+        const int64_t x0 = 16 * static_cast<int64_t>(i);
+        uint32_t rb[16];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int64_t x = 4 * static_cast<int64_t>(i) + j;
-          if (x >= rowbytes) break;
-          const uint32_t f = row[1 + x];
-          // a = recon[x - bpp], b = up[x], c = up[x - bpp] (0 before the row start)
-          uint32_t a = 0, c = 0;
-          if (x >= bpp) {
-            const int s = j - bpp;  // position of x - bpp relative to this chunk
-            a = s >= 0 ? (rec >> (8 * s)) & 255u : (cur_prev >> (8 * (s + 4))) & 255u;
-            c = s >= 0 ? (up >> (8 * s)) & 255u : (up_prev >> (8 * (s + 4))) & 255u;
-          }
-          const uint32_t b = (up >> (8 * j)) & 255u;
-          uint32_t pred;
-          switch (ft) {
-            case 1: pred = a; break;
-            case 2: pred = b; break;
-            case 3: pred = (a + b) >> 1; break;
-            case 4: pred = paeth(a, b, c); break;
-            default: pred = 0;
-          }
-          const uint32_t v = (f + pred) & 255u;
-          rec |= v << (8 * j);
-          if (bpp == 3) {
-            o[static_cast<int64_t>(y) * rowbytes + x] = static_cast<uint8_t>(v);
+        for (int j = 0; j < 16; ++j) {
+          uint32_t a, c;
+          if (j >= BPP) {
+            a = rb[j - BPP];
+            c = byte_at(up, j - BPP);
           } else {
-            uint8_t* px = o + (static_cast<int64_t>(y) * W + x) * 3;
+            a = x0 ? byte_at(rec_prev, 16 + j - BPP) : 0u;
+            c = x0 ? byte_at(up_prev, 16 + j - BPP) : 0u;
+          }
+          const uint32_t b = byte_at(up, j);
+          const int pp = static_cast<int>(a + b) - static_cast<int>(c);
+          const int pa = abs(pp - static_cast<int>(a)), pb = abs(pp - static_cast<int>(b)),
+                    pc = abs(pp - static_cast<int>(c));
+          const uint32_t pae = (pa <= pb && pa <= pc) ? a : (pb <= pc ? b : c);
+          const uint32_t pred = ft == 1 ? a : ft == 2 ? b : ft == 3 ? (a + b) >> 1 : ft == 4 ? pae : 0u;
+          rb[j] = (byte_at(f, j) + pred) & 255u;
+        }
+        const uint4 rec = make_uint4(pack4(rb), pack4(rb + 4), pack4(rb + 8), pack4(rb + 12));
+        const int nb = static_cast<int>(rowbytes - x0 < 16 ? rowbytes - x0 : 16);
+        if (BPP == 3) {
+          uint8_t* dst = orow + x0;
+          if (oal && nb == 16) {
+            __stcs(reinterpret_cast<uint4*>(dst), rec);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (j < nb) dst[j] = static_cast<uint8_t>(rb[j]);
+          }
+        } else {
+          uint32_t px[48];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const uint32_t v = rb[j];
             if (is_p) {
-              if (static_cast<int>(v) >= d.pal_n) bad_pal = true;
-              px[0] = pal[3 * v];
-              px[1] = pal[3 * v + 1];
-              px[2] = pal[3 * v + 2];
+              if (j < nb && static_cast<int>(v) >= d.pal_n) bad_pal = true;
+              px[3 * j] = pal[3 * v];
+              px[3 * j + 1] = pal[3 * v + 1];
+              px[3 * j + 2] = pal[3 * v + 2];
             } else {
-              px[0] = px[1] = px[2] = static_cast<uint8_t>(v);
+              px[3 * j] = px[3 * j + 1] = px[3 * j + 2] = v;
             }
           }
-        }
-        if (tid == rows - 1)  // the next group's first row reads this row's recon
-          for (int j = 0; j < 4; ++j) {
-            const int64_t x = 4 * static_cast<int64_t>(i) + j;
-            if (x < rowbytes) row[1 + x] = static_cast<uint8_t>(rec >> (8 * j));
+          uint8_t* dst = orow + 3 * x0;
+          if (oal && nb == 16) {
+#pragma unroll
+            for (int q = 0; q < 3; ++q)
+              __stcs(reinterpret_cast<uint4*>(dst) + q,
+                     make_uint4(pack4(px + 16 * q), pack4(px + 16 * q + 4), pack4(px + 16 * q + 8),
+                                pack4(px + 16 * q + 12)));
+          } else {
+#pragma unroll
+            for (int j = 0; j < 48; ++j)
+              if (j < 3 * nb) dst[j] = static_cast<uint8_t>(px[j]);
           }
+        }
+        if (tid == rows - 1 && g0 + rows < H)  // the next group's first row reads it
+          __stcg(reinterpret_cast<uint4*>(row) + i, rec);
         xch[t & 1][tid] = rec;
         up_prev = up;
-        cur_prev = rec;
+        rec_prev = rec;
       }
       __syncthreads();
     }
   }
+}
+
+__global__ void __launch_bounds__(kUnfilterThreads)
+    k_png_unfilter(const PDesc* __restrict__ desc, int n, uint8_t* __restrict__ R,
+                   uint8_t* __restrict__ out, int32_t* __restrict__ img_status) {
+  __shared__ uint4 xch[2][kUnfilterThreads];
+  __shared__ uint8_t pal[768];
+  const int k = blockIdx.x;
+  const PDesc& d = desc[k];
+  if (d.n_units == 0 || img_status[k] != kImgOk) return;
+  for (int i = threadIdx.x; i < 768; i += blockDim.x) pal[i] = d.pal[i];
+  __syncthreads();
+  bool bad_filter = false, bad_pal = false;
+  if (d.bpp == 3)
+    unfilter_image<3>(d, R + d.r_off, out + d.out_off, pal, xch, bad_filter, bad_pal);
+  else
+    unfilter_image<1>(d, R + d.r_off, out + d.out_off, pal, xch, bad_filter, bad_pal);
   if (bad_filter) atomicOr(img_status + k, kImgFilter);
   if (bad_pal) atomicOr(img_status + k, kImgPalette);
 }
@@ -1040,24 +1404,20 @@ extern "C" TP_API int tp_png_decode(const uint8_t* d_payload, const void* d_desc
   uint32_t* toks = reinterpret_cast<uint32_t*>(work + totals[4]);
   uint16_t* T = reinterpret_cast<uint16_t*>(work + totals[5]);
   uint8_t* R = work + totals[6];
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_png_inflate, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kInflateThreads * kThreadSmem);
-    attr_set = true;
-  }
   cudaMemsetAsync(d_status, 0, sizeof(int32_t) * n, s);
   if (U > 0) {
-    k_png_find<<<(U + 7) / 8, 256, 0, s>>>(d_payload, desc, n, units, U);
+    k_png_find<<<(U + kFindThreads / 32 - 1) / (kFindThreads / 32), kFindThreads, 0, s>>>(
+        d_payload, desc, n, units, U);
     for (int r = 0; r < kRounds; ++r) {
-      k_png_inflate<<<(U + kInflateThreads - 1) / kInflateThreads, kInflateThreads,
-                      kInflateThreads * kThreadSmem, s>>>(d_payload, desc, n, units, U, toks,
-                                                           d_status);
+      k_png_inflate<<<(U + kInflateWarps - 1) / kInflateWarps, 32 * kInflateWarps, 0, s>>>(
+          d_payload, desc, n, units, U, toks, d_status);
       k_png_chain<<<n, 32, 0, s>>>(desc, n, units, d_status, r == kRounds - 1);
     }
-    k_png_expand<<<(U + 7) / 8, 256, 0, s>>>(d_payload, desc, n, units, U, toks, T, d_status);
-    k_png_window<<<n, 1024, 0, s>>>(desc, n, units, T, R, d_status);
-    k_png_final<<<U, 256, 0, s>>>(desc, n, units, U, T, R, d_status);
+    uint32_t* M = reinterpret_cast<uint32_t*>(work + totals[9]);
+    k_png_expand<<<(U + 7) / 8, 256, 0, s>>>(d_payload, desc, n, units, U, toks, T, M, d_status);
+    if (totals[10] > 0)
+      k_png_final<<<static_cast<int>(totals[10]), 256, 0, s>>>(desc, n, T, R, d_status);
+    k_png_window<<<n, 1024, 0, s>>>(desc, n, units, T, M, R, d_status);
     k_png_adler<<<n, kAdlerThreads, 0, s>>>(d_payload, desc, n, units, R, d_status);
     k_png_unfilter<<<n, kUnfilterThreads, 0, s>>>(desc, n, R, d_out, d_status);
   }

@@ -8,8 +8,12 @@ namespace png {
 
 // Block-finder chunk: unit u of an image starts at the first deflate block header found
 // in bits [u * kUnitBits, (u + 1) * kUnitBits) of its zlib stream (unit 0 at bit 16,
-// right after the two-byte zlib header).  One thread inflates one unit.
-constexpr int64_t kUnitBits = 8 * 12288;
+// right after the two-byte zlib header).  One warp inflates one unit.  The finder scans
+// from the unit's start to the first header, so its work is about half a block per
+// unit: units a few blocks long (zlib's blocks are 16-32K symbols, ~12-24 KB of a
+// photo-like PNG) keep the scan to a fraction of the stream; the warp decodes each block
+// 32 subsequences at a time.
+constexpr int64_t kUnitBits = 8 * 49152;
 constexpr int kWindow = 32768;  // deflate's back-reference window
 
 // Unit states (PUnit::status): 0 ok; the rest send the image to the host decoder.
@@ -56,7 +60,9 @@ struct __align__(16) PDesc {
   int32_t unit_base;  // first unit of this image
   int32_t n_units;
   int32_t pal_n;      // PLTE entries (P)
-  int32_t pad_;
+  int32_t row_base;   // first row of this image in the batch's row numbering
+  int64_t r_off;      // R workspace: filter bytes (align16(height)), then the rows
+  int64_t r_stride;   // R row stride: rowbytes rounded up to 16 (rows 16-byte aligned)
   uint8_t pal[768];   // PLTE (P)
 };
 
@@ -74,10 +80,21 @@ struct __align__(16) PUnit {
   int32_t final_;   // the unit ended with the BFINAL block
   int32_t dirty;    // (re)decode in the next inflate round
   int32_t stored;   // start is the LEN field of a stored block (its header not read)
-  int32_t pad_[3];
+  int32_t nmark;    // bytes of this unit that are window markers (listed by expand)
+  int32_t pad_[2];
   int64_t final_end;  // (an image's first unit) bit after the final block, by the chain
   int64_t pad2_;
 };
+
+// tp_png_describe's totals[16]: [0] units, [1] tokens, [2] raw bytes (T entries),
+// [3..6] byte offsets of units / tokens / T / R, [7] workspace bytes, [8] R bytes,
+// [9] marker lists' byte offset (u32 image-relative positions; unit u's list starts at
+// the index of its first byte, raw_off + out_off), [10] rows in the batch
+constexpr int kTotals = 16;
+
+// R (inflated scanlines) per image: the filter-type bytes, then each row's rowbytes
+// data bytes at a 16-byte aligned stride (vector loads and stores in the unfilter)
+__host__ __device__ inline int64_t r_filter_bytes(int64_t h) { return (h + 15) / 16 * 16; }
 
 // Token (u32), what the inflate kernel writes and the expand kernel turns into bytes:
 //   type 0 (bits 31..30 = 00): 1-3 literals, count in bits 25..24, bytes in 7..0, 15..8, 23..16

@@ -223,7 +223,7 @@ TP_API int64_t tp_png_describe(const TpPngInfo* infos, int32_t n, const int64_t*
     return -tp::set_error(TP_ERR_INVALID_ARGUMENT, "tp_png_describe: invalid argument");
   }
   PDesc* d = static_cast<PDesc*>(desc);
-  int64_t units = 0, toks = 0, raw = 0;
+  int64_t units = 0, toks = 0, raw = 0, rbytes = 0, rows = 0;
   for (int k = 0; k < n; ++k) {
     const TpPngInfo& in = infos[k];
     PDesc& o = d[k];
@@ -235,31 +235,39 @@ TP_API int64_t tp_png_describe(const TpPngInfo* infos, int32_t n, const int64_t*
     o.bpp = in.color_type == 2 ? 3 : 1;
     o.pal_n = in.pal_n;
     std::memcpy(o.pal, in.pal, sizeof(o.pal));
+    o.unit_base = static_cast<int32_t>(units);
+    o.row_base = static_cast<int32_t>(rows);
     if (in.status != TP_PNG_OK || in_off[k] < 0) {
       o.n_units = 0;  // not a device image
-      o.unit_base = static_cast<int32_t>(units);
       continue;
     }
-    if (in_off[k] % 4 != 0) {
-      return -tp::set_error(TP_ERR_INVALID_ARGUMENT, "tp_png_describe: in_off[%d] not 4-byte aligned", k);
-    }
+    if (in_off[k] % 16 != 0)
+      return -tp::set_error(TP_ERR_INVALID_ARGUMENT, "tp_png_describe: in_off[%d] not 16-byte aligned", k);
     o.in_off = in_off[k];
     o.in_bits = in.zlib_len * 8;
-    o.raw_len = static_cast<int64_t>(in.height) * (1 + static_cast<int64_t>(in.width) * o.bpp);
+    const int64_t rowbytes = static_cast<int64_t>(in.width) * o.bpp;
+    o.raw_len = static_cast<int64_t>(in.height) * (1 + rowbytes);
     o.raw_off = raw;
     raw += (o.raw_len + 255) / 256 * 256;
+    o.r_stride = (rowbytes + 15) / 16 * 16;
+    o.r_off = rbytes;
+    rbytes += (tp::png::r_filter_bytes(in.height) + in.height * o.r_stride + 64 + 255) / 256 * 256;
+    rows += in.height;
     o.tok_off = toks;
     toks += o.in_bits / 2 + 256;
-    o.unit_base = static_cast<int32_t>(units);
     o.n_units = static_cast<int32_t>((o.in_bits + tp::png::kUnitBits - 1) / tp::png::kUnitBits);
     units += o.n_units;
   }
+  if (rows > (int64_t(1) << 31) - 1)
+    return -tp::set_error(TP_ERR_INVALID_ARGUMENT, "tp_png_describe: too many rows in one batch");
   auto al = [](int64_t v) { return (v + 255) / 256 * 256; };
   const int64_t units_at = 0;
   const int64_t tok_at = al(units_at + units * static_cast<int64_t>(sizeof(tp::png::PUnit)));
   const int64_t t_at = al(tok_at + toks * 4);
   const int64_t r_at = al(t_at + raw * 2);
-  const int64_t end = al(r_at + raw + 64);
+  const int64_t m_at = al(r_at + rbytes);
+  const int64_t end = al(m_at + raw * 4);
+  for (int i = 0; i < tp::png::kTotals; ++i) totals[i] = 0;
   totals[0] = units;
   totals[1] = toks;
   totals[2] = raw;
@@ -268,6 +276,9 @@ TP_API int64_t tp_png_describe(const TpPngInfo* infos, int32_t n, const int64_t*
   totals[5] = t_at;
   totals[6] = r_at;
   totals[7] = end;
+  totals[8] = rbytes;
+  totals[9] = m_at;
+  totals[10] = rows;
   return end;
 }
 

@@ -318,6 +318,7 @@ class _Session:
     def __init__(self, device: torch.device):
         self.device = device
         self.jpeg = None
+        self.png = None
         self.preps: dict = {}
         self.host = None  # pinned staging for host-decoded pixels
         self.dev = None
@@ -368,14 +369,16 @@ def preprocess(payload: bytes, cfg: PreprocessConfig, *,
                defer_normalize: bool = False) -> PreprocessResult:
     """decode -> plan -> resize -> tile -> normalize (or defer) -> mask
     (imgproc.py:538-598).  Stage keys are the reference's.  On the device path:
-    "decode" is the baseline-JPEG decode on the GPU (K7: host marker parse, upload of
-    the compressed bytes, device decode) -- or, for PNG and the JPEG variants K7 does
-    not take, the reference's Pillow decode on the host plus the pixel upload; "plan"
+    "decode" is the device decode of baseline JPEGs (K7) and 8-bit L / RGB / P PNGs (K8):
+    host marker / chunk parse, upload of the compressed bytes, device decode -- or, for
+    the payloads neither takes, the reference's Pillow decode on the host plus the pixel
+    upload; "plan"
     is K1's exact rule on the host (the TilePlan the result carries); "resize" is empty
     (fused into K2); "tile" is K1 + K2 in one launch (resample + crop + thumbnail, with
     normalize fused unless deferred); "normalize"/"defer" is the readback into
     ImageBuffers."""
     from .jpeg import TP_JPEG_OK, JpegDecoder, parse
+    from . import png as _png
 
     timings: dict[str, int] = {}
     device = require_device()
@@ -386,6 +389,11 @@ def preprocess(payload: bytes, cfg: PreprocessConfig, *,
         if sess.jpeg is None:
             sess.jpeg = JpegDecoder(device)
         images = sess.jpeg.decode([payload], stream=stream)  # host fallback inside
+        width, height = (int(v) for v in images.wh_host[0])
+    elif payload[:8] == _png.PNG_SIGNATURE and _png.parse(payload)[0].status == _png.TP_PNG_OK:
+        if sess.png is None:
+            sess.png = _png.PngDecoder(device)
+        images = sess.png.decode([payload], stream=stream)  # host fallback inside
         width, height = (int(v) for v in images.wh_host[0])
     else:
         arr = decode_rgb(payload)

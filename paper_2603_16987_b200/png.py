@@ -120,11 +120,11 @@ class PngDecoder:
         ok = np.array([infos[k].status == TP_PNG_OK for k in range(n)])
         zlen = np.array([infos[k].zlib_len for k in range(n)], dtype=np.int64)
         mark = _round_up(n * self.desc_bytes, 256)
-        sizes = np.where(ok, (zlen + 16 + 15) // 16 * 16, 0)  # 16 readable bytes after
+        sizes = np.where(ok, (zlen + 64 + 15) // 16 * 16, 0)  # 64 readable bytes after
         in_off = mark + np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.int64)
         in_off[~ok] = -1
         payload_bytes = _round_up(int(mark + sizes.sum()) + 64, 256)
-        totals = np.zeros(8, dtype=np.int64)
+        totals = np.zeros(16, dtype=np.int64)
         sl = self.slots[self._i % len(self.slots)]
         self._i += 1
         if sl.copied is not None:

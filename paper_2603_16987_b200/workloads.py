@@ -167,6 +167,23 @@ def jpeg_payloads(n: int, width: int = 1920, height: int = 1080, quality: int = 
     return [base[k % len(base)] for k in range(n)]
 
 
+def png_payloads(n: int, width: int = 1920, height: int = 1080, seed: int = 20260817,
+                 distinct: int = 8) -> list:
+    """n PNG payloads of `distinct` different scenes, repeated, written by Pillow with its
+    default settings (the encoder of the reference's own PNG path, decode_image's
+    re-encode, imgproc.py:252-256)."""
+    import io
+
+    from PIL import Image
+
+    base = []
+    for k in range(min(n, distinct)):
+        buf = io.BytesIO()
+        Image.fromarray(scene_image(width, height, seed + k)).save(buf, format="PNG")
+        base.append(buf.getvalue())
+    return [base[k % len(base)] for k in range(n)]
+
+
 # ---------------------------------------------------------------------------
 # C5 prompts: rendered chat prompts tokenized on the device (K6)
 

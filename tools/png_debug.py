@@ -12,11 +12,10 @@ import torch
 from png_cases import bad_cases, custom_cases, pil_cases
 from paper_2603_16987_b200 import png as P
 
-names = sys.argv[1:] or ["flip_400"]
-allc = dict(bad_cases() + custom_cases() + pil_cases())
+names = sys.argv[1:] if __name__ == "__main__" else []
 dec = P.PngDecoder(torch.device("cuda:0"))
 for name in names:
-    payload = allc[name]
+    payload = dict(bad_cases() + custom_cases() + pil_cases())[name]
     info, offs, lens = P.parse(payload)
     z = b"".join(payload[o: o + n] for o, n in zip(offs.tolist(), lens.tolist()))
     try:
@@ -37,3 +36,18 @@ for name in names:
         i32 = r[4:8].view(np.int32)
         print(f"  unit {u}: start {r[0]} end {r[1]} out_len {r[2]} out_off {r[3]} ntok {i32[0]} "
               f"status {i32[1]} final {i32[2]} dirty {i32[3]} stored {i32[4]} final_end {r[8]}")
+
+
+def unit_stats(payload):
+    """Valid units, and the longest unit (tokens, inflated bytes) of one payload."""
+    dec.decode([payload], sync=False)
+    sl, n, totals, out = dec._last
+    torch.cuda.synchronize()
+    U = int(totals[0])
+    rec = sl.work[int(totals[3]): int(totals[3]) + U * 80].cpu().numpy().view(np.int64).reshape(U, 10)
+    valid = rec[:, 0] >= 0
+    i32 = rec[:, 4:8].view(np.int32).reshape(U, 8)
+    runs = "".join("x" if v else "." for v in valid).split("x")
+    return {"units": U, "valid": int(valid.sum()), "max_ntok": int(i32[:, 0].max()),
+            "max_out": int(rec[:, 2].max()), "mean_out": float(rec[valid, 2].mean()),
+            "stored_starts": int(i32[:, 4].sum()), "max_invalid_run": max(len(r) for r in runs)}
