@@ -647,7 +647,11 @@ __global__ void __launch_bounds__(kFindThreads)
 // lane decodes its subsequence once more, writing its tokens at its prefix-sum offset.
 
 constexpr int kSubBits = 512;
-constexpr int kLeadBits = 384;
+constexpr int kLeadBits = 256;
+// a lane's tokens for one subsequence (<= kSubBits + one symbol of bits: at most one
+// token per 1.5 bits) wait in a per-lane staging area until the round's offsets are known
+constexpr int kStageTokens = kSubBits + 64;
+static_assert(kStageBytesPerUnit == 32 * kStageTokens * 4, "staging layout");
 constexpr int kInflateWarps = 4;
 
 struct SegResult {
@@ -661,7 +665,8 @@ struct SegResult {
 // end-of-block code or an invalid code.  out != nullptr: write the tokens (literal packs
 // are flushed at the segment's end, so counts depend only on the segment).
 __device__ SegResult decode_seg(const uint32_t* w, int64_t from, int64_t end, int64_t in_bits,
-                                const uint16_t* lt, const uint8_t* dt, uint32_t* out) {
+                                const uint16_t* lt, const uint8_t* dt, uint32_t* out,
+                                int out_cap = 1 << 30) {
   SegResult r;
   r.ntok = 0;
   r.nout = 0;
@@ -688,7 +693,7 @@ __device__ SegResult decode_seg(const uint32_t* w, int64_t from, int64_t end, in
       pack |= static_cast<uint32_t>(sym) << (8 * pc);
       ++r.nout;
       if (++pc == 3) {
-        if (out) out[r.ntok] = (3u << 24) | pack;
+        if (out && r.ntok < out_cap) out[r.ntok] = (3u << 24) | pack;
         ++r.ntok;
         pc = 0;
         pack = 0;
@@ -709,19 +714,21 @@ __device__ SegResult decode_seg(const uint32_t* w, int64_t from, int64_t end, in
     const int dist = dbase + static_cast<int>(br.peek(dextra));
     br.drop(dextra);
     if (pc) {
-      if (out) out[r.ntok] = (static_cast<uint32_t>(pc) << 24) | pack;
+      if (out && r.ntok < out_cap) out[r.ntok] = (static_cast<uint32_t>(pc) << 24) | pack;
       ++r.ntok;
       pc = 0;
       pack = 0;
     }
-    if (out) out[r.ntok] = kTokMatch | (static_cast<uint32_t>(len - 3) << 16) | static_cast<uint32_t>(dist - 1);
+    if (out && r.ntok < out_cap)
+      out[r.ntok] = kTokMatch | (static_cast<uint32_t>(len - 3) << 16) | static_cast<uint32_t>(dist - 1);
     ++r.ntok;
     r.nout += len;
   }
   if (pc && r.stop != 2) {
-    if (out) out[r.ntok] = (static_cast<uint32_t>(pc) << 24) | pack;
+    if (out && r.ntok < out_cap) out[r.ntok] = (static_cast<uint32_t>(pc) << 24) | pack;
     ++r.ntok;
   }
+  if (r.ntok > out_cap) r.stop = 2;  // more tokens than the staging holds
   r.exit = br.pos();
   return r;
 }
@@ -736,7 +743,7 @@ struct __align__(16) WarpTables {
 __global__ void __launch_bounds__(32 * kInflateWarps)
     k_png_inflate(const uint8_t* __restrict__ payload, const PDesc* __restrict__ desc, int n,
                   PUnit* __restrict__ units, int U, uint32_t* __restrict__ toks,
-                  const int32_t* __restrict__ img_status) {
+                  uint32_t* __restrict__ stage, const int32_t* __restrict__ img_status) {
   __shared__ WarpTables wt_all[kInflateWarps];
   const int lane = threadIdx.x & 31;
   const int u = blockIdx.x * kInflateWarps + (threadIdx.x >> 5);
@@ -766,6 +773,8 @@ __global__ void __launch_bounds__(32 * kInflateWarps)
   int status = kUnitOk, fin = 0;
   bool stored_start = me.stored != 0;
   const unsigned below = (1u << lane) - 1u;
+  uint32_t* warp_stage = stage + static_cast<int64_t>(u) * 32 * kStageTokens;
+  uint32_t* my_stage = warp_stage + lane * kStageTokens;
   while (true) {
     // ---- block boundary at `cur` (lane 0 reads the header; the state is broadcast)
     int btype = 0, bfinal = 0, action = 0;  // action: 0 data, 1 stored done, 2 stop, 3 error
@@ -866,13 +875,13 @@ __global__ void __launch_bounds__(32 * kInflateWarps)
       SegResult r;
       if (lane == 0) {
         entry = h;
-        r = decode_seg(w, h, nom_end, in_bits, wt.lit, wt.dist, nullptr);
+        r = decode_seg(w, h, nom_end, in_bits, wt.lit, wt.dist, my_stage, kStageTokens);
       } else {
         const SegResult lead = decode_seg(w, max(h, nom - kLeadBits), nom, in_bits, wt.lit,
                                           wt.dist, nullptr);
         if (lead.stop == 0) {
           entry = lead.exit;
-          r = decode_seg(w, entry, nom_end, in_bits, wt.lit, wt.dist, nullptr);
+          r = decode_seg(w, entry, nom_end, in_bits, wt.lit, wt.dist, my_stage, kStageTokens);
         } else {  // the speculative path stopped in the lead-in
           entry = -1;
           r = lead;
@@ -888,7 +897,7 @@ __global__ void __launch_bounds__(32 * kInflateWarps)
         if (!mb) break;
         if (lane == __ffs(mb) - 1) {
           entry = pexit;
-          r = decode_seg(w, entry, nom_end, in_bits, wt.lit, wt.dist, nullptr);
+          r = decode_seg(w, entry, nom_end, in_bits, wt.lit, wt.dist, my_stage, kStageTokens);
         }
       }
       const unsigned stops = __ballot_sync(0xffffffffu, r.stop != 0);
@@ -913,7 +922,14 @@ __global__ void __launch_bounds__(32 * kInflateWarps)
         end = h;
         break;
       }
-      if (in_round) decode_seg(w, entry, nom_end, in_bits, wt.lit, wt.dist, tk + ntok + incl - r.ntok);
+      // the round's tokens, lane by lane, from the staging areas (coalesced copies)
+      __syncwarp();
+      for (int j = 0; j <= J; ++j) {
+        const int nj = __shfl_sync(0xffffffffu, r.ntok, j);
+        const int bj = __shfl_sync(0xffffffffu, incl - r.ntok, j);
+        const uint32_t* src = warp_stage + j * kStageTokens;
+        for (int i = lane; i < nj; i += 32) tk[ntok + bj + i] = src[i];
+      }
       ntok += rtok;
       out += rout;
       h = __shfl_sync(0xffffffffu, r.exit, J);
@@ -1278,6 +1294,7 @@ __device__ void unfilter_image(const PDesc& d, uint8_t* __restrict__ r, uint8_t*
     uint8_t* row = rows_base + static_cast<int64_t>(y) * S;
     const uint32_t ft = has_row ? fbytes[y] : 0u;
     if (ft > 4) bad_filter = true;
+    const uint32_t m1 = 0u - (ft == 1), m2 = 0u - (ft == 2), m3 = 0u - (ft == 3), m4 = 0u - (ft == 4);
     const uint8_t* prior = y > 0 ? row - S : nullptr;  // recon of the previous group
     uint4 up_prev = make_uint4(0, 0, 0, 0), rec_prev = make_uint4(0, 0, 0, 0);
     uint4 fnext = make_uint4(0, 0, 0, 0);
@@ -1314,7 +1331,8 @@ __device__ void unfilter_image(const PDesc& d, uint8_t* __restrict__ r, uint8_t*
           const int pa = abs(pp - static_cast<int>(a)), pb = abs(pp - static_cast<int>(b)),
                     pc = abs(pp - static_cast<int>(c));
           const uint32_t pae = (pa <= pb && pa <= pc) ? a : (pb <= pc ? b : c);
-          const uint32_t pred = ft == 1 ? a : ft == 2 ? b : ft == 3 ? (a + b) >> 1 : ft == 4 ? pae : 0u;
+          // branch-free: neighbouring rows (lanes) use different filter types
+          const uint32_t pred = (a & m1) | (b & m2) | (((a + b) >> 1) & m3) | (pae & m4);
           rb[j] = (byte_at(f, j) + pred) & 255u;
         }
         const uint4 rec = make_uint4(pack4(rb), pack4(rb + 4), pack4(rb + 8), pack4(rb + 12));
@@ -1404,13 +1422,14 @@ extern "C" TP_API int tp_png_decode(const uint8_t* d_payload, const void* d_desc
   uint32_t* toks = reinterpret_cast<uint32_t*>(work + totals[4]);
   uint16_t* T = reinterpret_cast<uint16_t*>(work + totals[5]);
   uint8_t* R = work + totals[6];
+  uint32_t* stage = reinterpret_cast<uint32_t*>(work + totals[11]);
   cudaMemsetAsync(d_status, 0, sizeof(int32_t) * n, s);
   if (U > 0) {
     k_png_find<<<(U + kFindThreads / 32 - 1) / (kFindThreads / 32), kFindThreads, 0, s>>>(
         d_payload, desc, n, units, U);
     for (int r = 0; r < kRounds; ++r) {
       k_png_inflate<<<(U + kInflateWarps - 1) / kInflateWarps, 32 * kInflateWarps, 0, s>>>(
-          d_payload, desc, n, units, U, toks, d_status);
+          d_payload, desc, n, units, U, toks, stage, d_status);
       k_png_chain<<<n, 32, 0, s>>>(desc, n, units, d_status, r == kRounds - 1);
     }
     uint32_t* M = reinterpret_cast<uint32_t*>(work + totals[9]);

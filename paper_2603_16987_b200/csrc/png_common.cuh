@@ -89,8 +89,10 @@ struct __align__(16) PUnit {
 // tp_png_describe's totals[16]: [0] units, [1] tokens, [2] raw bytes (T entries),
 // [3..6] byte offsets of units / tokens / T / R, [7] workspace bytes, [8] R bytes,
 // [9] marker lists' byte offset (u32 image-relative positions; unit u's list starts at
-// the index of its first byte, raw_off + out_off), [10] rows in the batch
+// the index of its first byte, raw_off + out_off), [10] rows in the batch, [11] byte
+// offset of the inflate warps' token staging (kStageBytesPerUnit per unit)
 constexpr int kTotals = 16;
+constexpr int64_t kStageBytesPerUnit = 32 * (512 + 64) * 4;
 
 // R (inflated scanlines) per image: the filter-type bytes, then each row's rowbytes
 // data bytes at a 16-byte aligned stride (vector loads and stores in the unfilter)

@@ -266,7 +266,8 @@ TP_API int64_t tp_png_describe(const TpPngInfo* infos, int32_t n, const int64_t*
   const int64_t t_at = al(tok_at + toks * 4);
   const int64_t r_at = al(t_at + raw * 2);
   const int64_t m_at = al(r_at + rbytes);
-  const int64_t end = al(m_at + raw * 4);
+  const int64_t stage_at = al(m_at + raw * 4);
+  const int64_t end = al(stage_at + units * tp::png::kStageBytesPerUnit);
   for (int i = 0; i < tp::png::kTotals; ++i) totals[i] = 0;
   totals[0] = units;
   totals[1] = toks;
@@ -279,6 +280,7 @@ TP_API int64_t tp_png_describe(const TpPngInfo* infos, int32_t n, const int64_t*
   totals[8] = rbytes;
   totals[9] = m_at;
   totals[10] = rows;
+  totals[11] = stage_at;
   return end;
 }
 
