@@ -34,8 +34,10 @@ namespace {
 
 using namespace tp::png;
 
-constexpr int kLitRoot = 9;
-constexpr int kLitCap = 852;  // zlib's ENOUGH_LENS for a 9-bit root: worst-case entries
+// 10-bit root: a photo-like PNG's rarer literals have 10-12 bit codes, and with a 9-bit
+// root a third of the warp's decode steps took the subtable branch for some lane
+constexpr int kLitRoot = 10;
+constexpr int kLitCap = 1332;  // zlib's `enough 286 10 15`: worst-case entries, root 10
 constexpr int kDistRoot = 6;
 // distance table: root of 2^kDistRoot bytes, code counts (u8[16]) and the symbols in
 // canonical order (u8[32])
@@ -46,42 +48,26 @@ constexpr int kDistBytes = (1 << kDistRoot) + 16 + 32;
 // with 64 readable bytes after it
 
 struct Bits {
-  // 16-byte loads queued two ahead (`cur` being consumed, `nxt` in flight): a thread
-  // decodes ~16 symbols per 16 bytes, which covers the load latency
-  const uint4* w4;
-  int64_t qi;  // next 16-byte group to load
-  uint4 cur, nxt;
-  int ci;      // next word of `cur`
+  // 64-bit bit buffer refilled one 32-bit word at a time through the read-only path
+  // (the words of a lane's subsequence are L1 hits after the first)
+  const uint32_t* w;
+  int64_t wi;  // next word to load
   uint64_t buf;
   int n;
-  __device__ __forceinline__ static uint32_t word(const uint4& v, int i) {
-    return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
-  }
-  __device__ __forceinline__ uint32_t next_word() {
-    if (ci == 4) {
-      cur = nxt;
-      nxt = __ldg(w4 + qi++);
-      ci = 0;
-    }
-    return word(cur, ci++);
-  }
   __device__ __forceinline__ void init(const uint32_t* words, int64_t bit) {
-    w4 = reinterpret_cast<const uint4*>(words);
-    const int64_t wd = bit >> 5;
-    qi = wd >> 2;
-    cur = __ldg(w4 + qi);
-    nxt = __ldg(w4 + qi + 1);
-    qi += 2;
-    ci = static_cast<int>(wd & 3);
+    w = words;
+    wi = bit >> 5;
     const int s = static_cast<int>(bit & 31);
-    buf = static_cast<uint64_t>(word(cur, ci++)) >> s;
+    buf = static_cast<uint64_t>(__ldg(w + wi)) >> s;
     n = 32 - s;
+    ++wi;
     refill();
   }
   __device__ __forceinline__ void refill() {
     if (n <= 32) {
-      buf |= static_cast<uint64_t>(next_word()) << n;
+      buf |= static_cast<uint64_t>(__ldg(w + wi)) << n;
       n += 32;
+      ++wi;
     }
   }
   __device__ __forceinline__ uint32_t peek(int k) const {
@@ -91,7 +77,7 @@ struct Bits {
     buf >>= k;
     n -= k;
   }
-  __device__ __forceinline__ int64_t pos() const { return (((qi - 2) << 2) + ci) * 32 - n; }
+  __device__ __forceinline__ int64_t pos() const { return wi * 32 - n; }
 };
 
 // 64 bits starting at bit p (for the finder's header probes)
@@ -646,8 +632,11 @@ __global__ void __launch_bounds__(kFindThreads)
 // again from that exit, lowest first, until the subsequences tile the round; then every
 // lane decodes its subsequence once more, writing its tokens at its prefix-sum offset.
 
+#ifndef TP_PNG_LEAD
+#define TP_PNG_LEAD 256
+#endif
 constexpr int kSubBits = 512;
-constexpr int kLeadBits = 256;
+constexpr int kLeadBits = TP_PNG_LEAD;
 // a lane's tokens for one subsequence (<= kSubBits + one symbol of bits: at most one
 // token per 1.5 bits) wait in a per-lane staging area until the round's offsets are known
 constexpr int kStageTokens = kSubBits + 64;
@@ -675,11 +664,14 @@ __device__ SegResult decode_seg(const uint32_t* w, int64_t from, int64_t end, in
   br.init(w, from);
   uint32_t pack = 0;
   int pc = 0;
-  const int64_t qlim = (in_bits >> 7) + 3;
+  const int64_t wlim = (in_bits >> 5) + 12;  // past the stream (and its padding) by now
+  // bits left before `end` (a segment is at most a few thousand bits): one subtract per
+  // code instead of recomputing the reader's 64-bit position
+  int left = static_cast<int>(min(end - from, static_cast<int64_t>(1) << 30));
   while (true) {
-    if (br.pos() >= end) break;
-    if (br.qi > qlim) { r.stop = 2; break; }
+    if (left <= 0) break;
     br.refill();
+    if (br.wi > wlim) { r.stop = 2; break; }
     uint32_t e = lt[br.peek(kLitRoot)];
     if (e & 0x8000u) {
       const int sub = (e >> 12) & 7;
@@ -687,7 +679,9 @@ __device__ SegResult decode_seg(const uint32_t* w, int64_t from, int64_t end, in
       e = lt[(e & 0xFFFu) + (br.peek(kLitRoot + sub) >> kLitRoot)];
       if (e & 0x8000u) { r.stop = 2; break; }
     }
-    br.drop((e >> 11) & 15);
+    const int cl = (e >> 11) & 15;
+    br.drop(cl);
+    left -= cl;
     const int sym = static_cast<int>(e & 511u);
     if (sym < 256) {
       pack |= static_cast<uint32_t>(sym) << (8 * pc);
@@ -707,12 +701,14 @@ __device__ SegResult decode_seg(const uint32_t* w, int64_t from, int64_t end, in
     const int len = base + static_cast<int>(br.peek(extra));
     br.drop(extra);
     br.refill();
+    const int n0 = br.n;
     const int ds = decode_dist(br, dt);
     if (ds < 0 || ds > 29) { r.stop = 2; break; }
     int dbase, dextra;
     dist_base(ds, dbase, dextra);
     const int dist = dbase + static_cast<int>(br.peek(dextra));
     br.drop(dextra);
+    left -= extra + (n0 - br.n);
     if (pc) {
       if (out && r.ntok < out_cap) out[r.ntok] = (static_cast<uint32_t>(pc) << 24) | pack;
       ++r.ntok;
@@ -773,6 +769,7 @@ __global__ void __launch_bounds__(32 * kInflateWarps)
   int status = kUnitOk, fin = 0;
   bool stored_start = me.stored != 0;
   const unsigned below = (1u << lane) - 1u;
+  int nfix = 0, nround = 0;  // diagnostics (PUnit::pad_)
   uint32_t* warp_stage = stage + static_cast<int64_t>(u) * 32 * kStageTokens;
   uint32_t* my_stage = warp_stage + lane * kStageTokens;
   while (true) {
@@ -895,11 +892,13 @@ __global__ void __launch_bounds__(32 * kInflateWarps)
         const bool bad = lane > 0 && !(stops & below) && entry != pexit;
         const unsigned mb = __ballot_sync(0xffffffffu, bad);
         if (!mb) break;
+        ++nfix;
         if (lane == __ffs(mb) - 1) {
           entry = pexit;
           r = decode_seg(w, entry, nom_end, in_bits, wt.lit, wt.dist, my_stage, kStageTokens);
         }
       }
+      ++nround;
       const unsigned stops = __ballot_sync(0xffffffffu, r.stop != 0);
       const int J = stops ? __ffs(stops) - 1 : 31;  // last lane of the round
       const bool in_round = lane <= J;
@@ -953,6 +952,8 @@ __global__ void __launch_bounds__(32 * kInflateWarps)
     me.status = status;
     me.final_ = fin;
     me.dirty = 0;
+    me.pad_[0] = nfix;
+    me.pad_[1] = nround;
   }
 }
 
