@@ -90,6 +90,9 @@ __device__ unsigned int g_tp_checks;
                     // items, 2: not thumbnails, whose rows the tiles just read): C4 -3%, C2 +0.4%
 #define TP_K2_L2PF 2
 #endif
+#ifndef TP_K2_UFIX  // the exact fallback behind warp-uniform votes (A/B, tools/ab.py)
+#define TP_K2_UFIX 0
+#endif
 #ifndef TP_K2_DWIN  // affine path: window test on d = T - round(T) instead of N = round(8192 t)
 #define TP_K2_DWIN 1
 #endif
@@ -1011,9 +1014,43 @@ __device__ __forceinline__ void consume_pair_rows(
       if (EK > 0 && LAYOUT == TP_LAYOUT_NCHW) oc[0] += E;
     }
   };
+  // warp-uniform variant of fix (TP_K2_UFIX): the branches test __any_sync votes, so
+  // they compile to uniform branches without reconvergence barriers; an fp64 blend runs
+  // for every lane of the warp when any lane needs it and is kept where flagged
+  auto fix_uniform = [&](int jj, const PixTaps& a, const PixTaps& b, uint32_t (&ka)[C],
+                         uint32_t (&kb)[C], const uint32_t (&xa)[C], const uint32_t (&xb)[C]) {
+    const double fy64 = ldsd(pr.base + kPhFy64 + 8 * jj), omfy64 = __dsub_rn(1.0, fy64);
+    constexpr uint32_t kOut = DW ? 0x4B000000u : AFF ? 0x4B400000u : kKrawBias;
+    auto code = [&](uint32_t k) -> uint32_t {
+      return DW ? __float_as_uint(__uint_as_float(kOut + k) - 8388608.0f) : kOut + k;
+    };
+    const double nw1 = __dmul_rn(fy64, -4503599627370496.0),
+                 nw0 = __dmul_rn(omfy64, -4503599627370496.0);
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      const bool fa = flagged(xa[c]), fb = flagged(xb[c]);
+      if (__any_sync(0xffffffffu, fa)) {
+        const uint32_t v = code(blend_exact_fma(byte_of(a.r0w0, a.r0w1, c), byte_of(a.r0w0, a.r0w1, C + c),
+                                                byte_of(a.r1w0, a.r1w1, c), byte_of(a.r1w0, a.r1w1, C + c),
+                                                fy64, omfy64, nw1, nw0, fxa64, omfxa64));
+        ka[c] = fa ? v : ka[c];
+      }
+      if (__any_sync(0xffffffffu, fb)) {
+        const uint32_t v = code(blend_exact_fma(byte_of(b.r0w0, b.r0w1, c), byte_of(b.r0w0, b.r0w1, C + c),
+                                                byte_of(b.r1w0, b.r1w1, c), byte_of(b.r1w0, b.r1w1, C + c),
+                                                fy64, omfy64, nw1, nw0, fxb64, omfxb64));
+        kb[c] = fb ? v : kb[c];
+      }
+    }
+  };
   auto row = [&](int jj, const PixTaps& a, const PixTaps& b) {
     uint32_t ka[C], kb[C], xa[C], xb[C];
+#if TP_K2_UFIX
+    if (__any_sync(0xffffffffu, fast(jj, a, b, ka, kb, xa, xb))) fix_uniform(jj, a, b, ka, kb, xa, xb);
+#else
+    (void)fix_uniform;
     if (fast(jj, a, b, ka, kb, xa, xb)) fix(jj, a, b, ka, kb, xa, xb);
+#endif
     emit(jj, ka, kb);
   };
   constexpr uint32_t kLim = TP_CHECKS ? static_cast<uint32_t>(arena_bytes<C, OutT>()) : 0u;
