@@ -68,8 +68,9 @@ class PngDecoder:
     (chunk walk, packing the IDAT data into the pinned slab) overlaps the upload and
     decode of batch i.  Buffers grow on demand and are reused."""
 
-    def __init__(self, device=None, depth: int = 2):
+    def __init__(self, device=None, depth: int = 2, max_work_bytes: int = 8 << 30):
         self.device = require_device(device)
+        self.max_work_bytes = int(max_work_bytes)
         self.lib = _lib.load()
         self.desc_bytes = int(self.lib.tp_png_desc_bytes())
         self.slots = [_Slot() for _ in range(max(1, depth))]
@@ -119,6 +120,13 @@ class PngDecoder:
         out_off, out_total = layout_offsets(wh, 3)
         ok = np.array([infos[k].status == TP_PNG_OK for k in range(n)])
         zlen = np.array([infos[k].zlib_len for k in range(n)], dtype=np.int64)
+        # workspace per device image (csrc/png_host.cu tp_png_describe): tokens 16 B per
+        # compressed byte (indexed by bit / 2), T + R + marker lists 7 B per pixel byte,
+        # token staging per 48 KB unit; large batches decode in sub-batches that fit
+        est = np.where(ok, 16 * zlen + 7 * wh[:, 0].astype(np.int64) * wh[:, 1] * 3
+                       + (zlen // 49152 + 1) * 73728, 0)
+        if n > 1 and int(est.sum()) > self.max_work_bytes:
+            return self._decode_chunked(payloads, est, wh, out_off, out_total, out, stream, sync)
         mark = _round_up(n * self.desc_bytes, 256)
         sizes = np.where(ok, (zlen + 64 + 15) // 16 * 16, 0)  # 64 readable bytes after
         in_off = mark + np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.int64)
@@ -197,6 +205,34 @@ class PngDecoder:
         batch.finish()
         return out
 
+    def _decode_chunked(self, payloads, est, wh, out_off, out_total, out, stream, sync):
+        """Sub-batches of at most max_work_bytes of workspace, decoded in turn into one
+        output batch (the layout of a run of images is the batch layout shifted by the
+        run's first offset)."""
+        n = len(payloads)
+        if out is None:
+            out = PackedImages(torch.empty(out_total, dtype=torch.uint8, device=self.device),
+                               torch.as_tensor(out_off, device=self.device),
+                               torch.as_tensor(wh, device=self.device), 3, wh, out_off)
+        parts, i = [], 0
+        while i < n:
+            j, acc = i, 0
+            while j < n and (j == i or acc + int(est[j]) <= self.max_work_bytes):
+                acc += int(est[j])
+                j += 1
+            o0 = int(out_off[i])
+            sub_off = out_off[i:j] - o0
+            end = int(out_off[j]) if j < n else out_total
+            view = PackedImages(out.data[o0:end], out.offsets[i:j] - o0, out.wh[i:j], 3,
+                                wh[i:j], sub_off)
+            parts.append((i, self.decode(payloads[i:j], out=view, stream=stream, sync=False)))
+            i = j
+        batch = _ChunkedBatch(self, parts, out)
+        if not sync:
+            return batch
+        batch.finish()
+        return out
+
     def launch(self, stream: Optional[torch.cuda.Stream] = None) -> None:
         """(Re)launch the device decode of the last uploaded batch (K8 only: no host
         work, no copies) -- what the bench times as the decode kernels."""
@@ -213,6 +249,21 @@ class PngDecoder:
         sl, n, _, _ = self._last
         sl.done.synchronize()
         return sl.status_host[:n].numpy().copy()
+
+
+class _ChunkedBatch:
+    """Sub-batches of one decode: ``images`` is the whole output, ``finish()`` finishes
+    every part and returns the host-decoded indices of the whole batch."""
+
+    def __init__(self, dec, parts, images):
+        self._dec, self._parts, self.images = dec, parts, images
+        self.fallback: Optional[list] = None
+
+    def finish(self) -> list:
+        if self.fallback is None:
+            self.fallback = sorted(i0 + k for i0, b in self._parts for k in b.finish())
+            self._dec.last_fallback = self.fallback
+        return self.fallback
 
 
 def decode_images(payloads: Sequence[bytes], device=None) -> list[np.ndarray]:

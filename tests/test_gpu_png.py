@@ -86,3 +86,26 @@ def test_png_bad_payloads_match_reference():
         else:
             assert got_exc is None, (name, got_exc)
             assert np.array_equal(got, ref.reshape(-1)), name
+
+
+def test_png_chunked_batches():
+    """A workspace cap smaller than the batch: sub-batches decoded in turn into one output
+    (with a host-decoded payload in the middle)."""
+    import torch
+
+    from paper_2603_16987_b200.png import PngDecoder
+    from png_cases import content, pil_png
+
+    payloads = [pil_png(content("scene", 200 + 7 * i, 120 + 3 * i, i)) for i in range(5)]
+    payloads.insert(2, pil_png(content("scene", 50, 40, 9), "RGBA"[:3]))  # plain RGB
+    payloads.insert(4, dict(bad_cases())["truncated_tail"])  # Pillow decodes it, device may not
+    dec = PngDecoder(torch.device("cuda:0"), max_work_bytes=3 << 20)
+    for sync in (True, False):
+        res = dec.decode(payloads, sync=sync)
+        pk = res if sync else res.images
+        if not sync:
+            res.finish()
+        host = pk.data.cpu().numpy()
+        for k, (o, (w, h)) in enumerate(zip(pk.offsets_host, pk.wh_host)):
+            got = host[int(o): int(o) + int(w) * int(h) * 3].reshape(int(h), int(w), 3)
+            assert np.array_equal(got, _host(payloads[k])), k
