@@ -1262,32 +1262,56 @@ __global__ void __launch_bounds__(kAdlerThreads)
 
 constexpr int kUnfilterThreads = 1024;
 
-__device__ __forceinline__ uint32_t byte_at(const uint4& v, int j) {  // j: compile-time
-  const uint32_t w = j < 4 ? v.x : j < 8 ? v.y : j < 12 ? v.z : v.w;
-  return (w >> (8 * (j & 3))) & 255u;
+// chunk of one scanline per wavefront step: NW 32-bit words (TP_PNG_CHUNK bytes)
+#ifndef TP_PNG_CHUNK
+#define TP_PNG_CHUNK 16
+#endif
+constexpr int kChunkWords = TP_PNG_CHUNK / 4;
+template <int NW> struct ChunkVec;
+template <> struct ChunkVec<4> {
+  using T = uint4;
+  __device__ __forceinline__ static uint32_t w(const T& v, int i) {
+    return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
+  }
+  __device__ __forceinline__ static T make(const uint32_t* a) { return make_uint4(a[0], a[1], a[2], a[3]); }
+};
+template <> struct ChunkVec<2> {
+  using T = uint2;
+  __device__ __forceinline__ static uint32_t w(const T& v, int i) { return i == 0 ? v.x : v.y; }
+  __device__ __forceinline__ static T make(const uint32_t* a) { return make_uint2(a[0], a[1]); }
+};
+using CV = ChunkVec<kChunkWords>;
+using Chunk = CV::T;
+constexpr int kCh = 4 * kChunkWords;
+
+__device__ __forceinline__ uint32_t byte_at(const Chunk& v, int j) {  // j: compile-time
+  return (CV::w(v, j >> 2) >> (8 * (j & 3))) & 255u;
 }
 
 __device__ __forceinline__ uint32_t pack4(const uint32_t* b) {
   return b[0] | (b[1] << 8) | (b[2] << 16) | (b[3] << 24);
 }
 
-// One image per CTA, thread = scanline: at step t thread y reconstructs 16-byte chunk
-// t - y of its row, whose prior-row bytes thread y - 1 reconstructed at step t - 1
-// (shared-memory exchange, double-buffered).  Groups of blockDim rows run in turn; a
-// group's last row is written back in place for the next group's first row.  Rows sit
-// at a 16-byte aligned stride in R, so every chunk is one vector load.
+// One image per CTA, thread = scanline: at step t thread y reconstructs chunk t - y of
+// its row, whose prior-row bytes thread y - 1 reconstructed at step t - 1 (shared-memory
+// exchange, double-buffered).  Groups of blockDim rows run in turn; a group's last row is
+// written back in place for the next group's first row.  Rows sit at a 16-byte aligned
+// stride in R, so every chunk is one vector load.  16-byte chunks: 8-byte chunks widen
+// the wavefront's diagonal band (more rows active per step) but double the steps, and
+// the per-step barrier made them slower (1080p: 3.2 vs 2.8 ms per 64 images).
 template <int BPP>
 __device__ void unfilter_image(const PDesc& d, uint8_t* __restrict__ r, uint8_t* __restrict__ o,
-                               const uint8_t* pal, uint4 (*xch)[kUnfilterThreads], bool& bad_filter,
+                               const uint8_t* pal, Chunk (*xch)[kUnfilterThreads], bool& bad_filter,
                                bool& bad_pal) {
   const int tid = threadIdx.x;
   const int W = d.width, H = d.height;
   const bool is_p = d.ctype == 3;
   const int64_t rowbytes = static_cast<int64_t>(W) * BPP, S = d.r_stride;
-  const int nch = static_cast<int>((rowbytes + 15) >> 4);
+  const int nch = static_cast<int>((rowbytes + kCh - 1) / kCh);
   const uint8_t* fbytes = r;
   uint8_t* rows_base = r + r_filter_bytes(H);
   const int G = blockDim.x;
+  const Chunk zero = Chunk();
   for (int g0 = 0; g0 < H; g0 += G) {
     const int rows = min(G, H - g0);
     const int y = g0 + tid;
@@ -1297,35 +1321,34 @@ __device__ void unfilter_image(const PDesc& d, uint8_t* __restrict__ r, uint8_t*
     if (ft > 4) bad_filter = true;
     const uint32_t m1 = 0u - (ft == 1), m2 = 0u - (ft == 2), m3 = 0u - (ft == 3), m4 = 0u - (ft == 4);
     const uint8_t* prior = y > 0 ? row - S : nullptr;  // recon of the previous group
-    uint4 up_prev = make_uint4(0, 0, 0, 0), rec_prev = make_uint4(0, 0, 0, 0);
-    uint4 fnext = make_uint4(0, 0, 0, 0);
-    if (has_row) fnext = __ldcg(reinterpret_cast<const uint4*>(row));
-    // output rows: 16-byte stores when this row's output start is 16-byte aligned
+    Chunk up_prev = zero, rec_prev = zero, fnext = zero;
+    if (has_row) fnext = __ldcg(reinterpret_cast<const Chunk*>(row));
+    // output rows: vector stores when this row's output start is aligned
     uint8_t* orow = o + static_cast<int64_t>(y) * W * 3;
-    const bool oal = (reinterpret_cast<uintptr_t>(orow) & 15) == 0;
+    const bool oal = (reinterpret_cast<uintptr_t>(orow) & (kCh - 1)) == 0;
     const int steps = nch + rows - 1;
     for (int t = 0; t < steps; ++t) {
       const int i = t - tid;
       if (has_row && i >= 0 && i < nch) {
-        const uint4 f = fnext;
-        if (i + 1 < nch) fnext = __ldcg(reinterpret_cast<const uint4*>(row) + i + 1);
-        uint4 up = make_uint4(0, 0, 0, 0);
+        const Chunk f = fnext;
+        if (i + 1 < nch) fnext = __ldcg(reinterpret_cast<const Chunk*>(row) + i + 1);
+        Chunk up = zero;
         if (tid == 0) {
-          if (prior) up = __ldcg(reinterpret_cast<const uint4*>(prior) + i);
+          if (prior) up = __ldcg(reinterpret_cast<const Chunk*>(prior) + i);
         } else {
           up = xch[(t - 1) & 1][tid - 1];
         }
-        const int64_t x0 = 16 * static_cast<int64_t>(i);
-        uint32_t rb[16];
+        const int64_t x0 = kCh * static_cast<int64_t>(i);
+        uint32_t rb[kCh];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
+        for (int j = 0; j < kCh; ++j) {
           uint32_t a, c;
           if (j >= BPP) {
             a = rb[j - BPP];
             c = byte_at(up, j - BPP);
           } else {
-            a = x0 ? byte_at(rec_prev, 16 + j - BPP) : 0u;
-            c = x0 ? byte_at(up_prev, 16 + j - BPP) : 0u;
+            a = x0 ? byte_at(rec_prev, kCh + j - BPP) : 0u;
+            c = x0 ? byte_at(up_prev, kCh + j - BPP) : 0u;
           }
           const uint32_t b = byte_at(up, j);
           const int pp = static_cast<int>(a + b) - static_cast<int>(c);
@@ -1336,21 +1359,24 @@ __device__ void unfilter_image(const PDesc& d, uint8_t* __restrict__ r, uint8_t*
           const uint32_t pred = (a & m1) | (b & m2) | (((a + b) >> 1) & m3) | (pae & m4);
           rb[j] = (byte_at(f, j) + pred) & 255u;
         }
-        const uint4 rec = make_uint4(pack4(rb), pack4(rb + 4), pack4(rb + 8), pack4(rb + 12));
-        const int nb = static_cast<int>(rowbytes - x0 < 16 ? rowbytes - x0 : 16);
+        uint32_t rw[kChunkWords];
+#pragma unroll
+        for (int q = 0; q < kChunkWords; ++q) rw[q] = pack4(rb + 4 * q);
+        const Chunk rec = CV::make(rw);
+        const int nb = static_cast<int>(rowbytes - x0 < kCh ? rowbytes - x0 : kCh);
         if (BPP == 3) {
           uint8_t* dst = orow + x0;
-          if (oal && nb == 16) {
-            __stcs(reinterpret_cast<uint4*>(dst), rec);
+          if (oal && nb == kCh) {
+            __stcs(reinterpret_cast<Chunk*>(dst), rec);
           } else {
 #pragma unroll
-            for (int j = 0; j < 16; ++j)
+            for (int j = 0; j < kCh; ++j)
               if (j < nb) dst[j] = static_cast<uint8_t>(rb[j]);
           }
         } else {
-          uint32_t px[48];
+          uint32_t px[3 * kCh];
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
+          for (int j = 0; j < kCh; ++j) {
             const uint32_t v = rb[j];
             if (is_p) {
               if (j < nb && static_cast<int>(v) >= d.pal_n) bad_pal = true;
@@ -1362,20 +1388,22 @@ __device__ void unfilter_image(const PDesc& d, uint8_t* __restrict__ r, uint8_t*
             }
           }
           uint8_t* dst = orow + 3 * x0;
-          if (oal && nb == 16) {
+          if (oal && nb == kCh) {
 #pragma unroll
-            for (int q = 0; q < 3; ++q)
-              __stcs(reinterpret_cast<uint4*>(dst) + q,
-                     make_uint4(pack4(px + 16 * q), pack4(px + 16 * q + 4), pack4(px + 16 * q + 8),
-                                pack4(px + 16 * q + 12)));
+            for (int q = 0; q < 3; ++q) {
+              uint32_t pw[kChunkWords];
+#pragma unroll
+              for (int e = 0; e < kChunkWords; ++e) pw[e] = pack4(px + q * kCh + 4 * e);
+              __stcs(reinterpret_cast<Chunk*>(dst) + q, CV::make(pw));
+            }
           } else {
 #pragma unroll
-            for (int j = 0; j < 48; ++j)
+            for (int j = 0; j < 3 * kCh; ++j)
               if (j < 3 * nb) dst[j] = static_cast<uint8_t>(px[j]);
           }
         }
         if (tid == rows - 1 && g0 + rows < H)  // the next group's first row reads it
-          __stcg(reinterpret_cast<uint4*>(row) + i, rec);
+          __stcg(reinterpret_cast<Chunk*>(row) + i, rec);
         xch[t & 1][tid] = rec;
         up_prev = up;
         rec_prev = rec;
@@ -1388,7 +1416,7 @@ __device__ void unfilter_image(const PDesc& d, uint8_t* __restrict__ r, uint8_t*
 __global__ void __launch_bounds__(kUnfilterThreads)
     k_png_unfilter(const PDesc* __restrict__ desc, int n, uint8_t* __restrict__ R,
                    uint8_t* __restrict__ out, int32_t* __restrict__ img_status) {
-  __shared__ uint4 xch[2][kUnfilterThreads];
+  __shared__ Chunk xch[2][kUnfilterThreads];
   __shared__ uint8_t pal[768];
   const int k = blockIdx.x;
   const PDesc& d = desc[k];
