@@ -635,7 +635,6 @@ __global__ void __launch_bounds__(kFindThreads)
 #ifndef TP_PNG_LEAD
 #define TP_PNG_LEAD 256
 #endif
-constexpr int kSubBits = 512;
 constexpr int kLeadBits = TP_PNG_LEAD;
 // a lane's tokens for one subsequence (<= kSubBits + one symbol of bits: at most one
 // token per 1.5 bits) wait in a per-lane staging area until the round's offsets are known

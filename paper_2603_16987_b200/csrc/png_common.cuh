@@ -92,7 +92,11 @@ struct __align__(16) PUnit {
 // the index of its first byte, raw_off + out_off), [10] rows in the batch, [11] byte
 // offset of the inflate warps' token staging (kStageBytesPerUnit per unit)
 constexpr int kTotals = 16;
-constexpr int64_t kStageBytesPerUnit = 32 * (512 + 64) * 4;
+#ifndef TP_PNG_SUB
+#define TP_PNG_SUB 512
+#endif
+constexpr int kSubBits = TP_PNG_SUB;  // bits per lane per inflate round
+constexpr int64_t kStageBytesPerUnit = 32 * (kSubBits + 64) * 4;
 
 // R (inflated scanlines) per image: the filter-type bytes, then each row's rowbytes
 // data bytes at a 16-byte aligned stride (vector loads and stores in the unfilter)
