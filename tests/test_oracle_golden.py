@@ -204,9 +204,9 @@ def test_tokenize_vs_live_reference(reference, text):
 def test_port_costs_what_vlmfp_costs(reference, w, h, e):
     """The oracle port (bench.py's CPU leg when baseline/_ref is absent) restates vlmfp's
     fused path with the same band sharing and in-place ops, so it also costs what vlmfp
-    costs: C1 (1080p, E=512), C3 (4K) and a 13-tile image, best of 3 on one core, within
-    30% (the restatement was measured within 10%; the margin absorbs timer noise on a
-    shared build box)."""
+    costs: C1 (1080p, E=512), C3 (4K) and a 13-tile image, best of 5 interleaved rounds on
+    one core, within 40% (the restatement was measured within 10%; the margin absorbs
+    load on a shared build box)."""
     import time
 
     from oracle import tileprep_oracle as O
@@ -227,14 +227,13 @@ def test_port_costs_what_vlmfp_costs(reference, w, h, e):
     def port():
         O.preprocess_image(arr, e, 12, mean, std, True)
 
-    def best(fn):
-        fn()
-        ts = []
-        for _ in range(3):
+    # interleaved rounds, best of each: a load spike on the shared build box hits both
+    ref(), port()
+    rs, ps = [], []
+    for _ in range(5):
+        for fn, ts in ((ref, rs), (port, ps)):
             t0 = time.perf_counter()
             fn()
             ts.append(time.perf_counter() - t0)
-        return min(ts)
-
-    r, p = best(ref), best(port)
-    assert 1 / 1.3 <= p / r <= 1.3, (r, p)
+    r, p = min(rs), min(ps)
+    assert 1 / 1.4 <= p / r <= 1.4, (r, p)
