@@ -503,9 +503,51 @@ __device__ __forceinline__ uint32_t win32(uint32_t w0, uint32_t w1, uint32_t w2,
 // success of its first successful batch.
 constexpr int kFindQueue = 32;
 
+// Each unit is scanned by kFindParts warps, one per quarter: a unit's start is the first
+// header found in its lowest quarter that has one (k_png_find_select).  A warp stops early
+// once a lower quarter of its unit has found a header.  The scratch (per unit: found
+// position per quarter, lowest successful quarter) lives in the unit's token staging,
+// which the inflate only uses later.
+constexpr int kFindParts = 4;  // at most; the launch picks 1-4 by the number of units
+static_assert(kUnitBits % (3 * 4 * 1024) == 0, "1-4 parts of whole 1024-bit steps");
+struct FindScratch {
+  long long pos[kFindParts];  // found start | 1 << 62 for a stored start; -1: none
+  int lowest;                 // lowest quarter with a start (kFindParts: none yet)
+};
+__device__ __forceinline__ FindScratch* find_scratch(uint32_t* stage, int u) {
+  return reinterpret_cast<FindScratch*>(reinterpret_cast<uint8_t*>(stage) + u * kStageBytesPerUnit);
+}
+
+__global__ void k_png_find_init(uint32_t* stage, int U) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= U) return;
+  FindScratch* f = find_scratch(stage, u);
+  for (int p = 0; p < kFindParts; ++p) f->pos[p] = -1;
+  f->lowest = kFindParts;
+}
+
+__global__ void k_png_find_select(PUnit* __restrict__ units, uint32_t* stage, int U, int parts) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= U) return;
+  const FindScratch* f = find_scratch(stage, u);
+  long long v = -1;
+  for (int p = 0; p < parts && v < 0; ++p) v = f->pos[p];
+  const int64_t start = v < 0 ? -1 : (v & ((1ll << 62) - 1));
+  PUnit& o = units[u];
+  o.start = start;
+  o.end = -1;
+  o.out_len = 0;
+  o.out_off = 0;
+  o.ntok = 0;
+  o.status = kUnitOk;
+  o.final_ = 0;
+  o.dirty = start >= 0;
+  o.stored = v >= 0 && (v >> 62) != 0;
+}
+
 __global__ void __launch_bounds__(kFindThreads)
     k_png_find(const uint8_t* __restrict__ payload, const PDesc* __restrict__ desc, int n,
-               PUnit* __restrict__ units, int U) {
+               PUnit* __restrict__ units, int U, uint32_t* stage, int parts) {
   __shared__ uint8_t tabs[kFindThreads][128];  // code-length code of a lane's full check
   __shared__ uint8_t kraft9[512];              // Kraft terms of three 3-bit lengths
   __shared__ int64_t queue[kFindThreads / 32][kFindQueue];
@@ -518,9 +560,11 @@ __global__ void __launch_bounds__(kFindThreads)
     kraft9[i] = static_cast<uint8_t>(sum);
   }
   __syncthreads();
-  const int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int u = gw / parts, part = gw % parts;
   const int lane = threadIdx.x & 31;
   if (u >= U) return;
+  FindScratch* fs = find_scratch(stage, u);
   int64_t* q = queue[threadIdx.x >> 5];
   const int k = unit_image(desc, n, u);
   const PDesc& d = desc[k];
@@ -530,13 +574,16 @@ __global__ void __launch_bounds__(kFindThreads)
   int64_t start = -1;
   int stored = 0;
   if (local == 0) {
-    start = 16;  // after the zlib header
+    if (part == 0) start = 16;  // after the zlib header
   } else {
-    const int64_t lo = static_cast<int64_t>(local) * kUnitBits;  // multiple of 1024
-    const int64_t hi = min(lo + kUnitBits, d.in_bits - 3);
+    const int64_t part_bits = kUnitBits / parts;
+    const int64_t lo = static_cast<int64_t>(local) * kUnitBits + part * part_bits;
+    const int64_t hi = min(lo + part_bits, d.in_bits - 3);
     int qn = 0;  // queued candidates (warp-uniform)
+    int nsteps = 0, nflush = 0;  // diagnostics (PUnit::pad_ of the finder)
     // run the queued full checks, one per lane; the first success is the start
     auto flush = [&]() -> bool {
+      ++nflush;
       __syncwarp();
       const bool ok = lane < qn && dynamic_full(w, q[lane], d.in_bits, tab);
       const unsigned m = __ballot_sync(0xffffffffu, ok);
@@ -547,6 +594,11 @@ __global__ void __launch_bounds__(kFindThreads)
       return true;
     };
     for (int64_t p0 = lo; p0 < hi; p0 += 1024) {
+      ++nsteps;
+      // a lower quarter of this unit has its start: this one is not needed
+      if (part > 0 && (nsteps & 3) == 1 &&
+          __shfl_sync(0xffffffffu, lane == 0 ? *reinterpret_cast<volatile int*>(&fs->lowest) : 0, 0) < part)
+        break;
       const int64_t wi = (p0 >> 5) + lane;
       const int64_t pw = wi << 5;  // this lane's first position
       int64_t found = -1;
@@ -606,18 +658,11 @@ __global__ void __launch_bounds__(kFindThreads)
       if (start >= 0) break;
     }
     if (start < 0 && qn > 0) flush();
+    (void)nflush;
   }
-  if (lane == 0) {
-    PUnit& o = units[u];
-    o.start = start;
-    o.end = -1;
-    o.out_len = 0;
-    o.out_off = 0;
-    o.ntok = 0;
-    o.status = kUnitOk;
-    o.final_ = 0;
-    o.dirty = start >= 0;
-    o.stored = stored;
+  if (lane == 0 && start >= 0) {
+    fs->pos[part] = start | (stored ? (1ll << 62) : 0);
+    atomicMin(&fs->lowest, part);
   }
 }
 
@@ -1453,8 +1498,16 @@ extern "C" TP_API int tp_png_decode(const uint8_t* d_payload, const void* d_desc
   uint32_t* stage = reinterpret_cast<uint32_t*>(work + totals[11]);
   cudaMemsetAsync(d_status, 0, sizeof(int32_t) * n, s);
   if (U > 0) {
-    k_png_find<<<(U + kFindThreads / 32 - 1) / (kFindThreads / 32), kFindThreads, 0, s>>>(
-        d_payload, desc, n, units, U);
+    // finder warps per unit: split the scans while the units alone leave the GPU short of
+    // warps (small batches: latency-bound), one per unit when they fill it (64 1080p
+    // PNGs, 6,000 units: the extra scanning then costs more than it hides)
+    const int sms = std::max(1, tp::device_sm_count());
+    const int parts = std::max(1, std::min(kFindParts, (sms * 48) / std::max(U, 1)));
+    k_png_find_init<<<(U + 255) / 256, 256, 0, s>>>(stage, U);
+    const int64_t find_warps = static_cast<int64_t>(U) * parts;
+    k_png_find<<<static_cast<int>((find_warps + kFindThreads / 32 - 1) / (kFindThreads / 32)),
+                 kFindThreads, 0, s>>>(d_payload, desc, n, units, U, stage, parts);
+    k_png_find_select<<<(U + 255) / 256, 256, 0, s>>>(units, stage, U, parts);
     for (int r = 0; r < kRounds; ++r) {
       k_png_inflate<<<(U + kInflateWarps - 1) / kInflateWarps, 32 * kInflateWarps, 0, s>>>(
           d_payload, desc, n, units, U, toks, stage, d_status);
