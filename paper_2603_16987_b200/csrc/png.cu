@@ -1304,7 +1304,6 @@ __global__ void __launch_bounds__(kAdlerThreads)
 // unfilter (PNG §9.2) + L/P -> RGB: one CTA per image, thread = scanline
 
 
-constexpr int kUnfilterThreads = 1024;
 
 // chunk of one scanline per wavefront step: NW 32-bit words (TP_PNG_CHUNK bytes)
 #ifndef TP_PNG_CHUNK
@@ -1336,16 +1335,31 @@ __device__ __forceinline__ uint32_t pack4(const uint32_t* b) {
   return b[0] | (b[1] << 8) | (b[2] << 16) | (b[3] << 24);
 }
 
-// One image per CTA, thread = scanline: at step t thread y reconstructs chunk t - y of
-// its row, whose prior-row bytes thread y - 1 reconstructed at step t - 1 (shared-memory
-// exchange, double-buffered).  Groups of blockDim rows run in turn; a group's last row is
-// written back in place for the next group's first row.  Rows sit at a 16-byte aligned
-// stride in R, so every chunk is one vector load.  16-byte chunks: 8-byte chunks widen
-// the wavefront's diagonal band (more rows active per step) but double the steps, and
-// the per-step barrier made them slower (1080p: 3.2 vs 2.8 ms per 64 images).
+__device__ __forceinline__ int blk_image(const PDesc* __restrict__ desc, int n, int g) {
+  int lo = 0, hi = n;  // largest k with blk_base <= g
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (desc[mid].blk_base <= g) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// One row block (kUnfilterRows consecutive scanlines of one image) per work item, thread
+// = scanline: at step t thread y reconstructs chunk t - y of its row, whose prior-row bytes
+// thread y - 1 reconstructed at step t - 1 (shared-memory exchange, double-buffered).  The
+// block's first row reads its prior row from the previous block, which a CTA that claimed
+// it earlier is producing: its last row is written back in place in R chunk by chunk and
+// published through a progress counter (release: threadfence, then the counter; acquire:
+// the counter, then an L2 load).  CTAs are persistent and claim the blocks in order, so a
+// block only ever waits for a block that is already running: no deadlock, and an image's
+// blocks run as a pipeline over several SMs (a 1080p image is 9 blocks).
+constexpr int kPriorBatch = 8;
+
 template <int BPP>
-__device__ void unfilter_image(const PDesc& d, uint8_t* __restrict__ r, uint8_t* __restrict__ o,
-                               const uint8_t* pal, Chunk (*xch)[kUnfilterThreads], bool& bad_filter,
+__device__ void unfilter_block(const PDesc& d, int blk, uint8_t* __restrict__ r,
+                               uint8_t* __restrict__ o, const uint8_t* pal,
+                               Chunk (*xch)[kUnfilterRows], Chunk* pbuf,
+                               int* __restrict__ progress, int item, bool& bad_filter,
                                bool& bad_pal) {
   const int tid = threadIdx.x;
   const int W = d.width, H = d.height;
@@ -1354,126 +1368,159 @@ __device__ void unfilter_image(const PDesc& d, uint8_t* __restrict__ r, uint8_t*
   const int nch = static_cast<int>((rowbytes + kCh - 1) / kCh);
   const uint8_t* fbytes = r;
   uint8_t* rows_base = r + r_filter_bytes(H);
-  const int G = blockDim.x;
+  const int g0 = blk * kUnfilterRows;
+  const int rows = min(kUnfilterRows, H - g0);
+  const bool last_blk = g0 + rows >= H;
   const Chunk zero = Chunk();
-  for (int g0 = 0; g0 < H; g0 += G) {
-    const int rows = min(G, H - g0);
-    const int y = g0 + tid;
-    const bool has_row = tid < rows;
-    uint8_t* row = rows_base + static_cast<int64_t>(y) * S;
-    const uint32_t ft = has_row ? fbytes[y] : 0u;
-    if (ft > 4) bad_filter = true;
-    const uint32_t m1 = 0u - (ft == 1), m2 = 0u - (ft == 2), m3 = 0u - (ft == 3), m4 = 0u - (ft == 4);
-    const uint8_t* prior = y > 0 ? row - S : nullptr;  // recon of the previous group
-    Chunk up_prev = zero, rec_prev = zero, fnext = zero;
-    if (has_row) fnext = __ldcg(reinterpret_cast<const Chunk*>(row));
-    // output rows: vector stores when this row's output start is aligned
-    uint8_t* orow = o + static_cast<int64_t>(y) * W * 3;
-    const bool oal = (reinterpret_cast<uintptr_t>(orow) & (kCh - 1)) == 0;
-    const int steps = nch + rows - 1;
-    for (int t = 0; t < steps; ++t) {
-      const int i = t - tid;
-      if (has_row && i >= 0 && i < nch) {
-        const Chunk f = fnext;
-        if (i + 1 < nch) fnext = __ldcg(reinterpret_cast<const Chunk*>(row) + i + 1);
-        Chunk up = zero;
-        if (tid == 0) {
-          if (prior) up = __ldcg(reinterpret_cast<const Chunk*>(prior) + i);
-        } else {
-          up = xch[(t - 1) & 1][tid - 1];
+  const int y = g0 + tid;
+  const bool has_row = tid < rows;
+  uint8_t* row = rows_base + static_cast<int64_t>(y) * S;
+  const uint32_t ft = has_row ? fbytes[y] : 0u;
+  if (ft > 4) bad_filter = true;
+  const uint32_t m1 = 0u - (ft == 1), m2 = 0u - (ft == 2), m3 = 0u - (ft == 3), m4 = 0u - (ft == 4);
+  const uint8_t* prior = y > 0 ? row - S : nullptr;  // (thread 0) the previous block's last row
+  const volatile int* prior_progress = progress + item - 1;
+  Chunk up_prev = zero, rec_prev = zero, fnext = zero;
+  // own row: plain (L1-cached) loads -- 8 chunks per line; only this thread ever writes
+  // it, after reading
+  if (has_row) fnext = *reinterpret_cast<const Chunk*>(row);
+  uint8_t* orow = o + static_cast<int64_t>(y) * W * 3;
+  const bool oal = (reinterpret_cast<uintptr_t>(orow) & (kCh - 1)) == 0;
+  const int steps = nch + rows - 1;
+  for (int t = 0; t < steps; ++t) {
+    const int i = t - tid;
+    if (has_row && i >= 0 && i < nch) {
+      const Chunk f = fnext;
+      if (i + 1 < nch) fnext = reinterpret_cast<const Chunk*>(row)[i + 1];
+      Chunk up = zero;
+      if (tid == 0) {
+        if (prior) {
+          // the previous block's last row, kPriorBatch chunks at a time: one wait and one
+          // L2 round trip per batch instead of per step (the block lags a few steps more)
+          if (i % kPriorBatch == 0) {
+            const int need = min(i + kPriorBatch, nch);
+            while (*prior_progress < need) __nanosleep(32);
+            __threadfence();  // acquire: the chunks were written before the counter
+#pragma unroll
+            for (int q = 0; q < kPriorBatch; ++q)
+              if (i + q < nch) pbuf[q] = __ldcg(reinterpret_cast<const Chunk*>(prior) + i + q);
+          }
+          up = pbuf[i % kPriorBatch];
         }
-        const int64_t x0 = kCh * static_cast<int64_t>(i);
-        uint32_t rb[kCh];
+      } else {
+        up = xch[(t - 1) & 1][tid - 1];
+      }
+      const int64_t x0 = kCh * static_cast<int64_t>(i);
+      uint32_t rb[kCh];
+#pragma unroll
+      for (int j = 0; j < kCh; ++j) {
+        uint32_t a, c;
+        if (j >= BPP) {
+          a = rb[j - BPP];
+          c = byte_at(up, j - BPP);
+        } else {
+          a = x0 ? byte_at(rec_prev, kCh + j - BPP) : 0u;
+          c = x0 ? byte_at(up_prev, kCh + j - BPP) : 0u;
+        }
+        const uint32_t b = byte_at(up, j);
+        const int pp = static_cast<int>(a + b) - static_cast<int>(c);
+        const int pa = abs(pp - static_cast<int>(a)), pb = abs(pp - static_cast<int>(b)),
+                  pc = abs(pp - static_cast<int>(c));
+        const uint32_t pae = (pa <= pb && pa <= pc) ? a : (pb <= pc ? b : c);
+        // branch-free: neighbouring rows (lanes) use different filter types
+        const uint32_t pred = (a & m1) | (b & m2) | (((a + b) >> 1) & m3) | (pae & m4);
+        rb[j] = (byte_at(f, j) + pred) & 255u;
+      }
+      uint32_t rw[kChunkWords];
+#pragma unroll
+      for (int q = 0; q < kChunkWords; ++q) rw[q] = pack4(rb + 4 * q);
+      const Chunk rec = CV::make(rw);
+      const int nb = static_cast<int>(rowbytes - x0 < kCh ? rowbytes - x0 : kCh);
+      if (BPP == 3) {
+        uint8_t* dst = orow + x0;
+        if (oal && nb == kCh) {
+          __stcs(reinterpret_cast<Chunk*>(dst), rec);
+        } else {
+#pragma unroll
+          for (int j = 0; j < kCh; ++j)
+            if (j < nb) dst[j] = static_cast<uint8_t>(rb[j]);
+        }
+      } else {
+        uint32_t px[3 * kCh];
 #pragma unroll
         for (int j = 0; j < kCh; ++j) {
-          uint32_t a, c;
-          if (j >= BPP) {
-            a = rb[j - BPP];
-            c = byte_at(up, j - BPP);
+          const uint32_t v = rb[j];
+          if (is_p) {
+            if (j < nb && static_cast<int>(v) >= d.pal_n) bad_pal = true;
+            px[3 * j] = pal[3 * v];
+            px[3 * j + 1] = pal[3 * v + 1];
+            px[3 * j + 2] = pal[3 * v + 2];
           } else {
-            a = x0 ? byte_at(rec_prev, kCh + j - BPP) : 0u;
-            c = x0 ? byte_at(up_prev, kCh + j - BPP) : 0u;
+            px[3 * j] = px[3 * j + 1] = px[3 * j + 2] = v;
           }
-          const uint32_t b = byte_at(up, j);
-          const int pp = static_cast<int>(a + b) - static_cast<int>(c);
-          const int pa = abs(pp - static_cast<int>(a)), pb = abs(pp - static_cast<int>(b)),
-                    pc = abs(pp - static_cast<int>(c));
-          const uint32_t pae = (pa <= pb && pa <= pc) ? a : (pb <= pc ? b : c);
-          // branch-free: neighbouring rows (lanes) use different filter types
-          const uint32_t pred = (a & m1) | (b & m2) | (((a + b) >> 1) & m3) | (pae & m4);
-          rb[j] = (byte_at(f, j) + pred) & 255u;
         }
-        uint32_t rw[kChunkWords];
+        uint8_t* dst = orow + 3 * x0;
+        if (oal && nb == kCh) {
 #pragma unroll
-        for (int q = 0; q < kChunkWords; ++q) rw[q] = pack4(rb + 4 * q);
-        const Chunk rec = CV::make(rw);
-        const int nb = static_cast<int>(rowbytes - x0 < kCh ? rowbytes - x0 : kCh);
-        if (BPP == 3) {
-          uint8_t* dst = orow + x0;
-          if (oal && nb == kCh) {
-            __stcs(reinterpret_cast<Chunk*>(dst), rec);
-          } else {
+          for (int q = 0; q < 3; ++q) {
+            uint32_t pw[kChunkWords];
 #pragma unroll
-            for (int j = 0; j < kCh; ++j)
-              if (j < nb) dst[j] = static_cast<uint8_t>(rb[j]);
+            for (int e = 0; e < kChunkWords; ++e) pw[e] = pack4(px + q * kCh + 4 * e);
+            __stcs(reinterpret_cast<Chunk*>(dst) + q, CV::make(pw));
           }
         } else {
-          uint32_t px[3 * kCh];
 #pragma unroll
-          for (int j = 0; j < kCh; ++j) {
-            const uint32_t v = rb[j];
-            if (is_p) {
-              if (j < nb && static_cast<int>(v) >= d.pal_n) bad_pal = true;
-              px[3 * j] = pal[3 * v];
-              px[3 * j + 1] = pal[3 * v + 1];
-              px[3 * j + 2] = pal[3 * v + 2];
-            } else {
-              px[3 * j] = px[3 * j + 1] = px[3 * j + 2] = v;
-            }
-          }
-          uint8_t* dst = orow + 3 * x0;
-          if (oal && nb == kCh) {
-#pragma unroll
-            for (int q = 0; q < 3; ++q) {
-              uint32_t pw[kChunkWords];
-#pragma unroll
-              for (int e = 0; e < kChunkWords; ++e) pw[e] = pack4(px + q * kCh + 4 * e);
-              __stcs(reinterpret_cast<Chunk*>(dst) + q, CV::make(pw));
-            }
-          } else {
-#pragma unroll
-            for (int j = 0; j < 3 * kCh; ++j)
-              if (j < 3 * nb) dst[j] = static_cast<uint8_t>(px[j]);
-          }
+          for (int j = 0; j < 3 * kCh; ++j)
+            if (j < 3 * nb) dst[j] = static_cast<uint8_t>(px[j]);
         }
-        if (tid == rows - 1 && g0 + rows < H)  // the next group's first row reads it
-          __stcg(reinterpret_cast<Chunk*>(row) + i, rec);
-        xch[t & 1][tid] = rec;
-        up_prev = up;
-        rec_prev = rec;
       }
-      __syncthreads();
+      if (tid == rows - 1 && !last_blk) {  // the next block's first row reads it
+        __stcg(reinterpret_cast<Chunk*>(row) + i, rec);
+        __threadfence();  // release: the chunk before the counter
+        atomicExch(progress + item, i + 1);
+      }
+      xch[t & 1][tid] = rec;
+      up_prev = up;
+      rec_prev = rec;
     }
+    __syncthreads();
   }
 }
 
-__global__ void __launch_bounds__(kUnfilterThreads)
+__global__ void __launch_bounds__(kUnfilterRows)
     k_png_unfilter(const PDesc* __restrict__ desc, int n, uint8_t* __restrict__ R,
-                   uint8_t* __restrict__ out, int32_t* __restrict__ img_status) {
-  __shared__ Chunk xch[2][kUnfilterThreads];
+                   uint8_t* __restrict__ out, int32_t* __restrict__ img_status,
+                   int* __restrict__ progress, int n_items) {
+  __shared__ Chunk xch[2][kUnfilterRows];
+  __shared__ Chunk pbuf[kPriorBatch];
   __shared__ uint8_t pal[768];
-  const int k = blockIdx.x;
-  const PDesc& d = desc[k];
-  if (d.n_units == 0 || img_status[k] != kImgOk) return;
-  for (int i = threadIdx.x; i < 768; i += blockDim.x) pal[i] = d.pal[i];
-  __syncthreads();
-  bool bad_filter = false, bad_pal = false;
-  if (d.bpp == 3)
-    unfilter_image<3>(d, R + d.r_off, out + d.out_off, pal, xch, bad_filter, bad_pal);
-  else
-    unfilter_image<1>(d, R + d.r_off, out + d.out_off, pal, xch, bad_filter, bad_pal);
-  if (bad_filter) atomicOr(img_status + k, kImgFilter);
-  if (bad_pal) atomicOr(img_status + k, kImgPalette);
+  __shared__ int cur;
+  int* claim = progress + n_items;
+  while (true) {
+    __syncthreads();  // the previous item's readers of `cur` and `pal` are done
+    if (threadIdx.x == 0) cur = atomicAdd(claim, 1);
+    __syncthreads();
+    const int item = cur;
+    if (item >= n_items) break;
+    const int k = blk_image(desc, n, item);
+    const PDesc& d = desc[k];
+    // Skip only on what earlier kernels decided: the flags this kernel sets (filter,
+    // palette) appear while the image's blocks run, and a block must never skip while a
+    // later block of its image waits for it.
+    if (d.n_units == 0 || (img_status[k] & ~(kImgFilter | kImgPalette)) != kImgOk) continue;
+    if (d.ctype == 3)
+      for (int i = threadIdx.x; i < 768; i += blockDim.x) pal[i] = d.pal[i];
+    __syncthreads();
+    bool bad_filter = false, bad_pal = false;
+    if (d.bpp == 3)
+      unfilter_block<3>(d, item - d.blk_base, R + d.r_off, out + d.out_off, pal, xch, pbuf,
+                        progress, item, bad_filter, bad_pal);
+    else
+      unfilter_block<1>(d, item - d.blk_base, R + d.r_off, out + d.out_off, pal, xch, pbuf,
+                        progress, item, bad_filter, bad_pal);
+    if (bad_filter) atomicOr(img_status + k, kImgFilter);
+    if (bad_pal) atomicOr(img_status + k, kImgPalette);
+  }
 }
 
 }  // namespace
@@ -1519,7 +1566,14 @@ extern "C" TP_API int tp_png_decode(const uint8_t* d_payload, const void* d_desc
       k_png_final<<<static_cast<int>(totals[10]), 256, 0, s>>>(desc, n, T, R, d_status);
     k_png_window<<<n, 1024, 0, s>>>(desc, n, units, T, M, R, d_status);
     k_png_adler<<<n, kAdlerThreads, 0, s>>>(d_payload, desc, n, units, R, d_status);
-    k_png_unfilter<<<n, kUnfilterThreads, 0, s>>>(desc, n, R, d_out, d_status);
+    const int n_items = static_cast<int>(totals[12]);
+    if (n_items > 0) {
+      int* progress = reinterpret_cast<int*>(work + totals[13]);
+      cudaMemsetAsync(progress, 0, sizeof(int) * (n_items + 1), s);
+      const int sms = std::max(1, tp::device_sm_count());
+      k_png_unfilter<<<std::min(n_items, sms * 8), kUnfilterRows, 0, s>>>(
+          desc, n, R, d_out, d_status, progress, n_items);
+    }
   }
   return tp::check_launch("tp_png_decode");
 }

@@ -61,6 +61,8 @@ struct __align__(16) PDesc {
   int32_t n_units;
   int32_t pal_n;      // PLTE entries (P)
   int32_t row_base;   // first row of this image in the batch's row numbering
+  int32_t blk_base;   // first unfilter row block of this image (kUnfilterRows rows each)
+  int32_t pad3_;
   int64_t r_off;      // R workspace: filter bytes (align16(height)), then the rows
   int64_t r_stride;   // R row stride: rowbytes rounded up to 16 (rows 16-byte aligned)
   uint8_t pal[768];   // PLTE (P)
@@ -86,11 +88,16 @@ struct __align__(16) PUnit {
   int64_t pad2_;
 };
 
+// Unfilter work item: a block of consecutive scanlines of one image, one thread each.
+constexpr int kUnfilterRows = 128;
+
 // tp_png_describe's totals[16]: [0] units, [1] tokens, [2] raw bytes (T entries),
 // [3..6] byte offsets of units / tokens / T / R, [7] workspace bytes, [8] R bytes,
 // [9] marker lists' byte offset (u32 image-relative positions; unit u's list starts at
 // the index of its first byte, raw_off + out_off), [10] rows in the batch, [11] byte
-// offset of the inflate warps' token staging (kStageBytesPerUnit per unit)
+// offset of the inflate warps' token staging (kStageBytesPerUnit per unit), [12] unfilter
+// row blocks in the batch, [13] byte offset of their progress counters (int32 each, plus
+// one claim counter)
 constexpr int kTotals = 16;
 #ifndef TP_PNG_SUB
 #define TP_PNG_SUB 512

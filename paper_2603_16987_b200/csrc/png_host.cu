@@ -223,7 +223,7 @@ TP_API int64_t tp_png_describe(const TpPngInfo* infos, int32_t n, const int64_t*
     return -tp::set_error(TP_ERR_INVALID_ARGUMENT, "tp_png_describe: invalid argument");
   }
   PDesc* d = static_cast<PDesc*>(desc);
-  int64_t units = 0, toks = 0, raw = 0, rbytes = 0, rows = 0;
+  int64_t units = 0, toks = 0, raw = 0, rbytes = 0, rows = 0, blks = 0;
   for (int k = 0; k < n; ++k) {
     const TpPngInfo& in = infos[k];
     PDesc& o = d[k];
@@ -237,6 +237,7 @@ TP_API int64_t tp_png_describe(const TpPngInfo* infos, int32_t n, const int64_t*
     std::memcpy(o.pal, in.pal, sizeof(o.pal));
     o.unit_base = static_cast<int32_t>(units);
     o.row_base = static_cast<int32_t>(rows);
+    o.blk_base = static_cast<int32_t>(blks);
     if (in.status != TP_PNG_OK || in_off[k] < 0) {
       o.n_units = 0;  // not a device image
       continue;
@@ -253,6 +254,7 @@ TP_API int64_t tp_png_describe(const TpPngInfo* infos, int32_t n, const int64_t*
     o.r_off = rbytes;
     rbytes += (tp::png::r_filter_bytes(in.height) + in.height * o.r_stride + 64 + 255) / 256 * 256;
     rows += in.height;
+    blks += (in.height + tp::png::kUnfilterRows - 1) / tp::png::kUnfilterRows;
     o.tok_off = toks;
     toks += o.in_bits / 2 + 256;
     o.n_units = static_cast<int32_t>((o.in_bits + tp::png::kUnitBits - 1) / tp::png::kUnitBits);
@@ -267,7 +269,8 @@ TP_API int64_t tp_png_describe(const TpPngInfo* infos, int32_t n, const int64_t*
   const int64_t r_at = al(t_at + raw * 2);
   const int64_t m_at = al(r_at + rbytes);
   const int64_t stage_at = al(m_at + raw * 4);
-  const int64_t end = al(stage_at + units * tp::png::kStageBytesPerUnit);
+  const int64_t prog_at = al(stage_at + units * tp::png::kStageBytesPerUnit);
+  const int64_t end = al(prog_at + (blks + 1) * 4);
   for (int i = 0; i < tp::png::kTotals; ++i) totals[i] = 0;
   totals[0] = units;
   totals[1] = toks;
@@ -281,6 +284,8 @@ TP_API int64_t tp_png_describe(const TpPngInfo* infos, int32_t n, const int64_t*
   totals[9] = m_at;
   totals[10] = rows;
   totals[11] = stage_at;
+  totals[12] = blks;
+  totals[13] = prog_at;
   return end;
 }
 
