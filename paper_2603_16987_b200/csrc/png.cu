@@ -1230,41 +1230,62 @@ __global__ void k_png_window(const PDesc* __restrict__ desc, int n, const PUnit*
 // Adler-32 (RFC 1950 §8) of the inflated bytes, checked when the stream holds the four
 // trailer bytes after the final block.  Pillow's zlib verifies the trailer whenever it
 // is in the data it was fed (a wrong one raises "broken data stream"), and says nothing
-// when the stream ends before it (tests/test_gpu_png.py, bad payloads).  Thread t sums
-// its contiguous segment: s1 = sum d_i, s2 = sum (n - i) d_i; b = n + sum s2, a = 1 + sum s1.
+// when the stream ends before it (tests/test_gpu_png.py, bad payloads).  For n bytes,
+// a = 1 + sum d_i and b = n + sum (n - i) d_i (mod 65521): both are plain sums, so any
+// part of the stream can be summed anywhere and added up.
+
+__device__ __forceinline__ int blk_image(const PDesc* __restrict__ desc, int n, int g) {
+  int lo = 0, hi = n;  // largest k with blk_base <= g
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (desc[mid].blk_base <= g) lo = mid; else hi = mid;
+  }
+  return lo;
+}
 
 constexpr uint32_t kAdlerMod = 65521;
-constexpr int kAdlerThreads = 1024;
+constexpr int kAdlerThreads = 256;
 
-__global__ void __launch_bounds__(kAdlerThreads)
-    k_png_adler(const uint8_t* __restrict__ payload, const PDesc* __restrict__ desc, int n,
-                const PUnit* __restrict__ units, const uint8_t* __restrict__ R,
-                int32_t* __restrict__ img_status) {
-  __shared__ uint64_t red[2][kAdlerThreads / 32];
-  const int k = blockIdx.x;
-  const PDesc& d = desc[k];
-  if (d.n_units == 0 || img_status[k] != kImgOk) return;
+__device__ __forceinline__ bool adler_trailer(const PDesc& d, const PUnit* units, int64_t* at) {
   const int64_t fin = units[d.unit_base].final_end;
-  const int64_t at = (fin + 7) >> 3;  // trailer bytes, big-endian
-  if (at + 4 > (d.in_bits >> 3)) return;
+  *at = (fin + 7) >> 3;  // trailer bytes, big-endian
+  return *at + 4 <= (d.in_bits >> 3);
+}
+
+// One CTA per unfilter row block (128 scanlines) of an image, warp per row, lanes over
+// 16-byte chunks: sum d_i and sum (n - i) d_i (mod 65521) of the block's inflated bytes
+// (filter bytes included, i their index in the stream), added into the image's sums.
+__global__ void __launch_bounds__(kAdlerThreads)
+    k_png_adler_rows(const PDesc* __restrict__ desc, int n, const PUnit* __restrict__ units,
+                     const uint8_t* __restrict__ R, const int32_t* __restrict__ img_status,
+                     unsigned long long* __restrict__ acc, int n_blocks) {
+  __shared__ unsigned long long red[2][kAdlerThreads / 32];
+  const int g = blockIdx.x;
+  if (g >= n_blocks) return;
+  const int k = blk_image(desc, n, g);
+  const PDesc& d = desc[k];
+  int64_t at;
+  if (d.n_units == 0 || img_status[k] != kImgOk || !adler_trailer(d, units, &at)) return;
   const int64_t len = d.raw_len;
   const int64_t rowbytes = static_cast<int64_t>(d.width) * d.bpp, stride = rowbytes + 1;
   const int H = d.height;
-  // thread t: rows [y0, y1), the raw range [y0 * stride, y1 * stride)
-  const int per = (H + blockDim.x - 1) / blockDim.x;
-  const int y0 = min(H, per * static_cast<int>(threadIdx.x)), y1 = min(H, y0 + per);
-  const int64_t E = static_cast<int64_t>(y1) * stride;
+  const int y0 = (g - d.blk_base) * kUnfilterRows, y1 = min(H, y0 + kUnfilterRows);
   const uint8_t* fb = R + d.r_off;
   const uint8_t* rows = fb + r_filter_bytes(H);
-  uint64_t a = 0, b = 0;  // a: sum d_i; b: sum (E - i) d_i (mod, per row)
-  for (int y = y0; y < y1; ++y) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint64_t a = 0, b = 0;
+  for (int y = y0 + warp; y < y1; y += kAdlerThreads / 32) {
     const int64_t i0 = static_cast<int64_t>(y) * stride;
-    uint64_t la = fb[y], lb = static_cast<uint64_t>(E - i0) * fb[y];
+    uint64_t la = 0, lb = 0;
+    if (lane == 0) {
+      la = fb[y];
+      lb = static_cast<uint64_t>(len - i0) * fb[y];
+    }
     const uint8_t* row = rows + static_cast<int64_t>(y) * d.r_stride;
-    for (int64_t x = 0; x < rowbytes; x += 16) {
+    for (int64_t x = 16 * static_cast<int64_t>(lane); x < rowbytes; x += 16 * 32) {
       const uint4 v = *reinterpret_cast<const uint4*>(row + x);
       const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
-      const uint64_t wt0 = static_cast<uint64_t>(E - (i0 + 1 + x));  // weight of byte x
+      const uint64_t wt0 = static_cast<uint64_t>(len - (i0 + 1 + x));  // weight of byte x
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const uint32_t dj = x + j < rowbytes ? (wv[j >> 2] >> (8 * (j & 3))) & 255u : 0u;
@@ -1272,32 +1293,45 @@ __global__ void __launch_bounds__(kAdlerThreads)
         lb += (wt0 - j) * dj;
       }
     }
-    a = (a + la) % kAdlerMod;
-    b = (b + lb % kAdlerMod) % kAdlerMod;
+    a += la;
+    b += lb % kAdlerMod;
   }
-  b = (b + (static_cast<uint64_t>(len - E) % kAdlerMod) * a) % kAdlerMod;
+  a %= kAdlerMod;
+  b %= kAdlerMod;
   for (int o = 16; o > 0; o >>= 1) {
     a += __shfl_down_sync(0xffffffffu, a, o);
     b += __shfl_down_sync(0xffffffffu, b, o);
   }
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (lane == 0) {
     red[0][warp] = a;
     red[1][warp] = b;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    uint64_t A = 1, B = static_cast<uint64_t>(len) % kAdlerMod;
-    for (int w = 0; w < (blockDim.x >> 5); ++w) {
+    uint64_t A = 0, B = 0;
+    for (int w = 0; w < kAdlerThreads / 32; ++w) {
       A += red[0][w];
       B += red[1][w];
     }
-    A %= kAdlerMod;
-    B %= kAdlerMod;
-    const uint8_t* z = payload + d.in_off + at;
-    const uint32_t want = (uint32_t(z[0]) << 24) | (uint32_t(z[1]) << 16) | (uint32_t(z[2]) << 8) | z[3];
-    if (((B << 16) | A) != want) atomicOr(img_status + k, kImgAdler);
+    atomicAdd(acc + 2 * k, A % kAdlerMod);
+    atomicAdd(acc + 2 * k + 1, B % kAdlerMod);
   }
+}
+
+__global__ void k_png_adler_check(const uint8_t* __restrict__ payload, const PDesc* __restrict__ desc,
+                                  int n, const PUnit* __restrict__ units,
+                                  const unsigned long long* __restrict__ acc,
+                                  int32_t* __restrict__ img_status) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const PDesc& d = desc[k];
+  int64_t at;
+  if (d.n_units == 0 || img_status[k] != kImgOk || !adler_trailer(d, units, &at)) return;
+  const uint64_t A = (1 + acc[2 * k]) % kAdlerMod;
+  const uint64_t B = (static_cast<uint64_t>(d.raw_len) % kAdlerMod + acc[2 * k + 1]) % kAdlerMod;
+  const uint8_t* z = payload + d.in_off + at;
+  const uint32_t want = (uint32_t(z[0]) << 24) | (uint32_t(z[1]) << 16) | (uint32_t(z[2]) << 8) | z[3];
+  if (((B << 16) | A) != want) atomicOr(img_status + k, kImgAdler);
 }
 
 // ---------------------------------------------------------------------------
@@ -1335,14 +1369,6 @@ __device__ __forceinline__ uint32_t pack4(const uint32_t* b) {
   return b[0] | (b[1] << 8) | (b[2] << 16) | (b[3] << 24);
 }
 
-__device__ __forceinline__ int blk_image(const PDesc* __restrict__ desc, int n, int g) {
-  int lo = 0, hi = n;  // largest k with blk_base <= g
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (desc[mid].blk_base <= g) lo = mid; else hi = mid;
-  }
-  return lo;
-}
 
 // One row block (kUnfilterRows consecutive scanlines of one image) per work item, thread
 // = scanline: at step t thread y reconstructs chunk t - y of its row, whose prior-row bytes
@@ -1565,7 +1591,13 @@ extern "C" TP_API int tp_png_decode(const uint8_t* d_payload, const void* d_desc
     if (totals[10] > 0)
       k_png_final<<<static_cast<int>(totals[10]), 256, 0, s>>>(desc, n, T, R, d_status);
     k_png_window<<<n, 1024, 0, s>>>(desc, n, units, T, M, R, d_status);
-    k_png_adler<<<n, kAdlerThreads, 0, s>>>(d_payload, desc, n, units, R, d_status);
+    if (totals[12] > 0) {
+      unsigned long long* acc = reinterpret_cast<unsigned long long*>(work + totals[14]);
+      cudaMemsetAsync(acc, 0, sizeof(unsigned long long) * 2 * n, s);
+      k_png_adler_rows<<<static_cast<int>(totals[12]), kAdlerThreads, 0, s>>>(
+          desc, n, units, R, d_status, acc, static_cast<int>(totals[12]));
+      k_png_adler_check<<<(n + 255) / 256, 256, 0, s>>>(d_payload, desc, n, units, acc, d_status);
+    }
     const int n_items = static_cast<int>(totals[12]);
     if (n_items > 0) {
       int* progress = reinterpret_cast<int*>(work + totals[13]);

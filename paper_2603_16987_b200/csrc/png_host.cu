@@ -270,7 +270,8 @@ TP_API int64_t tp_png_describe(const TpPngInfo* infos, int32_t n, const int64_t*
   const int64_t m_at = al(r_at + rbytes);
   const int64_t stage_at = al(m_at + raw * 4);
   const int64_t prog_at = al(stage_at + units * tp::png::kStageBytesPerUnit);
-  const int64_t end = al(prog_at + (blks + 1) * 4);
+  const int64_t adler_at = al(prog_at + (blks + 1) * 4);
+  const int64_t end = al(adler_at + static_cast<int64_t>(n) * 16);
   for (int i = 0; i < tp::png::kTotals; ++i) totals[i] = 0;
   totals[0] = units;
   totals[1] = toks;
@@ -286,6 +287,7 @@ TP_API int64_t tp_png_describe(const TpPngInfo* infos, int32_t n, const int64_t*
   totals[11] = stage_at;
   totals[12] = blks;
   totals[13] = prog_at;
+  totals[14] = adler_at;
   return end;
 }
 
