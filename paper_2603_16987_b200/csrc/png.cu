@@ -223,7 +223,7 @@ __device__ bool read_dynamic_lengths(Bits& br, uint8_t* lens, uint8_t* tab, int&
 //   direct   bit 15 = 0, bits 14..11 total code length, bits 8..0 symbol
 //   pointer  bit 15 = 1, bits 14..12 subtable index bits, bits 11..0 subtable offset
 //   invalid  0xFFFF
-__device__ bool build_lit(const uint8_t* lens, int n, uint16_t* tbl) {
+__device__ bool build_lit(const uint8_t* lens, int n, uint16_t* tbl, uint16_t* sorted) {
   int count[16];
   if (!kraft_ok(lens, n, 15, count)) return false;
   int next[16];
@@ -249,8 +249,19 @@ __device__ bool build_lit(const uint8_t* lens, int n, uint16_t* tbl) {
     for (uint32_t i = r; i < (1u << kLitRoot); i += 1u << l) tbl[i] = e;
   }
   if (!nlong) return true;
-  // long codes in canonical order (length, then symbol) have non-decreasing 9-bit
-  // prefixes, so codes sharing a prefix are consecutive and the last is the longest
+  // the long codes in canonical order (length, then symbol), by one counting-sort pass
+  // instead of a scan of every symbol per length
+  int loff[16];
+  for (int l = 0, o = 0; l <= 15; ++l) {
+    loff[l] = o;
+    if (l > kLitRoot) o += count[l];
+  }
+  for (int s = 0; s < n; ++s) {
+    const int l = lens[s];
+    if (l > kLitRoot) sorted[loff[l]++] = static_cast<uint16_t>(s);
+  }
+  // their 10-bit prefixes are non-decreasing, so codes sharing a prefix are consecutive
+  // and the last of a group is its longest
   int off = 1 << kLitRoot;
   int cur = -1, cur_max = 0;
   auto close_group = [&](int prefix, int maxl) -> bool {
@@ -263,11 +274,14 @@ __device__ bool build_lit(const uint8_t* lens, int n, uint16_t* tbl) {
     off += 1 << bits;
     return true;
   };
-  for (int l = kLitRoot + 1; l <= 15; ++l) {
-    if (!count[l]) continue;
-    int c = next[l];
-    for (int s = 0; s < n; ++s) {
-      if (lens[s] != l) continue;
+  {
+    int l = kLitRoot + 1, c = next[l], left_in_l = count[l];
+    for (int k = 0; k < nlong; ++k) {
+      while (left_in_l == 0) {
+        ++l;
+        c = next[l];
+        left_in_l = count[l];
+      }
       const int prefix = c >> (l - kLitRoot);
       if (prefix != cur) {
         if (cur >= 0 && !close_group(cur, cur_max)) return false;
@@ -275,13 +289,19 @@ __device__ bool build_lit(const uint8_t* lens, int n, uint16_t* tbl) {
       }
       cur_max = l;
       ++c;
+      --left_in_l;
     }
   }
   if (!close_group(cur, cur_max)) return false;
-  for (int l = kLitRoot + 1; l <= 15; ++l) {
-    if (!count[l]) continue;
-    for (int s = 0; s < n; ++s) {
-      if (lens[s] != l) continue;
+  {
+    int l = kLitRoot + 1, left_in_l = count[l];
+    for (int k = 0; k < nlong; ++k) {
+      while (left_in_l == 0) {
+        ++l;
+        left_in_l = count[l];
+      }
+      --left_in_l;
+      const int s = sorted[k];
       const int c = snext[l]++;
       const int prefix = c >> (l - kLitRoot);
       const uint16_t p = tbl[rev_bits(static_cast<uint32_t>(prefix), kLitRoot)];
@@ -778,6 +798,7 @@ struct __align__(16) WarpTables {
   uint8_t dist[kDistBytes];
   uint8_t lens[320];   // code lengths of the block being set up
   uint8_t pre[128];    // code-length code
+  uint16_t sorted[288];  // long literal/length codes in canonical order (build_lit)
 };
 
 __global__ void __launch_bounds__(32 * kInflateWarps)
@@ -874,11 +895,11 @@ __global__ void __launch_bounds__(32 * kInflateWarps)
           for (int i = 256; i < 280; ++i) wt.lens[i] = 7;
           for (int i = 280; i < 288; ++i) wt.lens[i] = 8;
           for (int i = 0; i < 32; ++i) wt.lens[288 + i] = 5;
-          ok = build_lit(wt.lens, 288, wt.lit) && build_dist(wt.lens + 288, 32, wt.dist);
+          ok = build_lit(wt.lens, 288, wt.lit, wt.sorted) && build_dist(wt.lens + 288, 32, wt.dist);
         } else {
           int hlit, hdist;
           ok = read_dynamic_lengths(br, wt.lens, wt.pre, hlit, hdist, in_bits) &&
-               build_lit(wt.lens, hlit, wt.lit) && build_dist(wt.lens + hlit, hdist, wt.dist);
+               build_lit(wt.lens, hlit, wt.lit, wt.sorted) && build_dist(wt.lens + hlit, hdist, wt.dist);
         }
         if (!ok) {
           action = 3;
