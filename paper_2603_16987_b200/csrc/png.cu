@@ -522,6 +522,9 @@ __device__ __forceinline__ uint32_t win32(uint32_t w0, uint32_t w1, uint32_t w2,
 // boundary (LEN == ~NLEN).  Any true block start will do; the warp takes the first
 // success of its first successful batch.
 constexpr int kFindQueue = 32;
+#ifndef TP_PNG_QFLUSH  // queued candidates that trigger a batch of full checks
+#define TP_PNG_QFLUSH 16
+#endif
 
 // Each unit is scanned by kFindParts warps, one per quarter: a unit's start is the first
 // header found in its lowest quarter that has one (k_png_find_select).  A warp stops early
@@ -673,7 +676,7 @@ __global__ void __launch_bounds__(kFindThreads)
         const int slot = qn + __popc(mh & ((1u << lane) - 1u));
         if (has && slot < kFindQueue) q[slot] = mine[c];
         qn = min(kFindQueue, qn + __popc(mh));
-        if (qn == kFindQueue && flush()) break;
+        if (qn >= TP_PNG_QFLUSH && flush()) break;
       }
       if (start >= 0) break;
     }
