@@ -1363,6 +1363,9 @@ __global__ void k_png_adler_check(const uint8_t* __restrict__ payload, const PDe
 
 
 
+#ifndef TP_PNG_UNFILTER_SPLIT  // 1: one code path per filter type; 0: all predictors, selected
+#define TP_PNG_UNFILTER_SPLIT 1
+#endif
 // chunk of one scanline per wavefront step: NW 32-bit words (TP_PNG_CHUNK bytes)
 #ifndef TP_PNG_CHUNK
 #define TP_PNG_CHUNK 16
@@ -1461,7 +1464,62 @@ __device__ void unfilter_block(const PDesc& d, int blk, uint8_t* __restrict__ r,
         up = xch[(t - 1) & 1][tid - 1];
       }
       const int64_t x0 = kCh * static_cast<int64_t>(i);
+      // one path per filter type (TP_PNG_UNFILTER_SPLIT): a warp runs the paths of the
+      // types its 32 rows use -- photo-like PNGs mix mostly Sub and Up, whose paths are a
+      // few operations per byte (Up: four byte-wise adds per chunk) -- instead of every
+      // predictor for every byte
       uint32_t rb[kCh];
+      Chunk rec;
+#if TP_PNG_UNFILTER_SPLIT
+      auto prev_a = [&](int j) -> uint32_t {  // recon[x - bpp] for j < BPP
+        return x0 ? byte_at(rec_prev, kCh + j - BPP) : 0u;
+      };
+      auto prev_c = [&](int j) -> uint32_t {
+        return x0 ? byte_at(up_prev, kCh + j - BPP) : 0u;
+      };
+      if (ft == 2) {
+        uint32_t rw[kChunkWords];
+#pragma unroll
+        for (int q = 0; q < kChunkWords; ++q) rw[q] = __vadd4(CV::w(f, q), CV::w(up, q));
+        rec = CV::make(rw);
+#pragma unroll
+        for (int j = 0; j < kCh; ++j) rb[j] = byte_at(rec, j);
+      } else {
+        if (ft == 1) {
+#pragma unroll
+          for (int j = 0; j < kCh; ++j)
+            rb[j] = (byte_at(f, j) + (j >= BPP ? rb[j - BPP] : prev_a(j))) & 255u;
+        } else if (ft == 3) {
+#pragma unroll
+          for (int j = 0; j < kCh; ++j) {
+            const uint32_t a = j >= BPP ? rb[j - BPP] : prev_a(j);
+            rb[j] = (byte_at(f, j) + ((a + byte_at(up, j)) >> 1)) & 255u;
+          }
+        } else if (ft == 4) {
+#pragma unroll
+          for (int j = 0; j < kCh; ++j) {
+            const uint32_t a = j >= BPP ? rb[j - BPP] : prev_a(j);
+            const uint32_t c = j >= BPP ? byte_at(up, j - BPP) : prev_c(j);
+            const uint32_t b = byte_at(up, j);
+            const int pp = static_cast<int>(a + b) - static_cast<int>(c);
+            const int pa = abs(pp - static_cast<int>(a)), pb = abs(pp - static_cast<int>(b)),
+                      pc = abs(pp - static_cast<int>(c));
+            rb[j] = (byte_at(f, j) + ((pa <= pb && pa <= pc) ? a : (pb <= pc ? b : c))) & 255u;
+          }
+        } else {  // None (and > 4, flagged above: any bytes will do)
+#pragma unroll
+          for (int j = 0; j < kCh; ++j) rb[j] = byte_at(f, j);
+        }
+        uint32_t rw[kChunkWords];
+#pragma unroll
+        for (int q = 0; q < kChunkWords; ++q) rw[q] = pack4(rb + 4 * q);
+        rec = CV::make(rw);
+      }
+      (void)m1;
+      (void)m2;
+      (void)m3;
+      (void)m4;
+#else
 #pragma unroll
       for (int j = 0; j < kCh; ++j) {
         uint32_t a, c;
@@ -1481,10 +1539,13 @@ __device__ void unfilter_block(const PDesc& d, int blk, uint8_t* __restrict__ r,
         const uint32_t pred = (a & m1) | (b & m2) | (((a + b) >> 1) & m3) | (pae & m4);
         rb[j] = (byte_at(f, j) + pred) & 255u;
       }
-      uint32_t rw[kChunkWords];
+      {
+        uint32_t rw[kChunkWords];
 #pragma unroll
-      for (int q = 0; q < kChunkWords; ++q) rw[q] = pack4(rb + 4 * q);
-      const Chunk rec = CV::make(rw);
+        for (int q = 0; q < kChunkWords; ++q) rw[q] = pack4(rb + 4 * q);
+        rec = CV::make(rw);
+      }
+#endif
       const int nb = static_cast<int>(rowbytes - x0 < kCh ? rowbytes - x0 : kCh);
       if (BPP == 3) {
         uint8_t* dst = orow + x0;
