@@ -1029,12 +1029,17 @@ __global__ void __launch_bounds__(32 * kInflateWarps)
 // chain: one warp per image (lane 0 walks; the units are few)
 
 __global__ void k_png_chain(const PDesc* __restrict__ desc, int n, PUnit* __restrict__ units,
-                            int32_t* __restrict__ img_status, int last_round) {
+                            int32_t* __restrict__ img_status, int round) {
   const int k = blockIdx.x;
   if (k >= n || threadIdx.x != 0) return;
   const PDesc& d = desc[k];
   if (d.n_units == 0 || img_status[k] != kImgOk) return;
+  const bool last_round = round == kRounds - 1;
   const int u0 = d.unit_base, u1 = d.unit_base + d.n_units;
+  // after round 0, only images whose walk stopped at a re-decoded unit walk again (the
+  // first unit's pad2_ carries that mark from round to round)
+  if (round > 0 && units[u0].pad2_ == 0) return;
+  units[u0].pad2_ = 0;
   int64_t off = 0;
   int u = u0;  // unit 0 always starts at a real block
   // the start found for unit v is not a block start: the decode of u passed it
@@ -1042,11 +1047,13 @@ __global__ void k_png_chain(const PDesc* __restrict__ desc, int n, PUnit* __rest
     units[v].start = -1;
     units[v].dirty = 0;
     cu.dirty = 1;  // decode u again, up to the next start
+    units[u0].pad2_ = 1;
     if (last_round) img_status[k] = kImgChain;
   };
   while (true) {
     PUnit& cu = units[u];
     if (cu.dirty) {  // re-decoded next round
+      units[u0].pad2_ = 1;
       if (last_round) img_status[k] = kImgChain;
       return;
     }
@@ -1669,7 +1676,7 @@ extern "C" TP_API int tp_png_decode(const uint8_t* d_payload, const void* d_desc
     for (int r = 0; r < kRounds; ++r) {
       k_png_inflate<<<(U + kInflateWarps - 1) / kInflateWarps, 32 * kInflateWarps, 0, s>>>(
           d_payload, desc, n, units, U, toks, stage, d_status);
-      k_png_chain<<<n, 32, 0, s>>>(desc, n, units, d_status, r == kRounds - 1);
+      k_png_chain<<<n, 32, 0, s>>>(desc, n, units, d_status, r);
     }
     uint32_t* M = reinterpret_cast<uint32_t*>(work + totals[9]);
     k_png_expand<<<(U + 7) / 8, 256, 0, s>>>(d_payload, desc, n, units, U, toks, T, M, d_status);
