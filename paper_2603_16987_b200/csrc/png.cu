@@ -549,13 +549,18 @@ __global__ void k_png_find_init(uint32_t* stage, int U) {
   f->lowest = kFindParts;
 }
 
-__global__ void k_png_find_select(PUnit* __restrict__ units, uint32_t* stage, int U, int parts) {
+__global__ void k_png_find_select(PUnit* __restrict__ units, uint32_t* stage, int U, int parts,
+                                  int debug) {
   const int u = blockIdx.x * blockDim.x + threadIdx.x;
   if (u >= U) return;
   const FindScratch* f = find_scratch(stage, u);
   long long v = -1;
   for (int p = 0; p < parts && v < 0; ++p) v = f->pos[p];
-  const int64_t start = v < 0 ? -1 : (v & ((1ll << 62) - 1));
+  int64_t start = v < 0 ? -1 : (v & ((1ll << 62) - 1));
+  // test hook (tests/test_gpu_png.py): every third found start moved one bit on, a false
+  // header the chain check must catch -- the preceding unit's decode passes it, the start
+  // is dropped and that unit decodes again in the next round
+  if ((debug & 1) && start > 16 && u % 3 == 1 && (v >> 62) == 0) start += 1;
   PUnit& o = units[u];
   o.start = start;
   o.end = -1;
@@ -1036,61 +1041,86 @@ __global__ void k_png_chain(const PDesc* __restrict__ desc, int n, PUnit* __rest
   if (d.n_units == 0 || img_status[k] != kImgOk) return;
   const bool last_round = round == kRounds - 1;
   const int u0 = d.unit_base, u1 = d.unit_base + d.n_units;
-  // after round 0, only images whose walk stopped at a re-decoded unit walk again (the
-  // first unit's pad2_ carries that mark from round to round)
+  // after round 0, only images with re-decoded units walk again (the first unit's pad2_
+  // carries that mark from round to round)
   if (round > 0 && units[u0].pad2_ == 0) return;
   units[u0].pad2_ = 0;
-  int64_t off = 0;
-  int u = u0;  // unit 0 always starts at a real block
-  // the start found for unit v is not a block start: the decode of u passed it
-  auto drop_successor = [&](PUnit& cu, int v) {
-    units[v].start = -1;
-    units[v].dirty = 0;
-    cu.dirty = 1;  // decode u again, up to the next start
-    units[u0].pad2_ = 1;
-    if (last_round) img_status[k] = kImgChain;
-  };
-  while (true) {
-    PUnit& cu = units[u];
-    if (cu.dirty) {  // re-decoded next round
-      units[u0].pad2_ = 1;
-      if (last_round) img_status[k] = kImgChain;
-      return;
-    }
+  auto next_valid = [&](int u) {
     int v = u + 1;
     while (v < u1 && units[v].start < 0) ++v;
-    const bool has_v = v < u1;
-    if (cu.status == kUnitTokens && has_v && cu.end > units[v].start) {
-      drop_successor(cu, v);
-      return;
+    return v;
+  };
+  // pass 1: every unit must end where the next start is.  A start the preceding unit's
+  // decode passed is not a block start (a finder false positive): it is dropped and the
+  // preceding unit decodes again next round.  The walk goes on past such a pair, taking
+  // the next start as true until shown otherwise, so all the false starts of an image are
+  // dropped in one round and their re-decodes run in parallel.  (Taking a false start
+  // for true can at worst drop a true start after it: a longer unit, not a wrong one.)
+  bool redo = false;
+  bool validated = true;  // u's start is where its predecessor's decode ended (or bit 16)
+  for (int u = u0; u < u1;) {
+    PUnit& cu = units[u];
+    const int v = next_valid(u);
+    if (cu.dirty) {  // its end is not known yet: the next start cannot be judged now
+      redo = true;
+      validated = false;
+      u = v;
+      continue;
     }
+    if (cu.status != kUnitOk && !(cu.status == kUnitTokens && v < u1 && cu.end > units[v].start)) {
+      if (validated) {  // a true block start that does not decode: a corrupt stream
+        img_status[k] = kImgInflate;
+        return;
+      }
+      redo = true;  // possibly a false start: judged once its predecessor is settled
+      validated = false;
+      u = v;
+      continue;
+    }
+    if (v >= u1) break;
+    if (cu.final_ && cu.status == kUnitOk) {  // a header past the end of the final block
+      units[v].start = -1;
+      units[v].dirty = 0;
+      continue;  // the same unit against its next successor
+    }
+    if (cu.end != units[v].start) {  // (or a token overflow past the next start)
+      units[v].start = -1;
+      units[v].dirty = 0;
+      cu.dirty = 1;
+      redo = true;
+      validated = false;
+      u = next_valid(v);
+      continue;
+    }
+    validated = true;
+    u = v;
+  }
+  if (redo) {
+    units[u0].pad2_ = 1;
+    if (last_round) img_status[k] = kImgChain;
+    return;
+  }
+  // pass 2: the chain is whole; inflated offsets, the final block, the length
+  int64_t off = 0;
+  int u = u0;  // unit 0 always starts at a real block
+  while (true) {
+    PUnit& cu = units[u];
     if (cu.status != kUnitOk) {
       img_status[k] = kImgInflate;
       return;
     }
-    if (!has_v) {
+    cu.out_off = off;
+    off += cu.out_len;
+    const int v = next_valid(u);
+    if (v >= u1) {
       if (!cu.final_) {
         img_status[k] = kImgNotFinal;
         return;
       }
-      cu.out_off = off;
-      off += cu.out_len;
       units[u0].final_end = cu.end;
       break;
     }
-    if (cu.final_) {  // a header was found past the end of the final block
-      units[v].start = -1;
-      units[v].dirty = 0;
-      continue;  // look for u's next successor
-    }
-    if (cu.end == units[v].start) {
-      cu.out_off = off;
-      off += cu.out_len;
-      u = v;
-      continue;
-    }
-    drop_successor(cu, v);
-    return;
+    u = v;
   }
   if (off != d.raw_len) img_status[k] = kImgLength;
 }
@@ -1672,7 +1702,8 @@ extern "C" TP_API int tp_png_decode(const uint8_t* d_payload, const void* d_desc
     const int64_t find_warps = static_cast<int64_t>(U) * parts;
     k_png_find<<<static_cast<int>((find_warps + kFindThreads / 32 - 1) / (kFindThreads / 32)),
                  kFindThreads, 0, s>>>(d_payload, desc, n, units, U, stage, parts);
-    k_png_find_select<<<(U + 255) / 256, 256, 0, s>>>(units, stage, U, parts);
+    k_png_find_select<<<(U + 255) / 256, 256, 0, s>>>(units, stage, U, parts,
+                                                      static_cast<int>(totals[15]));
     for (int r = 0; r < kRounds; ++r) {
       k_png_inflate<<<(U + kInflateWarps - 1) / kInflateWarps, 32 * kInflateWarps, 0, s>>>(
           d_payload, desc, n, units, U, toks, stage, d_status);

@@ -97,7 +97,8 @@ constexpr int kUnfilterRows = 128;
 // the index of its first byte, raw_off + out_off), [10] rows in the batch, [11] byte
 // offset of the inflate warps' token staging (kStageBytesPerUnit per unit), [12] unfilter
 // row blocks in the batch, [13] byte offset of their progress counters (int32 each, plus
-// one claim counter), [14] byte offset of the Adler-32 sums (2 x u64 per image)
+// one claim counter), [14] byte offset of the Adler-32 sums (2 x u64 per image), [15]
+// test hooks set by the caller (bit 0: false finder starts, see k_png_find_select)
 constexpr int kTotals = 16;
 #ifndef TP_PNG_SUB
 #define TP_PNG_SUB 512

@@ -71,6 +71,7 @@ class PngDecoder:
     def __init__(self, device=None, depth: int = 2, max_work_bytes: int = 8 << 30):
         self.device = require_device(device)
         self.max_work_bytes = int(max_work_bytes)
+        self._debug_flags = 0  # tests only: bit 0 plants false finder starts
         self.lib = _lib.load()
         self.desc_bytes = int(self.lib.tp_png_desc_bytes())
         self.slots = [_Slot() for _ in range(max(1, depth))]
@@ -145,6 +146,7 @@ class PngDecoder:
             ctypes.cast(desc_host, ctypes.c_void_p), totals.ctypes.data))
         if work_bytes < 0:
             _lib.check(-work_bytes, "tp_png_describe")
+        totals[15] = self._debug_flags  # test hooks (csrc/png_common.cuh)
         self._buffers(sl, payload_bytes, max(work_bytes, 4096), n)
         ctypes.memmove(sl.host.data_ptr(), desc_host, n * self.desc_bytes)
         dev_idx = np.nonzero(ok)[0]

@@ -161,3 +161,24 @@ def test_png_fuzzed_payloads_match_reference():
         else:
             assert got_exc is None, (t, kind, got_exc)
             assert np.array_equal(got, ref), (t, kind)
+
+
+def test_png_false_finder_starts_are_dropped():
+    """Every third unit start moved one bit on (a planted finder false positive): the
+    chain check drops them all in one walk, the preceding units decode again, and the
+    images still decode on the device, bit-exact."""
+    import torch
+
+    from paper_2603_16987_b200.png import PngDecoder
+    from png_cases import content, pil_png
+
+    payloads = [pil_png(content("scene", 1280, 720, 21)), pil_png(content("scene", 640, 480, 22)),
+                pil_png(content("noise", 700, 500, 23))]
+    dec = PngDecoder(torch.device("cuda:0"))
+    dec._debug_flags = 1
+    pk = dec.decode(payloads)
+    assert dec.last_fallback == []
+    host = pk.data.cpu().numpy()
+    for k, (o, (w, h)) in enumerate(zip(pk.offsets_host, pk.wh_host)):
+        got = host[int(o): int(o) + int(w) * int(h) * 3].reshape(int(h), int(w), 3)
+        assert np.array_equal(got, _host(payloads[k])), k
