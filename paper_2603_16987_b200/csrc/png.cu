@@ -608,10 +608,9 @@ __global__ void __launch_bounds__(kFindThreads)
     const int64_t lo = static_cast<int64_t>(local) * kUnitBits + part * part_bits;
     const int64_t hi = min(lo + part_bits, d.in_bits - 3);
     int qn = 0;  // queued candidates (warp-uniform)
-    int nsteps = 0, nflush = 0;  // diagnostics (PUnit::pad_ of the finder)
+    int nsteps = 0;  // steps of this warp (the early-exit check runs every fourth)
     // run the queued full checks, one per lane; the first success is the start
     auto flush = [&]() -> bool {
-      ++nflush;
       __syncwarp();
       const bool ok = lane < qn && dynamic_full(w, q[lane], d.in_bits, tab);
       const unsigned m = __ballot_sync(0xffffffffu, ok);
@@ -686,7 +685,6 @@ __global__ void __launch_bounds__(kFindThreads)
       if (start >= 0) break;
     }
     if (start < 0 && qn > 0) flush();
-    (void)nflush;
   }
   if (lane == 0 && start >= 0) {
     fs->pos[part] = start | (stored ? (1ll << 62) : 0);
@@ -842,7 +840,7 @@ __global__ void __launch_bounds__(32 * kInflateWarps)
   int status = kUnitOk, fin = 0;
   bool stored_start = me.stored != 0;
   const unsigned below = (1u << lane) - 1u;
-  int nfix = 0, nround = 0;  // diagnostics (PUnit::pad_)
+  int nfix = 0, nround = 0;  // diagnostics (PUnit::fixups / rounds)
   uint32_t* warp_stage = stage + static_cast<int64_t>(u) * 32 * kStageTokens;
   uint32_t* my_stage = warp_stage + lane * kStageTokens;
   while (true) {
@@ -1025,8 +1023,8 @@ __global__ void __launch_bounds__(32 * kInflateWarps)
     me.status = status;
     me.final_ = fin;
     me.dirty = 0;
-    me.pad_[0] = nfix;
-    me.pad_[1] = nround;
+    me.fixups = nfix;
+    me.rounds = nround;
   }
 }
 
@@ -1041,10 +1039,10 @@ __global__ void k_png_chain(const PDesc* __restrict__ desc, int n, PUnit* __rest
   if (d.n_units == 0 || img_status[k] != kImgOk) return;
   const bool last_round = round == kRounds - 1;
   const int u0 = d.unit_base, u1 = d.unit_base + d.n_units;
-  // after round 0, only images with re-decoded units walk again (the first unit's pad2_
+  // after round 0, only images with re-decoded units walk again (the first unit's `redo`
   // carries that mark from round to round)
-  if (round > 0 && units[u0].pad2_ == 0) return;
-  units[u0].pad2_ = 0;
+  if (round > 0 && units[u0].redo == 0) return;
+  units[u0].redo = 0;
   auto next_valid = [&](int u) {
     int v = u + 1;
     while (v < u1 && units[v].start < 0) ++v;
@@ -1096,7 +1094,7 @@ __global__ void k_png_chain(const PDesc* __restrict__ desc, int n, PUnit* __rest
     u = v;
   }
   if (redo) {
-    units[u0].pad2_ = 1;
+    units[u0].redo = 1;
     if (last_round) img_status[k] = kImgChain;
     return;
   }

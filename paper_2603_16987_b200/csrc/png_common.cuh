@@ -83,9 +83,10 @@ struct __align__(16) PUnit {
   int32_t dirty;    // (re)decode in the next inflate round
   int32_t stored;   // start is the LEN field of a stored block (its header not read)
   int32_t nmark;    // bytes of this unit that are window markers (listed by expand)
-  int32_t pad_[2];
+  int32_t fixups;   // diagnostics: lane re-decodes in the inflate's rounds
+  int32_t rounds;   // diagnostics: inflate rounds
   int64_t final_end;  // (an image's first unit) bit after the final block, by the chain
-  int64_t pad2_;
+  int64_t redo;       // (an image's first unit) the chain dropped a start this round
 };
 
 // Unfilter work item: a block of consecutive scanlines of one image, one thread each.

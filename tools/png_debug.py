@@ -51,7 +51,4 @@ def unit_stats(payload):
     return {"units": U, "valid": int(valid.sum()), "max_ntok": int(i32[:, 0].max()),
             "max_out": int(rec[:, 2].max()), "mean_out": float(rec[valid, 2].mean()),
             "stored_starts": int(i32[:, 4].sum()), "max_invalid_run": max(len(r) for r in runs),
-            "fixups": int(i32[:, 6].sum()), "rounds": int(i32[:, 7].sum()),
-            "find_steps_mean": float((rec[:, 9] & 0xFFFFFFFF).mean()),
-            "find_steps_max": int((rec[:, 9] & 0xFFFFFFFF).max()),
-            "find_flush_mean": float((rec[:, 9] >> 32).mean()), "find_flush_max": int((rec[:, 9] >> 32).max())}
+            "fixups": int(i32[:, 5].sum()), "rounds": int(i32[:, 6].sum())}
