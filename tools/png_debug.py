@@ -51,4 +51,5 @@ def unit_stats(payload):
     return {"units": U, "valid": int(valid.sum()), "max_ntok": int(i32[:, 0].max()),
             "max_out": int(rec[:, 2].max()), "mean_out": float(rec[valid, 2].mean()),
             "stored_starts": int(i32[:, 4].sum()), "max_invalid_run": max(len(r) for r in runs),
-            "fixups": int(i32[:, 5].sum()), "rounds": int(i32[:, 6].sum())}
+            "fixups": int(i32[:, 6].sum()), "rounds": int(i32[:, 7].sum()),
+            "markers": int(i32[:, 5].sum())}
