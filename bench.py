@@ -724,13 +724,18 @@ def run_e2e_coded(args, dist, device, cfg, fmt: str = "jpeg") -> dict:
         payloads = jpeg_payloads(args.batch, seed=20260817 + 97 * dist.rank)
         dec = JpegDecoder(device, depth=2)
     prep = TilePreprocessor(cfg, device)
-    stream = torch.cuda.Stream(device)
+    # one stream per buffer set: batch i+1's decode runs beside batch i's on the GPU (the
+    # decode kernels are latency-bound chains that leave SMs idle); the uploads share the
+    # decoder's copy stream
+    streams = [torch.cuda.Stream(device), torch.cuda.Stream(device)]
+    stream = streams[0]
     outs, pend = [None, None], [None, None]
     plan_host = [None, None]
     refits = [0]
 
     def step(i):
         k = i % 2
+        stream = streams[k]
         if pend[k] is not None:  # the batch that used these buffers two steps ago
             b, o = pend[k]
             if b.finish():  # host-decoded images patched in: tile that batch again
@@ -759,6 +764,7 @@ def run_e2e_coded(args, dist, device, cfg, fmt: str = "jpeg") -> dict:
     torch.cuda.synchronize(device)
     wall = dist.max(time.perf_counter() - t0, device)
     # the decode kernels alone on the last batch (CUDA events around relaunches)
+    stream = streams[(steps - 1) % 2]
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record(stream)
     for _ in range(5):
