@@ -27,6 +27,8 @@
 // Everything the decode does not take cleanly sets d_status[k]: the host decodes that
 // image with Pillow, so pixels (or the error) are the reference's.
 
+#include <cstdlib>
+
 #include "png_common.cuh"
 #include "tp_common.cuh"
 
@@ -571,6 +573,10 @@ __global__ void k_png_find_select(PUnit* __restrict__ units, uint32_t* stage, in
   o.final_ = 0;
   o.dirty = start >= 0;
   o.stored = v >= 0 && (v >> 62) != 0;
+  o.nmark = 0;  // expand skips units without output: the window pass must see no list
+  o.fixups = 0;
+  o.rounds = 0;
+  o.redo = 0;
 }
 
 __global__ void __launch_bounds__(kFindThreads)
@@ -1272,7 +1278,7 @@ __global__ void k_png_window(const PDesc* __restrict__ desc, int n, const PUnit*
   const uint16_t* t = T + d.raw_off;
   uint8_t* r = R + d.r_off;
   for (int u = d.unit_base; u < d.unit_base + d.n_units; ++u) {
-    const int cnt = units[u].start < 0 ? 0 : units[u].nmark;
+    const int cnt = (units[u].start < 0 || units[u].out_len == 0) ? 0 : units[u].nmark;
     if (!cnt) continue;  // uniform across the CTA
     const int64_t os = units[u].out_off, wb = os - kWindow;
     const uint32_t* list = M + d.raw_off + os;
@@ -1690,6 +1696,19 @@ extern "C" TP_API int tp_png_decode(const uint8_t* d_payload, const void* d_desc
   uint8_t* R = work + totals[6];
   uint32_t* stage = reinterpret_cast<uint32_t*>(work + totals[11]);
   cudaMemsetAsync(d_status, 0, sizeof(int32_t) * n, s);
+  // TP_PNG_DEBUG_SYNC=1: synchronise after every kernel and name the one that failed
+  static const bool debug_sync = std::getenv("TP_PNG_DEBUG_SYNC") != nullptr;
+  auto dbg = [&](const char* what) -> int {
+    if (!debug_sync) return TP_OK;
+    const cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return tp::set_error(TP_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+    return TP_OK;
+  };
+#define TP_PNG_DBG(name) \
+  do {                   \
+    const int rc_ = dbg(name); \
+    if (rc_ != TP_OK) return rc_; \
+  } while (0)
   if (U > 0) {
     // finder warps per unit: split the scans while the units alone leave the GPU short of
     // warps (small batches: latency-bound), one per unit when they fill it (64 1080p
@@ -1697,27 +1716,37 @@ extern "C" TP_API int tp_png_decode(const uint8_t* d_payload, const void* d_desc
     const int sms = std::max(1, tp::device_sm_count());
     const int parts = std::max(1, std::min(kFindParts, (sms * 48) / std::max(U, 1)));
     k_png_find_init<<<(U + 255) / 256, 256, 0, s>>>(stage, U);
+    TP_PNG_DBG("k_png_find_init");
     const int64_t find_warps = static_cast<int64_t>(U) * parts;
     k_png_find<<<static_cast<int>((find_warps + kFindThreads / 32 - 1) / (kFindThreads / 32)),
                  kFindThreads, 0, s>>>(d_payload, desc, n, units, U, stage, parts);
+                 TP_PNG_DBG("k_png_find");
     k_png_find_select<<<(U + 255) / 256, 256, 0, s>>>(units, stage, U, parts,
                                                       static_cast<int>(totals[15]));
+                                                      TP_PNG_DBG("k_png_find_select");
     for (int r = 0; r < kRounds; ++r) {
       k_png_inflate<<<(U + kInflateWarps - 1) / kInflateWarps, 32 * kInflateWarps, 0, s>>>(
           d_payload, desc, n, units, U, toks, stage, d_status);
+          TP_PNG_DBG("k_png_inflate");
       k_png_chain<<<n, 32, 0, s>>>(desc, n, units, d_status, r);
+      TP_PNG_DBG("k_png_chain");
     }
     uint32_t* M = reinterpret_cast<uint32_t*>(work + totals[9]);
     k_png_expand<<<(U + 7) / 8, 256, 0, s>>>(d_payload, desc, n, units, U, toks, T, M, d_status);
+    TP_PNG_DBG("k_png_expand");
     if (totals[10] > 0)
       k_png_final<<<static_cast<int>(totals[10]), 256, 0, s>>>(desc, n, T, R, d_status);
+      TP_PNG_DBG("k_png_final");
     k_png_window<<<n, 1024, 0, s>>>(desc, n, units, T, M, R, d_status);
+    TP_PNG_DBG("k_png_window");
     if (totals[12] > 0) {
       unsigned long long* acc = reinterpret_cast<unsigned long long*>(work + totals[14]);
       cudaMemsetAsync(acc, 0, sizeof(unsigned long long) * 2 * n, s);
       k_png_adler_rows<<<static_cast<int>(totals[12]), kAdlerThreads, 0, s>>>(
           desc, n, units, R, d_status, acc, static_cast<int>(totals[12]));
+          TP_PNG_DBG("k_png_adler_rows");
       k_png_adler_check<<<(n + 255) / 256, 256, 0, s>>>(d_payload, desc, n, units, acc, d_status);
+      TP_PNG_DBG("k_png_adler_check");
     }
     const int n_items = static_cast<int>(totals[12]);
     if (n_items > 0) {
@@ -1726,6 +1755,7 @@ extern "C" TP_API int tp_png_decode(const uint8_t* d_payload, const void* d_desc
       const int sms = std::max(1, tp::device_sm_count());
       k_png_unfilter<<<std::min(n_items, sms * 8), kUnfilterRows, 0, s>>>(
           desc, n, R, d_out, d_status, progress, n_items);
+          TP_PNG_DBG("k_png_unfilter");
     }
   }
   return tp::check_launch("tp_png_decode");
