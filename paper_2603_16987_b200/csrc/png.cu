@@ -472,7 +472,9 @@ __device__ __forceinline__ bool stored_probe(const uint32_t* w, int64_t p, int64
   if (pad && ((x >> 3) & ((1ull << pad) - 1)) != 0) return false;
   const uint64_t v = peek64(w, q);
   const uint32_t len = static_cast<uint32_t>(v & 0xFFFF), nlen = static_cast<uint32_t>((v >> 16) & 0xFFFF);
-  if ((len ^ nlen) != 0xFFFF) return false;
+  // LEN = 0 (a flush marker) is left out: PNG encoders do not flush mid-stream, and the
+  // raw data of stored blocks of smooth images is full of 00 00 FF FF
+  if ((len ^ nlen) != 0xFFFF || len == 0) return false;
   *next = q + 32 + 8 * static_cast<int64_t>(len);
   return *next <= in_bits;
 }
@@ -659,7 +661,7 @@ __global__ void __launch_bounds__(kFindThreads)
         const uint32_t none = ~bits(1) & ~bits(2) & lim;  // BTYPE = 00 positions
         for (uint32_t qb = 8; qb <= 40 && found < 0; qb += 8) {
           const uint32_t v = bits(qb);
-          if (((v & 0xFFFF) ^ (v >> 16)) != 0xFFFF) continue;
+          if (((v & 0xFFFF) ^ (v >> 16)) != 0xFFFF || (v & 0xFFFF) == 0) continue;
           // a header position p in [q - 10, q - 3] of this word, zero-padded to q
           for (int pb = static_cast<int>(qb) - 10; pb <= static_cast<int>(qb) - 3; ++pb) {
             if (pb < 0 || pb > 31 || !((none >> pb) & 1)) continue;

@@ -3,7 +3,7 @@ Pillow compress levels 0-9 and optimize, custom encodes with random per-row filt
 zlib strategies, scene / noise / flat / smooth content), decoded on the device in batches
 of 32 and compared with Pillow (the reference's decoder) image by image.
 
-    python tools/png_corpus_check.py [n] > profiles/r02/png/corpus_check.json
+    python tools/png_corpus_check.py [n [seed]] > profiles/r02/png/corpus_check.json
 """
 import io
 import json
@@ -57,7 +57,8 @@ def corpus(n, seed=20261019):
 
 def main():
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 300
-    cases = corpus(n)
+    seed = int(sys.argv[2]) if len(sys.argv) > 2 else 20261019
+    cases = corpus(n, seed)
     dec = PngDecoder(torch.device("cuda:0"))
     bad, fallbacks, total_px = [], [], 0
     for b0 in range(0, len(cases), 32):
@@ -71,7 +72,7 @@ def main():
             total_px += int(w) * int(h)
             if not np.array_equal(got, want):
                 bad.append(name)
-    print(json.dumps({"payloads": len(cases), "pixels": total_px, "mismatches": bad,
+    print(json.dumps({"payloads": len(cases), "seed": seed, "pixels": total_px, "mismatches": bad,
                       "host_fallbacks": fallbacks,
                       "result": "bit-exact with Pillow" if not bad else "MISMATCH"}, indent=1))
 
