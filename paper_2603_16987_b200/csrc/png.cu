@@ -1064,12 +1064,14 @@ __global__ void k_png_chain(const PDesc* __restrict__ desc, int n, PUnit* __rest
   // for true can at worst drop a true start after it: a longer unit, not a wrong one.)
   bool redo = false;
   bool validated = true;  // u's start is where its predecessor's decode ended (or bit 16)
+  int prev = -1;          // the valid unit before u
   for (int u = u0; u < u1;) {
     PUnit& cu = units[u];
     const int v = next_valid(u);
     if (cu.dirty) {  // its end is not known yet: the next start cannot be judged now
       redo = true;
       validated = false;
+      prev = u;
       u = v;
       continue;
     }
@@ -1078,8 +1080,13 @@ __global__ void k_png_chain(const PDesc* __restrict__ desc, int n, PUnit* __rest
         img_status[k] = kImgInflate;
         return;
       }
-      redo = true;  // possibly a false start: judged once its predecessor is settled
-      validated = false;
+      // an unconfirmed start that does not decode is almost surely a false one: drop it
+      // now (the unit before decodes on over its range), so runs of false starts -- the
+      // raw data of stored blocks of flat images -- go in one round
+      cu.start = -1;
+      cu.dirty = 0;
+      if (prev >= 0) units[prev].dirty = 1;
+      redo = true;
       u = v;
       continue;
     }
@@ -1095,10 +1102,12 @@ __global__ void k_png_chain(const PDesc* __restrict__ desc, int n, PUnit* __rest
       cu.dirty = 1;
       redo = true;
       validated = false;
+      prev = u;
       u = next_valid(v);
       continue;
     }
     validated = true;
+    prev = u;
     u = v;
   }
   if (redo) {
