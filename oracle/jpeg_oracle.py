@@ -15,7 +15,9 @@ be checked stage by stage; parity is pinned to Pillow itself in tests/test_jpeg_
     coefficients stored as int16 (libjpeg's JCOEF), DC prediction per component,
     reset at each restart marker (jdhuff.c)
   * inverse DCT: jidctint.c jpeg_idct_islow (CONST_BITS 13, PASS1_BITS 2, 64-bit JLONG
-    arithmetic, the post-IDCT range-limit table of jdmaster.c prepare_range_limit_table)
+    arithmetic; the sample limit saturates as libjpeg-turbo's x86-64 SIMD IDCT does, which
+    equals jdmaster.c's range-limit table wherever that table does not wrap; blocks
+    outside the SIMD version's exact 16-bit range raise SimdRange)
   * upsampling: jdsample.c h2v1 / h1v2 / h2v2 fancy (triangle) filters, with the context
     rows of jdmainct.c (the row above the first row is the first row, rows below the last
     real row repeat it); plain replication when the downsampled width is <= 2
@@ -126,7 +128,9 @@ def parse(data: bytes) -> dict:
                 comp["td"], comp["ta"] = td, ta
             info["scan_start"] = pos + seg_len
             end = data.rfind(b"\xff\xd9")
-            info["scan_end"] = end if end >= info["scan_start"] else n
+            if end < info["scan_start"]:  # Pillow: "image file is truncated"
+                raise Corrupt("no EOI after the scan")
+            info["scan_end"] = end
             _check_supported(info)
             return info
         pos += seg_len
@@ -166,6 +170,8 @@ def unstuff(data: bytes, start: int, end: int):
                 i += 2
                 continue
             if 0xD0 <= nxt <= 0xD7:
+                if nxt != 0xD0 + (len(segs) & 7):  # jdmarker.c read_restart_marker resyncs
+                    raise Corrupt(f"RST{nxt - 0xD0} where RST{len(segs) & 7} is due")
                 segs.append(bytes(cur))
                 cur = bytearray()
                 i += 2
@@ -173,7 +179,9 @@ def unstuff(data: bytes, start: int, end: int):
             if nxt == 0xFF:
                 i += 1
                 continue
-            break  # another marker: end of scan
+            # any other marker inside the scan: libjpeg stops the scan there and conceals
+            # the rest; the device decoder hands such streams to Pillow (not restated)
+            raise Corrupt(f"marker FF{nxt:02X} inside the entropy-coded data")
         cur.append(b)
         i += 1
     segs.append(bytes(cur))
@@ -258,6 +266,8 @@ def decode_coefficients(data: bytes, info: dict):
     segs = unstuff(data, info["scan_start"], info["scan_end"])
     ri = info["dri"] or mcux * mcuy
     n_mcu = mcux * mcuy
+    if len(segs) != -(-n_mcu // ri):  # restart markers missing or extra: concealed by libjpeg
+        raise Corrupt(f"{len(segs)} restart intervals, {-(-n_mcu // ri)} expected")
     for s_idx, seg in enumerate(segs):
         first = s_idx * ri
         if first >= n_mcu:
@@ -279,6 +289,8 @@ def decode_coefficients(data: bytes, info: dict):
                     r, s = rs >> 4, rs & 15
                     if s:
                         k += r
+                        if k > 63:  # libjpeg writes it to coefficient 63 and goes on
+                            raise Corrupt("AC run past coefficient 63")
                         blk[ZIGZAG[k]] = _extend(br.bits(s), s)
                         k += 1
                     elif r == 15:
@@ -332,20 +344,40 @@ def _idct_1d(d0, d1, d2, d3, d4, d5, d6, d7, shift0):
             tmp13 - t0, tmp12 - t1, tmp11 - t2, tmp10 - t3)
 
 
+SIMD_BOUND = 1 << 13  # |dequantized coefficient|, |workspace value| below this: see idct_islow
+
+
 def range_limit(x: np.ndarray) -> np.ndarray:
-    """sample_range_limit[CENTERJSAMPLE + (x & RANGE_MASK)] (jdmaster.c): clamp of
-    x + 128 to [0, 255] for x in [-512, 511], wrapping beyond (RANGE_MASK = 1023)."""
-    v = x & 1023
-    return np.where(v < 128, v + 128, np.where(v < 512, 255, np.where(v < 896, 0, v - 896)))
+    """The sample limit after the IDCT, as Pillow's libjpeg-turbo applies it on x86-64.
+    jdmaster.c's table (sample_range_limit[CENTERJSAMPLE + (x & RANGE_MASK)]) clamps x + 128
+    to [0, 255] for x in [-512, 511] and wraps beyond; the SIMD ISLOW IDCT that
+    jsimd_idct_islow selects (simd/x86_64/jidctint-{sse2,avx2}.asm: packssdw, packsswb,
+    + CENTERJSAMPLE) saturates instead.  Inside [-512, 511] the two agree; outside, the
+    SIMD saturation is what Pillow returns (pinned by tests/test_jpeg_oracle.py)."""
+    return np.clip(x + 128, 0, 255)
+
+
+class SimdRange(Unsupported):
+    """A block whose IDCT leaves the range where libjpeg-turbo's 16-bit SIMD ISLOW IDCT
+    equals jidctint.c (only damaged streams get there): decoded by Pillow instead."""
 
 
 def idct_islow(coefs: np.ndarray, quant: np.ndarray) -> np.ndarray:
-    """[..., 64] int16 natural-order coefficients -> [..., 8, 8] uint8 samples."""
+    """[..., 64] int16 natural-order coefficients -> [..., 8, 8] uint8 samples.
+
+    The arithmetic is jidctint.c's (64-bit JLONG).  libjpeg-turbo's SIMD version keeps the
+    dequantized coefficients and the pass-1 workspace in 16-bit lanes (pmullw, paddw of
+    coefficient pairs, packssdw), so it equals jidctint.c only while every dequantized
+    coefficient and every workspace value is below 2^13 in magnitude (then no 16-bit sum
+    or DC shortcut overflows); beyond that SimdRange is raised."""
     c = (coefs.astype(np.int64) * quant.astype(np.int16).astype(np.int64)).reshape(-1, 8, 8)
+    if c.size and np.abs(c).max() >= SIMD_BOUND:
+        raise SimdRange("dequantized coefficient outside the SIMD IDCT's exact range")
     # pass 1: columns (index [row, col]; column inputs are rows 0..7)
     cols = _idct_1d(*(c[:, k, :] for k in range(8)), None)
     ws = np.stack([_descale(v, CONST_BITS - PASS1_BITS) for v in cols], axis=1)
-    ws = ws.astype(np.int32).astype(np.int64)  # libjpeg's int workspace
+    if ws.size and np.abs(ws).max() >= SIMD_BOUND:
+        raise SimdRange("IDCT workspace value outside the SIMD IDCT's exact range")
     # (the all-zero-AC column / row shortcuts give the same values as the full butterfly)
     rows = _idct_1d(*(ws[:, :, k] for k in range(8)), None)
     out = np.stack([range_limit(_descale(v, CONST_BITS + PASS1_BITS + 3)) for v in rows],

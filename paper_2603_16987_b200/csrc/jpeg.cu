@@ -281,6 +281,9 @@ __global__ void __launch_bounds__(kUnstuffThreads) k_jpeg_unstuff_write(
     for (int i = 0; i < 16; ++i) {
       if (f.keep >> i & 1) sout[o++] = raw[p0 + i];
       if (f.rst >> i & 1) {
+        // the r-th marker must be RST(r mod 8); libjpeg resynchronizes on any other
+        // (jdmarker.c read_restart_marker / jpeg_resync_to_restart): left to the host
+        if (raw[p0 + i] != 0xD0 + (r & 7)) atomicOr(status + k, TP_JPEG_CORRUPT);
         ++r;
         if (r < static_cast<unsigned>(d.n_seg)) seg_start[r] = static_cast<int32_t>(carry_k + o);
       }
@@ -895,9 +898,8 @@ __device__ constexpr int kNat2Zig[64] = {0,  1,  5,  6,  14, 15, 27, 28, 2,  4, 
                               10, 19, 23, 32, 39, 45, 52, 54, 20, 22, 33, 38, 46, 51, 55, 60,
                               21, 34, 37, 47, 50, 56, 59, 61, 35, 36, 48, 49, 57, 58, 62, 63};
 
-// One jidctint.c butterfly.  libjpeg computes in JLONG (64-bit on LP64); T = int is
-// exact whenever the inputs are bounded as the callers check (|in| <= 2^13 keeps every
-// intermediate below 2^30.3), T = long long otherwise (corrupt-looking coefficients).
+// One jidctint.c butterfly.  libjpeg computes in JLONG (64-bit on LP64); int is exact for
+// the inputs the caller lets through (|in| < 2^13 keeps every intermediate below 2^30.3).
 template <typename T>
 __device__ __forceinline__ void idct_1d(const T (&in)[8], T (&out)[8]) {
   T z2 = in[2], z3 = in[6];
@@ -935,15 +937,20 @@ __device__ __forceinline__ void idct_1d(const T (&in)[8], T (&out)[8]) {
   out[4] = tmp13 - t0;
 }
 
-// jdmaster.c prepare_range_limit_table + the IDCT's `range_limit[x & RANGE_MASK]` with
-// CENTERJSAMPLE folded into the descale: t = (x + 128) & 1023 maps [0, 256) to itself,
-// [256, 640) to 255 and [640, 1024) to 0 -- the table's wrap-around for corrupt data
+// The sample limit with CENTERJSAMPLE folded into the descale (x128 = x + 128).  The
+// decoder the reference runs is Pillow's libjpeg-turbo, whose x86-64 SIMD ISLOW IDCT
+// (jsimd_idct_islow: packssdw, packsswb, + CENTERJSAMPLE) saturates; jdmaster.c's
+// range-limit table agrees with that for x in [-512, 511] and wraps beyond (only damaged
+// streams get there), so the saturation is what Pillow returns.
 __device__ __forceinline__ uint32_t range_limit128(int x128) {
-  const uint32_t t = static_cast<uint32_t>(x128) & 1023u;
-  return t < 640u ? min(t, 255u) : 0u;
+  return static_cast<uint32_t>(min(max(x128, 0), 255));
 }
 
-// |v| <= 2^13 for all 64 values: min / max trees (three-input VIMNMX3)
+// |v| < 2^13 for all 64 values (min / max trees, three-input VIMNMX3).  The SIMD IDCT keeps
+// dequantized coefficients and the pass-1 workspace in 16-bit lanes (pmullw, paddw of
+// coefficient pairs, the DC-only << PASS1_BITS, packssdw); under this bound none of those
+// overflow and it equals jidctint.c.  A block outside it came from a damaged stream:
+// the image goes to Pillow.
 __device__ __forceinline__ bool all_small(const int (&v)[8][8]) {
   int mx = v[0][0], mn = v[0][0];
 #pragma unroll
@@ -952,7 +959,7 @@ __device__ __forceinline__ bool all_small(const int (&v)[8][8]) {
     mx = max(mx, max(a, b));
     mn = min(mn, min(a, b));
   }
-  return mx <= (1 << 13) && mn >= -(1 << 13);
+  return mx < (1 << 13) && mn > -(1 << 13);
 }
 
 // pass 1 (columns): DESCALE(x, CONST_BITS - PASS1_BITS) into the int workspace, in place
@@ -1005,13 +1012,13 @@ __device__ __forceinline__ void div_small(int a, int b, int& q, int& r) {
 // loads), DEQUANTIZE (short coef x short quant, ISLOW_MULT_TYPE) into natural order,
 // eight column transforms then eight row transforms, eight 8-byte row stores.  Each CTA
 // takes a contiguous range of blocks (one image lookup per CTA, not per block); each pass
-// checks its 64 inputs once for the int32 bound.
+// checks its 64 inputs once against the SIMD-exact bound (all_small).
 constexpr int kIdctThreads = 128;
 
 __global__ void __launch_bounds__(kIdctThreads) k_jpeg_idct(const JDesc* __restrict__ descs, int n,
                                                             int64_t total_blocks, int64_t per_cta,
                                                             uint8_t* __restrict__ work,
-                                                            const int32_t* __restrict__ status) {
+                                                            int32_t* __restrict__ status) {
   const int64_t b_lo = static_cast<int64_t>(blockIdx.x) * per_cta;
   const int64_t b_hi = min(total_blocks, b_lo + per_cta);
   if (b_lo >= b_hi) return;
@@ -1053,9 +1060,17 @@ __global__ void __launch_bounds__(kIdctThreads) k_jpeg_idct(const JDesc* __restr
         blk[nat >> 3][nat & 7] = coef * qs[e];
       }
     }
-    if (all_small(blk)) idct_pass1<int>(blk); else idct_pass1<long long>(blk);
+    if (!all_small(blk)) {
+      atomicOr(status + k, TP_JPEG_CORRUPT);
+      continue;
+    }
+    idct_pass1<int>(blk);
+    if (!all_small(blk)) {
+      atomicOr(status + k, TP_JPEG_CORRUPT);
+      continue;
+    }
     uint32_t lo[8], hi[8];
-    if (all_small(blk)) idct_pass2<int>(blk, lo, hi); else idct_pass2<long long>(blk, lo, hi);
+    idct_pass2<int>(blk, lo, hi);
     int my, mx;
     div_small(mcu, d->mcux, my, mx);
     const int by = d->ncomp == 1 ? my : my * d->comp_v[c] + d->slot_bv[u];

@@ -65,3 +65,32 @@ def small_cases(seed: int = 0):
     out.append(("gray", encode(px, 85, gray=True)))
     out.append(("gray_rst", encode(px, 85, gray=True, restart_marker_blocks=2)))
     return out
+
+
+def fuzzed(n: int, seed: int = 20261019):
+    """n damaged baseline JPEGs as (t, kind, payload): kind 0 flips bits in the entropy-
+    coded data, 1 drops 1-4 bytes from it, 2 truncates the file inside the scan.  The six
+    bases cover 4:2:0 / 4:4:4 / 4:2:2-free colour, restart markers, noise and grayscale."""
+    rng = np.random.default_rng(seed)
+    base = [encode(scene(160, 120, 1)), encode(scene(97, 61, 2), quality=95),
+            encode(scene(200, 90, 3), subsampling=0),
+            encode(scene(128, 128, 4), restart_marker_blocks=4),
+            encode(np.random.default_rng(5).integers(0, 256, (64, 80, 3), dtype=np.uint8)),
+            encode(scene(90, 70, 6), gray=True)]
+    out = []
+    for t in range(n):
+        p = bytearray(base[t % len(base)])
+        sos = p.find(b"\xff\xda")
+        start = sos + 2 + int.from_bytes(p[sos + 2: sos + 4], "big")
+        kind = t % 3
+        if kind == 0:
+            for _ in range(1 + t % 4):
+                i = int(rng.integers(start, len(p) - 2))
+                p[i] ^= 1 << int(rng.integers(0, 8))
+        elif kind == 1:
+            i = int(rng.integers(start, len(p) - 2))
+            del p[i: i + int(rng.integers(1, 5))]
+        else:
+            p = p[: int(rng.integers(start, len(p)))]
+        out.append((t, kind, bytes(p)))
+    return out

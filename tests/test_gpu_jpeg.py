@@ -13,7 +13,7 @@ import pytest
 import torch
 from PIL import Image
 
-from jpeg_cases import corpus_files, encode, pil_rgb, scene, small_cases
+from jpeg_cases import corpus_files, encode, fuzzed, pil_rgb, scene, small_cases
 from paper_2603_16987_b200.jpeg import JpegDecoder, decode_images
 
 pytestmark = pytest.mark.gpu
@@ -120,3 +120,37 @@ def test_decode_then_tile_matches_oracle():
 def test_decode_images_helper():
     p = encode(scene(50, 40, 9))
     assert np.array_equal(decode_images([p], DEV)[0], pil_rgb(p))
+
+
+def test_fuzzed_jpegs_match_pillow():
+    """Random damage to baseline JPEGs (bit flips and dropped bytes in the entropy-coded
+    data, with and without restart markers, truncation): every payload decodes exactly as
+    Pillow decodes it -- the same pixels (libjpeg conceals damage; a stream K7 does not find
+    clean goes to Pillow on the host) or the same exception -- and nothing faults."""
+    from paper_2603_16987_b200._decode import decode_rgb
+
+    dec = JpegDecoder(DEV)
+    good = []
+    for t, kind, p in fuzzed(240):
+        try:
+            ref, ref_exc = decode_rgb(p), None
+        except Exception as exc:  # noqa: BLE001 -- whatever the reference raises
+            ref, ref_exc = None, exc
+        try:
+            pk = dec.decode([p])
+            w, h = (int(v) for v in pk.wh_host[0])
+            got, got_exc = pk.data[: w * h * 3].cpu().numpy().reshape(h, w, 3), None
+        except Exception as exc:  # noqa: BLE001
+            got, got_exc = None, exc
+        if ref_exc is not None:
+            assert got_exc is not None and type(got_exc) is type(ref_exc), (t, kind, ref_exc, got_exc)
+        else:
+            assert got_exc is None, (t, kind, got_exc)
+            assert np.array_equal(got, ref), (t, kind, dec.last_fallback)
+            good.append((p, ref))
+    # the decodable ones again as one batch: damage in one image does not leak into another
+    pk = dec.decode([p for p, _ in good])
+    host = pk.data.cpu().numpy()
+    for k, ((p, ref), o, (w, h)) in enumerate(zip(good, pk.offsets_host, pk.wh_host)):
+        got = host[int(o): int(o) + int(w) * int(h) * 3].reshape(int(h), int(w), 3)
+        assert np.array_equal(got, ref), k

@@ -9,7 +9,7 @@ import ctypes
 import numpy as np
 import pytest
 
-from jpeg_cases import corpus_files, encode, pil_rgb, scene, small_cases
+from jpeg_cases import corpus_files, encode, fuzzed, pil_rgb, scene, small_cases
 from oracle import jpeg_oracle as J
 from paper_2603_16987_b200 import jpeg as PJ
 
@@ -17,6 +17,25 @@ from paper_2603_16987_b200 import jpeg as PJ
 @pytest.mark.parametrize("name,data", small_cases(0) + corpus_files()[:6])
 def test_oracle_matches_pillow(name, data):
     assert np.array_equal(J.decode(data), pil_rgb(data)), name
+
+
+def test_oracle_on_damaged_streams():
+    """Damaged streams (bit flips, dropped bytes, truncation): the oracle either decodes
+    them exactly as Pillow does -- including the saturating sample limit of libjpeg-turbo's
+    SIMD IDCT for out-of-range blocks -- or raises Corrupt / Unsupported (the cases the
+    device decoder hands to Pillow: bad codes, runs past 63, early data end, stray or
+    misnumbered markers, blocks outside the SIMD IDCT's exact range)."""
+    from paper_2603_16987_b200._decode import decode_rgb
+
+    decoded = 0
+    for t, kind, p in fuzzed(300):
+        try:
+            got = J.decode(p)
+        except (J.Corrupt, J.Unsupported):
+            continue
+        decoded += 1
+        assert np.array_equal(got, decode_rgb(p)), (t, kind)
+    assert decoded > 100
 
 
 def test_oracle_rejects_progressive():
