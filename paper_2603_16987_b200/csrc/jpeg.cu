@@ -878,8 +878,14 @@ __global__ void __launch_bounds__(256, TP_JPEG_HUFF_MINB) k_jpeg_huff(const JDes
     const int limit = r.s * d.ri * d.bmcu + seg_blocks(d, r.s);
     const int4 pv = W.dcs[g];
     const int pred[3] = {pv.y, pv.z, pv.w};
-    decode_run<2, false>(T, br, r.bit0, r.seg_bits, stop, pos, u, z,
-                         reinterpret_cast<int16_t*>(work + d.coef_off), W.bstart[g], limit, pred);
+    const DecOut o = decode_run<2, false>(T, br, r.bit0, r.seg_bits, stop, pos, u, z,
+                                          reinterpret_cast<int16_t*>(work + d.coef_off),
+                                          W.bstart[g], limit, pred);
+    // This pass walks the true path exactly once and stops at the interval's last block,
+    // so an unclean symbol here is damage that libjpeg would conceal.  (Phase 3 can miss
+    // one: a re-decode that rejoins a recorded path inherits that path's first error only,
+    // and a path that fell into the true one after an early error of its own had it there.)
+    if (o.err != kNoErr) atomicOr(status + r.k, TP_JPEG_CORRUPT);
   }
   if (tid == 0) W.stamps[4] = gtimer();
 }

@@ -166,3 +166,31 @@ def bad_cases():
     out.append(("palette_index_oob", custom_png(idx, 3, palette=pal)))
     out.append(("short_stream", custom_png(a, 2)[:-30] + _chunk(b"IEND", b"")))
     return out
+
+
+def fuzzed(n: int, seed: int = 20261019):
+    """n damaged PNGs as (t, kind, payload): kind 0 flips bits after the first IDAT tag,
+    1 drops 1-4 bytes there, 2 truncates the file.  Single- and multi-unit streams (the
+    finder, the chain and the re-decode rounds see the damage), Pillow and custom encodes."""
+    rng = np.random.default_rng(seed)
+    base = [pil_png(content("scene", 96, 64, 1)), pil_png(content("noise", 80, 48, 2)),
+            pil_png(content("flat", 120, 90, 3)), pil_png(content("scene", 64, 40, 4), "P"),
+            custom_png(content("scene", 70, 30, 5), 2, level=0),
+            custom_png(content("scene", 70, 30, 6), 2, strategy=zlib.Z_FIXED),
+            pil_png(content("scene", 640, 480, 7)), pil_png(content("noise", 400, 300, 8))]
+    out = []
+    for t in range(n):
+        p = bytearray(base[t % len(base)])
+        start = p.find(b"IDAT") + 4
+        kind = t % 3
+        if kind == 0:
+            for _ in range(1 + t % 4):
+                i = int(rng.integers(start, len(p) - 16))
+                p[i] ^= 1 << int(rng.integers(0, 8))
+        elif kind == 1:
+            i = int(rng.integers(start, len(p) - 16))
+            del p[i: i + int(rng.integers(1, 5))]
+        else:
+            p = p[: int(rng.integers(start, len(p)))]
+        out.append((t, kind, bytes(p)))
+    return out

@@ -120,31 +120,11 @@ def test_png_fuzzed_payloads_match_reference():
     import torch
 
     from paper_2603_16987_b200.png import PngDecoder
-    from png_cases import content, custom_png, pil_png
+    from png_cases import fuzzed
 
-    rng = np.random.default_rng(20261019)
-    base = [pil_png(content("scene", 96, 64, 1)), pil_png(content("noise", 80, 48, 2)),
-            pil_png(content("flat", 120, 90, 3)), pil_png(content("scene", 64, 40, 4), "P"),
-            custom_png(content("scene", 70, 30, 5), 2, level=0),
-            custom_png(content("scene", 70, 30, 6), 2, strategy=__import__("zlib").Z_FIXED)]
-    # multi-unit streams too (the finder, the chain and the re-decode rounds see damage)
-    base += [pil_png(content("scene", 640, 480, 7)), pil_png(content("noise", 400, 300, 8))]
     addr = re.compile(r"0x[0-9a-f]+")
     dec = PngDecoder(torch.device("cuda:0"))
-    for t in range(128):
-        p = bytearray(base[t % len(base)])
-        start = p.find(b"IDAT") + 4
-        kind = t % 3
-        if kind == 0:
-            for _ in range(1 + t % 4):
-                i = int(rng.integers(start, len(p) - 16))
-                p[i] ^= 1 << int(rng.integers(0, 8))
-        elif kind == 1:
-            i = int(rng.integers(start, len(p) - 16))
-            del p[i: i + int(rng.integers(1, 5))]
-        else:
-            p = p[: int(rng.integers(start, len(p)))]
-        p = bytes(p)
+    for t, kind, p in fuzzed(128):
         try:
             ref, ref_exc = _host(p), None
         except Exception as exc:  # noqa: BLE001
