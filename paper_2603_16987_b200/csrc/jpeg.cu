@@ -421,11 +421,58 @@ __device__ __forceinline__ long long pack_state(uint32_t pos, int u, int z) {
 // from `pred` (the interval's running DC of each component at this entry).  pos, stop
 // and seg_bits are bits from the interval start; bit0 is the interval's first bit in
 // the image's clean stream.  CK: record / compare checkpoints (MODE 0 and 1).
+#ifndef TP_JPEG_NOSTORE  // measurement only: the write pass without its stores (wrong output)
+#define TP_JPEG_NOSTORE 0
+#endif
+#ifndef TP_JPEG_STAGED  // write pass: blocks staged in shared memory, one bulk store each
+#define TP_JPEG_STAGED 1
+#endif
+
+// The write pass's coefficient staging: one 128-byte block per thread in shared memory
+// (144-byte stride: 16-byte aligned for the bulk copy, lanes spread over the banks; the
+// pad takes the dummy store of EOB / ZRL symbols, so every symbol stores unconditionally).
+// A block that completes inside the thread's range leaves with one cp.async.bulk (128
+// bytes, a whole line); the partial blocks at a subsequence's two ends store just their
+// own coefficient range [zlo, z) -- the neighbouring subsequence stores the rest -- so the
+// coefficient buffer needs no zeroing (the 400 MB memset of a 64 x 1080p batch is gone).
+// 64 x 1080p: K7 2.70 -> 2.57 ms (scattered 2-byte global stores + memset before;
+// profiles/r02/jpeg/ab_staged_write.log).
+#ifndef TP_JPEG_STAGE_BULK  // 1: a block leaves through cp.async.bulk; 0: plain 16-byte stores
+#define TP_JPEG_STAGE_BULK 1
+#endif
+#ifndef TP_JPEG_STAGE_SLOTS  // 128-byte blocks staged per thread (2: the copy out of one
+#define TP_JPEG_STAGE_SLOTS 1  // overlaps the decode into the other, but the extra 32 KB of
+#endif                         // shared memory per CTA costs the decode its L1: slower)
+constexpr int kStageStride = 128 * TP_JPEG_STAGE_SLOTS + 16;  // bytes per thread
+struct Stage {
+  uint8_t* base;  // this thread's 2 x 128 bytes
+  int slot;       // the current block's slot
+};
+
+__device__ __forceinline__ void stage_zero(uint8_t* p) {
+  uint4* q = reinterpret_cast<uint4*>(p);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) q[i] = make_uint4(0u, 0u, 0u, 0u);
+}
+
+__device__ __forceinline__ void bulk_store128(void* gdst, const void* ssrc) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // st.shared -> async proxy
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 128;" ::"l"(gdst),
+               "r"(static_cast<uint32_t>(__cvta_generic_to_shared(ssrc)))
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+
 template <int MODE, bool CK>
 __device__ DecOut decode_run(const Tabs& T, BitReader& br, uint32_t bit0, uint32_t seg_bits,
                              uint32_t stop, uint32_t pos, int u, int z, int16_t* coef, int block,
                              int block_limit, const int* pred_in, const Ckpt* ck = nullptr,
-                             uint32_t* errpos = nullptr) {
+                             uint32_t* errpos = nullptr, Stage* stage = nullptr) {
   DecOut o;
   o.blocks = 0;
   o.err = kNoErr;
@@ -441,6 +488,10 @@ __device__ DecOut decode_run(const Tabs& T, BitReader& br, uint32_t bit0, uint32
   uint32_t next_cp = CK ? ck->first : 0xFFFFFFFFu;
   if (MODE == 2 && block >= block_limit) stop = pos;
   if (pos < stop) br.prefetch(bit0 + pos, bit0 + stop);
+  // staged write pass: the current block's coefficients from zlo on are this thread's
+  const bool staged = MODE == 2 && TP_JPEG_STAGED && !TP_JPEG_NOSTORE;
+  int zlo = z;
+  int16_t* stg = staged ? reinterpret_cast<int16_t*>(stage->base + 128 * stage->slot) : nullptr;
   while (pos < stop) {
     if (CK && pos >= next_cp) {
       const long long st = pack_state(pos, u, z);
@@ -519,7 +570,10 @@ __device__ DecOut decode_run(const Tabs& T, BitReader& br, uint32_t bit0, uint32
     p0 += c == 0 ? dcv : 0;
     p1 += c == 1 ? dcv : 0;
     p2 += c == 2 ? dcv : 0;
-    if (MODE == 2) {
+    if (staged) {  // one unconditional store (EOB / ZRL write a zero into the pad)
+      int16_t* at = dc ? stg : s ? stg + z + r : reinterpret_cast<int16_t*>(stage->base + 128 * TP_JPEG_STAGE_SLOTS);
+      *at = static_cast<int16_t>(dc ? (c == 0 ? p0 : c == 1 ? p1 : p2) : val);  // zigzag order
+    } else if (MODE == 2 && !TP_JPEG_NOSTORE) {
       if (dc)
         coef[static_cast<int64_t>(block) * 64] = static_cast<int16_t>(c == 0 ? p0 : c == 1 ? p1 : p2);
       else if (s)
@@ -528,6 +582,24 @@ __device__ DecOut decode_run(const Tabs& T, BitReader& br, uint32_t bit0, uint32
     const int zn = (dc || s != 0 || r == 15) ? z + r + 1 : 64;
     pos += used;
     const bool bend = zn >= 64;
+    if (staged && bend) {  // the block is complete: out it goes, the other slot comes in
+      int16_t* dst = coef + static_cast<int64_t>(block) * 64;
+      if (zlo == 0 && TP_JPEG_STAGE_BULK) {
+        bulk_store128(dst, stg);
+      } else if (zlo == 0) {  // eight 16-byte stores: a whole line from one lane
+        const uint4* q = reinterpret_cast<const uint4*>(stg);
+        uint4* g4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) __stcs(g4 + i, q[i]);
+      } else {
+        for (int i = zlo; i < 64; ++i) dst[i] = stg[i];
+      }
+      stage->slot = TP_JPEG_STAGE_SLOTS == 2 ? stage->slot ^ 1 : 0;
+      stg = reinterpret_cast<int16_t*>(stage->base + 128 * stage->slot);
+      if (TP_JPEG_STAGE_BULK) bulk_wait_read<TP_JPEG_STAGE_SLOTS - 1>();  // its last copy read it
+      stage_zero(reinterpret_cast<uint8_t*>(stg));
+      zlo = 0;
+    }
     z = bend ? 0 : zn;
     o.blocks += bend ? 1 : 0;
     u = bend ? (u + 1 == T.bmcu ? 0 : u + 1) : u;
@@ -538,6 +610,11 @@ __device__ DecOut decode_run(const Tabs& T, BitReader& br, uint32_t bit0, uint32
   }
   if (CK)
     for (int i = ci; i < kCkpts; ++i) ck->state[i] = -1;  // not reached by this decode
+  if (staged && z != zlo) {  // the block the next subsequence finishes: [zlo, z) is ours
+    int16_t* dst = coef + static_cast<int64_t>(block) * 64;
+    for (int i = zlo; i < z; ++i) dst[i] = stg[i];
+    stage_zero(reinterpret_cast<uint8_t*>(stg));
+  }
   o.pos = pos;
   o.u = u;
   o.z = z;
@@ -860,6 +937,12 @@ __global__ void __launch_bounds__(256, TP_JPEG_HUFF_MINB) k_jpeg_huff(const JDes
   if (tid == 0) W.stamps[3] = gtimer();
 
   // (4) write pass: coefficients, with the DC values predicted in place
+  extern __shared__ __align__(16) uint8_t stage_mem[];
+  Stage stage{stage_mem + kStageStride * threadIdx.x, 0};
+  if (TP_JPEG_STAGED) {
+    stage_zero(stage.base);
+    if (TP_JPEG_STAGE_SLOTS == 2) stage_zero(stage.base + 128);
+  }
   for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x; base < total_slots; base += nthreads) {
     const int64_t g = base + threadIdx.x;
     SlotRef r;
@@ -880,13 +963,14 @@ __global__ void __launch_bounds__(256, TP_JPEG_HUFF_MINB) k_jpeg_huff(const JDes
     const int pred[3] = {pv.y, pv.z, pv.w};
     const DecOut o = decode_run<2, false>(T, br, r.bit0, r.seg_bits, stop, pos, u, z,
                                           reinterpret_cast<int16_t*>(work + d.coef_off),
-                                          W.bstart[g], limit, pred);
+                                          W.bstart[g], limit, pred, nullptr, nullptr, &stage);
     // This pass walks the true path exactly once and stops at the interval's last block,
     // so an unclean symbol here is damage that libjpeg would conceal.  (Phase 3 can miss
     // one: a re-decode that rejoins a recorded path inherits that path's first error only,
     // and a path that fell into the true one after an early error of its own had it there.)
     if (o.err != kNoErr) atomicOr(status + r.k, TP_JPEG_CORRUPT);
   }
+  if (TP_JPEG_STAGED && TP_JPEG_STAGE_BULK) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   if (tid == 0) W.stamps[4] = gtimer();
 }
 
@@ -1407,8 +1491,10 @@ TP_API int tp_jpeg_decode(const uint8_t* d_payload, const void* d_desc, int32_t 
   const int64_t coef_begin = totals[3], coef_end = totals[4];
   if (coef_end > work_bytes || coef_begin < 4096) return set_error(TP_ERR_INVALID_ARGUMENT, "tp_jpeg_decode: workspace too small");
   k_jpeg_status_init<<<(n + 255) / 256, 256, 0, s>>>(descs, n, d_status);
+  // (the coefficients need no zeroing when the write pass stages blocks: it stores every
+  // coefficient of every block, zeros included)
   if (cudaMemsetAsync(work, 0, 4096, s) != cudaSuccess ||
-      cudaMemsetAsync(work + coef_begin, 0, coef_end - coef_begin, s) != cudaSuccess)
+      (!TP_JPEG_STAGED && cudaMemsetAsync(work + coef_begin, 0, coef_end - coef_begin, s) != cudaSuccess))
     return set_error(TP_ERR_CUDA, "tp_jpeg_decode: memset failed");
   const int sms = device_sm_count();
   const int64_t chunks = totals[5];
@@ -1424,8 +1510,12 @@ TP_API int tp_jpeg_decode(const uint8_t* d_payload, const void* d_desc, int32_t 
   if (slots > 0) {
     static int per_sm_of[64];
     int& per_sm = per_sm_of[dev];
+    const int dyn = TP_JPEG_STAGED ? kStageStride * 256 : 0;
     if (per_sm == 0) {
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_jpeg_huff, 256, 0);
+      if (dyn > 0 &&
+          cudaFuncSetAttribute(k_jpeg_huff, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn) != cudaSuccess)
+        return set_error(TP_ERR_CUDA, "tp_jpeg_decode: decode kernel shared memory");
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_jpeg_huff, 256, dyn);
       if (per_sm <= 0) return set_error(TP_ERR_CUDA, "tp_jpeg_decode: decode kernel does not fit");
     }
     int grid = per_sm * sms;
@@ -1438,7 +1528,7 @@ TP_API int tp_jpeg_decode(const uint8_t* d_payload, const void* d_desc, int32_t 
     int32_t* st = d_status;
     void* args[] = {&descs, &nn, &ts, &sb, &lb, &work, &st};
     cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_jpeg_huff), grid, 256,
-                                                args, 0, s);
+                                                args, dyn, s);
     if (e != cudaSuccess) return set_error(TP_ERR_CUDA, "tp_jpeg_decode: %s", cudaGetErrorString(e));
   }
   if (blocks > 0) {
