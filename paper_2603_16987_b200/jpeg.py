@@ -263,7 +263,7 @@ class JpegDecoder:
         corpus-like 1080p JPEGs (profiles/r02/jpeg/): one image decodes fastest with short
         subsequences and a long lead-in (1024 + 2048: K7 0.69 ms, decode() 1.0 ms; 4096:
         1.71 ms per call), 64 images with 4096-bit subsequences and a 2048-bit lead-in
-        (2.8 ms; 3.8 ms at 2048)."""
+        (2.47 ms; 2.56 ms with a 4096-bit lead-in, profiles/r02/jpeg/lead_sweep.log)."""
         if self.sub_bits:
             return self.sub_bits, self.lead_bits
         if scan_bits < 32 * 2**20:  # fewer than ~8 corpus-like 1080p images

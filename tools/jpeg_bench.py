@@ -3,7 +3,7 @@ end to end through JpegDecoder.decode (host parse + pinned staging + H2D + K7 + 
 readback, host clock) and the K7 kernels alone (CUDA events around relaunches), against
 Pillow (the reference's decoder) on all host cores.
 
-    python tools/jpeg_bench.py [sub_bits ...]
+    python tools/jpeg_bench.py [sub_bits[:lead_bits] ...]   (default: the decoder's choice)
 """
 import io
 import json
@@ -80,7 +80,7 @@ def run(name, payloads, spec):
 
 
 def main():
-    subs = sys.argv[1:] or ["4096"]  # sub_bits[:lead_bits]
+    subs = sys.argv[1:] or ["0"]  # sub_bits[:lead_bits]; 0: the decoder's own choice by batch size
     sets = {"scene1080_q85": [encode(scene(1920, 1080, s)) for s in range(64)],
             "noise1080_q85": [encode(np.random.default_rng(s).integers(0, 256, (1080, 1920, 3),
                                                                         dtype=np.uint8)) for s in range(16)]}
