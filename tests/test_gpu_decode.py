@@ -38,3 +38,34 @@ def test_mixed_batch_in_order():
             assert np.array_equal(got, _pillow(batch[k])), k
     pk = dec.decode(payloads)
     assert dec.last_fallback == [2]  # the progressive JPEG: Pillow on the host
+
+
+def test_mixed_batches_of_damaged_payloads():
+    """Decodable damaged JPEGs and PNGs (tests' fuzz generators) interleaved with clean
+    ones in mixed batches: every image equals Pillow's decode, in the caller's order, and
+    a damaged image sent to the host does not disturb its neighbours on the device."""
+    import jpeg_cases
+    import png_cases
+    import torch
+
+    from paper_2603_16987_b200.decode import ImageDecoder
+
+    pool = []
+    for _, _, p in jpeg_cases.fuzzed(120, seed=3) + png_cases.fuzzed(240, seed=3):
+        try:
+            pool.append((p, _pillow(p)))
+        except Exception:  # noqa: BLE001 -- Pillow rejects it: not a decodable payload
+            pass
+    clean = [encode(scene(200, 150, 8)), pil_png(content("scene", 180, 100, 9)),
+             pil_png(content("smooth", 90, 60, 10), "P"), encode(scene(64, 64, 11), gray=True)]
+    pool += [(p, _pillow(p)) for p in clean]
+    rng = np.random.default_rng(4)
+    dec = ImageDecoder(torch.device("cuda:0"))
+    for _ in range(4):
+        pick = rng.permutation(len(pool))[:48]
+        batch = [pool[i] for i in pick]
+        pk = dec.decode([p for p, _ in batch])
+        host = pk.data.cpu().numpy()
+        for k, ((_, ref), o, (w, h)) in enumerate(zip(batch, pk.offsets_host, pk.wh_host)):
+            got = host[int(o): int(o) + int(w) * int(h) * 3].reshape(int(h), int(w), 3)
+            assert np.array_equal(got, ref), k
