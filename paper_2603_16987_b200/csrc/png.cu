@@ -540,7 +540,11 @@ static_assert(kUnitBits % (3 * 4 * 1024) == 0, "1-4 parts of whole 1024-bit step
 struct FindScratch {
   long long pos[kFindParts];  // found start | 1 << 62 for a stored start; -1: none
   int lowest;                 // lowest quarter with a start (kFindParts: none yet)
+  int next;                   // unit 0's: the next (unit, part) item a finder warp takes
 };
+#ifndef TP_PNG_FIND_DYN  // 1: a resident grid of finder warps taking (unit, part) items in
+#define TP_PNG_FIND_DYN 1  // order from a counter; 0: one warp per item (a partial last wave)
+#endif
 __device__ __forceinline__ FindScratch* find_scratch(uint32_t* stage, int u) {
   return reinterpret_cast<FindScratch*>(reinterpret_cast<uint8_t*>(stage) + u * kStageBytesPerUnit);
 }
@@ -551,6 +555,7 @@ __global__ void k_png_find_init(uint32_t* stage, int U) {
   FindScratch* f = find_scratch(stage, u);
   for (int p = 0; p < kFindParts; ++p) f->pos[p] = -1;
   f->lowest = kFindParts;
+  f->next = 0;
 }
 
 __global__ void k_png_find_select(PUnit* __restrict__ units, uint32_t* stage, int U, int parts,
@@ -596,10 +601,22 @@ __global__ void __launch_bounds__(kFindThreads)
     kraft9[i] = static_cast<uint8_t>(sum);
   }
   __syncthreads();
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int u = gw / parts, part = gw % parts;
   const int lane = threadIdx.x & 31;
-  if (u >= U) return;
+  // units need very different scan lengths (the distance from the unit start to the next
+  // block header): warps take items from a counter instead of one fixed item each
+  int* next_item = &find_scratch(stage, 0)->next;
+  for (int it = 0;; ++it) {
+  int gw;
+  if (TP_PNG_FIND_DYN) {
+    int v = 0;
+    if (lane == 0) v = atomicAdd(next_item, 1);
+    gw = __shfl_sync(0xffffffffu, v, 0);
+  } else {
+    if (it > 0) break;
+    gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  }
+  const int u = gw / parts, part = gw % parts;
+  if (u >= U) break;
   FindScratch* fs = find_scratch(stage, u);
   int64_t* q = queue[threadIdx.x >> 5];
   const int k = unit_image(desc, n, u);
@@ -698,6 +715,7 @@ __global__ void __launch_bounds__(kFindThreads)
     fs->pos[part] = start | (stored ? (1ll << 62) : 0);
     atomicMin(&fs->lowest, part);
   }
+  }  // items
 }
 
 // ---------------------------------------------------------------------------
@@ -1729,8 +1747,14 @@ extern "C" TP_API int tp_png_decode(const uint8_t* d_payload, const void* d_desc
     k_png_find_init<<<(U + 255) / 256, 256, 0, s>>>(stage, U);
     TP_PNG_DBG("k_png_find_init");
     const int64_t find_warps = static_cast<int64_t>(U) * parts;
-    k_png_find<<<static_cast<int>((find_warps + kFindThreads / 32 - 1) / (kFindThreads / 32)),
-                 kFindThreads, 0, s>>>(d_payload, desc, n, units, U, stage, parts);
+    int64_t find_ctas = (find_warps + kFindThreads / 32 - 1) / (kFindThreads / 32);
+    if (TP_PNG_FIND_DYN) {  // one resident wave: the warps take the items in turn
+      static int find_occ = 0;
+      if (find_occ == 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&find_occ, k_png_find, kFindThreads, 0);
+      find_ctas = std::min<int64_t>(find_ctas, static_cast<int64_t>(std::max(find_occ, 1)) * sms);
+    }
+    k_png_find<<<static_cast<int>(find_ctas), kFindThreads, 0, s>>>(d_payload, desc, n, units, U,
+                                                                    stage, parts);
                  TP_PNG_DBG("k_png_find");
     k_png_find_select<<<(U + 255) / 256, 256, 0, s>>>(units, stage, U, parts,
                                                       static_cast<int>(totals[15]));
