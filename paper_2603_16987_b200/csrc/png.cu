@@ -540,8 +540,13 @@ static_assert(kUnitBits % (3 * 4 * 1024) == 0, "1-4 parts of whole 1024-bit step
 struct FindScratch {
   long long pos[kFindParts];  // found start | 1 << 62 for a stored start; -1: none
   int lowest;                 // lowest quarter with a start (kFindParts: none yet)
-  int next;                   // unit 0's: the next (unit, part) item a finder warp takes
 };
+// Work counters of the finder and the inflate rounds: the first 1 + kRounds ints of the
+// unfilter's progress area (>= 64 ints; the unfilter zeroes it before its own use)
+constexpr int kSchedInts = 1 + kRounds;
+#ifndef TP_PNG_INFLATE_DYN  // the same for the inflate's units (per round)
+#define TP_PNG_INFLATE_DYN 1
+#endif
 #ifndef TP_PNG_FIND_DYN  // 1: a resident grid of finder warps taking (unit, part) items in
 #define TP_PNG_FIND_DYN 1  // order from a counter; 0: one warp per item (a partial last wave)
 #endif
@@ -549,13 +554,13 @@ __device__ __forceinline__ FindScratch* find_scratch(uint32_t* stage, int u) {
   return reinterpret_cast<FindScratch*>(reinterpret_cast<uint8_t*>(stage) + u * kStageBytesPerUnit);
 }
 
-__global__ void k_png_find_init(uint32_t* stage, int U) {
+__global__ void k_png_find_init(uint32_t* stage, int U, int* sched) {
   const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u < kSchedInts) sched[u] = 0;
   if (u >= U) return;
   FindScratch* f = find_scratch(stage, u);
   for (int p = 0; p < kFindParts; ++p) f->pos[p] = -1;
   f->lowest = kFindParts;
-  f->next = 0;
 }
 
 __global__ void k_png_find_select(PUnit* __restrict__ units, uint32_t* stage, int U, int parts,
@@ -588,7 +593,7 @@ __global__ void k_png_find_select(PUnit* __restrict__ units, uint32_t* stage, in
 
 __global__ void __launch_bounds__(kFindThreads)
     k_png_find(const uint8_t* __restrict__ payload, const PDesc* __restrict__ desc, int n,
-               PUnit* __restrict__ units, int U, uint32_t* stage, int parts) {
+               PUnit* __restrict__ units, int U, uint32_t* stage, int parts, int* sched) {
   __shared__ uint8_t tabs[kFindThreads][128];  // code-length code of a lane's full check
   __shared__ uint8_t kraft9[512];              // Kraft terms of three 3-bit lengths
   __shared__ int64_t queue[kFindThreads / 32][kFindQueue];
@@ -604,7 +609,7 @@ __global__ void __launch_bounds__(kFindThreads)
   const int lane = threadIdx.x & 31;
   // units need very different scan lengths (the distance from the unit start to the next
   // block header): warps take items from a counter instead of one fixed item each
-  int* next_item = &find_scratch(stage, 0)->next;
+  int* next_item = sched;
   for (int it = 0;; ++it) {
   int gw;
   if (TP_PNG_FIND_DYN) {
@@ -836,17 +841,30 @@ struct __align__(16) WarpTables {
 __global__ void __launch_bounds__(32 * kInflateWarps)
     k_png_inflate(const uint8_t* __restrict__ payload, const PDesc* __restrict__ desc, int n,
                   PUnit* __restrict__ units, int U, uint32_t* __restrict__ toks,
-                  uint32_t* __restrict__ stage, const int32_t* __restrict__ img_status) {
+                  uint32_t* __restrict__ stage, const int32_t* __restrict__ img_status, int* sched,
+                  int round) {
   __shared__ WarpTables wt_all[kInflateWarps];
   const int lane = threadIdx.x & 31;
-  const int u = blockIdx.x * kInflateWarps + (threadIdx.x >> 5);
-  if (u >= U) return;
   WarpTables& wt = wt_all[threadIdx.x >> 5];
+  // a resident wave of warps takes the units in order from a per-round counter (the units'
+  // decode times differ; one warp per unit left a partial last wave)
+  int* next_unit = sched + 1 + round;
+  for (int it = 0;; ++it) {
+  int u;
+  if (TP_PNG_INFLATE_DYN) {
+    int v = 0;
+    if (lane == 0) v = atomicAdd(next_unit, 1);
+    u = __shfl_sync(0xffffffffu, v, 0);
+  } else {
+    if (it > 0) break;
+    u = blockIdx.x * kInflateWarps + (threadIdx.x >> 5);
+  }
+  if (u >= U) break;
   PUnit& me = units[u];
-  if (!me.dirty) return;
+  if (!me.dirty) continue;
   const int k = unit_image(desc, n, u);
   const PDesc& d = desc[k];
-  if (img_status[k] != kImgOk) return;
+  if (img_status[k] != kImgOk) continue;
   const int64_t start = me.start;
   int64_t stop = -1;
   const int ulast = d.unit_base + d.n_units;
@@ -1052,6 +1070,8 @@ __global__ void __launch_bounds__(32 * kInflateWarps)
     me.fixups = nfix;
     me.rounds = nround;
   }
+  __syncwarp();  // the next unit's header rebuilds this warp's tables
+  }  // units
 }
 
 // ---------------------------------------------------------------------------
@@ -1744,7 +1764,8 @@ extern "C" TP_API int tp_png_decode(const uint8_t* d_payload, const void* d_desc
     // PNGs, 6,000 units: the extra scanning then costs more than it hides)
     const int sms = std::max(1, tp::device_sm_count());
     const int parts = std::max(1, std::min(kFindParts, (sms * 48) / std::max(U, 1)));
-    k_png_find_init<<<(U + 255) / 256, 256, 0, s>>>(stage, U);
+    int* sched = reinterpret_cast<int*>(work + totals[13]);  // (the unfilter's progress area)
+    k_png_find_init<<<(std::max(U, kSchedInts) + 255) / 256, 256, 0, s>>>(stage, U, sched);
     TP_PNG_DBG("k_png_find_init");
     const int64_t find_warps = static_cast<int64_t>(U) * parts;
     int64_t find_ctas = (find_warps + kFindThreads / 32 - 1) / (kFindThreads / 32);
@@ -1754,14 +1775,21 @@ extern "C" TP_API int tp_png_decode(const uint8_t* d_payload, const void* d_desc
       find_ctas = std::min<int64_t>(find_ctas, static_cast<int64_t>(std::max(find_occ, 1)) * sms);
     }
     k_png_find<<<static_cast<int>(find_ctas), kFindThreads, 0, s>>>(d_payload, desc, n, units, U,
-                                                                    stage, parts);
+                                                                    stage, parts, sched);
                  TP_PNG_DBG("k_png_find");
     k_png_find_select<<<(U + 255) / 256, 256, 0, s>>>(units, stage, U, parts,
                                                       static_cast<int>(totals[15]));
                                                       TP_PNG_DBG("k_png_find_select");
+    int64_t inflate_ctas = (U + kInflateWarps - 1) / kInflateWarps;
+    if (TP_PNG_INFLATE_DYN) {
+      static int inflate_occ = 0;
+      if (inflate_occ == 0)
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&inflate_occ, k_png_inflate, 32 * kInflateWarps, 0);
+      inflate_ctas = std::min<int64_t>(inflate_ctas, static_cast<int64_t>(std::max(inflate_occ, 1)) * sms);
+    }
     for (int r = 0; r < kRounds; ++r) {
-      k_png_inflate<<<(U + kInflateWarps - 1) / kInflateWarps, 32 * kInflateWarps, 0, s>>>(
-          d_payload, desc, n, units, U, toks, stage, d_status);
+      k_png_inflate<<<static_cast<int>(inflate_ctas), 32 * kInflateWarps, 0, s>>>(
+          d_payload, desc, n, units, U, toks, stage, d_status, sched, r);
           TP_PNG_DBG("k_png_inflate");
       k_png_chain<<<n, 32, 0, s>>>(desc, n, units, d_status, r);
       TP_PNG_DBG("k_png_chain");
