@@ -1183,7 +1183,11 @@ __global__ void k_png_chain(const PDesc* __restrict__ desc, int n, PUnit* __rest
 // positions of marker bytes go to the unit's list (a warp-aggregated append: the warp
 // walks its unit's tokens in order, so a register counter is the list's length).
 
-__global__ void k_png_expand(const uint8_t* __restrict__ payload, const PDesc* __restrict__ desc,
+#ifndef TP_PNG_EXPAND_MINB  // resident expand CTAs per SM: 6 (<= 40 registers) holds the
+#define TP_PNG_EXPAND_MINB 6  // 6,000 unit warps of 64 1080p PNGs in one wave (5: 5,920)
+#endif
+__global__ void __launch_bounds__(256, TP_PNG_EXPAND_MINB)
+    k_png_expand(const uint8_t* __restrict__ payload, const PDesc* __restrict__ desc,
                              int n, PUnit* __restrict__ units, int U,
                              const uint32_t* __restrict__ toks, uint16_t* __restrict__ T,
                              uint32_t* __restrict__ M, int32_t* __restrict__ img_status) {
