@@ -1402,14 +1402,25 @@ __global__ void __launch_bounds__(kAdlerThreads)
     const uint8_t* row = rows + static_cast<int64_t>(y) * d.r_stride;
     for (int64_t x = 16 * static_cast<int64_t>(lane); x < rowbytes; x += 16 * 32) {
       const uint4 v = *reinterpret_cast<const uint4*>(row + x);
-      const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
-      const uint64_t wt0 = static_cast<uint64_t>(len - (i0 + 1 + x));  // weight of byte x
+      uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+      if (x + 16 > rowbytes) {  // the row's last chunk: bytes past the row are padding
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const uint32_t dj = x + j < rowbytes ? (wv[j >> 2] >> (8 * (j & 3))) & 255u : 0u;
-        la += dj;
-        lb += (wt0 - j) * dj;
+        for (int q = 0; q < 4; ++q) {
+          const int64_t keep = rowbytes - (x + 4 * q);  // bytes of word q inside the row
+          wv[q] = keep >= 4 ? wv[q] : keep <= 0 ? 0u : wv[q] & ((1u << (8 * keep)) - 1u);
+        }
       }
+      // byte j of the chunk weighs wt0 - j: sum (wt0 - j) d_j = wt0 * S - T with S = sum d_j
+      // and T = sum j d_j, both from four byte dot products (dp4a) each
+      const uint64_t wt0 = static_cast<uint64_t>(len - (i0 + 1 + x));  // weight of byte x
+      uint32_t S = 0, T = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        S = __dp4a(wv[q], 0x01010101u, S);
+        T = __dp4a(wv[q], 0x03020100u + 0x04040404u * q, T);
+      }
+      la += S;
+      lb += wt0 * S - T;
     }
     a += la;
     b += lb % kAdlerMod;
