@@ -1512,6 +1512,9 @@ __device__ __forceinline__ uint32_t pack4(const uint32_t* b) {
 // block only ever waits for a block that is already running: no deadlock, and an image's
 // blocks run as a pipeline over several SMs (a 1080p image is 9 blocks).
 constexpr int kPriorBatch = 8;
+#ifndef TP_PNG_RELEASE_BATCH
+#define TP_PNG_RELEASE_BATCH 1
+#endif
 
 template <int BPP>
 __device__ void unfilter_block(const PDesc& d, int blk, uint8_t* __restrict__ r,
@@ -1692,8 +1695,18 @@ __device__ void unfilter_block(const PDesc& d, int blk, uint8_t* __restrict__ r,
       }
       if (tid == rows - 1 && !last_blk) {  // the next block's first row reads it
         __stcg(reinterpret_cast<Chunk*>(row) + i, rec);
+#if TP_PNG_RELEASE_BATCH
+        // published once per kPriorBatch chunks (the reader waits for whole batches): a
+        // fence per chunk held this warp -- and through the step barrier the whole CTA --
+        // for a memory-barrier round trip every step
+        if ((i + 1) % kPriorBatch == 0 || i + 1 == nch) {
+          __threadfence();  // release: the chunks before the counter
+          atomicExch(progress + item, i + 1);
+        }
+#else
         __threadfence();  // release: the chunk before the counter
         atomicExch(progress + item, i + 1);
+#endif
       }
       xch[t & 1][tid] = rec;
       up_prev = up;
