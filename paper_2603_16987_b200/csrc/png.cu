@@ -1489,6 +1489,36 @@ template <> struct ChunkVec<2> {
   __device__ __forceinline__ static uint32_t w(const T& v, int i) { return i == 0 ? v.x : v.y; }
   __device__ __forceinline__ static T make(const uint32_t* a) { return make_uint2(a[0], a[1]); }
 };
+struct Words8 {  // 32-byte chunk
+  uint4 a, b;
+};
+template <> struct ChunkVec<8> {
+  using T = Words8;
+  __device__ __forceinline__ static uint32_t w(const T& v, int i) {
+    return ChunkVec<4>::w(i < 4 ? v.a : v.b, i & 3);
+  }
+  __device__ __forceinline__ static T make(const uint32_t* a) {
+    return Words8{make_uint4(a[0], a[1], a[2], a[3]), make_uint4(a[4], a[5], a[6], a[7])};
+  }
+};
+// L2-coherent chunk loads / stores (the block-to-block row handoff)
+__device__ __forceinline__ uint4 chunk_ldcg(const uint4* p) { return __ldcg(p); }
+__device__ __forceinline__ uint2 chunk_ldcg(const uint2* p) { return __ldcg(p); }
+__device__ __forceinline__ Words8 chunk_ldcg(const Words8* p) {
+  return Words8{__ldcg(&p->a), __ldcg(&p->b)};
+}
+__device__ __forceinline__ void chunk_stcg(uint4* p, const uint4& v) { __stcg(p, v); }
+__device__ __forceinline__ void chunk_stcg(uint2* p, const uint2& v) { __stcg(p, v); }
+__device__ __forceinline__ void chunk_stcg(Words8* p, const Words8& v) {
+  __stcg(&p->a, v.a);
+  __stcg(&p->b, v.b);
+}
+__device__ __forceinline__ void chunk_stcs(uint4* p, const uint4& v) { __stcs(p, v); }
+__device__ __forceinline__ void chunk_stcs(uint2* p, const uint2& v) { __stcs(p, v); }
+__device__ __forceinline__ void chunk_stcs(Words8* p, const Words8& v) {
+  __stcs(&p->a, v.a);
+  __stcs(&p->b, v.b);
+}
 using CV = ChunkVec<kChunkWords>;
 using Chunk = CV::T;
 constexpr int kCh = 4 * kChunkWords;
@@ -1564,7 +1594,7 @@ __device__ void unfilter_block(const PDesc& d, int blk, uint8_t* __restrict__ r,
             __threadfence();  // acquire: the chunks were written before the counter
 #pragma unroll
             for (int q = 0; q < kPriorBatch; ++q)
-              if (i + q < nch) pbuf[q] = __ldcg(reinterpret_cast<const Chunk*>(prior) + i + q);
+              if (i + q < nch) pbuf[q] = chunk_ldcg(reinterpret_cast<const Chunk*>(prior) + i + q);
           }
           up = pbuf[i % kPriorBatch];
         }
@@ -1658,7 +1688,7 @@ __device__ void unfilter_block(const PDesc& d, int blk, uint8_t* __restrict__ r,
       if (BPP == 3) {
         uint8_t* dst = orow + x0;
         if (oal && nb == kCh) {
-          __stcs(reinterpret_cast<Chunk*>(dst), rec);
+          chunk_stcs(reinterpret_cast<Chunk*>(dst), rec);
         } else {
 #pragma unroll
           for (int j = 0; j < kCh; ++j)
@@ -1685,7 +1715,7 @@ __device__ void unfilter_block(const PDesc& d, int blk, uint8_t* __restrict__ r,
             uint32_t pw[kChunkWords];
 #pragma unroll
             for (int e = 0; e < kChunkWords; ++e) pw[e] = pack4(px + q * kCh + 4 * e);
-            __stcs(reinterpret_cast<Chunk*>(dst) + q, CV::make(pw));
+            chunk_stcs(reinterpret_cast<Chunk*>(dst) + q, CV::make(pw));
           }
         } else {
 #pragma unroll
@@ -1694,7 +1724,7 @@ __device__ void unfilter_block(const PDesc& d, int blk, uint8_t* __restrict__ r,
         }
       }
       if (tid == rows - 1 && !last_blk) {  // the next block's first row reads it
-        __stcg(reinterpret_cast<Chunk*>(row) + i, rec);
+        chunk_stcg(reinterpret_cast<Chunk*>(row) + i, rec);
 #if TP_PNG_RELEASE_BATCH
         // published once per kPriorBatch chunks (the reader waits for whole batches): a
         // fence per chunk held this warp -- and through the step barrier the whole CTA --
