@@ -1542,6 +1542,9 @@ __device__ __forceinline__ uint32_t pack4(const uint32_t* b) {
 // block only ever waits for a block that is already running: no deadlock, and an image's
 // blocks run as a pipeline over several SMs (a 1080p image is 9 blocks).
 constexpr int kPriorBatch = 8;
+#ifndef TP_PNG_ACQREL  // 1: ld.acquire / st.release on the progress counters instead of fences
+#define TP_PNG_ACQREL 1
+#endif
 #ifndef TP_PNG_RELEASE_BATCH
 #define TP_PNG_RELEASE_BATCH 1
 #endif
@@ -1590,8 +1593,18 @@ __device__ void unfilter_block(const PDesc& d, int blk, uint8_t* __restrict__ r,
           // L2 round trip per batch instead of per step (the block lags a few steps more)
           if (i % kPriorBatch == 0) {
             const int need = min(i + kPriorBatch, nch);
+#if TP_PNG_ACQREL
+            // acquire load: the chunks written before the counter are visible after it
+            for (;;) {
+              int v;
+              asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(prior_progress) : "memory");
+              if (v >= need) break;
+              __nanosleep(32);
+            }
+#else
             while (*prior_progress < need) __nanosleep(32);
             __threadfence();  // acquire: the chunks were written before the counter
+#endif
 #pragma unroll
             for (int q = 0; q < kPriorBatch; ++q)
               if (i + q < nch) pbuf[q] = chunk_ldcg(reinterpret_cast<const Chunk*>(prior) + i + q);
@@ -1730,8 +1743,12 @@ __device__ void unfilter_block(const PDesc& d, int blk, uint8_t* __restrict__ r,
         // fence per chunk held this warp -- and through the step barrier the whole CTA --
         // for a memory-barrier round trip every step
         if ((i + 1) % kPriorBatch == 0 || i + 1 == nch) {
+#if TP_PNG_ACQREL
+          asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(progress + item), "r"(i + 1) : "memory");
+#else
           __threadfence();  // release: the chunks before the counter
           atomicExch(progress + item, i + 1);
+#endif
         }
 #else
         __threadfence();  // release: the chunk before the counter
