@@ -90,7 +90,10 @@ struct __align__(16) PUnit {
 };
 
 // Unfilter work item: a block of consecutive scanlines of one image, one thread each.
-constexpr int kUnfilterRows = 128;
+#ifndef TP_PNG_UNFILTER_ROWS  // rows per unfilter block (= threads per unfilter CTA)
+#define TP_PNG_UNFILTER_ROWS 128
+#endif
+constexpr int kUnfilterRows = TP_PNG_UNFILTER_ROWS;
 
 // tp_png_describe's totals[16]: [0] units, [1] tokens, [2] raw bytes (T entries),
 // [3..6] byte offsets of units / tokens / T / R, [7] workspace bytes, [8] R bytes,
