@@ -233,7 +233,9 @@ TP_API int tp_stage_pack(int32_t n, const uint8_t* const* src, const int64_t* sr
  *                     subsequences of sub_bits bits) -> DC prediction -> ISLOW IDCT ->
  *                     fancy upsampling + colour conversion into d_out.  d_status[k] = 0,
  *                     or nonzero when image k's entropy data is not a clean baseline
- *                     stream (corrupt / truncated): decode that one on the host. */
+ *                     stream (corrupt / truncated, misnumbered restart markers, a block
+ *                     outside the range where libjpeg-turbo's 16-bit SIMD IDCT is exact):
+ *                     decode that one on the host. */
 #define TP_JPEG_OK 0
 #define TP_JPEG_UNSUPPORTED 1
 #define TP_JPEG_CORRUPT 2
