@@ -193,7 +193,8 @@ class JpegDecoder:
         raw_off[~ok] = 0
         payload_bytes = _round_up(int(mark + sizes.sum()), 256)
         totals = np.zeros(8, dtype=np.int64)
-        sub_bits, lead_bits = self._pick(int(8 * scan_len[ok].sum()))
+        pixels = sum(int(infos[k].width) * int(infos[k].height) for k in range(n) if ok[k])
+        sub_bits, lead_bits = self._pick(int(8 * scan_len[ok].sum()), pixels)
         sl = self.slots[self._i % len(self.slots)]
         self._i += 1
         if sl.copied is not None:
@@ -258,16 +259,21 @@ class JpegDecoder:
         batch.finish()
         return out
 
-    def _pick(self, scan_bits: int) -> tuple:
+    def _pick(self, scan_bits: int, pixels: int = 0) -> tuple:
         """(sub_bits, lead_bits) for a batch of `scan_bits` entropy-coded bits.  Measured on
         corpus-like 1080p JPEGs (profiles/r02/jpeg/): one image decodes fastest with short
         subsequences and a long lead-in (1024 + 2048: K7 0.69 ms, decode() 1.0 ms; 4096:
         1.71 ms per call), 64 images with 4096-bit subsequences and a 2048-bit lead-in
-        (2.47 ms; 2.56 ms with a 4096-bit lead-in, profiles/r02/jpeg/lead_sweep.log)."""
+        (2.47 ms; 2.56 ms with a 4096-bit lead-in, profiles/r02/jpeg/lead_sweep.log), and a
+        6144-bit lead-in for noise-like content."""
         if self.sub_bits:
             return self.sub_bits, self.lead_bits
         if scan_bits < 32 * 2**20:  # fewer than ~8 corpus-like 1080p images
             return 1024, 2048
+        if pixels and scan_bits >= 4 * pixels:
+            # high-entropy content (>= 4 coded bits per pixel, noise-like): longer lead-ins
+            # cut the re-decode half-rounds (16 noise 1080p JPEGs: 2.75 -> 2.63 ms)
+            return 4096, 6144
         return 4096, 2048
 
     def launch(self, stream: Optional[torch.cuda.Stream] = None) -> None:
