@@ -527,7 +527,7 @@ __device__ __forceinline__ uint32_t win32(uint32_t w0, uint32_t w1, uint32_t w2,
 // success of its first successful batch.
 constexpr int kFindQueue = 32;
 #ifndef TP_PNG_QFLUSH  // queued candidates that trigger a batch of full checks
-#define TP_PNG_QFLUSH 16
+#define TP_PNG_QFLUSH 24
 #endif
 
 // Each unit is scanned by kFindParts warps, one per quarter: a unit's start is the first
